@@ -1,0 +1,85 @@
+"""Pins for oracle/easgd.py (CPU only)."""
+
+import numpy as np
+import pytest
+
+import exact
+from oracle.easgd import easgd_sequence, easgd_update
+from paper_1605_08325_b200.inputs import worker_buffer
+
+F32 = np.float32
+
+
+def test_spec_example():
+    # alpha = 0.5, x = 2, centre 0 -> x' = 1, centre' = 1
+    x, c = easgd_update(np.array([2.0], F32), np.array([0.0], F32), 0.5)
+    assert x.tolist() == [1.0] and c.tolist() == [1.0]
+
+
+def test_alpha_one_swaps():
+    # alpha = 1: x' = c and c' = x whenever x - c is exact (integers here)
+    g = np.random.default_rng(1)
+    x = g.integers(-1000, 1000, 1000).astype(F32)
+    c = g.integers(-1000, 1000, 1000).astype(F32)
+    x2, c2 = easgd_update(x, c, 1.0)
+    assert np.array_equal(x2, c) and np.array_equal(c2, x)
+
+
+def test_alpha_half_meets_in_the_middle():
+    # alpha = 0.5 on integers: both become the exact midpoint (one exchange)
+    g = np.random.default_rng(2)
+    x = g.integers(-1000, 1000, 1000).astype(F32)
+    c = g.integers(-1000, 1000, 1000).astype(F32)
+    x2, c2 = easgd_update(x, c, 0.5)
+    mid = ((x.astype(np.float64) + c.astype(np.float64)) / 2).astype(F32)
+    assert np.array_equal(x2, mid) and np.array_equal(c2, mid)
+
+
+@pytest.mark.parametrize("alpha", [0.5, 0.0625, 0.3])
+@pytest.mark.parametrize("dist", ["D1", "D2", "D3", "D6"])
+def test_brute_force_steps(alpha, dist):
+    """Each of d = x - c, e = alpha d, x' = x - e, c' = c + e is one correctly
+    rounded fp32 operation (no FMA), checked with exact rationals."""
+    x = worker_buffer(64, dist, 0, config=21)
+    c = worker_buffer(64, dist, 1, config=21)
+    x2, c2 = easgd_update(x, c, alpha)
+    a = float(F32(alpha))
+    for i in range(64):
+        d = exact.sub(x[i], c[i])
+        e = exact.mul(a, d)
+        assert exact.same_bits32(x2[i], exact.sub(x[i], e)), (i, x[i], c[i])
+        assert exact.same_bits32(c2[i], exact.add(c[i], e))
+
+
+@pytest.mark.parametrize("alpha", [0.5, 0.0625, 0.3])
+def test_conservation(alpha):
+    """x + c is conserved exactly in rational arithmetic ((x-e)+(c+e) = x+c) and
+    within one rounding of each output in fp32: |(x'+c')-(x+c)| <= 2^-24(|x'|+|c'|)."""
+    x = worker_buffer(200000, "D1", 0, config=22)
+    c = worker_buffer(200000, "D1", 1, config=22)
+    x2, c2 = easgd_update(x, c, alpha)
+    lhs = np.abs((x2.astype(np.float64) + c2) - (x.astype(np.float64) + c))
+    assert np.all(lhs <= 2.0 ** -24 * (np.abs(x2.astype(np.float64)) + np.abs(c2)))
+
+
+def test_sequence_is_ordered_composition():
+    """'Without the Round-Robin scheme': updates apply one at a time
+    in arrival order; the sequence equals the explicit composition, and a
+    different order gives a different (valid) centre."""
+    ws = [worker_buffer(1000, "D1", r, config=23) for r in range(4)]
+    c = worker_buffer(1000, "D1", 9, config=23)
+    order = [2, 0, 3, 1, 2]
+    nws, nc = easgd_sequence(ws, c, 0.125, order)
+    ref = [w.copy() for w in ws]
+    cc = c.copy()
+    for w in order:
+        ref[w], cc = easgd_update(ref[w], cc, 0.125)
+    assert np.array_equal(nc, cc)
+    for a, b in zip(nws, ref):
+        assert np.array_equal(a, b)
+    _, nc2 = easgd_sequence(ws, c, 0.125, [0, 1, 2, 3, 2])
+    assert not np.array_equal(nc, nc2)
+    # conservation across a whole round: sum_w x_w + c conserved up to rounding
+    tot0 = sum(w.astype(np.float64) for w in ws) + c
+    tot1 = sum(w.astype(np.float64) for w in nws) + nc
+    assert np.max(np.abs(tot1 - tot0)) < 1e-5
