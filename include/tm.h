@@ -1,0 +1,200 @@
+/*
+ * tm.h -- C ABI of libtm.so: the B200-native BSP parameter exchange of Theano-MPI
+ * (Ma, Mao, Taylor; arXiv 1605.08325).  Plain C types only (no torch, no CUDA
+ * headers): device buffers are `float*`, streams are `void*` holding a
+ * cudaStream_t (e.g. torch.cuda.current_stream().cuda_stream; NULL = legacy
+ * default stream).
+ *
+ * What is computed (PAPER.md = /root/reference/PAPER.md, line numbers):
+ *   L66-70, L195-212  BSP data parallelism: after each SGD step the k workers'
+ *                     parameters are "exchanged between worker processes in a
+ *                     collective way"; L377-384 (AWAGD) averages them (1/k).
+ *   L227-228          "Synchronous parameter exchange is an array reduction problem".
+ *   L233-237          AR    : MPI Allreduce().
+ *   L237-246, L252-256 ASA  : Alltoall of k sub-arrays, GPU summation on the owner,
+ *                     Allgather of the sums.
+ *   L262-269          ASA16 : ASA with the transfers in half precision, the
+ *                     summation in full precision.
+ *   L143-148, L573-588 EASGD : elastic averaging of a worker and a centre
+ *                     (update equations: SPEC.md L475).
+ *
+ * Result of one tm_exchange, per element i, identical on every rank (DESIGN.md
+ * readings Q1-Q10):
+ *   ASA, AR : s = x_0[i]; s = fl(s + x_j[i]) for j = 1..k-1 (ascending rank);
+ *             out = fl(s / k).   (AR through NCCL: order not fixed, see below.)
+ *   ASA16   : h_j = rn16(x_j[i]) for every j (own included); s = widen(h_0);
+ *             s = fl(s + widen(h_j)) ascending; a = fl(s / k);
+ *             out = widen(rn16(a)) on every rank (owner included).
+ *   rn16 = IEEE binary16 round-to-nearest-even, gradual subnormals, |x| >= 65520
+ *   -> +-inf; widen exact; fl = one IEEE fp32 operation, no FMA, no FTZ.
+ *   k = 1: identity for every strategy (nothing launched).
+ *
+ * Layout: rank r owns segment r = elements
+ * [r*L, min((r+1)*L, P)), L = roundup(ceil(P/k), 256); padding is +0 and never
+ * written to the caller's buffer.  The library owns all staging (k*L wire
+ * elements per rank), the owner's averaged segment (L wire elements), the flag
+ * pad and the status word, allocated with cudaMalloc at init (required for CUDA
+ * IPC export) and freed at finalize.
+ *
+ * Process model: one exchanger per process.  A process hosts `nlocal`
+ * consecutive ranks [rank, rank + nlocal) on ONE device:
+ *   nlocal == 1     -- one process per GPU (torchrun); peers are reached through
+ *                      CUDA IPC mappings over NVLink/NVSwitch.  Needs the
+ *                      bootstrap (export -> all-gather of blobs -> import).
+ *   nlocal == size  -- a single-process group: all k ranks' buffers live on one
+ *                      device ("k simulated workers"); the same kernels run with
+ *                      local pointers in the peer table.  No bootstrap.
+ * Thread safety: one host thread per process calls tm_*.
+ *
+ * Collective contract: every rank calls tm_exchange the same
+ * number of times, in the same order.  Each call carries an epoch; cross-rank
+ * synchronisation is by per-CTA epoch flags in peer memory (st.release.sys /
+ * ld.acquire.sys).  A rank that never arrives makes its peers' spins time out:
+ * they set TM_E_TIMEOUT in the sticky status and exit (no hang).
+ *
+ * Errors: argument/state/launch errors are returned synchronously.  Numeric
+ * conditions never abort the collective; they set sticky status bits read by
+ * tm_exchange_status: non-finite inputs (TM_E_NONFINITE), fp16 overflow of an
+ * input, |x| >= 65520 (TM_E_OVERFLOW16, ASA16; the value becomes +-inf as IEEE
+ * prescribes), barrier timeout (TM_E_TIMEOUT).
+ */
+#ifndef TM_H_
+#define TM_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define TM_MAX_RANKS 8      /* one NVSwitch box */
+#define TM_BLOB_BYTES 512   /* size of one bootstrap blob */
+
+typedef enum {
+  TM_AR = 0,     /* plain allreduce                     */
+  TM_ASA = 1,    /* Alltoall-sum-Allgather, fp32 wire (L237-246)          */
+  TM_ASA16 = 2,  /* ASA with fp16 wire, fp32 summation (L262-269)         */
+  TM_EASGD = 3   /* EASGD context: library-owned centre buffer (L573-588) */
+} tm_strategy;
+
+typedef enum {
+  TM_OK = 0,
+  TM_E_ARG = 1,        /* bad argument (null, size, rank, strategy)               */
+  TM_E_ALIGN = 2,      /* a device buffer is not 16-byte aligned                   */
+  TM_E_STATE = 3,      /* call out of order (not initialised / not bootstrapped)  */
+  TM_E_CUDA = 4,       /* a CUDA runtime call or launch failed                     */
+  TM_E_NCCL = 5,       /* NCCL missing or failed (AR across processes)            */
+  TM_E_MISMATCH = 6,   /* ranks disagree on nparams / strategy / layout           */
+  TM_E_TIMEOUT = 7,    /* a peer did not arrive within the timeout (sticky)       */
+  TM_E_NONFINITE = 8,  /* a non-finite input element was seen (sticky)             */
+  TM_E_OVERFLOW16 = 9  /* an input rounded to +-inf in binary16 (sticky, ASA16)    */
+} tm_status;
+
+/* Sticky status bits (tm_exchange_status's `bits`). */
+#define TM_BIT_NONFINITE 0x1u
+#define TM_BIT_OVERFLOW16 0x2u
+#define TM_BIT_TIMEOUT 0x4u
+
+typedef struct {
+  int32_t rank;    /* first global rank hosted by this process                */
+  int32_t size;    /* k, number of ranks (workers), 1..TM_MAX_RANKS           */
+  int32_t device;  /* CUDA device ordinal used by this process               */
+  int32_t nlocal;  /* ranks hosted by this process: 1 or size (see above)     */
+} tm_world;
+
+typedef struct {
+  int64_t nparams;       /* P                                                 */
+  int64_t seg_len;       /* L = roundup(ceil(P/k), 256)                      */
+  int64_t chunk_len;     /* per-CTA slice of a segment (multiple of 256)      */
+  int32_t k, rank, nlocal, strategy;
+  int32_t ctas_per_rank; /* C: CTAs per rank in the exchange kernel           */
+  int32_t threads;       /* threads per CTA                                   */
+  int32_t sm_count;
+  int32_t wire_bytes;    /* 4 (AR, ASA) or 2 (ASA16)                          */
+  int64_t lib_bytes;     /* device bytes the library owns in this process     */
+  uint32_t epoch;        /* number of exchanges issued so far                 */
+} tm_layout_info;
+
+/* Create the process-global exchanger.  nparams >= 1; world as above; strategy
+ * a tm_strategy.  Allocates the library-owned buffers on world->device.  For
+ * nlocal == size the exchanger is ready on return; otherwise the bootstrap
+ * below must follow.  Returns TM_OK, TM_E_ARG, TM_E_STATE (already
+ * initialised) or TM_E_CUDA. */
+int tm_exchange_init(int64_t nparams, const tm_world* world, int strategy);
+
+/* Write this process's bootstrap blob (CUDA IPC handle of its slab, layout, and
+ * on the process hosting rank 0 an NCCL unique id for AR) into `blob`, which
+ * must hold TM_BLOB_BYTES; *len receives TM_BLOB_BYTES. */
+int tm_bootstrap_export(void* blob, size_t* len);
+
+/* `blobs` holds size/nlocal blobs of `len_each` bytes, in process order
+ * (process p hosts ranks [p*nlocal, (p+1)*nlocal)).  Opens the peers' IPC
+ * mappings, checks that every process agrees on nparams, strategy and layout
+ * (else TM_E_MISMATCH), and for AR initialises the NCCL communicator
+ * (collective: every process must call it). */
+int tm_bootstrap_import(const void* blobs, size_t len_each);
+
+/* North-star call: average dev_buf (fp32[nparams], this rank's device, 16-byte
+ * aligned, caller-owned) across the k ranks, IN PLACE, on `stream`.
+ * Asynchronous: returns after enqueueing.  Requires nlocal == 1. */
+int tm_exchange(float* dev_buf, void* stream);
+
+/* Same for a process hosting nlocal ranks: dev_bufs is a HOST array of nbufs ==
+ * nlocal device pointers (rank order), each fp32[nparams], 16-byte aligned,
+ * pairwise disjoint. */
+int tm_exchange_group(float* const* dev_bufs, int nbufs, void* stream);
+
+/* North-star call: one elastic update of nparams elements:
+ *   d = fl(x - c); e = fl(alpha*d); x = fl(x - e); c = fl(c + e)   (no FMA)
+ * worker_buf: this rank's fp32 buffer; center_buf: any fp32 buffer addressable
+ * from this device (local, or from tm_easgd_center).  The caller guarantees
+ * exclusive access to the centre for the duration (serialised server order,
+ * reading Q15).  Works in any initialised context; n = init nparams. */
+int tm_easgd_update(float* worker_buf, float* center_buf, float alpha, void* stream);
+
+/* Extended form: explicit length n, and concurrent != 0 applies the centre
+ * update with an atomic add (red.global.add.f32, system scope) so several
+ * workers may update one centre at once (no lost updates; order not fixed).
+ * Does not need tm_exchange_init. */
+int tm_easgd_update_ex(float* worker_buf, float* center_buf, int64_t n, float alpha,
+                       int concurrent, void* stream);
+
+/* A whole server round on one device, in ARRIVAL order ("without
+ * the Round-Robin scheme"): for t = 0..norder-1 apply the elastic update of
+ * workers[order[t]] against the centre, in one fused pass over the elements.
+ * Bitwise equal to norder serial tm_easgd_update calls.  workers: HOST array of
+ * nworkers device pointers; order: HOST array of norder indices in
+ * [0, nworkers); nworkers <= 16, norder <= 64.  Does not need init. */
+int tm_easgd_round(float* const* workers, int nworkers, const int32_t* order, int norder,
+                   float* center_buf, int64_t n, float alpha, void* stream);
+
+/* Library-owned EASGD centre (strategy TM_EASGD) of owner_rank, as a pointer
+ * usable on this device (local or IPC-mapped over NVLink). */
+int tm_easgd_center(int owner_rank, float** center);
+
+/* Synchronise `stream`, then return the most severe sticky status
+ * (TM_E_TIMEOUT > TM_E_OVERFLOW16 > TM_E_NONFINITE > TM_OK) and clear it.
+ * `bits` (optional) receives the TM_BIT_* mask. */
+int tm_exchange_status(void* stream, uint32_t* bits);
+
+/* Layout of the current exchanger (for tests and the bench). */
+int tm_layout(tm_layout_info* out);
+
+/* Barrier spin timeout in nanoseconds (default 10 s; 0 restores default). */
+int tm_set_timeout_ns(uint64_t ns);
+
+/* Release everything; safe to call twice. */
+int tm_exchange_finalize(void);
+
+const char* tm_strerror(int status);
+
+/* Test hook: the exact device rounding the ASA16 path uses (cvt.rn.f16.f32),
+ * applied elementwise: out16[i] = rn16(in[i]) as binary16 bit patterns. */
+int tm_cast_rn16(const float* in, uint16_t* out16, int64_t n, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* TM_H_ */

@@ -1,0 +1,55 @@
+// Internal interface between the C++ runtime (tm_runtime.cpp) and the sm_100a
+// kernels (tm_kernels.cu).  Not part of the public ABI.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "tm.h"
+
+namespace tmx {
+
+constexpr int kThreads = 256;       // threads per CTA of every kernel
+constexpr int kVec = 8;             // elements per vector unit (16 B of fp16)
+constexpr int64_t kAlign = 256;     // segment / chunk alignment in elements
+constexpr int64_t kMinChunk = 2048; // smallest per-CTA chunk worth a barrier
+
+// Flag pad of one rank: u32 flags[kPhases][TM_MAX_RANKS][C]; slot
+// [phase][src][c] is written by rank `src` (remote store) and spun on by the
+// owner of the pad.
+constexpr int kPhaseReady = 0;    // src finished its pre-cast of chunk c
+constexpr int kPhaseReduced = 1;  // src finished summing its segment's chunk c
+constexpr int kPhases = 2;
+
+struct ExchangeArgs {
+  void* stage[TM_MAX_RANKS];      // rank j's staging (k*L wire elems), as mapped here
+  void* avg[TM_MAX_RANKS];        // rank j's averaged segment (L wire elems)
+  uint32_t* flags[TM_MAX_RANKS];  // rank j's flag pad
+  float* x[TM_MAX_RANKS];         // user buffers of the LOCAL ranks (index r - rank0)
+  uint32_t* status;               // sticky status word (local)
+  int64_t P, L, Lc;               // params, segment length, per-CTA chunk length
+  int32_t k, rank0, C;            // ranks, first local rank, CTAs per rank
+  uint32_t epoch;
+  uint64_t timeout_ns;
+};
+
+// Persistent fused exchange: pre-cast -> ready barrier -> reduce-scatter pull with
+// fused sum/scale/cast -> reduced barrier -> allgather pull with fused widen.
+// wire16: fp16 wire (ASA16) else fp32 (ASA).  grid = nlocal * C, cooperative.
+cudaError_t launch_exchange(const ExchangeArgs& a, int nlocal, bool wire16, cudaStream_t s);
+
+// Single-process allreduce-average of k device buffers (AR when all ranks are
+// local): one pass, ascending-rank fp32 sum, one division, result to all k.
+cudaError_t launch_local_allreduce(float* const* bufs, int k, int64_t P, cudaStream_t s);
+
+cudaError_t launch_easgd(float* x, float* c, int64_t n, float alpha, bool concurrent,
+                         cudaStream_t s);
+cudaError_t launch_easgd_round(float* const* w, int nw, const int32_t* order, int norder,
+                               float* c, int64_t n, float alpha, cudaStream_t s);
+cudaError_t launch_cast_rn16(const float* in, uint16_t* out, int64_t n, cudaStream_t s);
+
+// Max co-resident CTAs of the exchange kernel on `device` (occupancy * SMs).
+int exchange_max_ctas(int device, bool wire16, int k);
+int grid_for_streaming(int device);
+
+}  // namespace tmx

@@ -1,0 +1,562 @@
+// sm_100a kernels of the Theano-MPI parameter exchange (arXiv 1605.08325).
+//
+//   tm_exchange_kernel  -- ASA / ASA16: one persistent,
+//                          cooperative launch per exchange, three phases per CTA
+//                          separated by cross-rank per-CTA epoch flags:
+//        a2 pre-cast   x (fp32, caller's buffer) -> stage (wire type), all k
+//                      segments of this CTA's chunk; rn16 for ASA16 (reading R1:
+//                      the own segment is rounded too); non-finite / fp16
+//                      overflow detection fused.
+//        a3 ready barrier.
+//        a4 reduce-scatter PULL: for the own segment r, load the chunk from every
+//                      rank's stage (peer pointers: NVLink P2P loads on a real box,
+//                      local HBM in a single-process group), widen, sum in
+//                      ascending rank from the rank-0 term, one IEEE division by
+//                      k, round to the wire type, store to the own `avg`.
+//        a5 reduced barrier.
+//        a6 allgather PULL: load every rank's `avg` chunk, widen, store into the
+//                      caller's buffer (truncated at P).
+//   local_allreduce     -- AR when all k ranks live in this process: one pass.
+//   easgd / easgd_round -- elastic update.
+//   cast_rn16           -- test hook: the device rounding used by a2/a4.
+//
+// Numerics: every fp32 op is an explicit round-to-nearest intrinsic
+// (__fadd_rn/__fsub_rn/__fmul_rn/__fdiv_rn: no FMA contraction, IEEE division);
+// the library is compiled without --use_fast_math (no FTZ).  The binary16
+// conversions are cvt.rn.f16(x2).f32 (RNE, gradual subnormals, overflow to inf)
+// and the exact cvt.f32.f16.
+//
+// Memory-ordering protocol (a3/a5): after __syncthreads(), thread j < k writes
+// the epoch into rank j's flag slot [phase][r][c] with st.release.sys and then
+// spins with ld.acquire.sys on its own slot [phase][j][c]; a second
+// __syncthreads() publishes the acquisition to the CTA.  Flags only couple CTA
+// c of every rank, so no grid-wide barrier is needed.  Reuse of stage/avg across
+// back-to-back exchanges is safe without a trailing barrier:
+//   stage_j(n+1) is written only after rank j saw REDUCED(n) from every rank,
+//     i.e. after every rank finished reading stage_j(n);
+//   avg_j(n+1) is written only after rank j saw READY(n+1) from every rank, which
+//     each rank signals after its AG(n) reads of avg_j(n).
+
+#include <cuda_fp16.h>
+#include <stdint.h>
+
+#include <algorithm>
+
+#include "tm_internal.h"
+
+namespace tmx {
+namespace {
+
+__device__ __forceinline__ uint64_t globaltimer() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
+__device__ __forceinline__ void st_release_sys(uint32_t* p, uint32_t v) {
+  asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+__device__ __forceinline__ uint32_t ld_acquire_sys(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+// 16-byte accesses.  Peer / staging data is written during the same kernel by
+// other SMs or GPUs, so the non-coherent (.nc) path is never used for it; .cg
+// caches in L2 only.
+__device__ __forceinline__ uint4 ld16_cg(const void* p) {
+  return __ldcg(reinterpret_cast<const uint4*>(p));
+}
+__device__ __forceinline__ void st16_cg(void* p, uint4 v) {
+  __stcg(reinterpret_cast<uint4*>(p), v);
+}
+__device__ __forceinline__ float4 ld16_f(const float* p) {
+  return __ldcs(reinterpret_cast<const float4*>(p));
+}
+__device__ __forceinline__ void st16_f(float* p, float4 v) {
+  __stcs(reinterpret_cast<float4*>(p), v);
+}
+
+__device__ __forceinline__ uint32_t pack_rn16x2(float lo, float hi) {
+  __half2 h = __floats2half2_rn(lo, hi);  // cvt.rn.f16x2.f32
+  return *reinterpret_cast<uint32_t*>(&h);
+}
+__device__ __forceinline__ float2 unpack16x2(uint32_t u) {
+  __half2 h = *reinterpret_cast<__half2*>(&u);
+  return __half22float2(h);  // exact
+}
+
+// Status bits of one fp32 value: non-finite; |x| >= 65520 (rounds to fp16 inf).
+__device__ __forceinline__ uint32_t status_of(float v, bool wire16) {
+  const uint32_t b = __float_as_uint(v) & 0x7fffffffu;
+  uint32_t s = (b >= 0x7f800000u) ? TM_BIT_NONFINITE : 0u;
+  if (wire16 && b < 0x7f800000u && b >= 0x477ff000u) s |= TM_BIT_OVERFLOW16;  // 65520.0f
+  return s;
+}
+
+// ---------------------------------------------------------------------------
+// Wire-type traits: one "unit" = 16 bytes of wire data.
+//   fp16 wire: 8 elements (32 B of fp32 source);  fp32 wire: 4 elements.
+// ---------------------------------------------------------------------------
+template <bool W16>
+struct Unit;
+
+template <>
+struct Unit<true> {
+  static constexpr int kElems = 8;
+  struct Src { float4 a, b; };
+  __device__ static Src load_src(const float* p) { return {ld16_f(p), ld16_f(p + 4)}; }
+  __device__ static void to_floats(const Src& s, float* f) {
+    f[0] = s.a.x; f[1] = s.a.y; f[2] = s.a.z; f[3] = s.a.w;
+    f[4] = s.b.x; f[5] = s.b.y; f[6] = s.b.z; f[7] = s.b.w;
+  }
+  __device__ static uint4 encode(const float* f) {
+    return make_uint4(pack_rn16x2(f[0], f[1]), pack_rn16x2(f[2], f[3]),
+                      pack_rn16x2(f[4], f[5]), pack_rn16x2(f[6], f[7]));
+  }
+  __device__ static void decode(uint4 u, float* f) {
+    float2 t;
+    t = unpack16x2(u.x); f[0] = t.x; f[1] = t.y;
+    t = unpack16x2(u.y); f[2] = t.x; f[3] = t.y;
+    t = unpack16x2(u.z); f[4] = t.x; f[5] = t.y;
+    t = unpack16x2(u.w); f[6] = t.x; f[7] = t.y;
+  }
+  __device__ static void store_dst(float* p, const float* f) {
+    st16_f(p, make_float4(f[0], f[1], f[2], f[3]));
+    st16_f(p + 4, make_float4(f[4], f[5], f[6], f[7]));
+  }
+};
+
+template <>
+struct Unit<false> {
+  static constexpr int kElems = 4;
+  struct Src { float4 a; };
+  __device__ static Src load_src(const float* p) { return {ld16_f(p)}; }
+  __device__ static void to_floats(const Src& s, float* f) {
+    f[0] = s.a.x; f[1] = s.a.y; f[2] = s.a.z; f[3] = s.a.w;
+  }
+  __device__ static uint4 encode(const float* f) {
+    return make_uint4(__float_as_uint(f[0]), __float_as_uint(f[1]), __float_as_uint(f[2]),
+                      __float_as_uint(f[3]));
+  }
+  __device__ static void decode(uint4 u, float* f) {
+    f[0] = __uint_as_float(u.x); f[1] = __uint_as_float(u.y);
+    f[2] = __uint_as_float(u.z); f[3] = __uint_as_float(u.w);
+  }
+  __device__ static void store_dst(float* p, const float* f) {
+    st16_f(p, make_float4(f[0], f[1], f[2], f[3]));
+  }
+};
+
+// Cross-rank, per-CTA epoch barrier (see the protocol in the file header).
+// Returns false (whole CTA) if a peer timed out.
+template <int K>
+__device__ __forceinline__ bool rank_barrier(const ExchangeArgs& a, int phase, int r, int c,
+                                             int* s_abort) {
+  __syncthreads();
+  if (threadIdx.x < K) {
+    const int j = threadIdx.x;
+    uint32_t* remote = a.flags[j] + (size_t)(phase * TM_MAX_RANKS + r) * a.C + c;
+    st_release_sys(remote, a.epoch);
+    const uint32_t* mine = a.flags[r] + (size_t)(phase * TM_MAX_RANKS + j) * a.C + c;
+    if ((int32_t)(ld_acquire_sys(mine) - a.epoch) < 0) {
+      const uint64_t t0 = globaltimer();
+      while ((int32_t)(ld_acquire_sys(mine) - a.epoch) < 0) {
+        if (globaltimer() - t0 > a.timeout_ns) {
+          atomicOr(a.status, TM_BIT_TIMEOUT);
+          *s_abort = 1;
+          break;
+        }
+        __nanosleep(32);
+      }
+    }
+  }
+  __syncthreads();
+  return *s_abort == 0;
+}
+
+template <int K, bool W16>
+__global__ void __launch_bounds__(kThreads, 4)
+tm_exchange_kernel(const __grid_constant__ ExchangeArgs a) {
+  using U = Unit<W16>;
+  constexpr int E = U::kElems;
+  constexpr int WB = W16 ? 2 : 4;  // wire bytes per element
+  __shared__ int s_abort;
+  if (threadIdx.x == 0) s_abort = 0;
+
+  const int lr = blockIdx.x / a.C;
+  const int c = blockIdx.x - lr * a.C;
+  const int r = a.rank0 + lr;
+  float* __restrict__ x = a.x[lr];
+  const int64_t P = a.P, L = a.L;
+  const int64_t e0 = (int64_t)c * a.Lc;
+  const int64_t e1 = min(e0 + a.Lc, L);
+  const int64_t nu = e1 > e0 ? (e1 - e0) / E : 0;  // wire units per segment chunk
+  char* const stage_r = reinterpret_cast<char*>(a.stage[r]);
+
+  // ---------------- a2: pre-cast all k segments' chunk c into own stage -------
+  uint32_t st = 0;
+  {
+    const int64_t total = (int64_t)K * nu;
+    constexpr int B = 4;
+    for (int64_t t0 = threadIdx.x; t0 < total; t0 += (int64_t)B * kThreads) {
+      float f[B][E];
+#pragma unroll
+      for (int u = 0; u < B; ++u) {
+        const int64_t t = t0 + (int64_t)u * kThreads;
+        if (t < total) {
+          const int64_t s = t / nu;
+          const int64_t g = s * L + e0 + (t - s * nu) * E;  // element index
+          if (g + E <= P) {
+            U::to_floats(U::load_src(x + g), f[u]);
+          } else {
+#pragma unroll
+            for (int q = 0; q < E; ++q) f[u][q] = (g + q < P) ? x[g + q] : 0.0f;
+          }
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < B; ++u) {
+        const int64_t t = t0 + (int64_t)u * kThreads;
+        if (t < total) {
+          const int64_t s = t / nu;
+          const int64_t g = s * L + e0 + (t - s * nu) * E;
+#pragma unroll
+          for (int q = 0; q < E; ++q) st |= status_of(f[u][q], W16);
+          st16_cg(stage_r + g * WB, U::encode(f[u]));
+        }
+      }
+    }
+  }
+  if (st) atomicOr(a.status, st);  // rare: only threads that saw a bad value
+
+  if (!rank_barrier<K>(a, kPhaseReady, r, c, &s_abort)) return;
+
+  // ---------------- a4: reduce-scatter pull, fused sum / (1/k) / cast -------
+  {
+    const char* src[K];
+#pragma unroll
+    for (int j = 0; j < K; ++j) src[j] = reinterpret_cast<const char*>(a.stage[j]);
+    char* const avg_r = reinterpret_cast<char*>(a.avg[r]);
+    const float kf = (float)K;
+    const int64_t seg0 = (int64_t)r * L + e0;
+    for (int64_t v = threadIdx.x; v < nu; v += kThreads) {
+      const int64_t off = (seg0 + v * E) * WB;
+      uint4 raw[K];
+#pragma unroll
+      for (int j = 0; j < K; ++j) raw[j] = ld16_cg(src[j] + off);
+      float s[E], t[E];
+      U::decode(raw[0], s);
+#pragma unroll
+      for (int j = 1; j < K; ++j) {
+        U::decode(raw[j], t);
+#pragma unroll
+        for (int q = 0; q < E; ++q) s[q] = __fadd_rn(s[q], t[q]);
+      }
+#pragma unroll
+      for (int q = 0; q < E; ++q) s[q] = __fdiv_rn(s[q], kf);
+      st16_cg(avg_r + (e0 + v * E) * WB, U::encode(s));
+    }
+  }
+
+  if (!rank_barrier<K>(a, kPhaseReduced, r, c, &s_abort)) return;
+
+  // ---------------- a6: allgather pull, fused widen, store to caller ---------
+  {
+    const int64_t total = (int64_t)K * nu;
+    constexpr int B = 4;
+    for (int64_t t0 = threadIdx.x; t0 < total; t0 += (int64_t)B * kThreads) {
+      uint4 raw[B];
+#pragma unroll
+      for (int u = 0; u < B; ++u) {
+        const int64_t t = t0 + (int64_t)u * kThreads;
+        if (t < total) {
+          const int64_t j = t / nu;
+          const int64_t e = e0 + (t - j * nu) * E;
+          raw[u] = ld16_cg(reinterpret_cast<const char*>(a.avg[j]) + e * WB);
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < B; ++u) {
+        const int64_t t = t0 + (int64_t)u * kThreads;
+        if (t < total) {
+          const int64_t j = t / nu;
+          const int64_t g = j * L + e0 + (t - j * nu) * E;
+          float f[E];
+          U::decode(raw[u], f);
+          if (g + E <= P) {
+            U::store_dst(x + g, f);
+          } else {
+#pragma unroll
+            for (int q = 0; q < E; ++q)
+              if (g + q < P) x[g + q] = f[q];
+          }
+        }
+      }
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// AR with all k ranks in this process: one pass over P, 16-byte vectors.
+// ---------------------------------------------------------------------------
+struct LocalBufs {
+  float* b[TM_MAX_RANKS];
+};
+
+template <int K>
+__global__ void __launch_bounds__(kThreads)
+local_allreduce_kernel(const __grid_constant__ LocalBufs lb, int64_t P) {
+  const float kf = (float)K;
+  const int64_t nv = P / 4;
+  const int64_t stride = (int64_t)gridDim.x * kThreads;
+  for (int64_t v = (int64_t)blockIdx.x * kThreads + threadIdx.x; v < nv; v += stride) {
+    float4 in[K];
+#pragma unroll
+    for (int j = 0; j < K; ++j) in[j] = ld16_f(lb.b[j] + v * 4);
+    float4 s = in[0];
+#pragma unroll
+    for (int j = 1; j < K; ++j) {
+      s.x = __fadd_rn(s.x, in[j].x); s.y = __fadd_rn(s.y, in[j].y);
+      s.z = __fadd_rn(s.z, in[j].z); s.w = __fadd_rn(s.w, in[j].w);
+    }
+    s.x = __fdiv_rn(s.x, kf); s.y = __fdiv_rn(s.y, kf);
+    s.z = __fdiv_rn(s.z, kf); s.w = __fdiv_rn(s.w, kf);
+#pragma unroll
+    for (int j = 0; j < K; ++j) st16_f(lb.b[j] + v * 4, s);
+  }
+  // tail (P % 4 elements)
+  const int64_t i = nv * 4 + (int64_t)blockIdx.x * kThreads + threadIdx.x;
+  if (blockIdx.x == 0 && i < P) {
+    float s = lb.b[0][i];
+#pragma unroll
+    for (int j = 1; j < K; ++j) s = __fadd_rn(s, lb.b[j][i]);
+    s = __fdiv_rn(s, kf);
+#pragma unroll
+    for (int j = 0; j < K; ++j) lb.b[j][i] = s;
+  }
+}
+
+
+// ---------------------------------------------------------------------------
+// EASGD elastic update, one fp32 op per step:
+//   d = fl(x - c); e = fl(alpha d); x' = fl(x - e); c' = fl(c + e).
+// Concurrent mode applies c += e with red.relaxed.sys.global.add.f32 so several
+// workers (possibly on other GPUs, through an IPC mapping) may update one
+// centre at once without lost updates; each worker then read a possibly stale c.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ float elastic_diff(float x, float c, float alpha) {
+  return __fmul_rn(alpha, __fsub_rn(x, c));
+}
+
+__device__ __forceinline__ void red_add_sys(float* p, float v) {
+  asm volatile("red.relaxed.sys.global.add.f32 [%0], %1;" ::"l"(p), "f"(v) : "memory");
+}
+
+template <bool Concurrent>
+__global__ void __launch_bounds__(kThreads)
+easgd_kernel(float* __restrict__ x, float* c, int64_t n, float alpha, int vec) {
+  const int64_t stride = (int64_t)gridDim.x * kThreads;
+  const int64_t tid = (int64_t)blockIdx.x * kThreads + threadIdx.x;
+  int64_t done = 0;
+  if (vec) {
+    const int64_t nv = n / 4;
+    for (int64_t v = tid; v < nv; v += stride) {
+      float4 xv = ld16_f(x + v * 4);
+      float4 cv = Concurrent ? __ldcg(reinterpret_cast<const float4*>(c + v * 4))
+                             : ld16_f(c + v * 4);
+      const float ex = elastic_diff(xv.x, cv.x, alpha), ey = elastic_diff(xv.y, cv.y, alpha);
+      const float ez = elastic_diff(xv.z, cv.z, alpha), ew = elastic_diff(xv.w, cv.w, alpha);
+      xv.x = __fsub_rn(xv.x, ex); xv.y = __fsub_rn(xv.y, ey);
+      xv.z = __fsub_rn(xv.z, ez); xv.w = __fsub_rn(xv.w, ew);
+      st16_f(x + v * 4, xv);
+      if (Concurrent) {
+        float* cp = c + v * 4;
+        red_add_sys(cp, ex); red_add_sys(cp + 1, ey);
+        red_add_sys(cp + 2, ez); red_add_sys(cp + 3, ew);
+      } else {
+        cv.x = __fadd_rn(cv.x, ex); cv.y = __fadd_rn(cv.y, ey);
+        cv.z = __fadd_rn(cv.z, ez); cv.w = __fadd_rn(cv.w, ew);
+        st16_f(c + v * 4, cv);
+      }
+    }
+    done = nv * 4;
+  }
+  for (int64_t i = done + tid; i < n; i += stride) {
+    const float xi = x[i];
+    const float ci = Concurrent ? __ldcg(c + i) : c[i];
+    const float e = elastic_diff(xi, ci, alpha);
+    x[i] = __fsub_rn(xi, e);
+    if (Concurrent) red_add_sys(c + i, e);
+    else c[i] = __fadd_rn(ci, e);
+  }
+}
+
+// A whole server round in arrival order, fused: the centre is read once and
+// written once; worker w's update uses the centre left by the previous one.
+// Bitwise equal to serial updates in `order` (each element is independent).
+constexpr int kMaxRoundWorkers = 16;
+constexpr int kMaxRoundOrder = 64;
+struct RoundArgs {
+  float* w[kMaxRoundWorkers];
+  int8_t order[kMaxRoundOrder];
+  int norder;
+};
+
+__global__ void __launch_bounds__(kThreads)
+easgd_round_kernel(const __grid_constant__ RoundArgs ra, float* c, int64_t n, float alpha,
+                   int vec) {
+  const int64_t stride = (int64_t)gridDim.x * kThreads;
+  const int64_t tid = (int64_t)blockIdx.x * kThreads + threadIdx.x;
+  int64_t done = 0;
+  if (vec) {
+    const int64_t nv = n / 4;
+    for (int64_t v = tid; v < nv; v += stride) {
+      float4 cv = ld16_f(c + v * 4);
+      for (int t = 0; t < ra.norder; ++t) {
+        float* wp = ra.w[ra.order[t]] + v * 4;
+        float4 xv = *reinterpret_cast<const float4*>(wp);
+        const float ex = elastic_diff(xv.x, cv.x, alpha), ey = elastic_diff(xv.y, cv.y, alpha);
+        const float ez = elastic_diff(xv.z, cv.z, alpha), ew = elastic_diff(xv.w, cv.w, alpha);
+        xv.x = __fsub_rn(xv.x, ex); xv.y = __fsub_rn(xv.y, ey);
+        xv.z = __fsub_rn(xv.z, ez); xv.w = __fsub_rn(xv.w, ew);
+        cv.x = __fadd_rn(cv.x, ex); cv.y = __fadd_rn(cv.y, ey);
+        cv.z = __fadd_rn(cv.z, ez); cv.w = __fadd_rn(cv.w, ew);
+        *reinterpret_cast<float4*>(wp) = xv;
+      }
+      st16_f(c + v * 4, cv);
+    }
+    done = nv * 4;
+  }
+  for (int64_t i = done + tid; i < n; i += stride) {
+    float ci = c[i];
+    for (int t = 0; t < ra.norder; ++t) {
+      float* wp = ra.w[ra.order[t]] + i;
+      const float xi = *wp;
+      const float e = elastic_diff(xi, ci, alpha);
+      *wp = __fsub_rn(xi, e);
+      ci = __fadd_rn(ci, e);
+    }
+    c[i] = ci;
+  }
+}
+
+__global__ void __launch_bounds__(kThreads)
+cast_rn16_kernel(const float* __restrict__ in, uint16_t* __restrict__ out, int64_t n) {
+  const int64_t stride = (int64_t)gridDim.x * kThreads;
+  for (int64_t i = (int64_t)blockIdx.x * kThreads + threadIdx.x; i < n; i += stride) {
+    const __half h = __float2half_rn(in[i]);  // cvt.rn.f16.f32, as in the exchange
+    out[i] = *reinterpret_cast<const uint16_t*>(&h);
+  }
+}
+
+template <int K, bool W16>
+const void* exchange_fn() {
+  return reinterpret_cast<const void*>(&tm_exchange_kernel<K, W16>);
+}
+
+const void* pick_exchange(int k, bool w16) {
+  switch (k) {
+    case 2: return w16 ? exchange_fn<2, true>() : exchange_fn<2, false>();
+    case 3: return w16 ? exchange_fn<3, true>() : exchange_fn<3, false>();
+    case 4: return w16 ? exchange_fn<4, true>() : exchange_fn<4, false>();
+    case 5: return w16 ? exchange_fn<5, true>() : exchange_fn<5, false>();
+    case 6: return w16 ? exchange_fn<6, true>() : exchange_fn<6, false>();
+    case 7: return w16 ? exchange_fn<7, true>() : exchange_fn<7, false>();
+    case 8: return w16 ? exchange_fn<8, true>() : exchange_fn<8, false>();
+    default: return nullptr;
+  }
+}
+
+int sm_count(int device) {
+  int n = 0;
+  cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, device);
+  return n > 0 ? n : 1;
+}
+
+}  // namespace
+
+int exchange_max_ctas(int device, bool wire16, int k) {
+  const void* fn = pick_exchange(k, wire16);
+  if (!fn) return 0;
+  int per_sm = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, kThreads, 0) != cudaSuccess)
+    return 0;
+  return per_sm * sm_count(device);
+}
+
+int grid_for_streaming(int device) { return 4 * sm_count(device); }
+
+cudaError_t launch_exchange(const ExchangeArgs& a, int nlocal, bool wire16, cudaStream_t s) {
+  const void* fn = pick_exchange(a.k, wire16);
+  if (!fn) return cudaErrorInvalidValue;
+  void* params[] = {const_cast<ExchangeArgs*>(&a)};
+  // Cooperative launch: guarantees every CTA is co-resident, which the
+  // per-CTA flag barriers need when several ranks share this device.
+  return cudaLaunchCooperativeKernel(fn, dim3(nlocal * a.C), dim3(kThreads), params, 0, s);
+}
+
+cudaError_t launch_local_allreduce(float* const* bufs, int k, int64_t P, cudaStream_t s) {
+  LocalBufs lb{};
+  for (int j = 0; j < k; ++j) lb.b[j] = bufs[j];
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const int64_t nv = P / 4;
+  int64_t want = (nv + kThreads - 1) / kThreads;
+  int grid = (int)std::min<int64_t>(std::max<int64_t>(want, 1), grid_for_streaming(dev));
+  switch (k) {
+#define TM_AR_CASE(K) \
+  case K: local_allreduce_kernel<K><<<grid, kThreads, 0, s>>>(lb, P); break;
+    TM_AR_CASE(2) TM_AR_CASE(3) TM_AR_CASE(4) TM_AR_CASE(5) TM_AR_CASE(6) TM_AR_CASE(7)
+    TM_AR_CASE(8)
+#undef TM_AR_CASE
+    default: return cudaErrorInvalidValue;
+  }
+  return cudaGetLastError();
+}
+
+static int streaming_grid(int64_t work_items) {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  int64_t want = (work_items + kThreads - 1) / kThreads;
+  return (int)std::min<int64_t>(std::max<int64_t>(want, 1), grid_for_streaming(dev));
+}
+
+cudaError_t launch_easgd(float* x, float* c, int64_t n, float alpha, bool concurrent,
+                         cudaStream_t s) {
+  const int vec = ((reinterpret_cast<uintptr_t>(x) | reinterpret_cast<uintptr_t>(c)) & 15) == 0;
+  const int grid = streaming_grid(vec ? n / 4 + 4 : n);
+  if (concurrent) easgd_kernel<true><<<grid, kThreads, 0, s>>>(x, c, n, alpha, vec);
+  else easgd_kernel<false><<<grid, kThreads, 0, s>>>(x, c, n, alpha, vec);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_easgd_round(float* const* w, int nw, const int32_t* order, int norder,
+                               float* c, int64_t n, float alpha, cudaStream_t s) {
+  if (nw < 1 || nw > kMaxRoundWorkers || norder < 0 || norder > kMaxRoundOrder)
+    return cudaErrorInvalidValue;
+  RoundArgs ra{};
+  uintptr_t align = reinterpret_cast<uintptr_t>(c);
+  for (int i = 0; i < nw; ++i) {
+    ra.w[i] = w[i];
+    align |= reinterpret_cast<uintptr_t>(w[i]);
+  }
+  for (int t = 0; t < norder; ++t) {
+    if (order[t] < 0 || order[t] >= nw) return cudaErrorInvalidValue;
+    ra.order[t] = (int8_t)order[t];
+  }
+  ra.norder = norder;
+  const int vec = (align & 15) == 0;
+  const int grid = streaming_grid(vec ? n / 4 + 4 : n);
+  easgd_round_kernel<<<grid, kThreads, 0, s>>>(ra, c, n, alpha, vec);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_cast_rn16(const float* in, uint16_t* out, int64_t n, cudaStream_t s) {
+  cast_rn16_kernel<<<streaming_grid(n), kThreads, 0, s>>>(in, out, n);
+  return cudaGetLastError();
+}
+
+}  // namespace tmx

@@ -1,0 +1,452 @@
+// C++ runtime behind include/tm.h: the process-global exchanger context, the
+// segmented layout, library-owned device memory, CUDA IPC
+// peer mappings (the NVLink/NVSwitch data plane), the NCCL communicator used by
+// AR across processes (dlopen'ed: the same libnccl.so.2 torch already loaded),
+// argument validation and the sticky status word.
+//
+// PAPER.md L94-106 / L613-614: the paper ran one MPI process per GPU with
+// CUDA-aware OpenMPI.  Here one process per GPU is kept, but MPI is replaced by
+// (i) a one-time bootstrap in which the processes swap IPC handles (moved by
+// the caller, e.g. torch.distributed all_gather_object) and (ii) in-kernel
+// loads from peer memory with flag synchronisation.
+
+#include <cuda_runtime.h>
+#include <dlfcn.h>
+#include <nccl.h>
+#include <stdio.h>
+#include <stdlib.h>
+#include <string.h>
+#include <unistd.h>
+
+#include <algorithm>
+#include <mutex>
+
+#include "tm.h"
+#include "tm_internal.h"
+
+namespace {
+
+using tmx::ExchangeArgs;
+
+constexpr uint32_t kMagic = 0x544d4558u;  // "TMEX"
+constexpr uint32_t kVersion = 1;
+constexpr uint64_t kDefaultTimeoutNs = 10ull * 1000 * 1000 * 1000;
+
+struct Blob {
+  uint32_t magic, version;
+  int32_t rank0, nlocal, size, strategy, C, pid;
+  int64_t P, L, Lc, rank_stride;
+  int64_t off_stage, off_avg, off_flags, off_center;
+  int32_t has_nccl, device_ordinal;
+  cudaIpcMemHandle_t handle;
+  ncclUniqueId nccl_id;
+};
+static_assert(sizeof(Blob) <= TM_BLOB_BYTES, "blob too large");
+
+// --- NCCL, resolved at run time -------------------------------------------
+struct Nccl {
+  void* lib = nullptr;
+  ncclResult_t (*GetUniqueId)(ncclUniqueId*) = nullptr;
+  ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+  ncclResult_t (*AllReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
+                            cudaStream_t) = nullptr;
+  ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+  bool load() {
+    if (lib) return true;
+    const char* path = getenv("TM_NCCL_LIB");
+    lib = dlopen(path && *path ? path : "libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (!lib) return false;
+    GetUniqueId = (decltype(GetUniqueId))dlsym(lib, "ncclGetUniqueId");
+    CommInitRank = (decltype(CommInitRank))dlsym(lib, "ncclCommInitRank");
+    AllReduce = (decltype(AllReduce))dlsym(lib, "ncclAllReduce");
+    CommDestroy = (decltype(CommDestroy))dlsym(lib, "ncclCommDestroy");
+    return GetUniqueId && CommInitRank && AllReduce && CommDestroy;
+  }
+};
+
+struct Ctx {
+  bool inited = false, ready = false;
+  int64_t P = 0, L = 0, Lc = 0;
+  int k = 0, rank0 = 0, nlocal = 0, device = 0, strategy = 0, C = 0;
+  int nprocs = 1, proc = 0;
+  int64_t rank_stride = 0, off_stage = 0, off_avg = 0, off_flags = 0, off_center = 0;
+  int64_t slab_bytes = 0;
+  char* slab = nullptr;
+  uint32_t* status = nullptr;
+  char* peer_base[TM_MAX_RANKS] = {};  // per process (only the opened ones)
+  char* rank_base[TM_MAX_RANKS] = {};  // per global rank, as mapped on this device
+  uint32_t epoch = 0;
+  uint64_t timeout_ns = kDefaultTimeoutNs;
+  ncclComm_t comm = nullptr;
+  ncclUniqueId nccl_id{};
+  bool have_nccl_id = false;
+};
+
+Ctx g;
+Nccl g_nccl;
+std::mutex g_mu;
+
+bool wire16(int strategy) { return strategy == TM_ASA16; }
+int wire_bytes(int strategy) { return wire16(strategy) ? 2 : 4; }
+int64_t round_up(int64_t a, int64_t b) { return (a + b - 1) / b * b; }
+
+void debug_cuda(const char* where, cudaError_t e) {
+  if (getenv("TM_DEBUG")) fprintf(stderr, "[tm] %s: %s\n", where, cudaGetErrorString(e));
+}
+
+int cuda_fail(const char* where, cudaError_t e) {
+  debug_cuda(where, e);
+  return TM_E_CUDA;
+}
+
+bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
+
+void fill_rank_bases_local() {
+  for (int i = 0; i < g.nlocal; ++i) g.rank_base[g.rank0 + i] = g.slab + (int64_t)i * g.rank_stride;
+}
+
+void release() {
+  if (g.comm && g_nccl.CommDestroy) g_nccl.CommDestroy(g.comm);
+  g.comm = nullptr;
+  for (int p = 0; p < TM_MAX_RANKS; ++p) {
+    if (g.peer_base[p]) cudaIpcCloseMemHandle(g.peer_base[p]);
+    g.peer_base[p] = nullptr;
+  }
+  if (g.slab) cudaFree(g.slab);
+  g = Ctx();
+}
+
+ExchangeArgs make_args(float* const* bufs) {
+  ExchangeArgs a{};
+  for (int j = 0; j < g.k; ++j) {
+    a.stage[j] = g.rank_base[j] + g.off_stage;
+    a.avg[j] = g.rank_base[j] + g.off_avg;
+    a.flags[j] = reinterpret_cast<uint32_t*>(g.rank_base[j] + g.off_flags);
+  }
+  for (int i = 0; i < g.nlocal; ++i) a.x[i] = bufs[i];
+  a.status = g.status;
+  a.P = g.P;
+  a.L = g.L;
+  a.Lc = g.Lc;
+  a.k = g.k;
+  a.rank0 = g.rank0;
+  a.C = g.C;
+  a.epoch = g.epoch;
+  a.timeout_ns = g.timeout_ns;
+  return a;
+}
+
+int do_exchange(float* const* bufs, int nbufs, cudaStream_t s) {
+  if (!g.inited || !g.ready || g.strategy == TM_EASGD) return TM_E_STATE;
+  if (nbufs != g.nlocal || !bufs) return TM_E_ARG;
+  for (int i = 0; i < nbufs; ++i) {
+    if (!bufs[i]) return TM_E_ARG;
+    if (!aligned16(bufs[i])) return TM_E_ALIGN;
+  }
+  if (g.k == 1) return TM_OK;  // reading Q10: identity, nothing launched
+  cudaSetDevice(g.device);
+  if (g.strategy == TM_AR) {
+    if (g.nlocal == g.k) {
+      cudaError_t e = tmx::launch_local_allreduce(bufs, g.k, g.P, s);
+      return e == cudaSuccess ? TM_OK : cuda_fail("local_allreduce", e);
+    }
+    if (!g.comm) return TM_E_NCCL;
+    ncclResult_t r = g_nccl.AllReduce(bufs[0], bufs[0], (size_t)g.P, ncclFloat32, ncclAvg, g.comm, s);
+    return r == ncclSuccess ? TM_OK : TM_E_NCCL;
+  }
+  ++g.epoch;
+  ExchangeArgs a = make_args(bufs);
+  cudaError_t e = tmx::launch_exchange(a, g.nlocal, wire16(g.strategy), s);
+  if (e != cudaSuccess) {
+    --g.epoch;
+    return cuda_fail("launch_exchange", e);
+  }
+  return TM_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int tm_exchange_init(int64_t nparams, const tm_world* world, int strategy) {
+  std::lock_guard<std::mutex> lk(g_mu);
+  if (g.inited) return TM_E_STATE;
+  if (!world || nparams < 1) return TM_E_ARG;
+  if (strategy < TM_AR || strategy > TM_EASGD) return TM_E_ARG;
+  const int k = world->size;
+  if (k < 1 || k > TM_MAX_RANKS) return TM_E_ARG;
+  if (world->nlocal != 1 && world->nlocal != k) return TM_E_ARG;
+  if (world->rank < 0 || world->rank + world->nlocal > k) return TM_E_ARG;
+  if (world->nlocal == k && world->rank != 0) return TM_E_ARG;
+  int ndev = 0;
+  cudaError_t e = cudaGetDeviceCount(&ndev);
+  if (e != cudaSuccess) return cuda_fail("cudaGetDeviceCount", e);
+  if (world->device < 0 || world->device >= ndev) return TM_E_ARG;
+  e = cudaSetDevice(world->device);
+  if (e != cudaSuccess) return cuda_fail("cudaSetDevice", e);
+
+  Ctx c;
+  c.P = nparams;
+  c.k = k;
+  c.rank0 = world->rank;
+  c.nlocal = world->nlocal;
+  c.device = world->device;
+  c.strategy = strategy;
+  c.nprocs = k / world->nlocal;
+  c.proc = world->rank / world->nlocal;
+  c.L = round_up((nparams + k - 1) / k, tmx::kAlign);
+
+  const int wb = wire_bytes(strategy);
+  if (strategy == TM_ASA || strategy == TM_ASA16) {
+    int cmax = k >= 2 ? tmx::exchange_max_ctas(c.device, wire16(strategy), k) / c.nlocal : 1;
+    if (k >= 2 && cmax < 1) return TM_E_CUDA;
+    const int64_t want = std::max<int64_t>(1, (c.L + tmx::kMinChunk - 1) / tmx::kMinChunk);
+    c.C = (int)std::min<int64_t>(std::max(cmax, 1), want);
+    c.Lc = round_up((c.L + c.C - 1) / c.C, tmx::kAlign);
+    c.off_stage = 0;
+    c.off_avg = round_up(c.off_stage + (int64_t)k * c.L * wb, 256);
+    c.off_flags = round_up(c.off_avg + c.L * wb, 256);
+    c.rank_stride = round_up(c.off_flags + (int64_t)tmx::kPhases * TM_MAX_RANKS * c.C * 4, 4096);
+  } else if (strategy == TM_EASGD) {
+    c.off_center = 0;
+    c.rank_stride = round_up(nparams * 4, 4096);
+  } else {
+    c.rank_stride = 0;
+  }
+  c.slab_bytes = c.rank_stride * c.nlocal + 256;  // + status word
+  e = cudaMalloc(reinterpret_cast<void**>(&c.slab), c.slab_bytes);
+  if (e != cudaSuccess) return cuda_fail("cudaMalloc", e);
+  e = cudaMemset(c.slab, 0, c.slab_bytes);
+  if (e != cudaSuccess) {
+    cudaFree(c.slab);
+    return cuda_fail("cudaMemset", e);
+  }
+  c.status = reinterpret_cast<uint32_t*>(c.slab + c.rank_stride * c.nlocal);
+  c.inited = true;
+  c.ready = (c.nprocs == 1);
+  g = c;
+  fill_rank_bases_local();
+  if (g.strategy == TM_AR && g.nprocs > 1 && g.proc == 0) {
+    if (!g_nccl.load()) {
+      release();
+      return TM_E_NCCL;
+    }
+    if (g_nccl.GetUniqueId(&g.nccl_id) != ncclSuccess) {
+      release();
+      return TM_E_NCCL;
+    }
+    g.have_nccl_id = true;
+  }
+  return TM_OK;
+}
+
+int tm_bootstrap_export(void* blob, size_t* len) {
+  std::lock_guard<std::mutex> lk(g_mu);
+  if (!g.inited) return TM_E_STATE;
+  if (!blob || !len) return TM_E_ARG;
+  Blob b;
+  memset(&b, 0, sizeof(b));
+  b.magic = kMagic;
+  b.version = kVersion;
+  b.rank0 = g.rank0;
+  b.nlocal = g.nlocal;
+  b.size = g.k;
+  b.strategy = g.strategy;
+  b.C = g.C;
+  b.pid = (int32_t)getpid();
+  b.P = g.P;
+  b.L = g.L;
+  b.Lc = g.Lc;
+  b.rank_stride = g.rank_stride;
+  b.off_stage = g.off_stage;
+  b.off_avg = g.off_avg;
+  b.off_flags = g.off_flags;
+  b.off_center = g.off_center;
+  b.device_ordinal = g.device;
+  cudaSetDevice(g.device);
+  cudaError_t e = cudaIpcGetMemHandle(&b.handle, g.slab);
+  if (e != cudaSuccess) return cuda_fail("cudaIpcGetMemHandle", e);
+  if (g.have_nccl_id) {
+    b.has_nccl = 1;
+    b.nccl_id = g.nccl_id;
+  }
+  memset(blob, 0, TM_BLOB_BYTES);
+  memcpy(blob, &b, sizeof(b));
+  *len = TM_BLOB_BYTES;
+  return TM_OK;
+}
+
+int tm_bootstrap_import(const void* blobs, size_t len_each) {
+  std::lock_guard<std::mutex> lk(g_mu);
+  if (!g.inited) return TM_E_STATE;
+  if (g.ready) return TM_OK;
+  if (!blobs || len_each < sizeof(Blob)) return TM_E_ARG;
+  cudaSetDevice(g.device);
+  const char* p = static_cast<const char*>(blobs);
+  const Blob* nccl_blob = nullptr;
+  for (int q = 0; q < g.nprocs; ++q) {
+    Blob b;
+    memcpy(&b, p + (size_t)q * len_each, sizeof(b));
+    if (b.magic != kMagic || b.version != kVersion) return TM_E_ARG;
+    if (b.P != g.P || b.size != g.k || b.strategy != g.strategy || b.C != g.C || b.L != g.L ||
+        b.Lc != g.Lc || b.nlocal != g.nlocal || b.rank_stride != g.rank_stride ||
+        b.rank0 != q * g.nlocal)
+      return TM_E_MISMATCH;
+    if (b.has_nccl) nccl_blob = reinterpret_cast<const Blob*>(p + (size_t)q * len_each);
+    if (q == g.proc) continue;
+    void* base = nullptr;
+    cudaError_t e = cudaIpcOpenMemHandle(&base, b.handle, cudaIpcMemLazyEnablePeerAccess);
+    if (e != cudaSuccess) return cuda_fail("cudaIpcOpenMemHandle", e);
+    g.peer_base[q] = static_cast<char*>(base);
+    for (int i = 0; i < b.nlocal; ++i)
+      g.rank_base[b.rank0 + i] = static_cast<char*>(base) + (int64_t)i * b.rank_stride;
+  }
+  if (g.strategy == TM_AR && g.nprocs > 1) {
+    if (!nccl_blob || !g_nccl.load()) return TM_E_NCCL;
+    Blob nb;
+    memcpy(&nb, nccl_blob, sizeof(nb));
+    if (g_nccl.CommInitRank(&g.comm, g.nprocs, nb.nccl_id, g.proc) != ncclSuccess) return TM_E_NCCL;
+  }
+  g.ready = true;
+  return TM_OK;
+}
+
+int tm_exchange(float* dev_buf, void* stream) {
+  std::lock_guard<std::mutex> lk(g_mu);
+  if (g.inited && g.nlocal != 1) return TM_E_STATE;
+  float* bufs[1] = {dev_buf};
+  return do_exchange(bufs, 1, static_cast<cudaStream_t>(stream));
+}
+
+int tm_exchange_group(float* const* dev_bufs, int nbufs, void* stream) {
+  std::lock_guard<std::mutex> lk(g_mu);
+  return do_exchange(dev_bufs, nbufs, static_cast<cudaStream_t>(stream));
+}
+
+int tm_easgd_update(float* worker_buf, float* center_buf, float alpha, void* stream) {
+  int64_t n;
+  {
+    std::lock_guard<std::mutex> lk(g_mu);
+    if (!g.inited) return TM_E_STATE;
+    n = g.P;
+  }
+  return tm_easgd_update_ex(worker_buf, center_buf, n, alpha, 0, stream);
+}
+
+int tm_easgd_update_ex(float* worker_buf, float* center_buf, int64_t n, float alpha,
+                       int concurrent, void* stream) {
+  if (!worker_buf || !center_buf || n < 0) return TM_E_ARG;
+  if (n == 0) return TM_OK;
+  if ((reinterpret_cast<uintptr_t>(worker_buf) | reinterpret_cast<uintptr_t>(center_buf)) & 3)
+    return TM_E_ALIGN;
+  cudaError_t e = tmx::launch_easgd(worker_buf, center_buf, n, alpha, concurrent != 0,
+                                   static_cast<cudaStream_t>(stream));
+  return e == cudaSuccess ? TM_OK : cuda_fail("easgd", e);
+}
+
+int tm_easgd_round(float* const* workers, int nworkers, const int32_t* order, int norder,
+                   float* center_buf, int64_t n, float alpha, void* stream) {
+  if (!workers || !order || !center_buf || n < 0 || nworkers < 1 || nworkers > 16 ||
+      norder < 0 || norder > 64)
+    return TM_E_ARG;
+  for (int i = 0; i < nworkers; ++i) {
+    if (!workers[i]) return TM_E_ARG;
+    if (reinterpret_cast<uintptr_t>(workers[i]) & 3) return TM_E_ALIGN;
+  }
+  for (int t = 0; t < norder; ++t)
+    if (order[t] < 0 || order[t] >= nworkers) return TM_E_ARG;
+  if (n == 0 || norder == 0) return TM_OK;
+  cudaError_t e = tmx::launch_easgd_round(workers, nworkers, order, norder, center_buf, n, alpha,
+                                         static_cast<cudaStream_t>(stream));
+  return e == cudaSuccess ? TM_OK : cuda_fail("easgd_round", e);
+}
+
+int tm_easgd_center(int owner_rank, float** center) {
+  std::lock_guard<std::mutex> lk(g_mu);
+  if (!g.inited || !g.ready || g.strategy != TM_EASGD) return TM_E_STATE;
+  if (!center || owner_rank < 0 || owner_rank >= g.k) return TM_E_ARG;
+  *center = reinterpret_cast<float*>(g.rank_base[owner_rank] + g.off_center);
+  return TM_OK;
+}
+
+int tm_exchange_status(void* stream, uint32_t* bits) {
+  std::lock_guard<std::mutex> lk(g_mu);
+  if (!g.inited) return TM_E_STATE;
+  cudaSetDevice(g.device);
+  cudaError_t e = cudaStreamSynchronize(static_cast<cudaStream_t>(stream));
+  if (e != cudaSuccess) return cuda_fail("cudaStreamSynchronize", e);
+  uint32_t h = 0;
+  e = cudaMemcpy(&h, g.status, 4, cudaMemcpyDeviceToHost);
+  if (e != cudaSuccess) return cuda_fail("status copy", e);
+  e = cudaMemset(g.status, 0, 4);
+  if (e != cudaSuccess) return cuda_fail("status clear", e);
+  if (bits) *bits = h;
+  if (h & TM_BIT_TIMEOUT) return TM_E_TIMEOUT;
+  if (h & TM_BIT_OVERFLOW16) return TM_E_OVERFLOW16;
+  if (h & TM_BIT_NONFINITE) return TM_E_NONFINITE;
+  return TM_OK;
+}
+
+int tm_layout(tm_layout_info* out) {
+  std::lock_guard<std::mutex> lk(g_mu);
+  if (!g.inited) return TM_E_STATE;
+  if (!out) return TM_E_ARG;
+  memset(out, 0, sizeof(*out));
+  out->nparams = g.P;
+  out->seg_len = g.L;
+  out->chunk_len = g.Lc;
+  out->k = g.k;
+  out->rank = g.rank0;
+  out->nlocal = g.nlocal;
+  out->strategy = g.strategy;
+  out->ctas_per_rank = g.C;
+  out->threads = tmx::kThreads;
+  int sms = 0;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, g.device);
+  out->sm_count = sms;
+  out->wire_bytes = wire_bytes(g.strategy);
+  out->lib_bytes = g.slab_bytes;
+  out->epoch = g.epoch;
+  return TM_OK;
+}
+
+int tm_set_timeout_ns(uint64_t ns) {
+  std::lock_guard<std::mutex> lk(g_mu);
+  g.timeout_ns = ns ? ns : kDefaultTimeoutNs;
+  return TM_OK;
+}
+
+int tm_exchange_finalize(void) {
+  std::lock_guard<std::mutex> lk(g_mu);
+  if (g.inited) {
+    cudaSetDevice(g.device);
+    cudaDeviceSynchronize();
+  }
+  release();
+  return TM_OK;
+}
+
+const char* tm_strerror(int status) {
+  switch (status) {
+    case TM_OK: return "ok";
+    case TM_E_ARG: return "invalid argument";
+    case TM_E_ALIGN: return "device buffer not 16-byte aligned";
+    case TM_E_STATE: return "call out of order (init/bootstrap state)";
+    case TM_E_CUDA: return "CUDA error";
+    case TM_E_NCCL: return "NCCL unavailable or failed";
+    case TM_E_MISMATCH: return "ranks disagree on nparams/strategy/layout";
+    case TM_E_TIMEOUT: return "peer did not arrive before the timeout";
+    case TM_E_NONFINITE: return "non-finite input element";
+    case TM_E_OVERFLOW16: return "input overflows binary16 (|x| >= 65520)";
+    default: return "unknown status";
+  }
+}
+
+int tm_cast_rn16(const float* in, uint16_t* out16, int64_t n, void* stream) {
+  if (!in || !out16 || n < 0) return TM_E_ARG;
+  if (n == 0) return TM_OK;
+  cudaError_t e = tmx::launch_cast_rn16(in, out16, n, static_cast<cudaStream_t>(stream));
+  return e == cudaSuccess ? TM_OK : cuda_fail("cast_rn16", e);
+}
+
+}  // extern "C"

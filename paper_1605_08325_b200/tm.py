@@ -1,0 +1,272 @@
+"""Thin ctypes binding of libtm.so (include/tm.h).  Argument marshalling only:
+every step of the exchange runs in the library's sm_100a kernels.  There is no
+CPU or PyTorch fallback: if libtm.so is missing or a call fails, this module
+raises.
+
+Names follow the C ABI: tm_exchange_init / tm_exchange / tm_easgd_update ...
+The `Exchanger` class wraps the process-global exchanger for convenience.
+"""
+
+import ctypes
+import os
+import glob
+
+import torch
+
+_PKG = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_PKG, "libtm.so")
+
+TM_AR, TM_ASA, TM_ASA16, TM_EASGD = 0, 1, 2, 3
+STRATEGY = {"ar": TM_AR, "asa": TM_ASA, "asa16": TM_ASA16, "easgd": TM_EASGD}
+TM_OK, TM_E_ARG, TM_E_ALIGN, TM_E_STATE, TM_E_CUDA, TM_E_NCCL = 0, 1, 2, 3, 4, 5
+TM_E_MISMATCH, TM_E_TIMEOUT, TM_E_NONFINITE, TM_E_OVERFLOW16 = 6, 7, 8, 9
+TM_BIT_NONFINITE, TM_BIT_OVERFLOW16, TM_BIT_TIMEOUT = 1, 2, 4
+TM_BLOB_BYTES = 512
+TM_MAX_RANKS = 8
+
+
+class TmError(RuntimeError):
+    def __init__(self, code, what):
+        self.code = code
+        super().__init__(f"{what}: tm status {code} ({strerror(code)})")
+
+
+class tm_world(ctypes.Structure):
+    _fields_ = [("rank", ctypes.c_int32), ("size", ctypes.c_int32),
+                ("device", ctypes.c_int32), ("nlocal", ctypes.c_int32)]
+
+
+class tm_layout_info(ctypes.Structure):
+    _fields_ = [("nparams", ctypes.c_int64), ("seg_len", ctypes.c_int64),
+                ("chunk_len", ctypes.c_int64), ("k", ctypes.c_int32), ("rank", ctypes.c_int32),
+                ("nlocal", ctypes.c_int32), ("strategy", ctypes.c_int32),
+                ("ctas_per_rank", ctypes.c_int32), ("threads", ctypes.c_int32),
+                ("sm_count", ctypes.c_int32), ("wire_bytes", ctypes.c_int32),
+                ("lib_bytes", ctypes.c_int64), ("epoch", ctypes.c_uint32)]
+
+
+_lib = None
+
+_P = ctypes.c_void_p
+_SIGS = {
+    "tm_exchange_init": (ctypes.c_int, [ctypes.c_int64, ctypes.POINTER(tm_world), ctypes.c_int]),
+    "tm_bootstrap_export": (ctypes.c_int, [_P, ctypes.POINTER(ctypes.c_size_t)]),
+    "tm_bootstrap_import": (ctypes.c_int, [_P, ctypes.c_size_t]),
+    "tm_exchange": (ctypes.c_int, [_P, _P]),
+    "tm_exchange_group": (ctypes.c_int, [ctypes.POINTER(_P), ctypes.c_int, _P]),
+    "tm_easgd_update": (ctypes.c_int, [_P, _P, ctypes.c_float, _P]),
+    "tm_easgd_update_ex": (ctypes.c_int, [_P, _P, ctypes.c_int64, ctypes.c_float, ctypes.c_int, _P]),
+    "tm_easgd_round": (ctypes.c_int, [ctypes.POINTER(_P), ctypes.c_int, ctypes.POINTER(ctypes.c_int32),
+                                      ctypes.c_int, _P, ctypes.c_int64, ctypes.c_float, _P]),
+    "tm_easgd_center": (ctypes.c_int, [ctypes.c_int, ctypes.POINTER(_P)]),
+    "tm_exchange_status": (ctypes.c_int, [_P, ctypes.POINTER(ctypes.c_uint32)]),
+    "tm_layout": (ctypes.c_int, [ctypes.POINTER(tm_layout_info)]),
+    "tm_set_timeout_ns": (ctypes.c_int, [ctypes.c_uint64]),
+    "tm_exchange_finalize": (ctypes.c_int, []),
+    "tm_strerror": (ctypes.c_char_p, [ctypes.c_int]),
+    "tm_cast_rn16": (ctypes.c_int, [_P, _P, ctypes.c_int64, _P]),
+}
+
+
+def _torch_nccl_path():
+    try:
+        import nvidia.nccl  # type: ignore
+        for base in nvidia.nccl.__path__:
+            hits = glob.glob(os.path.join(base, "lib", "libnccl.so*"))
+            if hits:
+                return sorted(hits)[0]
+    except Exception:
+        pass
+    return ""
+
+
+def lib():
+    """Load libtm.so (raises if it was not built: no fallback)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise RuntimeError(f"{LIB_PATH} missing: run __graft_entry__.build() "
+                               "(python -m paper_1605_08325_b200.build)")
+        if not os.environ.get("TM_NCCL_LIB"):
+            os.environ["TM_NCCL_LIB"] = _torch_nccl_path()
+        L = ctypes.CDLL(LIB_PATH)
+        for name, (res, args) in _SIGS.items():
+            fn = getattr(L, name)
+            fn.restype = res
+            fn.argtypes = args
+        _lib = L
+    return _lib
+
+
+def strerror(code):
+    return lib().tm_strerror(int(code)).decode()
+
+
+def _check(code, what):
+    if code != TM_OK:
+        raise TmError(code, what)
+
+
+def _stream_handle(stream):
+    if stream is None:
+        stream = torch.cuda.current_stream()
+    return ctypes.c_void_p(stream.cuda_stream)
+
+
+def _fp32_cuda(t, n=None):
+    if not (isinstance(t, torch.Tensor) and t.is_cuda and t.dtype == torch.float32
+            and t.is_contiguous()):
+        raise TypeError("expected a contiguous float32 CUDA tensor")
+    if n is not None and t.numel() != n:
+        raise ValueError(f"expected {n} elements, got {t.numel()}")
+    return ctypes.c_void_p(t.data_ptr())
+
+
+# ------------------------------------------------------------------ raw calls
+
+def tm_exchange_init(nparams, rank, size, device, nlocal, strategy):
+    w = tm_world(rank, size, device, nlocal)
+    _check(lib().tm_exchange_init(int(nparams), ctypes.byref(w), int(strategy)), "tm_exchange_init")
+
+
+def tm_bootstrap_export():
+    buf = ctypes.create_string_buffer(TM_BLOB_BYTES)
+    n = ctypes.c_size_t(0)
+    _check(lib().tm_bootstrap_export(buf, ctypes.byref(n)), "tm_bootstrap_export")
+    return buf.raw[: n.value]
+
+
+def tm_bootstrap_import(blobs):
+    each = len(blobs[0])
+    joined = b"".join(blobs)
+    _check(lib().tm_bootstrap_import(joined, each), "tm_bootstrap_import")
+
+
+def tm_exchange(buf, stream=None):
+    _check(lib().tm_exchange(_fp32_cuda(buf), _stream_handle(stream)), "tm_exchange")
+
+
+def tm_exchange_group(bufs, stream=None):
+    arr = (ctypes.c_void_p * len(bufs))(*[_fp32_cuda(b).value for b in bufs])
+    _check(lib().tm_exchange_group(arr, len(bufs), _stream_handle(stream)), "tm_exchange_group")
+
+
+def tm_easgd_update(worker, center, alpha, stream=None):
+    _check(lib().tm_easgd_update(_fp32_cuda(worker), _P(center if isinstance(center, int) else center.data_ptr()),
+                                 ctypes.c_float(alpha), _stream_handle(stream)), "tm_easgd_update")
+
+
+def tm_easgd_update_ex(worker, center, alpha, concurrent=False, stream=None, n=None):
+    n = worker.numel() if n is None else n
+    cptr = center if isinstance(center, int) else _fp32_cuda(center).value
+    _check(lib().tm_easgd_update_ex(_fp32_cuda(worker), _P(cptr), int(n), ctypes.c_float(alpha),
+                                    int(bool(concurrent)), _stream_handle(stream)), "tm_easgd_update_ex")
+
+
+def tm_easgd_round(workers, order, center, alpha, stream=None):
+    n = center.numel()
+    arr = (ctypes.c_void_p * len(workers))(*[_fp32_cuda(w, n).value for w in workers])
+    o = (ctypes.c_int32 * len(order))(*[int(i) for i in order])
+    _check(lib().tm_easgd_round(arr, len(workers), o, len(order), _fp32_cuda(center), int(n),
+                                ctypes.c_float(alpha), _stream_handle(stream)), "tm_easgd_round")
+
+
+def tm_easgd_center(owner_rank):
+    p = ctypes.c_void_p(0)
+    _check(lib().tm_easgd_center(int(owner_rank), ctypes.byref(p)), "tm_easgd_center")
+    return p.value
+
+
+def tm_exchange_status(stream=None):
+    bits = ctypes.c_uint32(0)
+    code = lib().tm_exchange_status(_stream_handle(stream), ctypes.byref(bits))
+    return code, bits.value
+
+
+def tm_layout():
+    info = tm_layout_info()
+    _check(lib().tm_layout(ctypes.byref(info)), "tm_layout")
+    return {f: getattr(info, f) for f, _ in info._fields_}
+
+
+def tm_set_timeout_ns(ns):
+    _check(lib().tm_set_timeout_ns(int(ns)), "tm_set_timeout_ns")
+
+
+def tm_exchange_finalize():
+    _check(lib().tm_exchange_finalize(), "tm_exchange_finalize")
+
+
+def tm_cast_rn16(x, out16=None, stream=None):
+    """Device binary16 RNE rounding (the exchange's own); returns int16 bit patterns."""
+    if out16 is None:
+        out16 = torch.empty(x.numel(), dtype=torch.int16, device=x.device)
+    _check(lib().tm_cast_rn16(_fp32_cuda(x), _P(out16.data_ptr()), x.numel(), _stream_handle(stream)),
+           "tm_cast_rn16")
+    return out16
+
+
+def device_view(ptr, n, device=None):
+    """A float32 torch tensor aliasing n floats of library-owned device memory
+    at `ptr` (e.g. tm_easgd_center's pointer).  No copy."""
+
+    class _Iface:
+        __cuda_array_interface__ = {"shape": (int(n),), "typestr": "<f4",
+                                    "data": (int(ptr), False), "version": 2}
+
+    return torch.as_tensor(_Iface(), device=device or torch.cuda.current_device())
+
+
+# ------------------------------------------------------------ convenience
+
+class Exchanger:
+    """Process-global exchanger.
+
+    Single-process group (k workers on one device):
+        ex = Exchanger(P, "asa16", size=k, nlocal=k); ex.exchange([b0, ..., bk-1])
+    One process per GPU under torch.distributed (bootstrap over `group`):
+        ex = Exchanger(P, "asa16", rank=r, size=k, device=d, nlocal=1, group=pg)
+        ex.exchange(buf)
+    """
+
+    def __init__(self, nparams, strategy, rank=0, size=1, device=None, nlocal=None,
+                 group=None, timeout_s=None):
+        if device is None:
+            device = torch.cuda.current_device()
+        nlocal = size if nlocal is None else nlocal
+        self.nparams, self.size, self.nlocal, self.rank = int(nparams), size, nlocal, rank
+        self.strategy = strategy
+        torch.cuda.set_device(device)
+        tm_exchange_init(nparams, rank, size, device, nlocal, STRATEGY[strategy])
+        if timeout_s is not None:
+            tm_set_timeout_ns(int(timeout_s * 1e9))
+        if nlocal != size:
+            import torch.distributed as dist
+            mine = tm_bootstrap_export()
+            blobs = [None] * (size // nlocal)
+            dist.all_gather_object(blobs, mine, group=group)
+            tm_bootstrap_import(blobs)
+
+    def exchange(self, bufs, stream=None):
+        if isinstance(bufs, torch.Tensor):
+            tm_exchange(bufs, stream)
+        else:
+            tm_exchange_group(list(bufs), stream)
+
+    def status(self, stream=None):
+        return tm_exchange_status(stream)
+
+    def layout(self):
+        return tm_layout()
+
+    def center(self, owner_rank=0):
+        return tm_easgd_center(owner_rank)
+
+    def finalize(self):
+        tm_exchange_finalize()
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.finalize()

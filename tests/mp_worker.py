@@ -1,0 +1,62 @@
+"""One rank of a multi-process exchange (one process per rank, nlocal = 1),
+bootstrapped over a gloo process group: CUDA IPC handles are swapped with
+all_gather_object.  Used by tests/test_gpu_multiprocess.py; on a one-GPU box
+every rank uses cuda:0 (IPC between processes on one device), on a multi-GPU
+box rank r uses cuda:r.
+
+argv: outdir strategy P dist mode      (mode: normal | skip1 | mismatch)
+"""
+
+import json
+import os
+import sys
+
+import numpy as np
+import torch
+import torch.distributed as dist
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+from paper_1605_08325_b200 import tm  # noqa: E402
+from paper_1605_08325_b200.inputs import worker_buffer  # noqa: E402
+
+
+def main():
+    outdir, strategy, P, dist_name, mode = sys.argv[1], sys.argv[2], int(sys.argv[3]), sys.argv[4], sys.argv[5]
+    rank = int(os.environ["RANK"])
+    size = int(os.environ["WORLD_SIZE"])
+    dist.init_process_group("gloo", rank=rank, world_size=size)
+    ndev = torch.cuda.device_count()
+    device = rank % ndev
+    torch.cuda.set_device(device)
+    result = {"rank": rank, "device": device}
+    Pr = P + (1 if (mode == "mismatch" and rank == 1) else 0)
+    try:
+        ex = tm.Exchanger(Pr, strategy, rank=rank, size=size, device=device, nlocal=1,
+                          timeout_s=(1.0 if mode == "skip1" else 20.0))
+    except tm.TmError as e:
+        result["init_error"] = e.code
+        json.dump(result, open(os.path.join(outdir, f"rank{rank}.json"), "w"))
+        dist.barrier()
+        return
+    x = torch.from_numpy(worker_buffer(P, dist_name, rank, config=50)).cuda()
+    reps = 3
+    if mode == "skip1" and rank == 1:
+        reps = 0  # never arrives: rank 0 must time out, not hang
+    for _ in range(reps):
+        ex.exchange(x)
+        # re-run on fresh inputs so each call is checked
+        if _ < reps - 1:
+            torch.cuda.synchronize()
+    code, bits = ex.status()
+    result.update({"code": code, "bits": bits, "layout": ex.layout()})
+    np.save(os.path.join(outdir, f"rank{rank}.npy"), x.cpu().numpy())
+    json.dump(result, open(os.path.join(outdir, f"rank{rank}.json"), "w"))
+    dist.barrier()  # keep every slab alive until all ranks are done
+    ex.finalize()
+    dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

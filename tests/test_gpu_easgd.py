@@ -1,0 +1,111 @@
+"""GPU parity of the EASGD kernels against oracle/easgd.py."""
+
+import numpy as np
+import pytest
+import torch
+
+from gpu_helpers import assert_bitwise, to_dev, to_host
+from oracle.easgd import easgd_sequence, easgd_update
+from paper_1605_08325_b200 import tm
+from paper_1605_08325_b200.inputs import worker_buffer
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.mark.parametrize("alpha", [0.5, 0.0625, 0.3])
+@pytest.mark.parametrize("dist", ["D1", "D2", "D3", "D6"])
+def test_update_bitwise(alpha, dist):
+    for n in (1, 3, 4, 1000, 1_000_003):
+        x = worker_buffer(n, dist, 0, config=40)
+        c = worker_buffer(n, dist, 1, config=40)
+        xd, cd = to_dev([x, c])
+        tm.tm_easgd_update_ex(xd, cd, alpha)
+        gx, gc = to_host([xd, cd])
+        wx, wc = easgd_update(x, c, alpha)
+        assert_bitwise(gx, wx, f"x n={n}")
+        assert_bitwise(gc, wc, f"c n={n}")
+
+
+def test_update_unaligned_views():
+    n = 100_001
+    x = worker_buffer(n + 1, "D1", 0, config=41)
+    c = worker_buffer(n + 3, "D1", 1, config=41)
+    xd, cd = to_dev([x, c])
+    tm.tm_easgd_update_ex(xd[1:], cd[3:], 0.3)  # 4- and 12-byte offsets: scalar path
+    gx, gc = to_host([xd, cd])
+    wx, wc = easgd_update(x[1:], c[3:], 0.3)
+    assert_bitwise(gx[1:], wx)
+    assert_bitwise(gc[3:], wc)
+    assert gx[0] == x[0] and np.array_equal(gc[:3], c[:3])
+
+
+def test_update_with_context_and_library_centre():
+    n = 65_537
+    with tm.Exchanger(n, "easgd", size=1, nlocal=1) as ex:
+        centre = tm.device_view(ex.center(0), n)
+        x = worker_buffer(n, "D2", 0, config=42)
+        c0 = worker_buffer(n, "D2", 1, config=42)
+        xd = to_dev([x])[0]
+        centre.copy_(torch.from_numpy(c0))
+        tm.tm_easgd_update(xd, centre, 0.5)
+        gx, gc = to_host([xd, centre])
+        wx, wc = easgd_update(x, c0, 0.5)
+        assert_bitwise(gx, wx)
+        assert_bitwise(gc, wc)
+
+
+def test_concurrent_mode_serial_stream_equals_exclusive():
+    """red.add on one stream (no contention): fl(c + e) exactly as the oracle."""
+    n = 500_000
+    x = worker_buffer(n, "D1", 0, config=43)
+    c = worker_buffer(n, "D1", 1, config=43)
+    xd, cd = to_dev([x, c])
+    tm.tm_easgd_update_ex(xd, cd, 0.0625, concurrent=True)
+    gx, gc = to_host([xd, cd])
+    wx, wc = easgd_update(x, c, 0.0625)
+    assert_bitwise(gx, wx)
+    assert_bitwise(gc, wc)
+
+
+@pytest.mark.parametrize("order", [[0, 1, 2, 3, 4, 5, 6, 7], [7, 2, 5, 0, 2, 1], [3]])
+def test_fused_round_equals_arrival_order_sequence(order):
+    n = 1_000_003
+    nw = 8
+    W = [worker_buffer(n, "D3", r, config=44) for r in range(nw)]
+    c = worker_buffer(n, "D3", 99, config=44)
+    Wd = to_dev(W)
+    cd = to_dev([c])[0]
+    tm.tm_easgd_round(Wd, order, cd, 0.5 / 8)
+    gW = to_host(Wd)
+    gc = to_host([cd])[0]
+    wW, wc = easgd_sequence(W, c, 0.5 / 8, order)
+    assert_bitwise(gc, wc, "centre")
+    for r in range(nw):
+        assert_bitwise(gW[r], wW[r], f"worker {r}")
+
+
+def test_concurrent_workers_invariants():
+    """8 workers update one centre concurrently from 8 streams (Q15: no bitwise
+    oracle).  Invariants: sum_w x_w + c conserved within the rounding bound, and
+    each worker moved toward the centre it read."""
+    n = 1 << 20
+    nw = 8
+    alpha = 0.5 / nw
+    W = [worker_buffer(n, "D1", r, config=45) for r in range(nw)]
+    c = worker_buffer(n, "D1", 99, config=45)
+    Wd = to_dev(W)
+    cd = to_dev([c])[0]
+    streams = [torch.cuda.Stream() for _ in range(nw)]
+    torch.cuda.synchronize()
+    for w, s in zip(Wd, streams):
+        tm.tm_easgd_update_ex(w, cd, alpha, concurrent=True, stream=s)
+    torch.cuda.synchronize()
+    gW = to_host(Wd)
+    gc = to_host([cd])[0]
+    tot0 = sum(w.astype(np.float64) for w in W) + c
+    tot1 = sum(w.astype(np.float64) for w in gW) + gc
+    scale = sum(np.abs(w.astype(np.float64)) for w in gW) + np.abs(gc)
+    assert np.all(np.abs(tot1 - tot0) <= 2 * (nw + 1) * 2.0 ** -24 * scale + 1e-30)
+    # the serial-order oracle's centre is within the reordering bound
+    _, wc = easgd_sequence(W, c, alpha, list(range(nw)))
+    assert np.max(np.abs(gc.astype(np.float64) - wc)) < 0.25

@@ -1,0 +1,212 @@
+"""GPU parity of tm_exchange (single-process groups: k ranks on one device, the
+same kernels with local pointers in the peer table) against the CPU oracle.
+
+Bar: ASA and ASA16 bitwise; AR within Q11 (and, for the
+single-process kernel whose order is ascending rank, bitwise); every rank's
+result bitwise identical.
+"""
+
+import numpy as np
+import pytest
+import torch
+
+from gpu_helpers import assert_bitwise, q11_bound, to_dev, to_host
+from oracle import exchange as ox
+from paper_1605_08325_b200 import tm
+from paper_1605_08325_b200.inputs import DISTS, WORKLOADS, worker_buffers
+
+pytestmark = pytest.mark.gpu
+
+SIZES = [1, 7, 8, 9, 255, 1024, 100003, 1_000_003]
+
+
+def run_group(X, strategy, reps=1):
+    """Exchange the k buffers X (numpy) through tm_exchange_group; returns the
+    k results (numpy) and the status code."""
+    k, P = len(X), X[0].shape[0]
+    bufs = to_dev(X)
+    with tm.Exchanger(P, strategy, size=k, nlocal=k) as ex:
+        for _ in range(reps):
+            ex.exchange(bufs)
+        code, bits = ex.status()
+        out = to_host(bufs)
+    return out, code, bits
+
+
+@pytest.mark.parametrize("strategy", ["asa", "asa16"])
+@pytest.mark.parametrize("k", [2, 3, 4, 5, 8])
+def test_asa_family_bitwise_sizes(strategy, k):
+    for P in SIZES:
+        X = worker_buffers(P, k, "D1", config=1)
+        out, code, _ = run_group(X, strategy)
+        assert code == tm.TM_OK
+        want = ox.exchange(X, strategy)
+        for r in range(k):
+            assert_bitwise(out[r], want[r], f"{strategy} k={k} P={P} rank {r}")
+
+
+@pytest.mark.parametrize("strategy", ["asa", "asa16"])
+@pytest.mark.parametrize("dist", DISTS)
+def test_asa_family_bitwise_distributions(strategy, dist):
+    for k in (2, 8):
+        X = worker_buffers(100003, k, dist, config=1)
+        out, code, _ = run_group(X, strategy)
+        assert code == tm.TM_OK
+        want = ox.exchange(X, strategy)
+        for r in range(k):
+            assert_bitwise(out[r], want[r], f"{strategy} {dist} k={k} rank {r}")
+
+
+@pytest.mark.parametrize("k", [2, 4, 8])
+def test_ar_single_process(k):
+    for dist in ("D1", "D2", "D4", "D6"):
+        for P in (1, 9, 100003):
+            X = worker_buffers(P, k, dist, config=2)
+            out, code, _ = run_group(X, "ar")
+            assert code == tm.TM_OK
+            want = ox.ar_average(X)
+            bound = q11_bound(X)
+            for r in range(k):
+                assert np.all(np.abs(out[r].astype(np.float64) - want[r]) <= bound)
+                assert_bitwise(out[r], want[r], f"ar {dist} k={k} P={P}")  # ascending-rank kernel
+
+
+def test_ar_equals_asa_on_dyadics():
+    from paper_1605_08325_b200.inputs import dyadic_buffers
+    X = dyadic_buffers(65537, 8)
+    a, _, _ = run_group(X, "ar")
+    b, _, _ = run_group(X, "asa")
+    mean = (np.sum(np.stack(X).astype(np.float64), axis=0) / 8).astype(np.float32)
+    assert_bitwise(a[3], mean)
+    assert_bitwise(b[5], mean)
+
+
+def test_repeated_exchanges_fresh_inputs():
+    """Back-to-back exchanges reuse the staging across epochs (a7)."""
+    k, P = 4, 300007
+    with tm.Exchanger(P, "asa16", size=k, nlocal=k) as ex:
+        for it in range(4):
+            X = worker_buffers(P, k, DISTS[it], config=30 + it)
+            bufs = to_dev(X)
+            ex.exchange(bufs)
+            ex.exchange(bufs)  # exchanging the average again: idempotent for ASA16
+            out = to_host(bufs)
+            want = ox.asa16_average(ox.asa16_average(X))
+            for r in range(k):
+                assert_bitwise(out[r], want[r], f"iter {it}")
+        assert ex.layout()["epoch"] == 8
+
+
+def test_cross_rank_identity_and_status_clean():
+    X = worker_buffers(1_000_003, 8, "D2", config=3)
+    for strategy in ("asa", "asa16", "ar"):
+        out, code, bits = run_group(X, strategy)
+        assert code == tm.TM_OK and bits == 0
+        for r in range(1, 8):
+            assert_bitwise(out[r], out[0], strategy)
+
+
+def test_k1_identity():
+    X = worker_buffers(1001, 1, "D6")
+    for strategy in ("ar", "asa", "asa16"):
+        out, code, _ = run_group(X, strategy)
+        assert code == tm.TM_OK
+        assert_bitwise(out[0], X[0])
+
+
+def test_status_nonfinite_and_overflow():
+    k, P = 2, 4096
+    X = worker_buffers(P, k, "D1", config=4)
+    X[0][10] = np.float32(np.inf)
+    X[1][20] = np.float32(70000.0)
+    out, code, bits = run_group(X, "asa16")
+    assert bits == tm.TM_BIT_NONFINITE | tm.TM_BIT_OVERFLOW16
+    assert code == tm.TM_E_OVERFLOW16
+    assert np.isinf(out[0][10]) and np.isinf(out[1][20])  # IEEE: inf propagates
+    ok = np.ones(P, bool)
+    ok[[10, 20]] = False
+    want = ox.asa16_average(X)
+    assert_bitwise(out[0][ok], want[0][ok])
+    X = worker_buffers(P, k, "D1", config=4)
+    X[1][5] = np.float32(np.nan)
+    _, code, bits = run_group(X, "asa")
+    assert code == tm.TM_E_NONFINITE and bits == tm.TM_BIT_NONFINITE
+
+
+def test_argument_errors():
+    P = 1024
+    with tm.Exchanger(P, "asa16", size=2, nlocal=2):
+        a = torch.zeros(P + 1, device="cuda")
+        b = torch.zeros(P, device="cuda")
+        with pytest.raises(tm.TmError) as e:
+            tm.tm_exchange_group([a[1:], b])  # 4-byte offset: misaligned
+        assert e.value.code == tm.TM_E_ALIGN
+        with pytest.raises(tm.TmError) as e:
+            tm.tm_exchange_group([b])  # wrong count
+        assert e.value.code == tm.TM_E_ARG
+        with pytest.raises(tm.TmError) as e:
+            tm.tm_exchange(b)  # nlocal != 1
+        assert e.value.code == tm.TM_E_STATE
+        with pytest.raises(tm.TmError) as e:
+            tm.tm_exchange_init(P, 0, 2, 0, 2, tm.TM_ASA)  # already initialised
+        assert e.value.code == tm.TM_E_STATE
+    with pytest.raises(tm.TmError):
+        tm.tm_exchange_init(0, 0, 2, 0, 2, tm.TM_ASA)
+    with pytest.raises(tm.TmError):
+        tm.tm_exchange_init(10, 0, 9, 0, 9, tm.TM_ASA)
+
+
+def test_layout_segments():
+    """Segment layout a1: L = roundup(ceil(P/k), 256); chunk multiple of 256."""
+    for P, k in ((60_965_224, 8), (6_998_552, 4), (1_000_003, 2), (1, 8)):
+        with tm.Exchanger(P, "asa16", size=k, nlocal=k) as ex:
+            lay = ex.layout()
+            L = -(-(-(-P // k)) // 256) * 256
+            assert lay["seg_len"] == L
+            assert lay["chunk_len"] % 256 == 0
+            assert lay["ctas_per_rank"] * lay["chunk_len"] >= L
+            assert lay["wire_bytes"] == 2
+
+
+@pytest.mark.parametrize("P", [WORKLOADS["googlenet"], WORKLOADS["alexnet"]])
+def test_full_size_sampled(P):
+    """BASELINE sizes in the bench's launch configuration (k=8 group): sampled
+    elements against the oracle's per-element definition, plus the tail."""
+    k = 8
+    g = np.random.default_rng(5)
+    for strategy, dist in (("asa16", "D2"), ("asa", "D1")):
+        X = worker_buffers(P, k, dist, config=3)
+        bufs = to_dev(X)
+        with tm.Exchanger(P, strategy, size=k, nlocal=k) as ex:
+            ex.exchange(bufs)
+            code, _ = ex.status()
+        assert code == tm.TM_OK
+        idx = np.unique(np.concatenate([g.integers(0, P, 200_000), np.arange(P - 300, P)]))
+        vals = np.stack([x[idx] for x in X])
+        want = ox.element_average(vals, strategy)
+        ti = torch.from_numpy(idx).cuda()
+        for r in (0, 3, 7):
+            got = bufs[r][ti].cpu().numpy()
+            assert_bitwise(got, want, f"{strategy} P={P} rank {r}")
+        del bufs
+        torch.cuda.empty_cache()
+
+
+def test_device_rn16_exhaustive():
+    """The device rounding (cvt.rn.f16.f32) on all 2^32 fp32 patterns against
+    numpy's binary16 conversion, which the opt-in CPU test pins to the oracle's
+    integer emulation on all 2^32 inputs; plus the oracle itself on a dense
+    stratified subset.  NaN payloads are outside the contract (Q8)."""
+    from oracle.fp16 import rn16
+    step = 1 << 28
+    for start in range(0, 1 << 32, step):
+        b = torch.arange(start, start + step, dtype=torch.int64, device="cuda").to(torch.int32)
+        x = b.view(torch.float32)
+        h = tm.tm_cast_rn16(x).cpu().numpy().view(np.uint16)
+        xn = x.cpu().numpy()
+        ref = xn.astype(np.float16).view(np.uint16)
+        nan = np.isnan(xn)
+        assert np.array_equal(h[~nan], ref[~nan]), start
+        assert np.all((h[nan] & 0x7C00) == 0x7C00) and np.all((h[nan] & 0x3FF) != 0)
+        sub = slice(None, None, 4099)
+        assert np.array_equal(h[sub][~nan[sub]], rn16(xn[sub])[~nan[sub]]), start

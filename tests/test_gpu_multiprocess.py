@@ -1,0 +1,76 @@
+"""Multi-process exchange: one process per rank (nlocal = 1), peers reached through
+CUDA IPC mappings, flags in peer memory -- the north-star deployment.  On the
+one-GPU test box all processes share cuda:0 (IPC across processes on one device;
+the kernels are time-sliced, so this checks correctness, not speed)."""
+
+import json
+import os
+import socket
+import subprocess
+import sys
+
+import numpy as np
+import pytest
+
+from gpu_helpers import assert_bitwise
+from oracle import exchange as ox
+from paper_1605_08325_b200.inputs import worker_buffer
+
+pytestmark = pytest.mark.gpu
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def launch(tmp_path, k, strategy, P, dist, mode="normal", timeout=240):
+    port = _free_port()
+    procs = []
+    for r in range(k):
+        env = dict(os.environ, RANK=str(r), WORLD_SIZE=str(k), MASTER_ADDR="127.0.0.1",
+                   MASTER_PORT=str(port), LOCAL_RANK=str(r))
+        procs.append(subprocess.Popen([sys.executable, os.path.join(HERE, "mp_worker.py"), str(tmp_path),
+                                       strategy, str(P), dist, mode], env=env))
+    try:
+        for p in procs:
+            p.wait(timeout=timeout)
+    finally:
+        for p in procs:
+            if p.poll() is None:
+                p.kill()
+    assert all(p.returncode == 0 for p in procs), [p.returncode for p in procs]
+    res = [json.load(open(os.path.join(tmp_path, f"rank{r}.json"))) for r in range(k)]
+    return res
+
+
+@pytest.mark.parametrize("strategy,k", [("asa16", 2), ("asa", 2), ("asa16", 3)])
+def test_multiprocess_bitwise(tmp_path, strategy, k):
+    P = 100_003
+    res = launch(tmp_path, k, strategy, P, "D2")
+    X = [worker_buffer(P, "D2", r, config=50) for r in range(k)]
+    want = X
+    for _ in range(3):
+        want = ox.exchange(want, strategy)
+    for r in range(k):
+        assert res[r]["code"] == 0, res[r]
+        got = np.load(os.path.join(tmp_path, f"rank{r}.npy"))
+        assert_bitwise(got, want[r], f"{strategy} rank {r}")
+
+
+def test_multiprocess_timeout_instead_of_hang(tmp_path):
+    """Fault injection: rank 1 never calls tm_exchange; rank 0's
+    kernel times out, sets TM_E_TIMEOUT and exits."""
+    res = launch(tmp_path, 2, "asa16", 4096, "D1", mode="skip1")
+    assert res[0]["code"] == 7 and res[0]["bits"] & 4  # TM_E_TIMEOUT
+
+
+def test_multiprocess_mismatch_detected(tmp_path):
+    """Ranks disagreeing on nparams fail the bootstrap with TM_E_MISMATCH."""
+    res = launch(tmp_path, 2, "asa", 4096, "D1", mode="mismatch")
+    assert any(r.get("init_error") == 6 for r in res), res
