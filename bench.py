@@ -5,16 +5,16 @@ Metric (BASELINE.json): exchange time per iteration and algorithm GB/s of an
 ASA16 exchange of an AlexNet-sized (60,965,224 fp32) parameter vector.
 
   python bench.py                      # N=1: the k=8 exchange, all 8 ranks' buffers
-                                       # resident on one B200 (single-process group;
-                                       # the same kernels as the multi-GPU path with
-                                       # local pointers in the peer table)
+                                       # resident on one B200 (single-process group,
+                                       # direct one-pass path; the staged multi-GPU
+                                       # kernel is timed beside it on the same GPU)
   torchrun --nproc-per-node N bench.py --gpus N   # N>1: one process per GPU, k = N,
                                        # peers over CUDA IPC / NVLink
   python bench.py --impl reference     # the CPU oracle (the reference arm)
 
 One "step" = one tm_exchange of every rank's buffer (the whole hot path:
-pre-cast, reduce-scatter pull with fused sum/scale/cast, allgather pull with
-fused widen).  value = sum over ranks of 4P bytes / step time (algorithm
+reduce-scatter pull with fused cast/sum/scale/cast and allgather; on the staged
+path with the pre-cast and flag barriers).  value = sum over ranks of 4P bytes / step time (algorithm
 bandwidth of the whole job); inputs (k x 244 MB) exceed the 126 MB L2, so no
 flush is needed between steps.  Prints ONE JSON line on rank 0.
 """
@@ -50,6 +50,10 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=5)
+    ap.add_argument("--path", choices=["auto", "staged", "direct"], default="auto",
+                    help="data path of the exchange (auto: direct for a one-GPU group)")
+    ap.add_argument("--no-staged", action="store_true",
+                    help="skip the secondary timing of the staged (multi-GPU) kernel on one GPU")
     return ap.parse_args()
 
 
@@ -62,11 +66,14 @@ def hbm_peak():
         return HBM_FALLBACK_GBS, "fallback (B200_PROFILING.md)"
 
 
-def design_hbm_bytes(strategy, P, k):
+def design_hbm_bytes(strategy, P, k, path):
     """Algorithmic HBM bytes of one exchange summed over the k ranks (SURVEY 8(d);
-    DESIGN.md 'Roofline'):  ASA16 per rank: read x 4P + write stage 2P + RS reads
-    2P + write avg 2P/k + AG reads 2P + write x 4P = (14 + 2/k) P.
-    ASA per rank: (20 + 4/k) P.  AR in one pass: read + write 4P per rank = 8P."""
+    DESIGN.md 'Roofline').  Direct path (and AR in one process): every rank's
+    buffer is read once and written once, 8P per rank -- the irreducible bytes.
+    Staged path, ASA16 per rank: read x 4P + write stage 2P + RS reads 2P +
+    write avg 2P/k + AG reads 2P + write x 4P = (14 + 2/k) P; ASA (20 + 4/k) P."""
+    if path == "direct" or strategy == "ar":
+        return k * 8.0 * P
     if strategy == "asa16":
         return k * (14 + 2.0 / k) * P
     if strategy == "asa":
@@ -128,18 +135,30 @@ class ClockSampler:
 
 # ----------------------------------------------------------------- reference arm
 
+def workload_name(args, k, multi):
+    return f"{args.workload}_{args.strategy}_k{k}" + ("" if multi else "_one_gpu")
+
+
 def run_reference(args):
     """The CPU oracle (oracle/exchange.py, as it stands) on the host cores: each
-    step is a bounded sample of the workload (a contiguous slice of P), timed
-    with perf_counter; the metric is scaled to the same unit."""
+    step is one oracle exchange of a bounded sample of the workload (the first
+    `sample` elements of all k buffers), sized from a quick calibration so that
+    warmup + steps take about REF_BUDGET_S; the metric is the same unit."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
     from oracle import exchange as ox
     from paper_1605_08325_b200.inputs import WORKLOADS, worker_buffers
     P = WORKLOADS[args.workload]
-    k = args.k if args.gpus == 1 else args.gpus
-    sample = min(P, 1 << 20 if args.strategy == "asa16" else 1 << 22)
+    multi = args.gpus > 1
+    k = args.gpus if multi else args.k
+    budget = float(os.environ.get("REF_BUDGET_S", "120"))
+    cal = worker_buffers(1 << 16, k, args.dist, config=3)
+    t = time.perf_counter()
+    ox.exchange(cal, args.strategy)
+    rate = (1 << 16) / max(time.perf_counter() - t, 1e-6)  # elements (x k ranks) per second
+    per_step = budget / max(1, args.steps + args.warmup)
+    sample = int(min(P, max(4096, rate * per_step)) // 4096 * 4096) or min(P, 4096)
     X = worker_buffers(sample, k, args.dist, config=3)
     for _ in range(args.warmup):
         ox.exchange(X, args.strategy)
@@ -156,11 +175,12 @@ def run_reference(args):
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": scaled_ms, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-        "config": {"workload": f"{args.workload}_{args.strategy}_k{k}", "P": P, "k": k,
+        "config": {"workload": workload_name(args, k, multi), "P": P, "k": k,
                    "strategy": args.strategy, "dist": args.dist},
         "cpu_baseline": {"value": gbs, "unit": "GB/s", "cores": 1, "kind": "oracle",
-                         "sample": f"{sample} of {P} elements x {k} ranks per step "
-                                   f"(ms_per_step scaled to full P)"},
+                         "sample": f"{sample} of {P} elements x {k} ranks per step, numpy "
+                                   f"single-threaded (ms_per_step scaled to full P)",
+                         "cpu": _cpu_model(), "host_cpus": os.cpu_count()},
         "e2e": {"value": gbs, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -189,6 +209,16 @@ def _cpu_model():
     except Exception:
         pass
     return None
+
+
+def roofline(strategy, P, k, path, ms, peak, peak_src, workload):
+    alg = design_hbm_bytes(strategy, P, k, path)
+    ach = alg / (ms * 1e-3) / 1e9
+    kernel = "tm_exchange_kernel" if path == "staged" and strategy != "ar" else "tm_direct_kernel"
+    return {"bound": "hbm", "achieved": ach, "peak": peak, "unit": "GB/s", "frac": ach / peak,
+            "traffic": traffic_from_profiles(f"{workload}_{strategy}_k{k}_{path}"),
+            "algorithmic_bytes_per_launch": alg, "peak_source": peak_src, "kernel": kernel,
+            "irreducible_frac": (8.0 * P * k / (ms * 1e-3) / 1e9) / peak}
 
 
 def traffic_from_profiles(workload_key):
@@ -228,7 +258,9 @@ def main():
 
     host = [worker_buffer(P, args.dist, first + i, config=3) for i in range(nlocal)]
     bufs = [torch.from_numpy(h).to(dev) for h in host]
-    ex = tm.Exchanger(P, args.strategy, rank=first, size=k, device=local, nlocal=nlocal)
+    ex = tm.Exchanger(P, args.strategy, rank=first, size=k, device=local, nlocal=nlocal,
+                      path=args.path)
+    path = {0: "auto", 1: "staged", 2: "direct"}[ex.layout()["path"]]
     stream = torch.cuda.current_stream()
 
     def step():
@@ -280,14 +312,25 @@ def main():
                 "peak_source": "measured peer copy per direction (B200_PROFILING.md)"}
         roof["frac"] = roof["achieved"] / roof["peak"]
     else:
-        alg = design_hbm_bytes(args.strategy, P, k)
-        ach = alg / (ms * 1e-3) / 1e9
-        key = f"{args.workload}_{args.strategy}_k{k}"
-        tr = traffic_from_profiles(key)
-        roof = {"bound": "hbm", "achieved": ach, "peak": peak, "unit": "GB/s", "frac": ach / peak,
-                "traffic": tr, "algorithmic_bytes_per_launch": alg, "peak_source": peak_src,
-                "kernel": "tm_exchange_kernel" if args.strategy != "ar" else "local_allreduce_kernel",
-                "irreducible_frac": (8.0 * P * k / (ms * 1e-3) / 1e9) / peak}
+        roof = roofline(args.strategy, P, k, path, ms, peak, peak_src, args.workload)
+
+    # secondary: the staged (multi-GPU) kernel timed on this GPU, same buffers
+    staged = None
+    if not multi and not args.no_staged and args.strategy != "ar" and path != "staged":
+        tm.tm_set_path("staged")
+        for _ in range(args.warmup):
+            step()
+        torch.cuda.synchronize()
+        g0, g1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        g0.record(stream)
+        for _ in range(args.steps):
+            step()
+        g1.record(stream)
+        torch.cuda.synchronize()
+        sms = g0.elapsed_time(g1) / args.steps
+        staged = {"ms_per_step": sms, "value": bytes_alg / (sms * 1e-3) / 1e9, "unit": "GB/s",
+                  "roofline": roofline(args.strategy, P, k, "staged", sms, peak, peak_src, args.workload)}
+        tm.tm_set_path(path)
 
     # end to end through the public API with host buffers
     e2e = None
@@ -321,13 +364,14 @@ def main():
             "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f32", "wire_dtype": "f16" if args.strategy == "asa16" else "f32",
             "data": "synthetic",
-            "config": {"workload": f"{args.workload}_{args.strategy}_k{k}" + ("" if multi else "_one_gpu"),
+            "config": {"workload": workload_name(args, k, multi),
                        "P": P, "k": k, "strategy": args.strategy, "dist": args.dist,
-                       "ranks_per_gpu": nlocal, "seg_len": lay["seg_len"],
+                       "ranks_per_gpu": nlocal, "path": path, "seg_len": lay["seg_len"],
                        "ctas_per_rank": lay["ctas_per_rank"],
                        "l2": f"inputs larger than L2 ({k * 4 * P / 1e9:.2f} GB per step), no flush"},
             "roofline": roof,
             "gpu_launches": args.steps,
+            "staged_path_one_gpu": staged,
             "clocks": clk.summary(),
             "e2e": e2e,
             "status": code, "parity_spot_check": parity,

@@ -113,8 +113,24 @@ typedef struct {
   int32_t sm_count;
   int32_t wire_bytes;    /* 4 (AR, ASA) or 2 (ASA16)                          */
   int64_t lib_bytes;     /* device bytes the library owns in this process     */
-  uint32_t epoch;        /* number of exchanges issued so far                 */
+  uint32_t epoch;        /* number of staged exchanges issued so far          */
+  int32_t path;          /* effective tm_path of the next exchange            */
 } tm_layout_info;
+
+/* How an ASA / ASA16 exchange moves data (results are bitwise identical):
+ *   TM_PATH_STAGED  pre-cast into library-owned staging, flag barrier,
+ *                   reduce-scatter PULL from every rank's staging (NVLink P2P
+ *                   loads across GPUs), flag barrier, allgather PULL.  The wire
+ *                   carries fp16 for ASA16.  Required when ranks live in
+ *                   different processes (nlocal == 1).
+ *   TM_PATH_DIRECT  single-process groups only (nlocal == size): one pass in
+ *                   which the owner of each element pulls the k fp32
+ *                   contributions straight from the k caller buffers, applies
+ *                   the same arithmetic (rn16 of each contribution for ASA16,
+ *                   ascending-rank sum, /k, rn16) in registers and pushes the
+ *                   result to all k buffers: no staging, no flags.
+ *   TM_PATH_AUTO    DIRECT when nlocal == size, else STAGED (default). */
+typedef enum { TM_PATH_AUTO = 0, TM_PATH_STAGED = 1, TM_PATH_DIRECT = 2 } tm_path;
 
 /* Create the process-global exchanger.  nparams >= 1; world as above; strategy
  * a tm_strategy.  Allocates the library-owned buffers on world->device.  For
@@ -180,6 +196,10 @@ int tm_exchange_status(void* stream, uint32_t* bits);
 
 /* Layout of the current exchanger (for tests and the bench). */
 int tm_layout(tm_layout_info* out);
+
+/* Select the data path (tm_path) for later exchanges of this exchanger.
+ * TM_E_ARG for TM_PATH_DIRECT unless nlocal == size; TM_E_STATE before init. */
+int tm_set_path(int path);
 
 /* Barrier spin timeout in nanoseconds (default 10 s; 0 restores default). */
 int tm_set_timeout_ns(uint64_t ns);

@@ -38,9 +38,12 @@ struct ExchangeArgs {
 // wire16: fp16 wire (ASA16) else fp32 (ASA).  grid = nlocal * C, cooperative.
 cudaError_t launch_exchange(const ExchangeArgs& a, int nlocal, bool wire16, cudaStream_t s);
 
-// Single-process allreduce-average of k device buffers (AR when all ranks are
-// local): one pass, ascending-rank fp32 sum, one division, result to all k.
-cudaError_t launch_local_allreduce(float* const* bufs, int k, int64_t P, cudaStream_t s);
+// Single-process group, one pass (the "direct" path): pull the k contributions
+// of each element from the k buffers, fused rn16 (q16) / ascending-rank sum /
+// (1/k) / rn16, push the result to all k buffers.  Also AR when all ranks are
+// local (q16 = false).
+cudaError_t launch_direct(float* const* bufs, int k, int64_t P, bool q16, uint32_t* status,
+                          cudaStream_t s);
 
 cudaError_t launch_easgd(float* x, float* c, int64_t n, float alpha, bool concurrent,
                          cudaStream_t s);

@@ -96,6 +96,30 @@ __device__ __forceinline__ uint32_t status_of(float v, bool wire16) {
   return s;
 }
 
+// fl(s / k).  For k a power of two the product with the exact 1/k is the same
+// correctly rounded value (x/2^n and x*2^-n are the same real number), and is
+// cheaper; otherwise an IEEE division.
+template <int K>
+__device__ __forceinline__ float div_k(float s) {
+  if constexpr ((K & (K - 1)) == 0) return __fmul_rn(s, 1.0f / (float)K);
+  else return __fdiv_rn(s, (float)K);
+}
+
+// Status of a unit of E fp32 values: a max over |bits| screens the unit (one
+// LOP + one IMNMX per element); the exact bits are computed only when the max
+// reaches the fp16-overflow (ASA16) or non-finite (ASA) threshold.
+template <bool W16, int E>
+__device__ __forceinline__ uint32_t unit_status(const float* f) {
+  uint32_t m = 0;
+#pragma unroll
+  for (int q = 0; q < E; ++q) m = max(m, __float_as_uint(f[q]) & 0x7fffffffu);
+  if (m < (W16 ? 0x477ff000u : 0x7f800000u)) return 0u;
+  uint32_t st = 0;
+#pragma unroll
+  for (int q = 0; q < E; ++q) st |= status_of(f[q], W16);
+  return st;
+}
+
 // ---------------------------------------------------------------------------
 // Wire-type traits: one "unit" = 16 bytes of wire data.
 //   fp16 wire: 8 elements (32 B of fp32 source);  fp32 wire: 4 elements.
@@ -178,7 +202,7 @@ __device__ __forceinline__ bool rank_barrier(const ExchangeArgs& a, int phase, i
 }
 
 template <int K, bool W16>
-__global__ void __launch_bounds__(kThreads, 4)
+__global__ void __launch_bounds__(kThreads, K == 6 ? 3 : 4)
 tm_exchange_kernel(const __grid_constant__ ExchangeArgs a) {
   using U = Unit<W16>;
   constexpr int E = U::kElems;
@@ -197,35 +221,36 @@ tm_exchange_kernel(const __grid_constant__ ExchangeArgs a) {
   char* const stage_r = reinterpret_cast<char*>(a.stage[r]);
 
   // ---------------- a2: pre-cast all k segments' chunk c into own stage -------
+  // Thread-contiguous units within a segment (coalesced); G segments per batch
+  // so G independent 32-byte (ASA16) / 16-byte (ASA) loads are in flight.
+  const int nu32 = (int)nu;
   uint32_t st = 0;
   {
-    const int64_t total = (int64_t)K * nu;
-    constexpr int B = 4;
-    for (int64_t t0 = threadIdx.x; t0 < total; t0 += (int64_t)B * kThreads) {
-      float f[B][E];
+    constexpr int G = K < 4 ? K : 4;
+    for (int v = threadIdx.x; v < nu32; v += kThreads) {
+      const int64_t ev = e0 + (int64_t)v * E;
 #pragma unroll
-      for (int u = 0; u < B; ++u) {
-        const int64_t t = t0 + (int64_t)u * kThreads;
-        if (t < total) {
-          const int64_t s = t / nu;
-          const int64_t g = s * L + e0 + (t - s * nu) * E;  // element index
-          if (g + E <= P) {
-            U::to_floats(U::load_src(x + g), f[u]);
-          } else {
+      for (int s0 = 0; s0 < K; s0 += G) {
+        float f[G][E];
 #pragma unroll
-            for (int q = 0; q < E; ++q) f[u][q] = (g + q < P) ? x[g + q] : 0.0f;
+        for (int u = 0; u < G; ++u) {
+          if (s0 + u < K) {
+            const int64_t g = (int64_t)(s0 + u) * L + ev;
+            if (g + E <= P) {
+              U::to_floats(U::load_src(x + g), f[u]);
+            } else {
+#pragma unroll
+              for (int q = 0; q < E; ++q) f[u][q] = (g + q < P) ? x[g + q] : 0.0f;
+            }
           }
         }
-      }
 #pragma unroll
-      for (int u = 0; u < B; ++u) {
-        const int64_t t = t0 + (int64_t)u * kThreads;
-        if (t < total) {
-          const int64_t s = t / nu;
-          const int64_t g = s * L + e0 + (t - s * nu) * E;
-#pragma unroll
-          for (int q = 0; q < E; ++q) st |= status_of(f[u][q], W16);
-          st16_cg(stage_r + g * WB, U::encode(f[u]));
+        for (int u = 0; u < G; ++u) {
+          if (s0 + u < K) {
+            const int64_t g = (int64_t)(s0 + u) * L + ev;
+            st |= unit_status<W16, E>(f[u]);
+            st16_cg(stage_r + g * WB, U::encode(f[u]));
+          }
         }
       }
     }
@@ -240,7 +265,6 @@ tm_exchange_kernel(const __grid_constant__ ExchangeArgs a) {
 #pragma unroll
     for (int j = 0; j < K; ++j) src[j] = reinterpret_cast<const char*>(a.stage[j]);
     char* const avg_r = reinterpret_cast<char*>(a.avg[r]);
-    const float kf = (float)K;
     const int64_t seg0 = (int64_t)r * L + e0;
     for (int64_t v = threadIdx.x; v < nu; v += kThreads) {
       const int64_t off = (seg0 + v * E) * WB;
@@ -256,7 +280,7 @@ tm_exchange_kernel(const __grid_constant__ ExchangeArgs a) {
         for (int q = 0; q < E; ++q) s[q] = __fadd_rn(s[q], t[q]);
       }
 #pragma unroll
-      for (int q = 0; q < E; ++q) s[q] = __fdiv_rn(s[q], kf);
+      for (int q = 0; q < E; ++q) s[q] = div_k<K>(s[q]);
       st16_cg(avg_r + (e0 + v * E) * WB, U::encode(s));
     }
   }
@@ -265,34 +289,24 @@ tm_exchange_kernel(const __grid_constant__ ExchangeArgs a) {
 
   // ---------------- a6: allgather pull, fused widen, store to caller ---------
   {
-    const int64_t total = (int64_t)K * nu;
-    constexpr int B = 4;
-    for (int64_t t0 = threadIdx.x; t0 < total; t0 += (int64_t)B * kThreads) {
-      uint4 raw[B];
+    constexpr int G = K;  // all k owners' units in flight at once
+    for (int v = threadIdx.x; v < nu32; v += kThreads) {
+      const int64_t ev = e0 + (int64_t)v * E;
+      uint4 raw[G];
 #pragma unroll
-      for (int u = 0; u < B; ++u) {
-        const int64_t t = t0 + (int64_t)u * kThreads;
-        if (t < total) {
-          const int64_t j = t / nu;
-          const int64_t e = e0 + (t - j * nu) * E;
-          raw[u] = ld16_cg(reinterpret_cast<const char*>(a.avg[j]) + e * WB);
-        }
-      }
+      for (int j = 0; j < G; ++j)
+        raw[j] = ld16_cg(reinterpret_cast<const char*>(a.avg[j]) + ev * WB);
 #pragma unroll
-      for (int u = 0; u < B; ++u) {
-        const int64_t t = t0 + (int64_t)u * kThreads;
-        if (t < total) {
-          const int64_t j = t / nu;
-          const int64_t g = j * L + e0 + (t - j * nu) * E;
-          float f[E];
-          U::decode(raw[u], f);
-          if (g + E <= P) {
-            U::store_dst(x + g, f);
-          } else {
+      for (int j = 0; j < G; ++j) {
+        const int64_t g = (int64_t)j * L + ev;
+        float f[E];
+        U::decode(raw[j], f);
+        if (g + E <= P) {
+          U::store_dst(x + g, f);
+        } else {
 #pragma unroll
-            for (int q = 0; q < E; ++q)
-              if (g + q < P) x[g + q] = f[q];
-          }
+          for (int q = 0; q < E; ++q)
+            if (g + q < P) x[g + q] = f[q];
         }
       }
     }
@@ -300,45 +314,79 @@ tm_exchange_kernel(const __grid_constant__ ExchangeArgs a) {
 }
 
 // ---------------------------------------------------------------------------
-// AR with all k ranks in this process: one pass over P, 16-byte vectors.
+// Single-process group, one pass ("direct" path).  When all k ranks' buffers
+// are addressable by one kernel there is no wire: the owner of each element
+// pulls the k contributions straight from the k buffers (the Alltoall leg),
+// applies the method's arithmetic in registers -- rn16 of every contribution
+// (ASA16, reading R1), ascending-rank fp32 sum from the rank-0 term, fl(s/k),
+// rn16 of the average -- and pushes widen(result) into all k buffers (the
+// Allgather leg).  Element i is read and written only by the thread that owns
+// it, so no flags are needed; the kernel boundary orders consecutive
+// exchanges.  Results are bitwise those of the staged path (elementwise
+// method, readings Q7/Q9).  Also AR for a single-process group (Q16 = false).
 // ---------------------------------------------------------------------------
 struct LocalBufs {
   float* b[TM_MAX_RANKS];
 };
 
-template <int K>
-__global__ void __launch_bounds__(kThreads)
-local_allreduce_kernel(const __grid_constant__ LocalBufs lb, int64_t P) {
-  const float kf = (float)K;
+__device__ __forceinline__ float4 q16(float4 v) {
+  const float2 lo = unpack16x2(pack_rn16x2(v.x, v.y));
+  const float2 hi = unpack16x2(pack_rn16x2(v.z, v.w));
+  return make_float4(lo.x, lo.y, hi.x, hi.y);
+}
+
+template <int K, bool Q16>
+__global__ void __launch_bounds__(kThreads, K >= 7 ? 3 : 4)
+tm_direct_kernel(const __grid_constant__ LocalBufs lb, int64_t P, uint32_t* status) {
   const int64_t nv = P / 4;
   const int64_t stride = (int64_t)gridDim.x * kThreads;
+  uint32_t st = 0;
   for (int64_t v = (int64_t)blockIdx.x * kThreads + threadIdx.x; v < nv; v += stride) {
     float4 in[K];
 #pragma unroll
     for (int j = 0; j < K; ++j) in[j] = ld16_f(lb.b[j] + v * 4);
-    float4 s = in[0];
+    // running max of |bits| screens for non-finite / fp16-overflow inputs
+    uint32_t m = max(max(__float_as_uint(in[0].x) & 0x7fffffffu, __float_as_uint(in[0].y) & 0x7fffffffu),
+                     max(__float_as_uint(in[0].z) & 0x7fffffffu, __float_as_uint(in[0].w) & 0x7fffffffu));
+    float4 s = Q16 ? q16(in[0]) : in[0];
 #pragma unroll
     for (int j = 1; j < K; ++j) {
-      s.x = __fadd_rn(s.x, in[j].x); s.y = __fadd_rn(s.y, in[j].y);
-      s.z = __fadd_rn(s.z, in[j].z); s.w = __fadd_rn(s.w, in[j].w);
+      m = max(m, max(max(__float_as_uint(in[j].x) & 0x7fffffffu, __float_as_uint(in[j].y) & 0x7fffffffu),
+                     max(__float_as_uint(in[j].z) & 0x7fffffffu, __float_as_uint(in[j].w) & 0x7fffffffu)));
+      const float4 t = Q16 ? q16(in[j]) : in[j];
+      s.x = __fadd_rn(s.x, t.x); s.y = __fadd_rn(s.y, t.y);
+      s.z = __fadd_rn(s.z, t.z); s.w = __fadd_rn(s.w, t.w);
     }
-    s.x = __fdiv_rn(s.x, kf); s.y = __fdiv_rn(s.y, kf);
-    s.z = __fdiv_rn(s.z, kf); s.w = __fdiv_rn(s.w, kf);
+    if (m >= (Q16 ? 0x477ff000u : 0x7f800000u)) {  // rare: exact bits from the inputs
+#pragma unroll
+      for (int j = 0; j < K; ++j)
+        st |= status_of(in[j].x, Q16) | status_of(in[j].y, Q16) | status_of(in[j].z, Q16) |
+              status_of(in[j].w, Q16);
+    }
+    s.x = div_k<K>(s.x); s.y = div_k<K>(s.y); s.z = div_k<K>(s.z); s.w = div_k<K>(s.w);
+    if (Q16) s = q16(s);
 #pragma unroll
     for (int j = 0; j < K; ++j) st16_f(lb.b[j] + v * 4, s);
   }
-  // tail (P % 4 elements)
-  const int64_t i = nv * 4 + (int64_t)blockIdx.x * kThreads + threadIdx.x;
+  // tail (P % 4 elements), scalar
+  const int64_t i = nv * 4 + threadIdx.x;
   if (blockIdx.x == 0 && i < P) {
-    float s = lb.b[0][i];
+    float in[K];
 #pragma unroll
-    for (int j = 1; j < K; ++j) s = __fadd_rn(s, lb.b[j][i]);
-    s = __fdiv_rn(s, kf);
+    for (int j = 0; j < K; ++j) in[j] = lb.b[j][i];
+#pragma unroll
+    for (int j = 0; j < K; ++j) st |= status_of(in[j], Q16);
+    float s = Q16 ? __half2float(__float2half_rn(in[0])) : in[0];
+#pragma unroll
+    for (int j = 1; j < K; ++j)
+      s = __fadd_rn(s, Q16 ? __half2float(__float2half_rn(in[j])) : in[j]);
+    s = div_k<K>(s);
+    if (Q16) s = __half2float(__float2half_rn(s));
 #pragma unroll
     for (int j = 0; j < K; ++j) lb.b[j][i] = s;
   }
+  if (st) atomicOr(status, st);
 }
-
 
 // ---------------------------------------------------------------------------
 // EASGD elastic update, one fp32 op per step:
@@ -498,20 +546,30 @@ cudaError_t launch_exchange(const ExchangeArgs& a, int nlocal, bool wire16, cuda
   return cudaLaunchCooperativeKernel(fn, dim3(nlocal * a.C), dim3(kThreads), params, 0, s);
 }
 
-cudaError_t launch_local_allreduce(float* const* bufs, int k, int64_t P, cudaStream_t s) {
+template <int K>
+void direct_k(const LocalBufs& lb, int64_t P, uint32_t* status, bool q16, int grid,
+              cudaStream_t s) {
+  if (q16) tm_direct_kernel<K, true><<<grid, kThreads, 0, s>>>(lb, P, status);
+  else tm_direct_kernel<K, false><<<grid, kThreads, 0, s>>>(lb, P, status);
+}
+
+cudaError_t launch_direct(float* const* bufs, int k, int64_t P, bool q16, uint32_t* status,
+                          cudaStream_t s) {
   LocalBufs lb{};
   for (int j = 0; j < k; ++j) lb.b[j] = bufs[j];
   int dev = 0;
   cudaGetDevice(&dev);
-  const int64_t nv = P / 4;
-  int64_t want = (nv + kThreads - 1) / kThreads;
-  int grid = (int)std::min<int64_t>(std::max<int64_t>(want, 1), grid_for_streaming(dev));
+  const int64_t want = (P / 4 + kThreads - 1) / kThreads;
+  const int per_sm = k >= 7 ? 3 : 4;  // = the kernel's __launch_bounds__ residency
+  const int grid = (int)std::min<int64_t>(std::max<int64_t>(want, 1), per_sm * sm_count(dev));
   switch (k) {
-#define TM_AR_CASE(K) \
-  case K: local_allreduce_kernel<K><<<grid, kThreads, 0, s>>>(lb, P); break;
-    TM_AR_CASE(2) TM_AR_CASE(3) TM_AR_CASE(4) TM_AR_CASE(5) TM_AR_CASE(6) TM_AR_CASE(7)
-    TM_AR_CASE(8)
-#undef TM_AR_CASE
+    case 2: direct_k<2>(lb, P, status, q16, grid, s); break;
+    case 3: direct_k<3>(lb, P, status, q16, grid, s); break;
+    case 4: direct_k<4>(lb, P, status, q16, grid, s); break;
+    case 5: direct_k<5>(lb, P, status, q16, grid, s); break;
+    case 6: direct_k<6>(lb, P, status, q16, grid, s); break;
+    case 7: direct_k<7>(lb, P, status, q16, grid, s); break;
+    case 8: direct_k<8>(lb, P, status, q16, grid, s); break;
     default: return cudaErrorInvalidValue;
   }
   return cudaGetLastError();

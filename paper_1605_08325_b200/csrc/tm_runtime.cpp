@@ -76,6 +76,7 @@ struct Ctx {
   char* peer_base[TM_MAX_RANKS] = {};  // per process (only the opened ones)
   char* rank_base[TM_MAX_RANKS] = {};  // per global rank, as mapped on this device
   uint32_t epoch = 0;
+  int path = TM_PATH_AUTO;
   uint64_t timeout_ns = kDefaultTimeoutNs;
   ncclComm_t comm = nullptr;
   ncclUniqueId nccl_id{};
@@ -136,6 +137,11 @@ ExchangeArgs make_args(float* const* bufs) {
   return a;
 }
 
+int effective_path() {
+  if (g.path != TM_PATH_AUTO) return g.path;
+  return g.nlocal == g.k ? TM_PATH_DIRECT : TM_PATH_STAGED;
+}
+
 int do_exchange(float* const* bufs, int nbufs, cudaStream_t s) {
   if (!g.inited || !g.ready || g.strategy == TM_EASGD) return TM_E_STATE;
   if (nbufs != g.nlocal || !bufs) return TM_E_ARG;
@@ -145,11 +151,11 @@ int do_exchange(float* const* bufs, int nbufs, cudaStream_t s) {
   }
   if (g.k == 1) return TM_OK;  // reading Q10: identity, nothing launched
   cudaSetDevice(g.device);
+  if (g.nlocal == g.k && (g.strategy == TM_AR || effective_path() == TM_PATH_DIRECT)) {
+    cudaError_t e = tmx::launch_direct(bufs, g.k, g.P, g.strategy == TM_ASA16, g.status, s);
+    return e == cudaSuccess ? TM_OK : cuda_fail("launch_direct", e);
+  }
   if (g.strategy == TM_AR) {
-    if (g.nlocal == g.k) {
-      cudaError_t e = tmx::launch_local_allreduce(bufs, g.k, g.P, s);
-      return e == cudaSuccess ? TM_OK : cuda_fail("local_allreduce", e);
-    }
     if (!g.comm) return TM_E_NCCL;
     ncclResult_t r = g_nccl.AllReduce(bufs[0], bufs[0], (size_t)g.P, ncclFloat32, ncclAvg, g.comm, s);
     return r == ncclSuccess ? TM_OK : TM_E_NCCL;
@@ -407,6 +413,16 @@ int tm_layout(tm_layout_info* out) {
   out->wire_bytes = wire_bytes(g.strategy);
   out->lib_bytes = g.slab_bytes;
   out->epoch = g.epoch;
+  out->path = effective_path();
+  return TM_OK;
+}
+
+int tm_set_path(int path) {
+  std::lock_guard<std::mutex> lk(g_mu);
+  if (!g.inited) return TM_E_STATE;
+  if (path < TM_PATH_AUTO || path > TM_PATH_DIRECT) return TM_E_ARG;
+  if (path == TM_PATH_DIRECT && g.nlocal != g.k) return TM_E_ARG;
+  g.path = path;
   return TM_OK;
 }
 

@@ -21,6 +21,8 @@ STRATEGY = {"ar": TM_AR, "asa": TM_ASA, "asa16": TM_ASA16, "easgd": TM_EASGD}
 TM_OK, TM_E_ARG, TM_E_ALIGN, TM_E_STATE, TM_E_CUDA, TM_E_NCCL = 0, 1, 2, 3, 4, 5
 TM_E_MISMATCH, TM_E_TIMEOUT, TM_E_NONFINITE, TM_E_OVERFLOW16 = 6, 7, 8, 9
 TM_BIT_NONFINITE, TM_BIT_OVERFLOW16, TM_BIT_TIMEOUT = 1, 2, 4
+TM_PATH_AUTO, TM_PATH_STAGED, TM_PATH_DIRECT = 0, 1, 2
+PATH = {"auto": TM_PATH_AUTO, "staged": TM_PATH_STAGED, "direct": TM_PATH_DIRECT}
 TM_BLOB_BYTES = 512
 TM_MAX_RANKS = 8
 
@@ -42,7 +44,8 @@ class tm_layout_info(ctypes.Structure):
                 ("nlocal", ctypes.c_int32), ("strategy", ctypes.c_int32),
                 ("ctas_per_rank", ctypes.c_int32), ("threads", ctypes.c_int32),
                 ("sm_count", ctypes.c_int32), ("wire_bytes", ctypes.c_int32),
-                ("lib_bytes", ctypes.c_int64), ("epoch", ctypes.c_uint32)]
+                ("lib_bytes", ctypes.c_int64), ("epoch", ctypes.c_uint32),
+                ("path", ctypes.c_int32)]
 
 
 _lib = None
@@ -62,6 +65,7 @@ _SIGS = {
     "tm_exchange_status": (ctypes.c_int, [_P, ctypes.POINTER(ctypes.c_uint32)]),
     "tm_layout": (ctypes.c_int, [ctypes.POINTER(tm_layout_info)]),
     "tm_set_timeout_ns": (ctypes.c_int, [ctypes.c_uint64]),
+    "tm_set_path": (ctypes.c_int, [ctypes.c_int]),
     "tm_exchange_finalize": (ctypes.c_int, []),
     "tm_strerror": (ctypes.c_char_p, [ctypes.c_int]),
     "tm_cast_rn16": (ctypes.c_int, [_P, _P, ctypes.c_int64, _P]),
@@ -193,6 +197,10 @@ def tm_set_timeout_ns(ns):
     _check(lib().tm_set_timeout_ns(int(ns)), "tm_set_timeout_ns")
 
 
+def tm_set_path(path):
+    _check(lib().tm_set_path(PATH[path] if isinstance(path, str) else int(path)), "tm_set_path")
+
+
 def tm_exchange_finalize():
     _check(lib().tm_exchange_finalize(), "tm_exchange_finalize")
 
@@ -230,7 +238,7 @@ class Exchanger:
     """
 
     def __init__(self, nparams, strategy, rank=0, size=1, device=None, nlocal=None,
-                 group=None, timeout_s=None):
+                 group=None, timeout_s=None, path="auto"):
         if device is None:
             device = torch.cuda.current_device()
         nlocal = size if nlocal is None else nlocal
@@ -240,6 +248,8 @@ class Exchanger:
         tm_exchange_init(nparams, rank, size, device, nlocal, STRATEGY[strategy])
         if timeout_s is not None:
             tm_set_timeout_ns(int(timeout_s * 1e9))
+        if path != "auto":
+            tm_set_path(path)
         if nlocal != size:
             import torch.distributed as dist
             mine = tm_bootstrap_export()

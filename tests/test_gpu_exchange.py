@@ -20,12 +20,15 @@ pytestmark = pytest.mark.gpu
 SIZES = [1, 7, 8, 9, 255, 1024, 100003, 1_000_003]
 
 
-def run_group(X, strategy, reps=1):
+PATHS = ["staged", "direct"]
+
+
+def run_group(X, strategy, reps=1, path="auto"):
     """Exchange the k buffers X (numpy) through tm_exchange_group; returns the
     k results (numpy) and the status code."""
     k, P = len(X), X[0].shape[0]
     bufs = to_dev(X)
-    with tm.Exchanger(P, strategy, size=k, nlocal=k) as ex:
+    with tm.Exchanger(P, strategy, size=k, nlocal=k, path=path) as ex:
         for _ in range(reps):
             ex.exchange(bufs)
         code, bits = ex.status()
@@ -33,24 +36,26 @@ def run_group(X, strategy, reps=1):
     return out, code, bits
 
 
+@pytest.mark.parametrize("path", PATHS)
 @pytest.mark.parametrize("strategy", ["asa", "asa16"])
-@pytest.mark.parametrize("k", [2, 3, 4, 5, 8])
-def test_asa_family_bitwise_sizes(strategy, k):
+@pytest.mark.parametrize("k", [2, 3, 4, 5, 6, 7, 8])
+def test_asa_family_bitwise_sizes(strategy, k, path):
     for P in SIZES:
         X = worker_buffers(P, k, "D1", config=1)
-        out, code, _ = run_group(X, strategy)
+        out, code, _ = run_group(X, strategy, path=path)
         assert code == tm.TM_OK
         want = ox.exchange(X, strategy)
         for r in range(k):
             assert_bitwise(out[r], want[r], f"{strategy} k={k} P={P} rank {r}")
 
 
+@pytest.mark.parametrize("path", PATHS)
 @pytest.mark.parametrize("strategy", ["asa", "asa16"])
 @pytest.mark.parametrize("dist", DISTS)
-def test_asa_family_bitwise_distributions(strategy, dist):
+def test_asa_family_bitwise_distributions(strategy, dist, path):
     for k in (2, 8):
         X = worker_buffers(100003, k, dist, config=1)
-        out, code, _ = run_group(X, strategy)
+        out, code, _ = run_group(X, strategy, path=path)
         assert code == tm.TM_OK
         want = ox.exchange(X, strategy)
         for r in range(k):
@@ -71,11 +76,12 @@ def test_ar_single_process(k):
                 assert_bitwise(out[r], want[r], f"ar {dist} k={k} P={P}")  # ascending-rank kernel
 
 
-def test_ar_equals_asa_on_dyadics():
+@pytest.mark.parametrize("path", PATHS)
+def test_ar_equals_asa_on_dyadics(path):
     from paper_1605_08325_b200.inputs import dyadic_buffers
     X = dyadic_buffers(65537, 8)
     a, _, _ = run_group(X, "ar")
-    b, _, _ = run_group(X, "asa")
+    b, _, _ = run_group(X, "asa", path=path)
     mean = (np.sum(np.stack(X).astype(np.float64), axis=0) / 8).astype(np.float32)
     assert_bitwise(a[3], mean)
     assert_bitwise(b[5], mean)
@@ -84,7 +90,7 @@ def test_ar_equals_asa_on_dyadics():
 def test_repeated_exchanges_fresh_inputs():
     """Back-to-back exchanges reuse the staging across epochs (a7)."""
     k, P = 4, 300007
-    with tm.Exchanger(P, "asa16", size=k, nlocal=k) as ex:
+    with tm.Exchanger(P, "asa16", size=k, nlocal=k, path="staged") as ex:
         for it in range(4):
             X = worker_buffers(P, k, DISTS[it], config=30 + it)
             bufs = to_dev(X)
@@ -97,10 +103,11 @@ def test_repeated_exchanges_fresh_inputs():
         assert ex.layout()["epoch"] == 8
 
 
-def test_cross_rank_identity_and_status_clean():
+@pytest.mark.parametrize("path", PATHS)
+def test_cross_rank_identity_and_status_clean(path):
     X = worker_buffers(1_000_003, 8, "D2", config=3)
     for strategy in ("asa", "asa16", "ar"):
-        out, code, bits = run_group(X, strategy)
+        out, code, bits = run_group(X, strategy, path=path)
         assert code == tm.TM_OK and bits == 0
         for r in range(1, 8):
             assert_bitwise(out[r], out[0], strategy)
@@ -114,22 +121,25 @@ def test_k1_identity():
         assert_bitwise(out[0], X[0])
 
 
-def test_status_nonfinite_and_overflow():
-    k, P = 2, 4096
+@pytest.mark.parametrize("path", PATHS)
+def test_status_nonfinite_and_overflow(path):
+    k, P = 2, 4099
     X = worker_buffers(P, k, "D1", config=4)
     X[0][10] = np.float32(np.inf)
     X[1][20] = np.float32(70000.0)
-    out, code, bits = run_group(X, "asa16")
+    X[1][P - 1] = np.float32(-65520.0)  # scalar tail element of the direct path
+    out, code, bits = run_group(X, "asa16", path=path)
     assert bits == tm.TM_BIT_NONFINITE | tm.TM_BIT_OVERFLOW16
     assert code == tm.TM_E_OVERFLOW16
     assert np.isinf(out[0][10]) and np.isinf(out[1][20])  # IEEE: inf propagates
     ok = np.ones(P, bool)
-    ok[[10, 20]] = False
+    ok[[10, 20, P - 1]] = False
+    assert np.isinf(out[0][P - 1])
     want = ox.asa16_average(X)
     assert_bitwise(out[0][ok], want[0][ok])
     X = worker_buffers(P, k, "D1", config=4)
     X[1][5] = np.float32(np.nan)
-    _, code, bits = run_group(X, "asa")
+    _, code, bits = run_group(X, "asa", path=path)
     assert code == tm.TM_E_NONFINITE and bits == tm.TM_BIT_NONFINITE
 
 
@@ -150,6 +160,10 @@ def test_argument_errors():
         with pytest.raises(tm.TmError) as e:
             tm.tm_exchange_init(P, 0, 2, 0, 2, tm.TM_ASA)  # already initialised
         assert e.value.code == tm.TM_E_STATE
+        with pytest.raises(tm.TmError) as e:
+            tm.tm_set_path(7)
+        assert e.value.code == tm.TM_E_ARG
+        assert tm.tm_layout()["path"] == tm.TM_PATH_DIRECT  # auto, single process
     with pytest.raises(tm.TmError):
         tm.tm_exchange_init(0, 0, 2, 0, 2, tm.TM_ASA)
     with pytest.raises(tm.TmError):
@@ -168,8 +182,9 @@ def test_layout_segments():
             assert lay["wire_bytes"] == 2
 
 
+@pytest.mark.parametrize("path", PATHS)
 @pytest.mark.parametrize("P", [WORKLOADS["googlenet"], WORKLOADS["alexnet"]])
-def test_full_size_sampled(P):
+def test_full_size_sampled(P, path):
     """BASELINE sizes in the bench's launch configuration (k=8 group): sampled
     elements against the oracle's per-element definition, plus the tail."""
     k = 8
@@ -177,7 +192,7 @@ def test_full_size_sampled(P):
     for strategy, dist in (("asa16", "D2"), ("asa", "D1")):
         X = worker_buffers(P, k, dist, config=3)
         bufs = to_dev(X)
-        with tm.Exchanger(P, strategy, size=k, nlocal=k) as ex:
+        with tm.Exchanger(P, strategy, size=k, nlocal=k, path=path) as ex:
             ex.exchange(bufs)
             code, _ = ex.status()
         assert code == tm.TM_OK
