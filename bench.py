@@ -217,6 +217,7 @@ def roofline(strategy, P, k, path, ms, peak, peak_src, workload):
     kernel = "tm_exchange_kernel" if path == "staged" and strategy != "ar" else "tm_direct_kernel"
     return {"bound": "hbm", "achieved": ach, "peak": peak, "unit": "GB/s", "frac": ach / peak,
             "traffic": traffic_from_profiles(f"{workload}_{strategy}_k{k}_{path}"),
+            "traffic_unit": "bytes per launch (ncu dram read+write, profiles/ncu_traffic.json)",
             "algorithmic_bytes_per_launch": alg, "peak_source": peak_src, "kernel": kernel,
             "irreducible_frac": (8.0 * P * k / (ms * 1e-3) / 1e9) / peak}
 
@@ -224,7 +225,8 @@ def roofline(strategy, P, k, path, ms, peak, peak_src, workload):
 def traffic_from_profiles(workload_key):
     p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     try:
-        return json.load(open(p)).get(workload_key)
+        v = json.load(open(p)).get(workload_key)
+        return None if v is None else float(v)
     except Exception:
         return None
 
