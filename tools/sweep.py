@@ -1,0 +1,163 @@
+#!/usr/bin/env python
+"""One-GPU timing sweep over the BASELINE.json configs:
+
+  config 2  GoogLeNet 6,998,552      ASA, ASA16        k = 2, 4, 8   direct + staged
+  config 3  AlexNet   60,965,224     AR, ASA, ASA16    k = 2, 4, 8   direct + staged
+  config 4  EASGD 8 workers + centre, AlexNet size, alpha = 0.5/8:
+            8 serial exclusive updates / one fused arrival-order round /
+            8 concurrent updates (red.add) from 8 streams
+  config 5  message-size sweep 64 KB .. 1 GB (fp32 bytes per rank), ASA16, k = 2, 4, 8
+
+All ranks of an exchange live on this one GPU (single-process group), so every
+number is HBM-bound; the roofline is the measured HBM copy bandwidth.  Inputs are
+N(0, 0.01^2) drawn on the device (timing only; parity lives in tests/).
+Writes JSON lines to stdout and a markdown table to --md.
+"""
+
+import argparse
+import json
+import os
+import sys
+
+import torch
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+from paper_1605_08325_b200 import tm  # noqa: E402
+
+ALEXNET, GOOGLENET = 60_965_224, 6_998_552
+
+
+def peak():
+    try:
+        return float(json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"])
+    except Exception:
+        return 6650.0
+
+
+def timeit(fn, min_ms=60.0, warmup=5):
+    for _ in range(warmup):
+        fn()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    fn()
+    e1.record()
+    torch.cuda.synchronize()
+    one = max(e0.elapsed_time(e1), 1e-3)
+    n = max(5, min(2000, int(min_ms / one)))
+    e0.record()
+    for _ in range(n):
+        fn()
+    e1.record()
+    torch.cuda.synchronize()
+    return e0.elapsed_time(e1) / n
+
+
+def hbm_bytes(strategy, P, k, path):
+    if path == "direct" or strategy == "ar":
+        return 8.0 * P * k
+    return (14 + 2.0 / k) * P * k if strategy == "asa16" else (20 + 4.0 / k) * P * k
+
+
+def exchange_row(P, k, strategy, path, pk):
+    g = torch.Generator(device="cuda").manual_seed(1605)
+    bufs = [torch.randn(P, device="cuda", generator=g) * 0.01 for _ in range(k)]
+    with tm.Exchanger(P, strategy, size=k, nlocal=k, path=path) as ex:
+        ms = timeit(lambda: ex.exchange(bufs))
+        code, _ = ex.status()
+    alg = hbm_bytes(strategy, P, k, path)
+    row = {"P": P, "k": k, "strategy": strategy, "path": path if strategy != "ar" else "direct",
+           "us": ms * 1e3, "algbw_GBps": 4.0 * P * k / (ms * 1e-3) / 1e9,
+           "hbm_GBps": alg / (ms * 1e-3) / 1e9, "frac": alg / (ms * 1e-3) / 1e9 / pk, "status": code}
+    del bufs
+    torch.cuda.empty_cache()
+    return row
+
+
+def easgd_rows(P, nw, alpha, pk):
+    g = torch.Generator(device="cuda").manual_seed(8325)
+    W = [torch.randn(P, device="cuda", generator=g) * 0.01 for _ in range(nw)]
+    c = torch.randn(P, device="cuda", generator=g) * 0.01
+    rows = []
+
+    def serial():
+        for w in W:
+            tm.tm_easgd_update_ex(w, c, alpha)
+    ms = timeit(serial)
+    rows.append({"mode": f"{nw} serial exclusive updates", "us": ms * 1e3,
+                 "hbm_GBps": 16.0 * P * nw / (ms * 1e-3) / 1e9})
+    order = list(range(nw))
+    ms = timeit(lambda: tm.tm_easgd_round(W, order, c, alpha))
+    rows.append({"mode": f"fused round, arrival order of {nw}", "us": ms * 1e3,
+                 "hbm_GBps": (8.0 * P * nw + 8.0 * P) / (ms * 1e-3) / 1e9})
+    streams = [torch.cuda.Stream() for _ in range(nw)]
+
+    def concurrent():
+        cur = torch.cuda.current_stream()
+        ev = torch.cuda.Event()
+        ev.record(cur)
+        for w, s in zip(W, streams):
+            s.wait_event(ev)
+            tm.tm_easgd_update_ex(w, c, alpha, concurrent=True, stream=s)
+        for s in streams:
+            cur.wait_stream(s)
+    ms = timeit(concurrent)
+    rows.append({"mode": f"{nw} concurrent updates (red.add, {nw} streams)", "us": ms * 1e3,
+                 "hbm_GBps": 16.0 * P * nw / (ms * 1e-3) / 1e9})
+    for r in rows:
+        r["frac"] = r["hbm_GBps"] / pk
+        r["P"] = P
+    return rows
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--md", default=None)
+    ap.add_argument("--quick", action="store_true")
+    a = ap.parse_args()
+    torch.cuda.set_device(0)
+    pk = peak()
+    out = {"config2": [], "config3": [], "config4": [], "config5": []}
+    ks = (2, 4, 8)
+    for strategy in ("asa", "asa16"):
+        for k in ks:
+            for path in ("direct", "staged"):
+                out["config2"].append(exchange_row(GOOGLENET, k, strategy, path, pk))
+    for strategy in ("ar", "asa", "asa16"):
+        for k in ks:
+            for path in (("direct",) if strategy == "ar" else ("direct", "staged")):
+                out["config3"].append(exchange_row(ALEXNET, k, strategy, path, pk))
+    out["config4"] = easgd_rows(ALEXNET, 8, 0.5 / 8, pk)
+    sizes = [1 << e for e in range(16, 31, 2 if a.quick else 1)]
+    for nbytes in sizes:
+        P = nbytes // 4
+        for k in ks:
+            if P * k * 4 > 24 * (1 << 30):
+                continue
+            for path in ("direct", "staged"):
+                out["config5"].append(exchange_row(P, k, "asa16", path, pk))
+    for key, rows in out.items():
+        for r in rows:
+            print(json.dumps({"config": key, **r}))
+    if a.md:
+        with open(a.md, "w") as f:
+            f.write(f"# One-GPU sweep (measured HBM peak {pk:.0f} GB/s)\n\n")
+            f.write("frac = algorithmic HBM bytes / time / peak. Direct path: 8 B per element "
+                    "per rank; staged: (14 + 2/k) B (ASA16), (20 + 4/k) B (ASA).\n\n")
+            for key in ("config2", "config3", "config5"):
+                f.write(f"## {key}\n\n| P | k | strategy | path | µs | algbw GB/s | HBM GB/s | frac |\n"
+                        "|---|---|---|---|---|---|---|---|\n")
+                for r in out[key]:
+                    f.write(f"| {r['P']:,} | {r['k']} | {r['strategy']} | {r['path']} | {r['us']:.1f} | "
+                            f"{r['algbw_GBps']:.0f} | {r['hbm_GBps']:.0f} | {r['frac']:.3f} |\n")
+                f.write("\n")
+            f.write("## config4 (EASGD, 8 workers + centre, P = 60,965,224, alpha = 0.5/8)\n\n"
+                    "| mode | µs | HBM GB/s | frac |\n|---|---|---|---|\n")
+            for r in out["config4"]:
+                f.write(f"| {r['mode']} | {r['us']:.1f} | {r['hbm_GBps']:.0f} | {r['frac']:.3f} |\n")
+
+
+if __name__ == "__main__":
+    main()
