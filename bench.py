@@ -135,6 +135,21 @@ class ClockSampler:
 
 # ----------------------------------------------------------------- reference arm
 
+def reduce_max(value, device):
+    """Max over ranks of a per-rank time (device-timed), the contract's job time.
+    `device` is where the collective runs: cuda for NCCL, cpu for gloo."""
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([float(value)], dtype=torch.float64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def job_value(bytes_per_rank, nranks, ms):
+    """Whole-job algorithm bandwidth: every rank's fp32 buffer, over the max time."""
+    return bytes_per_rank * nranks / (ms * 1e-3) / 1e9
+
+
 def workload_name(args, k, multi):
     return f"{args.workload}_{args.strategy}_k{k}" + ("" if multi else "_one_gpu")
 
@@ -298,13 +313,11 @@ def main():
         torch.cuda.synchronize()
     ms = e0.elapsed_time(e1) / args.steps
     if multi:
-        t = torch.tensor([ms], device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms = float(t.item())
+        ms = reduce_max(ms, dev)
     code, bits = ex.status()
 
     bytes_alg = 4.0 * P * k  # every rank's fp32 buffer is averaged
-    value = bytes_alg / (ms * 1e-3) / 1e9
+    value = job_value(4.0 * P, k, ms)
 
     # roofline of the dominant (only) kernel in the step
     peak, peak_src = hbm_peak()
@@ -353,9 +366,7 @@ def main():
         torch.cuda.synchronize()
         e2e_ms = f0.elapsed_time(f1) / args.e2e_steps
         if multi:
-            t = torch.tensor([e2e_ms], device=dev)
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            e2e_ms = float(t.item())
+            e2e_ms = reduce_max(e2e_ms, dev)
         e2e = {"value": bytes_alg / (e2e_ms * 1e-3) / 1e9, "unit": "GB/s", "ms_per_step": e2e_ms,
                "h2d_bytes_per_step": 4 * P * nlocal, "d2h_bytes_per_step": 4 * P}
 

@@ -14,9 +14,10 @@ constexpr int kVec = 8;             // elements per vector unit (16 B of fp16)
 constexpr int64_t kAlign = 256;     // segment / chunk alignment in elements
 constexpr int64_t kMinChunk = 2048; // smallest per-CTA chunk worth a barrier
 
-// Flag pad of one rank: u32 flags[kPhases][TM_MAX_RANKS][C]; slot
-// [phase][src][c] is written by rank `src` (remote store) and spun on by the
-// owner of the pad.
+// Flag pad of one rank: u32 flags[kPhases][TM_MAX_RANKS][C] followed by the
+// per-CTA epoch counters u32 ctr[C]; slot [phase][src][c] is written by rank
+// `src` (remote store) and spun on by the owner of the pad; ctr[c] is private
+// to CTA c of the owner.
 constexpr int kPhaseReady = 0;    // src finished its pre-cast of chunk c
 constexpr int kPhaseReduced = 1;  // src finished summing its segment's chunk c
 constexpr int kPhases = 2;
@@ -29,7 +30,6 @@ struct ExchangeArgs {
   uint32_t* status;               // sticky status word (local)
   int64_t P, L, Lc;               // params, segment length, per-CTA chunk length
   int32_t k, rank0, C;            // ranks, first local rank, CTAs per rank
-  uint32_t epoch;
   uint64_t timeout_ns;
 };
 

@@ -180,16 +180,16 @@ struct Unit<false> {
 // Returns false (whole CTA) if a peer timed out.
 template <int K>
 __device__ __forceinline__ bool rank_barrier(const ExchangeArgs& a, int phase, int r, int c,
-                                             int* s_abort) {
+                                             uint32_t epoch, int* s_abort) {
   __syncthreads();
   if (threadIdx.x < K) {
     const int j = threadIdx.x;
     uint32_t* remote = a.flags[j] + (size_t)(phase * TM_MAX_RANKS + r) * a.C + c;
-    st_release_sys(remote, a.epoch);
+    st_release_sys(remote, epoch);
     const uint32_t* mine = a.flags[r] + (size_t)(phase * TM_MAX_RANKS + j) * a.C + c;
-    if ((int32_t)(ld_acquire_sys(mine) - a.epoch) < 0) {
+    if ((int32_t)(ld_acquire_sys(mine) - epoch) < 0) {
       const uint64_t t0 = globaltimer();
-      while ((int32_t)(ld_acquire_sys(mine) - a.epoch) < 0) {
+      while ((int32_t)(ld_acquire_sys(mine) - epoch) < 0) {
         if (globaltimer() - t0 > a.timeout_ns) {
           atomicOr(a.status, TM_BIT_TIMEOUT);
           *s_abort = 1;
@@ -210,11 +210,24 @@ tm_exchange_kernel(const __grid_constant__ ExchangeArgs a) {
   constexpr int E = U::kElems;
   constexpr int WB = W16 ? 2 : 4;  // wire bytes per element
   __shared__ int s_abort;
-  if (threadIdx.x == 0) s_abort = 0;
+  __shared__ uint32_t s_epoch;
 
   const int lr = blockIdx.x / a.C;
   const int c = blockIdx.x - lr * a.C;
   const int r = a.rank0 + lr;
+  // Device-side epoch: CTA c of rank r owns counter ctr[c] in its own flag pad
+  // (after the [kPhases][TM_MAX_RANKS][C] slots).  Every rank performs the same
+  // sequence of exchanges, so the counters advance in lockstep; keeping the
+  // epoch on the device leaves the launch parameters constant across calls,
+  // which makes the exchange capturable in a CUDA graph.
+  if (threadIdx.x == 0) {
+    s_abort = 0;
+    uint32_t* ctr = a.flags[r] + (size_t)kPhases * TM_MAX_RANKS * a.C + c;
+    s_epoch = *ctr + 1;
+    *ctr = s_epoch;
+  }
+  __syncthreads();
+  const uint32_t epoch = s_epoch;
   float* __restrict__ x = a.x[lr];
   const int64_t P = a.P, L = a.L;
   const int64_t e0 = (int64_t)c * a.Lc;
@@ -259,7 +272,7 @@ tm_exchange_kernel(const __grid_constant__ ExchangeArgs a) {
   }
   if (st) atomicOr(a.status, st);  // rare: only threads that saw a bad value
 
-  if (!rank_barrier<K>(a, kPhaseReady, r, c, &s_abort)) return;
+  if (!rank_barrier<K>(a, kPhaseReady, r, c, epoch, &s_abort)) return;
 
   // ---------------- a4: reduce-scatter pull, fused sum / (1/k) / cast -------
   {
@@ -287,7 +300,7 @@ tm_exchange_kernel(const __grid_constant__ ExchangeArgs a) {
     }
   }
 
-  if (!rank_barrier<K>(a, kPhaseReduced, r, c, &s_abort)) return;
+  if (!rank_barrier<K>(a, kPhaseReduced, r, c, epoch, &s_abort)) return;
 
   // ---------------- a6: allgather pull, fused widen, store to caller ---------
   {
@@ -652,6 +665,51 @@ easgd_round_kernel(const __grid_constant__ RoundArgs ra, float* c, int64_t n, fl
   }
 }
 
+// Arrival order with N DISTINCT workers (the common round: each worker once):
+// all N worker loads are issued before the dependent chain of centre updates,
+// so N + 1 independent 16-byte loads are in flight per thread.  `wo` holds the
+// workers' pointers already in arrival order.
+struct OrderedWorkers {
+  float* wo[8];
+};
+
+template <int N>
+__global__ void __launch_bounds__(kThreads)
+easgd_round_distinct_kernel(const __grid_constant__ OrderedWorkers ow, float* c, int64_t n,
+                            float alpha) {
+  const int64_t stride = (int64_t)gridDim.x * kThreads;
+  const int64_t tid = (int64_t)blockIdx.x * kThreads + threadIdx.x;
+  const int64_t nv = n / 4;
+  for (int64_t v = tid; v < nv; v += stride) {
+    float4 cv = ld16_f(c + v * 4);
+    float4 xv[N];
+#pragma unroll
+    for (int t = 0; t < N; ++t) xv[t] = ld16_f(ow.wo[t] + v * 4);
+#pragma unroll
+    for (int t = 0; t < N; ++t) {
+      const float ex = elastic_diff(xv[t].x, cv.x, alpha), ey = elastic_diff(xv[t].y, cv.y, alpha);
+      const float ez = elastic_diff(xv[t].z, cv.z, alpha), ew = elastic_diff(xv[t].w, cv.w, alpha);
+      xv[t].x = __fsub_rn(xv[t].x, ex); xv[t].y = __fsub_rn(xv[t].y, ey);
+      xv[t].z = __fsub_rn(xv[t].z, ez); xv[t].w = __fsub_rn(xv[t].w, ew);
+      cv.x = __fadd_rn(cv.x, ex); cv.y = __fadd_rn(cv.y, ey);
+      cv.z = __fadd_rn(cv.z, ez); cv.w = __fadd_rn(cv.w, ew);
+      st16_f(ow.wo[t] + v * 4, xv[t]);
+    }
+    st16_f(c + v * 4, cv);
+  }
+  for (int64_t i = nv * 4 + tid; i < n; i += stride) {  // tail, scalar
+    float ci = c[i];
+#pragma unroll
+    for (int t = 0; t < N; ++t) {
+      const float xi = ow.wo[t][i];
+      const float e = elastic_diff(xi, ci, alpha);
+      ow.wo[t][i] = __fsub_rn(xi, e);
+      ci = __fadd_rn(ci, e);
+    }
+    c[i] = ci;
+  }
+}
+
 __global__ void __launch_bounds__(kThreads)
 cast_rn16_kernel(const float* __restrict__ in, uint16_t* __restrict__ out, int64_t n) {
   const int64_t stride = (int64_t)gridDim.x * kThreads;
@@ -815,6 +873,22 @@ cudaError_t launch_easgd_round(float* const* w, int nw, const int32_t* order, in
   }
   ra.norder = norder;
   const int vec = (align & 15) == 0;
+  bool distinct = norder >= 1 && norder <= 8;
+  for (int t = 0; distinct && t < norder; ++t)
+    for (int u = 0; u < t; ++u)
+      if (order[u] == order[t]) distinct = false;
+  if (vec && distinct) {
+    OrderedWorkers ow{};
+    for (int t = 0; t < norder; ++t) ow.wo[t] = w[order[t]];
+    const int grid = streaming_grid(n / 4 + 4);
+    switch (norder) {
+#define TM_RD(N) \
+  case N: easgd_round_distinct_kernel<N><<<grid, kThreads, 0, s>>>(ow, c, n, alpha); break;
+      TM_RD(1) TM_RD(2) TM_RD(3) TM_RD(4) TM_RD(5) TM_RD(6) TM_RD(7) TM_RD(8)
+#undef TM_RD
+    }
+    return cudaGetLastError();
+  }
   const int grid = streaming_grid(vec ? n / 4 + 4 : n);
   easgd_round_kernel<<<grid, kThreads, 0, s>>>(ra, c, n, alpha, vec);
   return cudaGetLastError();

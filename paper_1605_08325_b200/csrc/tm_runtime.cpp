@@ -132,7 +132,6 @@ ExchangeArgs make_args(float* const* bufs) {
   a.k = g.k;
   a.rank0 = g.rank0;
   a.C = g.C;
-  a.epoch = g.epoch;
   a.timeout_ns = g.timeout_ns;
   return a;
 }
@@ -160,13 +159,10 @@ int do_exchange(float* const* bufs, int nbufs, cudaStream_t s) {
     ncclResult_t r = g_nccl.AllReduce(bufs[0], bufs[0], (size_t)g.P, ncclFloat32, ncclAvg, g.comm, s);
     return r == ncclSuccess ? TM_OK : TM_E_NCCL;
   }
-  ++g.epoch;
   ExchangeArgs a = make_args(bufs);
   cudaError_t e = tmx::launch_exchange(a, g.nlocal, wire16(g.strategy), s);
-  if (e != cudaSuccess) {
-    --g.epoch;
-    return cuda_fail("launch_exchange", e);
-  }
+  if (e != cudaSuccess) return cuda_fail("launch_exchange", e);
+  ++g.epoch;  // host-side count for tm_layout; the kernels keep their own
   return TM_OK;
 }
 
@@ -212,7 +208,7 @@ int tm_exchange_init(int64_t nparams, const tm_world* world, int strategy) {
     c.off_stage = 0;
     c.off_avg = round_up(c.off_stage + (int64_t)k * c.L * wb, 256);
     c.off_flags = round_up(c.off_avg + c.L * wb, 256);
-    c.rank_stride = round_up(c.off_flags + (int64_t)tmx::kPhases * TM_MAX_RANKS * c.C * 4, 4096);
+    c.rank_stride = round_up(c.off_flags + ((int64_t)tmx::kPhases * TM_MAX_RANKS + 1) * c.C * 4, 4096);
   } else if (strategy == TM_EASGD) {
     c.off_center = 0;
     c.rank_stride = round_up(nparams * 4, 4096);

@@ -227,6 +227,19 @@ def device_view(ptr, n, device=None):
 
 # ------------------------------------------------------------ convenience
 
+def gather_blobs(mine, nprocs, group=None):
+    """All-gather this process's bootstrap blob over torch.distributed; returns
+    the nprocs blobs in process (rank) order, as tm_bootstrap_import expects."""
+    import torch.distributed as dist
+    if dist.get_world_size(group) != nprocs:
+        raise ValueError(f"process group has {dist.get_world_size(group)} ranks, expected {nprocs}")
+    blobs = [None] * nprocs
+    dist.all_gather_object(blobs, bytes(mine), group=group)
+    if any(len(b) != len(blobs[0]) for b in blobs):
+        raise ValueError("bootstrap blobs differ in length")
+    return blobs
+
+
 class Exchanger:
     """Process-global exchanger.
 
@@ -251,11 +264,7 @@ class Exchanger:
         if path != "auto":
             tm_set_path(path)
         if nlocal != size:
-            import torch.distributed as dist
-            mine = tm_bootstrap_export()
-            blobs = [None] * (size // nlocal)
-            dist.all_gather_object(blobs, mine, group=group)
-            tm_bootstrap_import(blobs)
+            tm_bootstrap_import(gather_blobs(tm_bootstrap_export(), size // nlocal, group))
 
     def exchange(self, bufs, stream=None):
         if isinstance(bufs, torch.Tensor):

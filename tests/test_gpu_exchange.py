@@ -225,3 +225,30 @@ def test_device_rn16_exhaustive():
         assert np.all((h[nan] & 0x7C00) == 0x7C00) and np.all((h[nan] & 0x3FF) != 0)
         sub = slice(None, None, 4099)
         assert np.array_equal(h[sub][~nan[sub]], rn16(xn[sub])[~nan[sub]]), start
+
+
+@pytest.mark.parametrize("strategy", ["asa16", "asa", "ar"])
+@pytest.mark.parametrize("path", PATHS)
+def test_cuda_graph_capture_and_replay(strategy, path):
+    """The exchange captured once in a CUDA graph and replayed on fresh inputs
+    (the staged kernel keeps its epochs on the device, so its launch parameters
+    are constant)."""
+    k, P = 4, 300_007
+    bufs = to_dev(worker_buffers(P, k, "D2", config=60))
+    with tm.Exchanger(P, strategy, size=k, nlocal=k, path=path) as ex:
+        ex.exchange(bufs)  # warm-up outside capture
+        torch.cuda.synchronize()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            ex.exchange(bufs)
+        for it in range(3):
+            X = worker_buffers(P, k, DISTS[it], config=61 + it)
+            for b, x in zip(bufs, X):
+                b.copy_(torch.from_numpy(x))
+            g.replay()
+            out = to_host(bufs)
+            want = ox.exchange(X, strategy)
+            for r in range(k):
+                assert_bitwise(out[r], want[r], f"{strategy} {path} replay {it} rank {r}")
+        code, _ = ex.status()
+        assert code == tm.TM_OK
