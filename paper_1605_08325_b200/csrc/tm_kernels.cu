@@ -65,6 +65,28 @@ __device__ __forceinline__ uint32_t ld_acquire_sys(const uint32_t* p) {
   return v;
 }
 
+// GPU-scope versions: enough when every rank of the exchange runs on this GPU
+// (a single-process group), where system scope would only add fence cost.
+__device__ __forceinline__ void st_release_gpu(uint32_t* p, uint32_t v) {
+  asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ uint32_t ld_acquire_gpu(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+template <bool SYS>
+__device__ __forceinline__ void st_release(uint32_t* p, uint32_t v) {
+  if constexpr (SYS) st_release_sys(p, v);
+  else st_release_gpu(p, v);
+}
+template <bool SYS>
+__device__ __forceinline__ uint32_t ld_acquire(const uint32_t* p) {
+  if constexpr (SYS) return ld_acquire_sys(p);
+  else return ld_acquire_gpu(p);
+}
+
 // 16-byte accesses.  Peer / staging data is written during the same kernel by
 // other SMs or GPUs, so the non-coherent (.nc) path is never used for it; .cg
 // caches in L2 only.
@@ -178,18 +200,18 @@ struct Unit<false> {
 
 // Cross-rank, per-CTA epoch barrier (see the protocol in the file header).
 // Returns false (whole CTA) if a peer timed out.
-template <int K>
+template <int K, bool SYS>
 __device__ __forceinline__ bool rank_barrier(const ExchangeArgs& a, int phase, int r, int c,
                                              uint32_t epoch, int* s_abort) {
   __syncthreads();
   if (threadIdx.x < K) {
     const int j = threadIdx.x;
     uint32_t* remote = a.flags[j] + (size_t)(phase * TM_MAX_RANKS + r) * a.C + c;
-    st_release_sys(remote, epoch);
+    st_release<SYS>(remote, epoch);
     const uint32_t* mine = a.flags[r] + (size_t)(phase * TM_MAX_RANKS + j) * a.C + c;
-    if ((int32_t)(ld_acquire_sys(mine) - epoch) < 0) {
+    if ((int32_t)(ld_acquire<SYS>(mine) - epoch) < 0) {
       const uint64_t t0 = globaltimer();
-      while ((int32_t)(ld_acquire_sys(mine) - epoch) < 0) {
+      while ((int32_t)(ld_acquire<SYS>(mine) - epoch) < 0) {
         if (globaltimer() - t0 > a.timeout_ns) {
           atomicOr(a.status, TM_BIT_TIMEOUT);
           *s_abort = 1;
@@ -203,7 +225,7 @@ __device__ __forceinline__ bool rank_barrier(const ExchangeArgs& a, int phase, i
   return *s_abort == 0;
 }
 
-template <int K, bool W16>
+template <int K, bool W16, bool SYS>
 __global__ void __launch_bounds__(kThreads, K == 6 ? 3 : 4)
 tm_exchange_kernel(const __grid_constant__ ExchangeArgs a) {
   using U = Unit<W16>;
@@ -272,7 +294,7 @@ tm_exchange_kernel(const __grid_constant__ ExchangeArgs a) {
   }
   if (st) atomicOr(a.status, st);  // rare: only threads that saw a bad value
 
-  if (!rank_barrier<K>(a, kPhaseReady, r, c, epoch, &s_abort)) return;
+  if (!rank_barrier<K, SYS>(a, kPhaseReady, r, c, epoch, &s_abort)) return;
 
   // ---------------- a4: reduce-scatter pull, fused sum / (1/k) / cast -------
   {
@@ -300,7 +322,7 @@ tm_exchange_kernel(const __grid_constant__ ExchangeArgs a) {
     }
   }
 
-  if (!rank_barrier<K>(a, kPhaseReduced, r, c, epoch, &s_abort)) return;
+  if (!rank_barrier<K, SYS>(a, kPhaseReduced, r, c, epoch, &s_abort)) return;
 
   // ---------------- a6: allgather pull, fused widen, store to caller ---------
   {
@@ -720,19 +742,20 @@ cast_rn16_kernel(const float* __restrict__ in, uint16_t* __restrict__ out, int64
 }
 
 template <int K, bool W16>
-const void* exchange_fn() {
-  return reinterpret_cast<const void*>(&tm_exchange_kernel<K, W16>);
+const void* exchange_fn(bool sys) {
+  return sys ? reinterpret_cast<const void*>(&tm_exchange_kernel<K, W16, true>)
+             : reinterpret_cast<const void*>(&tm_exchange_kernel<K, W16, false>);
 }
 
-const void* pick_exchange(int k, bool w16) {
+const void* pick_exchange(int k, bool w16, bool sys) {
   switch (k) {
-    case 2: return w16 ? exchange_fn<2, true>() : exchange_fn<2, false>();
-    case 3: return w16 ? exchange_fn<3, true>() : exchange_fn<3, false>();
-    case 4: return w16 ? exchange_fn<4, true>() : exchange_fn<4, false>();
-    case 5: return w16 ? exchange_fn<5, true>() : exchange_fn<5, false>();
-    case 6: return w16 ? exchange_fn<6, true>() : exchange_fn<6, false>();
-    case 7: return w16 ? exchange_fn<7, true>() : exchange_fn<7, false>();
-    case 8: return w16 ? exchange_fn<8, true>() : exchange_fn<8, false>();
+    case 2: return w16 ? exchange_fn<2, true>(sys) : exchange_fn<2, false>(sys);
+    case 3: return w16 ? exchange_fn<3, true>(sys) : exchange_fn<3, false>(sys);
+    case 4: return w16 ? exchange_fn<4, true>(sys) : exchange_fn<4, false>(sys);
+    case 5: return w16 ? exchange_fn<5, true>(sys) : exchange_fn<5, false>(sys);
+    case 6: return w16 ? exchange_fn<6, true>(sys) : exchange_fn<6, false>(sys);
+    case 7: return w16 ? exchange_fn<7, true>(sys) : exchange_fn<7, false>(sys);
+    case 8: return w16 ? exchange_fn<8, true>(sys) : exchange_fn<8, false>(sys);
     default: return nullptr;
   }
 }
@@ -746,7 +769,7 @@ int sm_count(int device) {
 }  // namespace
 
 int exchange_max_ctas(int device, bool wire16, int k) {
-  const void* fn = pick_exchange(k, wire16);
+  const void* fn = pick_exchange(k, wire16, true);
   if (!fn) return 0;
   int per_sm = 0;
   if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, kThreads, 0) != cudaSuccess)
@@ -757,7 +780,9 @@ int exchange_max_ctas(int device, bool wire16, int k) {
 int grid_for_streaming(int device) { return 4 * sm_count(device); }
 
 cudaError_t launch_exchange(const ExchangeArgs& a, int nlocal, bool wire16, cudaStream_t s) {
-  const void* fn = pick_exchange(a.k, wire16);
+  // System-scope flags only when some peer rank lives in another process
+  // (another GPU, over NVLink); a single-process group syncs at GPU scope.
+  const void* fn = pick_exchange(a.k, wire16, nlocal != a.k);
   if (!fn) return cudaErrorInvalidValue;
   void* params[] = {const_cast<ExchangeArgs*>(&a)};
   // Cooperative launch: guarantees every CTA is co-resident, which the
