@@ -185,9 +185,20 @@ int tm_easgd_update_ex(float* worker_buf, float* center_buf, int64_t n, float al
 int tm_easgd_round(float* const* workers, int nworkers, const int32_t* order, int norder,
                    float* center_buf, int64_t n, float alpha, void* stream);
 
-/* Library-owned EASGD centre (strategy TM_EASGD) of owner_rank, as a pointer
- * usable on this device (local or IPC-mapped over NVLink). */
+/* EASGD context (strategy TM_EASGD): the centre x~ is SHARDED by segment
+ * (SURVEY 8(e)): rank s hosts c[s*L, min((s+1)*L, P)) (L = seg_len of
+ * tm_layout), so k workers updating it spread the traffic over all k GPUs'
+ * NVLink ports instead of funnelling it into one server GPU.
+ * tm_easgd_center returns owner_rank's shard as a pointer usable on this device
+ * (local, or IPC-mapped over NVLink); its length is max(0, min(L, P - owner*L)). */
 int tm_easgd_center(int owner_rank, float** center);
+
+/* One elastic update (as tm_easgd_update) of this worker's full fp32[nparams]
+ * buffer against the sharded centre: element i meets the shard of rank i / L.
+ * concurrent == 0: the caller serialises the workers (bitwise equal to the
+ * oracle's arrival order); concurrent != 0: centre += e by atomic add (system
+ * scope across processes), no lost updates, order not fixed. */
+int tm_easgd_update_sharded(float* worker_buf, float alpha, int concurrent, void* stream);
 
 /* Synchronise `stream`, then return the most severe sticky status
  * (TM_E_TIMEOUT > TM_E_OVERFLOW16 > TM_E_NONFINITE > TM_OK) and clear it.

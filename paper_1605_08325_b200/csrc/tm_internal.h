@@ -49,6 +49,15 @@ cudaError_t launch_easgd(float* x, float* c, int64_t n, float alpha, bool concur
                          cudaStream_t s);
 cudaError_t launch_easgd_round(float* const* w, int nw, const int32_t* order, int norder,
                                float* c, int64_t n, float alpha, cudaStream_t s);
+// EASGD against a centre sharded by segment: shard[s] holds c[s*L, (s+1)*L).
+struct ShardArgs {
+  float* shard[TM_MAX_RANKS];
+  int32_t k;
+  int64_t L, P;
+  bool sys;
+};
+cudaError_t launch_easgd_sharded(float* x, const ShardArgs& sa, float alpha, bool concurrent,
+                                 cudaStream_t s);
 cudaError_t launch_cast_rn16(const float* in, uint16_t* out, int64_t n, cudaStream_t s);
 
 // Max co-resident CTAs of the exchange kernel on `device` (occupancy * SMs).

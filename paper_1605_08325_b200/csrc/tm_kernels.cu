@@ -638,6 +638,56 @@ easgd_kernel(float* __restrict__ x, float* c, int64_t n, float alpha, int vec) {
   }
 }
 
+// Elastic update against a centre sharded by segment: element i
+// of segment s = i / L lives at shard[s][i - s*L], local or on peer s over NVLink.
+// Segments are multiples of 256 elements, so a 16-byte vector never straddles
+// two shards.  Concurrent mode: c += e by red.add at system scope when the
+// shard may be on another GPU.
+__device__ __forceinline__ void red_add_gpu(float* p, float v) {
+  asm volatile("red.relaxed.gpu.global.add.f32 [%0], %1;" ::"l"(p), "f"(v) : "memory");
+}
+
+template <bool Concurrent, bool SYS>
+__global__ void __launch_bounds__(kThreads)
+easgd_sharded_kernel(float* __restrict__ x, const __grid_constant__ ShardArgs sa, float alpha) {
+  const int64_t stride = (int64_t)gridDim.x * kThreads;
+  const int64_t tid = (int64_t)blockIdx.x * kThreads + threadIdx.x;
+  for (int s = 0; s < sa.k; ++s) {
+    const int64_t base = (int64_t)s * sa.L;
+    const int64_t len = min(sa.L, sa.P - base);
+    if (len <= 0) break;
+    float* c = sa.shard[s];
+    float* xs = x + base;
+    const int64_t nv = len / 4;
+    for (int64_t v = tid; v < nv; v += stride) {
+      float4 xv = ld16_f(xs + v * 4);
+      float4 cv = __ldcg(reinterpret_cast<const float4*>(c + v * 4));
+      const float ex = elastic_diff(xv.x, cv.x, alpha), ey = elastic_diff(xv.y, cv.y, alpha);
+      const float ez = elastic_diff(xv.z, cv.z, alpha), ew = elastic_diff(xv.w, cv.w, alpha);
+      xv.x = __fsub_rn(xv.x, ex); xv.y = __fsub_rn(xv.y, ey);
+      xv.z = __fsub_rn(xv.z, ez); xv.w = __fsub_rn(xv.w, ew);
+      st16_f(xs + v * 4, xv);
+      if (Concurrent) {
+        float* cp = c + v * 4;
+        if (SYS) { red_add_sys(cp, ex); red_add_sys(cp + 1, ey); red_add_sys(cp + 2, ez); red_add_sys(cp + 3, ew); }
+        else { red_add_gpu(cp, ex); red_add_gpu(cp + 1, ey); red_add_gpu(cp + 2, ez); red_add_gpu(cp + 3, ew); }
+      } else {
+        cv.x = __fadd_rn(cv.x, ex); cv.y = __fadd_rn(cv.y, ey);
+        cv.z = __fadd_rn(cv.z, ez); cv.w = __fadd_rn(cv.w, ew);
+        __stcg(reinterpret_cast<float4*>(c + v * 4), cv);
+      }
+    }
+    for (int64_t i = nv * 4 + tid; i < len; i += stride) {  // segment tail (last segment only)
+      const float xi = xs[i];
+      const float ci = __ldcg(c + i);
+      const float e = elastic_diff(xi, ci, alpha);
+      xs[i] = __fsub_rn(xi, e);
+      if (Concurrent) { if (SYS) red_add_sys(c + i, e); else red_add_gpu(c + i, e); }
+      else c[i] = __fadd_rn(ci, e);
+    }
+  }
+}
+
 // A whole server round in arrival order, fused: the centre is read once and
 // written once; worker w's update uses the centre left by the previous one.
 // Bitwise equal to serial updates in `order` (each element is independent).
@@ -916,6 +966,18 @@ cudaError_t launch_easgd_round(float* const* w, int nw, const int32_t* order, in
   }
   const int grid = streaming_grid(vec ? n / 4 + 4 : n);
   easgd_round_kernel<<<grid, kThreads, 0, s>>>(ra, c, n, alpha, vec);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_easgd_sharded(float* x, const ShardArgs& sa, float alpha, bool concurrent,
+                                 cudaStream_t s) {
+  const int grid = streaming_grid(sa.L / 4 + 4);
+  if (concurrent) {
+    if (sa.sys) easgd_sharded_kernel<true, true><<<grid, kThreads, 0, s>>>(x, sa, alpha);
+    else easgd_sharded_kernel<true, false><<<grid, kThreads, 0, s>>>(x, sa, alpha);
+  } else {
+    easgd_sharded_kernel<false, false><<<grid, kThreads, 0, s>>>(x, sa, alpha);
+  }
   return cudaGetLastError();
 }
 

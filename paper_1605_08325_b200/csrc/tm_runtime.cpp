@@ -210,8 +210,9 @@ int tm_exchange_init(int64_t nparams, const tm_world* world, int strategy) {
     c.off_flags = round_up(c.off_avg + c.L * wb, 256);
     c.rank_stride = round_up(c.off_flags + ((int64_t)tmx::kPhases * TM_MAX_RANKS + 1) * c.C * 4, 4096);
   } else if (strategy == TM_EASGD) {
+    // Centre sharded by segment: rank s hosts c[s*L, min((s+1)*L, P)).
     c.off_center = 0;
-    c.rank_stride = round_up(nparams * 4, 4096);
+    c.rank_stride = round_up(c.L * 4, 4096);
   } else {
     c.rank_stride = 0;
   }
@@ -369,6 +370,27 @@ int tm_easgd_center(int owner_rank, float** center) {
   if (!center || owner_rank < 0 || owner_rank >= g.k) return TM_E_ARG;
   *center = reinterpret_cast<float*>(g.rank_base[owner_rank] + g.off_center);
   return TM_OK;
+}
+
+int tm_easgd_update_sharded(float* worker_buf, float alpha, int concurrent, void* stream) {
+  tmx::ShardArgs sa{};
+  {
+    std::lock_guard<std::mutex> lk(g_mu);
+    if (!g.inited || !g.ready || g.strategy != TM_EASGD) return TM_E_STATE;
+    if (!worker_buf) return TM_E_ARG;
+    if (!aligned16(worker_buf)) return TM_E_ALIGN;
+    for (int s = 0; s < g.k; ++s)
+      sa.shard[s] = reinterpret_cast<float*>(g.rank_base[s] + g.off_center);
+    sa.k = g.k;
+    sa.L = g.L;
+    sa.P = g.P;
+    // a remote shard needs system-scope atomics when peers live in other processes
+    sa.sys = g.nprocs > 1;
+    cudaSetDevice(g.device);
+  }
+  cudaError_t e = tmx::launch_easgd_sharded(worker_buf, sa, alpha, concurrent != 0,
+                                            static_cast<cudaStream_t>(stream));
+  return e == cudaSuccess ? TM_OK : cuda_fail("easgd_sharded", e);
 }
 
 int tm_exchange_status(void* stream, uint32_t* bits) {

@@ -62,6 +62,7 @@ _SIGS = {
     "tm_easgd_round": (ctypes.c_int, [ctypes.POINTER(_P), ctypes.c_int, ctypes.POINTER(ctypes.c_int32),
                                       ctypes.c_int, _P, ctypes.c_int64, ctypes.c_float, _P]),
     "tm_easgd_center": (ctypes.c_int, [ctypes.c_int, ctypes.POINTER(_P)]),
+    "tm_easgd_update_sharded": (ctypes.c_int, [_P, ctypes.c_float, ctypes.c_int, _P]),
     "tm_exchange_status": (ctypes.c_int, [_P, ctypes.POINTER(ctypes.c_uint32)]),
     "tm_layout": (ctypes.c_int, [ctypes.POINTER(tm_layout_info)]),
     "tm_set_timeout_ns": (ctypes.c_int, [ctypes.c_uint64]),
@@ -175,6 +176,12 @@ def tm_easgd_round(workers, order, center, alpha, stream=None):
                                 ctypes.c_float(alpha), _stream_handle(stream)), "tm_easgd_round")
 
 
+def tm_easgd_update_sharded(worker, alpha, concurrent=False, stream=None):
+    _check(lib().tm_easgd_update_sharded(_fp32_cuda(worker), ctypes.c_float(alpha),
+                                         int(bool(concurrent)), _stream_handle(stream)),
+           "tm_easgd_update_sharded")
+
+
 def tm_easgd_center(owner_rank):
     p = ctypes.c_void_p(0)
     _check(lib().tm_easgd_center(int(owner_rank), ctypes.byref(p)), "tm_easgd_center")
@@ -280,6 +287,12 @@ class Exchanger:
 
     def center(self, owner_rank=0):
         return tm_easgd_center(owner_rank)
+
+    def center_shard(self, owner_rank):
+        """owner_rank's centre shard as a torch tensor view (no copy)."""
+        L = self.layout()["seg_len"]
+        n = max(0, min(L, self.nparams - owner_rank * L))
+        return device_view(tm_easgd_center(owner_rank), n)
 
     def finalize(self):
         tm_exchange_finalize()

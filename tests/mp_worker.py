@@ -40,6 +40,31 @@ def main():
         json.dump(result, open(os.path.join(outdir, f"rank{rank}.json"), "w"))
         dist.barrier()
         return
+    if strategy == "easgd":
+        # sharded centre across processes: each rank fills its own shard, then the
+        # workers update the whole centre one at a time (rank order), remote
+        # shards through the IPC mapping.
+        c0 = worker_buffer(P, dist_name, 99, config=51)
+        L = ex.layout()["seg_len"]
+        mine = ex.center_shard(rank)
+        mine.copy_(torch.from_numpy(c0[rank * L: rank * L + mine.numel()]))
+        x = torch.from_numpy(worker_buffer(P, dist_name, rank, config=51)).cuda()
+        torch.cuda.synchronize()
+        for w in range(size):
+            dist.barrier()
+            if w == rank:
+                tm.tm_easgd_update_sharded(x, 0.3)
+                torch.cuda.synchronize()
+        dist.barrier()
+        shard = ex.center_shard(rank).cpu().numpy()
+        np.save(os.path.join(outdir, f"rank{rank}.npy"), x.cpu().numpy())
+        np.save(os.path.join(outdir, f"shard{rank}.npy"), shard)
+        result.update({"code": 0, "bits": 0, "seg_len": L})
+        json.dump(result, open(os.path.join(outdir, f"rank{rank}.json"), "w"))
+        dist.barrier()
+        ex.finalize()
+        dist.destroy_process_group()
+        return
     x = torch.from_numpy(worker_buffer(P, dist_name, rank, config=50)).cuda()
     reps = 3
     if mode == "skip1" and rank == 1:

@@ -109,3 +109,76 @@ def test_concurrent_workers_invariants():
     # the serial-order oracle's centre is within the reordering bound
     _, wc = easgd_sequence(W, c, alpha, list(range(nw)))
     assert np.max(np.abs(gc.astype(np.float64) - wc)) < 0.25
+
+
+def _sharded_setup(P, k, config):
+    W = [worker_buffer(P, "D1", r, config=config) for r in range(k)]
+    c0 = worker_buffer(P, "D1", 99, config=config)
+    return W, c0
+
+
+def _read_centre(ex, P, k):
+    return np.concatenate([ex.center_shard(s).cpu().numpy() for s in range(k)])[:P]
+
+
+@pytest.mark.parametrize("k,P", [(2, 1000), (4, 100_003), (8, 1_000_003), (3, 5)])
+def test_sharded_centre_serial_bitwise(k, P):
+    """Centre sharded by segment (rank s hosts c[s*L:(s+1)*L]); workers update
+    it one at a time in arrival order -> bitwise the oracle's sequence."""
+    W, c0 = _sharded_setup(P, k, 46)
+    order = [(3 * t + 1) % k for t in range(k)] + [0]
+    with tm.Exchanger(P, "easgd", size=k, nlocal=k) as ex:
+        L = ex.layout()["seg_len"]
+        for s in range(k):
+            sh = ex.center_shard(s)
+            if sh.numel():
+                sh.copy_(torch.from_numpy(c0[s * L: s * L + sh.numel()]))
+        Wd = to_dev(W)
+        for w in order:
+            tm.tm_easgd_update_sharded(Wd[w], 0.3)
+        gW = to_host(Wd)
+        gc = _read_centre(ex, P, k)
+    wW, wc = easgd_sequence(W, c0, 0.3, order)
+    assert_bitwise(gc, wc, "sharded centre")
+    for r in range(k):
+        assert_bitwise(gW[r], wW[r], f"worker {r}")
+
+
+def test_sharded_centre_concurrent():
+    """Concurrent mode on one stream equals the serial order; on k streams the
+    invariants hold (conservation of sum_w x_w + c)."""
+    k, P = 4, 262_147
+    W, c0 = _sharded_setup(P, k, 47)
+    alpha = 0.5 / k
+    with tm.Exchanger(P, "easgd", size=k, nlocal=k) as ex:
+        L = ex.layout()["seg_len"]
+        for s in range(k):
+            sh = ex.center_shard(s)
+            sh.copy_(torch.from_numpy(c0[s * L: s * L + sh.numel()]))
+        Wd = to_dev(W)
+        for w in range(k):
+            tm.tm_easgd_update_sharded(Wd[w], alpha, concurrent=True)
+        gW, gc = to_host(Wd), _read_centre(ex, P, k)
+        wW, wc = easgd_sequence(W, c0, alpha, list(range(k)))
+        assert_bitwise(gc, wc)
+        for r in range(k):
+            assert_bitwise(gW[r], wW[r])
+        # concurrent streams
+        streams = [torch.cuda.Stream() for _ in range(k)]
+        torch.cuda.synchronize()
+        for w, s in zip(Wd, streams):
+            tm.tm_easgd_update_sharded(w, alpha, concurrent=True, stream=s)
+        torch.cuda.synchronize()
+        gW2, gc2 = to_host(Wd), _read_centre(ex, P, k)
+    tot0 = sum(w.astype(np.float64) for w in gW) + gc
+    tot1 = sum(w.astype(np.float64) for w in gW2) + gc2
+    scale = sum(np.abs(w.astype(np.float64)) for w in gW2) + np.abs(gc2)
+    assert np.all(np.abs(tot1 - tot0) <= 2 * (k + 1) * 2.0 ** -24 * scale + 1e-30)
+
+
+def test_sharded_requires_easgd_context():
+    x = torch.zeros(1024, device="cuda")
+    with tm.Exchanger(1024, "asa16", size=2, nlocal=2):
+        with pytest.raises(tm.TmError) as e:
+            tm.tm_easgd_update_sharded(x, 0.5)
+        assert e.value.code == tm.TM_E_STATE

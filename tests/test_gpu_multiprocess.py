@@ -74,3 +74,19 @@ def test_multiprocess_mismatch_detected(tmp_path):
     """Ranks disagreeing on nparams fail the bootstrap with TM_E_MISMATCH."""
     res = launch(tmp_path, 2, "asa", 4096, "D1", mode="mismatch")
     assert any(r.get("init_error") == 6 for r in res), res
+
+
+def test_multiprocess_sharded_easgd(tmp_path):
+    """EASGD centre sharded across two processes; worker updates reach the peer's
+    shard through the IPC mapping; bitwise the oracle's serial order."""
+    from oracle.easgd import easgd_sequence
+    P, k = 100_003, 2
+    res = launch(tmp_path, k, "easgd", P, "D1")
+    W = [worker_buffer(P, "D1", r, config=51) for r in range(k)]
+    c0 = worker_buffer(P, "D1", 99, config=51)
+    wW, wc = easgd_sequence(W, c0, 0.3, [0, 1])
+    L = res[0]["seg_len"]
+    for r in range(k):
+        assert_bitwise(np.load(os.path.join(tmp_path, f"rank{r}.npy")), wW[r], f"worker {r}")
+        sh = np.load(os.path.join(tmp_path, f"shard{r}.npy"))
+        assert_bitwise(sh, wc[r * L: r * L + sh.shape[0]], f"shard {r}")

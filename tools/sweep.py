@@ -115,6 +115,17 @@ def easgd_rows(P, nw, alpha, pk):
     ms = timeit(concurrent)
     rows.append({"mode": f"{nw} concurrent updates (red.add, {nw} streams)", "us": ms * 1e3,
                  "hbm_GBps": 16.0 * P * nw / (ms * 1e-3) / 1e9})
+    del c
+    with tm.Exchanger(P, "easgd", size=nw, nlocal=nw) as ex:
+        for sidx in range(nw):
+            ex.center_shard(sidx).normal_(0, 0.01)
+
+        def sharded():
+            for w in W:
+                tm.tm_easgd_update_sharded(w, alpha)
+        ms = timeit(sharded, graph=True)
+        rows.append({"mode": f"{nw} serial updates, centre sharded by segment over {nw} ranks",
+                     "us": ms * 1e3, "hbm_GBps": 16.0 * P * nw / (ms * 1e-3) / 1e9})
     for r in rows:
         r["frac"] = r["hbm_GBps"] / pk
         r["P"] = P
