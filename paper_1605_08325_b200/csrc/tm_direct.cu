@@ -1,0 +1,272 @@
+// sm_100a kernels of the single-process ("direct") exchange path: all k ranks'
+// buffers on one device, one pass, no staging and no flags (include/tm.h,
+// TM_PATH_DIRECT).  PAPER L237-269 (ASA / ASA16), L233-237 (AR).
+#include <cuda_fp16.h>
+#include <stdint.h>
+#include <stdlib.h>
+
+#include <algorithm>
+
+#include "tm_device.cuh"
+#include "tm_internal.h"
+
+namespace tmx {
+namespace {
+using namespace dev;
+
+// ---------------------------------------------------------------------------
+// Single-process group, one pass ("direct" path).  When all k ranks' buffers
+// are addressable by one kernel there is no wire: the owner of each element
+// pulls the k contributions straight from the k buffers (the Alltoall leg),
+// applies the method's arithmetic in registers -- rn16 of every contribution
+// (ASA16, reading R1), ascending-rank fp32 sum from the rank-0 term, fl(s/k),
+// rn16 of the average -- and pushes widen(result) into all k buffers (the
+// Allgather leg).  Element i is read and written only by the thread that owns
+// it, so no flags are needed; the kernel boundary orders consecutive
+// exchanges.  Results are bitwise those of the staged path (elementwise
+// method, readings Q7/Q9).  Also AR for a single-process group (Q16 = false).
+// ---------------------------------------------------------------------------
+struct LocalBufs {
+  float* b[TM_MAX_RANKS];
+};
+
+// The method's arithmetic on 4 elements of k contributions (registers in, one
+// float4 out): rn16 of each contribution (Q16), ascending-rank sum from the
+// rank-0 term, fl(s/k), rn16 of the average.  `st` accumulates status bits.
+template <int K, bool Q16>
+__device__ __forceinline__ float4 average4(const float4 (&in)[K], uint32_t& st) {
+  // running max of |bits| screens for non-finite / fp16-overflow inputs
+  uint32_t m = max(max(__float_as_uint(in[0].x) & 0x7fffffffu, __float_as_uint(in[0].y) & 0x7fffffffu),
+                   max(__float_as_uint(in[0].z) & 0x7fffffffu, __float_as_uint(in[0].w) & 0x7fffffffu));
+  float4 s = Q16 ? q16(in[0]) : in[0];
+#pragma unroll
+  for (int j = 1; j < K; ++j) {
+    m = max(m, max(max(__float_as_uint(in[j].x) & 0x7fffffffu, __float_as_uint(in[j].y) & 0x7fffffffu),
+                   max(__float_as_uint(in[j].z) & 0x7fffffffu, __float_as_uint(in[j].w) & 0x7fffffffu)));
+    const float4 t = Q16 ? q16(in[j]) : in[j];
+    s.x = __fadd_rn(s.x, t.x); s.y = __fadd_rn(s.y, t.y);
+    s.z = __fadd_rn(s.z, t.z); s.w = __fadd_rn(s.w, t.w);
+  }
+  if (m >= (Q16 ? 0x477ff000u : 0x7f800000u)) {  // rare: exact bits from the inputs
+#pragma unroll
+    for (int j = 0; j < K; ++j)
+      st |= status_of(in[j].x, Q16) | status_of(in[j].y, Q16) | status_of(in[j].z, Q16) |
+            status_of(in[j].w, Q16);
+  }
+  s.x = div_k<K>(s.x); s.y = div_k<K>(s.y); s.z = div_k<K>(s.z); s.w = div_k<K>(s.w);
+  if (Q16) s = q16(s);
+  return s;
+}
+
+// Scalar version for the last P % 4 elements.
+template <int K, bool Q16>
+__device__ __forceinline__ void average1(const LocalBufs& lb, int64_t i, uint32_t& st) {
+  float in[K];
+#pragma unroll
+  for (int j = 0; j < K; ++j) in[j] = lb.b[j][i];
+#pragma unroll
+  for (int j = 0; j < K; ++j) st |= status_of(in[j], Q16);
+  float s = Q16 ? __half2float(__float2half_rn(in[0])) : in[0];
+#pragma unroll
+  for (int j = 1; j < K; ++j) s = __fadd_rn(s, Q16 ? __half2float(__float2half_rn(in[j])) : in[j]);
+  s = div_k<K>(s);
+  if (Q16) s = __half2float(__float2half_rn(s));
+#pragma unroll
+  for (int j = 0; j < K; ++j) lb.b[j][i] = s;
+}
+
+// Register-staged variant (16-byte LDG/STG, grid-stride over [e_begin, P)).
+template <int K, bool Q16>
+__global__ void __launch_bounds__(kThreads, K >= 7 ? 3 : 4)
+tm_direct_kernel(const __grid_constant__ LocalBufs lb, int64_t e_begin, int64_t P,
+                 uint32_t* status) {
+  const int64_t v0 = e_begin / 4, nv = P / 4;
+  const int64_t stride = (int64_t)gridDim.x * kThreads;
+  uint32_t st = 0;
+  for (int64_t v = v0 + (int64_t)blockIdx.x * kThreads + threadIdx.x; v < nv; v += stride) {
+    float4 in[K];
+#pragma unroll
+    for (int j = 0; j < K; ++j) in[j] = ld16_f(lb.b[j] + v * 4);
+    const float4 s = average4<K, Q16>(in, st);
+#pragma unroll
+    for (int j = 0; j < K; ++j) st16_f(lb.b[j] + v * 4, s);
+  }
+  const int64_t i = nv * 4 + threadIdx.x;  // tail (P % 4 elements), scalar
+  if (blockIdx.x == 0 && i < P) average1<K, Q16>(lb, i, st);
+  if (st) atomicOr(status, st);
+}
+
+// ---------------------------------------------------------------------------
+// Bulk-async (TMA engine) variant of the direct path.  Persistent: one CTA per
+// SM walks tiles of kTile elements.  Thread 0 streams each tile of all k
+// buffers into a kStages-deep shared-memory ring with cp.async.bulk (1-D bulk
+// copies completing on an mbarrier with expect_tx), every thread averages 4
+// elements from shared memory, writes the result tile once to a small output
+// ring, and thread 0 bulk-stores it into all k buffers
+// (cp.async.bulk.global.shared::cta).  Bytes in flight are set by the ring
+// depth, not by registers or LSU instruction count.  Elements past the last
+// whole tile go through the register path above (same arithmetic).
+// ---------------------------------------------------------------------------
+constexpr int kOutRing = 4;  // output tiles in flight
+
+// TILE: elements per buffer per tile; RING_KB: input ring budget; MINB: CTAs per SM.
+template <int K, int TILE, int RING_KB, int MINB>
+struct TmaCfg {
+  static constexpr int kTileBytes = TILE * 4;
+  static constexpr int kStagesRaw = RING_KB * 1024 / (K * kTileBytes);
+  static constexpr int kStages = kStagesRaw > 8 ? 8 : (kStagesRaw < 2 ? 2 : kStagesRaw);
+  static constexpr int kSmem = kStages * K * kTileBytes + kOutRing * kTileBytes;
+  static constexpr int kVecPerThread = TILE / (4 * kThreads);
+  static_assert(TILE % (4 * kThreads) == 0, "whole float4s per thread");
+};
+
+template <int K, bool Q16, int TILE, int RING_KB, int MINB>
+__global__ void __launch_bounds__(kThreads, MINB)
+tm_direct_tma_kernel(const __grid_constant__ LocalBufs lb, int64_t ntiles, int64_t P,
+                     uint32_t* status) {
+  using Cfg = TmaCfg<K, TILE, RING_KB, MINB>;
+  constexpr int S = Cfg::kStages;
+  constexpr int V = Cfg::kVecPerThread;
+  constexpr uint32_t TB = Cfg::kTileBytes;
+  extern __shared__ __align__(128) unsigned char smem[];
+  float* ring = reinterpret_cast<float*>(smem);                  // [S][K][TILE]
+  float* outr = ring + (size_t)S * K * TILE;                     // [kOutRing][TILE]
+  __shared__ __align__(8) uint64_t full[S];
+
+  const int tid = threadIdx.x;
+  // tiles of this CTA: blockIdx.x, blockIdx.x + gridDim.x, ...
+  const int64_t my = blockIdx.x < ntiles ? (ntiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+  auto tile_of = [&](int64_t i) { return (int64_t)blockIdx.x + i * gridDim.x; };
+  auto issue = [&](int64_t i) {
+    const int s = (int)(i % S);
+    const int64_t t = tile_of(i);
+    mbar_expect_tx(&full[s], K * TB);
+#pragma unroll
+    for (int j = 0; j < K; ++j)
+      bulk_load(ring + ((size_t)s * K + j) * TILE, lb.b[j] + t * TILE, TB, &full[s]);
+  };
+
+  if (tid == 0) {
+    for (int s = 0; s < S; ++s) mbar_init(&full[s], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    for (int64_t i = 0; i < S && i < my; ++i) issue(i);
+  }
+  __syncthreads();
+
+  uint32_t st = 0;
+  for (int64_t i = 0; i < my; ++i) {
+    const int s = (int)(i % S);
+    mbar_wait(&full[s], (uint32_t)((i / S) & 1));
+    float* out = outr + (size_t)(i % kOutRing) * TILE;
+#pragma unroll
+    for (int u = 0; u < V; ++u) {
+      float4 in[K];
+#pragma unroll
+      for (int j = 0; j < K; ++j)
+        in[j] = reinterpret_cast<const float4*>(ring + ((size_t)s * K + j) * TILE)[tid + u * kThreads];
+      reinterpret_cast<float4*>(out)[tid + u * kThreads] = average4<K, Q16>(in, st);
+    }
+    fence_proxy_async_smem();  // generic-proxy smem writes -> visible to the bulk store
+    if (tid == 0) bulk_wait_read<kOutRing - 2>();  // out slot of tile i+1 is free
+    __syncthreads();
+    if (tid == 0) {
+      const int64_t t = tile_of(i);
+#pragma unroll
+      for (int j = 0; j < K; ++j) bulk_store(lb.b[j] + t * TILE, out, TB);
+      bulk_commit();
+      if (i + S < my) issue(i + S);  // every thread has finished reading ring slot s
+    }
+  }
+  if (tid == 0) bulk_wait_all<0>();
+
+  // elements past the last whole tile: register path (one CTA)
+  if (blockIdx.x == gridDim.x - 1) {
+    const int64_t e0 = ntiles * TILE;
+    for (int64_t v = e0 / 4 + tid; v < P / 4; v += kThreads) {
+      float4 in[K];
+#pragma unroll
+      for (int j = 0; j < K; ++j) in[j] = ld16_f(lb.b[j] + v * 4);
+      const float4 r = average4<K, Q16>(in, st);
+#pragma unroll
+      for (int j = 0; j < K; ++j) st16_f(lb.b[j] + v * 4, r);
+    }
+    const int64_t i = (P / 4) * 4 + tid;
+    if (i < P) average1<K, Q16>(lb, i, st);
+  }
+  if (st) atomicOr(status, st);
+}
+
+}  // namespace
+
+template <int K, bool Q16, int TILE, int RING_KB, int MINB>
+cudaError_t launch_tma(const LocalBufs& lb, int64_t P, uint32_t* status, int dev, cudaStream_t s) {
+  using Cfg = TmaCfg<K, TILE, RING_KB, MINB>;
+  const int64_t ntiles = P / TILE;
+  auto fn = tm_direct_tma_kernel<K, Q16, TILE, RING_KB, MINB>;
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::kSmem);
+    if (e != cudaSuccess) return e;
+    attr_set = true;
+  }
+  const int grid = (int)std::min<int64_t>(ntiles, (int64_t)MINB * sm_count(dev));
+  fn<<<grid, kThreads, Cfg::kSmem, s>>>(lb, ntiles, P, status);
+  return cudaGetLastError();
+}
+
+// Tuning knobs (diagnostics only): TM_TMA_CFG selects the tile / ring / residency
+// of the bulk-async kernel for k = 8; TM_DIRECT_LDG=1 forces the register path.
+template <int K, bool Q16>
+cudaError_t direct_tma(const LocalBufs& lb, int64_t P, uint32_t* status, int dev, cudaStream_t s) {
+  if constexpr (K == 8) {
+    static const int cfg = env_int("TM_TMA_CFG", 0);
+    switch (cfg) {
+      case 8: return launch_tma<K, Q16, 1024, 160, 1>(lb, P, status, dev, s);
+      case 1: return launch_tma<K, Q16, 1024, 96, 2>(lb, P, status, dev, s);
+      case 2: return launch_tma<K, Q16, 2048, 192, 1>(lb, P, status, dev, s);
+      case 3: return launch_tma<K, Q16, 1024, 64, 2>(lb, P, status, dev, s);
+      case 4: return launch_tma<K, Q16, 2048, 96, 2>(lb, P, status, dev, s);
+      case 5: return launch_tma<K, Q16, 2048, 96, 1>(lb, P, status, dev, s);
+      case 6: return launch_tma<K, Q16, 2048, 96, 3>(lb, P, status, dev, s);
+      case 7: return launch_tma<K, Q16, 2048, 192, 1>(lb, P, status, dev, s);
+      default: break;
+    }
+  }
+  // Default, from the r01 sweep at k = 8 (profiles/r01/README.md): 8 KB tiles per
+  // buffer, a 2-deep ring for k = 8 (128 KB in flight per SM), one CTA per SM.
+  return launch_tma<K, Q16, 2048, 96, 1>(lb, P, status, dev, s);
+}
+
+template <int K>
+cudaError_t direct_k(const LocalBufs& lb, int64_t P, uint32_t* status, bool q16, int dev,
+                     cudaStream_t s) {
+  static const bool force_ldg = env_int("TM_DIRECT_LDG", 0) == 1;
+  if (P >= 2048 && !force_ldg)
+    return q16 ? direct_tma<K, true>(lb, P, status, dev, s) : direct_tma<K, false>(lb, P, status, dev, s);
+  const int64_t want = (P / 4 + kThreads - 1) / kThreads;
+  const int per_sm = K >= 7 ? 3 : 4;  // = the kernel's __launch_bounds__ residency
+  const int grid = (int)std::min<int64_t>(std::max<int64_t>(want, 1), per_sm * sm_count(dev));
+  if (q16) tm_direct_kernel<K, true><<<grid, kThreads, 0, s>>>(lb, 0, P, status);
+  else tm_direct_kernel<K, false><<<grid, kThreads, 0, s>>>(lb, 0, P, status);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_direct(float* const* bufs, int k, int64_t P, bool q16, uint32_t* status,
+                          cudaStream_t s) {
+  LocalBufs lb{};
+  for (int j = 0; j < k; ++j) lb.b[j] = bufs[j];
+  int dev = 0;
+  cudaGetDevice(&dev);
+  switch (k) {
+    case 2: return direct_k<2>(lb, P, status, q16, dev, s);
+    case 3: return direct_k<3>(lb, P, status, q16, dev, s);
+    case 4: return direct_k<4>(lb, P, status, q16, dev, s);
+    case 5: return direct_k<5>(lb, P, status, q16, dev, s);
+    case 6: return direct_k<6>(lb, P, status, q16, dev, s);
+    case 7: return direct_k<7>(lb, P, status, q16, dev, s);
+    case 8: return direct_k<8>(lb, P, status, q16, dev, s);
+    default: return cudaErrorInvalidValue;
+  }
+}
+
+}  // namespace tmx

@@ -1,0 +1,276 @@
+// sm_100a kernels of the EASGD elastic update (SPEC
+// L475) and the fp16 rounding test hook.
+#include <cuda_fp16.h>
+#include <stdint.h>
+#include <stdlib.h>
+
+#include <algorithm>
+
+#include "tm_device.cuh"
+#include "tm_internal.h"
+
+namespace tmx {
+namespace {
+using namespace dev;
+
+// ---------------------------------------------------------------------------
+// EASGD elastic update, one fp32 op per step:
+//   d = fl(x - c); e = fl(alpha d); x' = fl(x - e); c' = fl(c + e).
+// Concurrent mode applies c += e with red.relaxed.sys.global.add.f32 so several
+// workers (possibly on other GPUs, through an IPC mapping) may update one
+// centre at once without lost updates; each worker then read a possibly stale c.
+// ---------------------------------------------------------------------------
+template <bool Concurrent>
+__global__ void __launch_bounds__(kThreads)
+easgd_kernel(float* __restrict__ x, float* c, int64_t n, float alpha, int vec) {
+  const int64_t stride = (int64_t)gridDim.x * kThreads;
+  const int64_t tid = (int64_t)blockIdx.x * kThreads + threadIdx.x;
+  int64_t done = 0;
+  if (vec) {
+    const int64_t nv = n / 4;
+    for (int64_t v = tid; v < nv; v += stride) {
+      float4 xv = ld16_f(x + v * 4);
+      float4 cv = Concurrent ? __ldcg(reinterpret_cast<const float4*>(c + v * 4))
+                             : ld16_f(c + v * 4);
+      const float ex = elastic_diff(xv.x, cv.x, alpha), ey = elastic_diff(xv.y, cv.y, alpha);
+      const float ez = elastic_diff(xv.z, cv.z, alpha), ew = elastic_diff(xv.w, cv.w, alpha);
+      xv.x = __fsub_rn(xv.x, ex); xv.y = __fsub_rn(xv.y, ey);
+      xv.z = __fsub_rn(xv.z, ez); xv.w = __fsub_rn(xv.w, ew);
+      st16_f(x + v * 4, xv);
+      if (Concurrent) {
+        float* cp = c + v * 4;
+        red_add_sys(cp, ex); red_add_sys(cp + 1, ey);
+        red_add_sys(cp + 2, ez); red_add_sys(cp + 3, ew);
+      } else {
+        cv.x = __fadd_rn(cv.x, ex); cv.y = __fadd_rn(cv.y, ey);
+        cv.z = __fadd_rn(cv.z, ez); cv.w = __fadd_rn(cv.w, ew);
+        st16_f(c + v * 4, cv);
+      }
+    }
+    done = nv * 4;
+  }
+  for (int64_t i = done + tid; i < n; i += stride) {
+    const float xi = x[i];
+    const float ci = Concurrent ? __ldcg(c + i) : c[i];
+    const float e = elastic_diff(xi, ci, alpha);
+    x[i] = __fsub_rn(xi, e);
+    if (Concurrent) red_add_sys(c + i, e);
+    else c[i] = __fadd_rn(ci, e);
+  }
+}
+
+// Elastic update against a centre sharded by segment: element i
+// of segment s = i / L lives at shard[s][i - s*L], local or on peer s over NVLink.
+// Segments are multiples of 256 elements, so a 16-byte vector never straddles
+// two shards.  Concurrent mode: c += e by red.add at system scope when the
+// shard may be on another GPU.
+template <bool Concurrent, bool SYS>
+__global__ void __launch_bounds__(kThreads)
+easgd_sharded_kernel(float* __restrict__ x, const __grid_constant__ ShardArgs sa, float alpha) {
+  const int64_t stride = (int64_t)gridDim.x * kThreads;
+  const int64_t tid = (int64_t)blockIdx.x * kThreads + threadIdx.x;
+  for (int s = 0; s < sa.k; ++s) {
+    const int64_t base = (int64_t)s * sa.L;
+    const int64_t len = min(sa.L, sa.P - base);
+    if (len <= 0) break;
+    float* c = sa.shard[s];
+    float* xs = x + base;
+    const int64_t nv = len / 4;
+    for (int64_t v = tid; v < nv; v += stride) {
+      float4 xv = ld16_f(xs + v * 4);
+      float4 cv = __ldcg(reinterpret_cast<const float4*>(c + v * 4));
+      const float ex = elastic_diff(xv.x, cv.x, alpha), ey = elastic_diff(xv.y, cv.y, alpha);
+      const float ez = elastic_diff(xv.z, cv.z, alpha), ew = elastic_diff(xv.w, cv.w, alpha);
+      xv.x = __fsub_rn(xv.x, ex); xv.y = __fsub_rn(xv.y, ey);
+      xv.z = __fsub_rn(xv.z, ez); xv.w = __fsub_rn(xv.w, ew);
+      st16_f(xs + v * 4, xv);
+      if (Concurrent) {
+        float* cp = c + v * 4;
+        if (SYS) { red_add_sys(cp, ex); red_add_sys(cp + 1, ey); red_add_sys(cp + 2, ez); red_add_sys(cp + 3, ew); }
+        else { red_add_gpu(cp, ex); red_add_gpu(cp + 1, ey); red_add_gpu(cp + 2, ez); red_add_gpu(cp + 3, ew); }
+      } else {
+        cv.x = __fadd_rn(cv.x, ex); cv.y = __fadd_rn(cv.y, ey);
+        cv.z = __fadd_rn(cv.z, ez); cv.w = __fadd_rn(cv.w, ew);
+        __stcg(reinterpret_cast<float4*>(c + v * 4), cv);
+      }
+    }
+    for (int64_t i = nv * 4 + tid; i < len; i += stride) {  // segment tail (last segment only)
+      const float xi = xs[i];
+      const float ci = __ldcg(c + i);
+      const float e = elastic_diff(xi, ci, alpha);
+      xs[i] = __fsub_rn(xi, e);
+      if (Concurrent) { if (SYS) red_add_sys(c + i, e); else red_add_gpu(c + i, e); }
+      else c[i] = __fadd_rn(ci, e);
+    }
+  }
+}
+
+// A whole server round in arrival order, fused: the centre is read once and
+// written once; worker w's update uses the centre left by the previous one.
+// Bitwise equal to serial updates in `order` (each element is independent).
+constexpr int kMaxRoundWorkers = 16;
+constexpr int kMaxRoundOrder = 64;
+struct RoundArgs {
+  float* w[kMaxRoundWorkers];
+  int8_t order[kMaxRoundOrder];
+  int norder;
+};
+
+__global__ void __launch_bounds__(kThreads)
+easgd_round_kernel(const __grid_constant__ RoundArgs ra, float* c, int64_t n, float alpha,
+                   int vec) {
+  const int64_t stride = (int64_t)gridDim.x * kThreads;
+  const int64_t tid = (int64_t)blockIdx.x * kThreads + threadIdx.x;
+  int64_t done = 0;
+  if (vec) {
+    const int64_t nv = n / 4;
+    for (int64_t v = tid; v < nv; v += stride) {
+      float4 cv = ld16_f(c + v * 4);
+      for (int t = 0; t < ra.norder; ++t) {
+        float* wp = ra.w[ra.order[t]] + v * 4;
+        float4 xv = *reinterpret_cast<const float4*>(wp);
+        const float ex = elastic_diff(xv.x, cv.x, alpha), ey = elastic_diff(xv.y, cv.y, alpha);
+        const float ez = elastic_diff(xv.z, cv.z, alpha), ew = elastic_diff(xv.w, cv.w, alpha);
+        xv.x = __fsub_rn(xv.x, ex); xv.y = __fsub_rn(xv.y, ey);
+        xv.z = __fsub_rn(xv.z, ez); xv.w = __fsub_rn(xv.w, ew);
+        cv.x = __fadd_rn(cv.x, ex); cv.y = __fadd_rn(cv.y, ey);
+        cv.z = __fadd_rn(cv.z, ez); cv.w = __fadd_rn(cv.w, ew);
+        *reinterpret_cast<float4*>(wp) = xv;
+      }
+      st16_f(c + v * 4, cv);
+    }
+    done = nv * 4;
+  }
+  for (int64_t i = done + tid; i < n; i += stride) {
+    float ci = c[i];
+    for (int t = 0; t < ra.norder; ++t) {
+      float* wp = ra.w[ra.order[t]] + i;
+      const float xi = *wp;
+      const float e = elastic_diff(xi, ci, alpha);
+      *wp = __fsub_rn(xi, e);
+      ci = __fadd_rn(ci, e);
+    }
+    c[i] = ci;
+  }
+}
+
+// Arrival order with N DISTINCT workers (the common round: each worker once):
+// all N worker loads are issued before the dependent chain of centre updates,
+// so N + 1 independent 16-byte loads are in flight per thread.  `wo` holds the
+// workers' pointers already in arrival order.
+struct OrderedWorkers {
+  float* wo[8];
+};
+
+template <int N>
+__global__ void __launch_bounds__(kThreads)
+easgd_round_distinct_kernel(const __grid_constant__ OrderedWorkers ow, float* c, int64_t n,
+                            float alpha) {
+  const int64_t stride = (int64_t)gridDim.x * kThreads;
+  const int64_t tid = (int64_t)blockIdx.x * kThreads + threadIdx.x;
+  const int64_t nv = n / 4;
+  for (int64_t v = tid; v < nv; v += stride) {
+    float4 cv = ld16_f(c + v * 4);
+    float4 xv[N];
+#pragma unroll
+    for (int t = 0; t < N; ++t) xv[t] = ld16_f(ow.wo[t] + v * 4);
+#pragma unroll
+    for (int t = 0; t < N; ++t) {
+      const float ex = elastic_diff(xv[t].x, cv.x, alpha), ey = elastic_diff(xv[t].y, cv.y, alpha);
+      const float ez = elastic_diff(xv[t].z, cv.z, alpha), ew = elastic_diff(xv[t].w, cv.w, alpha);
+      xv[t].x = __fsub_rn(xv[t].x, ex); xv[t].y = __fsub_rn(xv[t].y, ey);
+      xv[t].z = __fsub_rn(xv[t].z, ez); xv[t].w = __fsub_rn(xv[t].w, ew);
+      cv.x = __fadd_rn(cv.x, ex); cv.y = __fadd_rn(cv.y, ey);
+      cv.z = __fadd_rn(cv.z, ez); cv.w = __fadd_rn(cv.w, ew);
+      st16_f(ow.wo[t] + v * 4, xv[t]);
+    }
+    st16_f(c + v * 4, cv);
+  }
+  for (int64_t i = nv * 4 + tid; i < n; i += stride) {  // tail, scalar
+    float ci = c[i];
+#pragma unroll
+    for (int t = 0; t < N; ++t) {
+      const float xi = ow.wo[t][i];
+      const float e = elastic_diff(xi, ci, alpha);
+      ow.wo[t][i] = __fsub_rn(xi, e);
+      ci = __fadd_rn(ci, e);
+    }
+    c[i] = ci;
+  }
+}
+
+__global__ void __launch_bounds__(kThreads)
+cast_rn16_kernel(const float* __restrict__ in, uint16_t* __restrict__ out, int64_t n) {
+  const int64_t stride = (int64_t)gridDim.x * kThreads;
+  for (int64_t i = (int64_t)blockIdx.x * kThreads + threadIdx.x; i < n; i += stride) {
+    const __half h = __float2half_rn(in[i]);  // cvt.rn.f16.f32, as in the exchange
+    out[i] = *reinterpret_cast<const uint16_t*>(&h);
+  }
+}
+
+}  // namespace
+
+cudaError_t launch_easgd(float* x, float* c, int64_t n, float alpha, bool concurrent,
+                         cudaStream_t s) {
+  const int vec = ((reinterpret_cast<uintptr_t>(x) | reinterpret_cast<uintptr_t>(c)) & 15) == 0;
+  const int grid = streaming_grid(vec ? n / 4 + 4 : n);
+  if (concurrent) easgd_kernel<true><<<grid, kThreads, 0, s>>>(x, c, n, alpha, vec);
+  else easgd_kernel<false><<<grid, kThreads, 0, s>>>(x, c, n, alpha, vec);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_easgd_round(float* const* w, int nw, const int32_t* order, int norder,
+                               float* c, int64_t n, float alpha, cudaStream_t s) {
+  if (nw < 1 || nw > kMaxRoundWorkers || norder < 0 || norder > kMaxRoundOrder)
+    return cudaErrorInvalidValue;
+  RoundArgs ra{};
+  uintptr_t align = reinterpret_cast<uintptr_t>(c);
+  for (int i = 0; i < nw; ++i) {
+    ra.w[i] = w[i];
+    align |= reinterpret_cast<uintptr_t>(w[i]);
+  }
+  for (int t = 0; t < norder; ++t) {
+    if (order[t] < 0 || order[t] >= nw) return cudaErrorInvalidValue;
+    ra.order[t] = (int8_t)order[t];
+  }
+  ra.norder = norder;
+  const int vec = (align & 15) == 0;
+  bool distinct = norder >= 1 && norder <= 8;
+  for (int t = 0; distinct && t < norder; ++t)
+    for (int u = 0; u < t; ++u)
+      if (order[u] == order[t]) distinct = false;
+  if (vec && distinct) {
+    OrderedWorkers ow{};
+    for (int t = 0; t < norder; ++t) ow.wo[t] = w[order[t]];
+    const int grid = streaming_grid(n / 4 + 4);
+    switch (norder) {
+#define TM_RD(N) \
+  case N: easgd_round_distinct_kernel<N><<<grid, kThreads, 0, s>>>(ow, c, n, alpha); break;
+      TM_RD(1) TM_RD(2) TM_RD(3) TM_RD(4) TM_RD(5) TM_RD(6) TM_RD(7) TM_RD(8)
+#undef TM_RD
+    }
+    return cudaGetLastError();
+  }
+  const int grid = streaming_grid(vec ? n / 4 + 4 : n);
+  easgd_round_kernel<<<grid, kThreads, 0, s>>>(ra, c, n, alpha, vec);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_easgd_sharded(float* x, const ShardArgs& sa, float alpha, bool concurrent,
+                                 cudaStream_t s) {
+  const int grid = streaming_grid(sa.L / 4 + 4);
+  if (concurrent) {
+    if (sa.sys) easgd_sharded_kernel<true, true><<<grid, kThreads, 0, s>>>(x, sa, alpha);
+    else easgd_sharded_kernel<true, false><<<grid, kThreads, 0, s>>>(x, sa, alpha);
+  } else {
+    easgd_sharded_kernel<false, false><<<grid, kThreads, 0, s>>>(x, sa, alpha);
+  }
+  return cudaGetLastError();
+}
+
+cudaError_t launch_cast_rn16(const float* in, uint16_t* out, int64_t n, cudaStream_t s) {
+  cast_rn16_kernel<<<streaming_grid(n), kThreads, 0, s>>>(in, out, n);
+  return cudaGetLastError();
+}
+
+}  // namespace tmx

@@ -62,6 +62,5 @@ cudaError_t launch_cast_rn16(const float* in, uint16_t* out, int64_t n, cudaStre
 
 // Max co-resident CTAs of the exchange kernel on `device` (occupancy * SMs).
 int exchange_max_ctas(int device, bool wire16, int k);
-int grid_for_streaming(int device);
 
 }  // namespace tmx
