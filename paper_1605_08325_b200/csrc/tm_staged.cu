@@ -199,32 +199,303 @@ tm_exchange_kernel(const __grid_constant__ ExchangeArgs a) {
   }
 }
 
+// ---------------------------------------------------------------------------
+// The same three phases on the TMA engine (default staged kernel).
+//
+// One CTA per SM (224 KB of shared memory).  Each phase is a tile pipeline:
+// thread 0 issues 1-D bulk copies (cp.async.bulk, completing on an mbarrier)
+// of the phase's source tiles into a 4-slot x 32 KB input ring -- for a4 the k
+// sources are peer staging buffers, i.e. the TMA engine pulls over NVLink --
+// all threads transform the tile in shared memory into a 3-slot x 32 KB output
+// ring, and thread 0 bulk-stores it.  Bytes in flight are set by the rings, not
+// by registers or LSU queue depth (the register kernel above was lg_throttle-
+// bound).  Cross-proxy ordering: before a phase's flags are released, thread 0
+// waits for its bulk stores to complete and issues fence.proxy.async.global;
+// after a barrier it fences again before issuing bulk loads of peer data.
+// Elements in [P & ~3, P) (at most 3, in the last segment) are read / written
+// with plain accesses; elements >= P are zero on the wire and never stored.
+// ---------------------------------------------------------------------------
+constexpr int kSlotBytes = 32 * 1024;
+constexpr int kInSlots = 4;
+constexpr int kOutSlots = 3;
+
+__device__ __forceinline__ void fence_proxy_async_global() {
+  asm volatile("fence.proxy.async.global;" ::: "memory");
+}
+
+// Runs n_items through the rings.  issue(i, slot, bar) [thread 0] starts the
+// bulk loads of item i and arms `bar` with their byte count; compute(i, in, out)
+// [all threads] transforms; store(i, out) [thread 0] issues the bulk stores.
+// `use` / `outn` continue across phases so slot parities stay consistent.
+template <class IssueF, class ComputeF, class StoreF>
+__device__ __forceinline__ void tile_pipeline(int n_items, uint32_t& use, uint32_t& outn,
+                                              char* in_ring, char* out_ring, uint64_t* full,
+                                              IssueF issue, ComputeF compute, StoreF store) {
+  const int tid = threadIdx.x;
+  if (tid == 0) {
+    for (int i = 0; i < kInSlots && i < n_items; ++i) {
+      const uint32_t slot = (use + i) % kInSlots;
+      issue(i, in_ring + slot * kSlotBytes, &full[slot]);
+    }
+  }
+  for (int i = 0; i < n_items; ++i) {
+    const uint32_t u = use + i;
+    const uint32_t slot = u % kInSlots;
+    mbar_wait(&full[slot], (u / kInSlots) & 1);
+    char* out = out_ring + (outn % kOutSlots) * kSlotBytes;
+    compute(i, in_ring + slot * kSlotBytes, out);
+    fence_proxy_async_smem();                      // generic smem writes -> bulk store
+    if (tid == 0) bulk_wait_read<kOutSlots - 2>();  // out slot of item i+1 is free
+    __syncthreads();                               // every thread is done with slot / out
+    if (tid == 0) {
+      store(i, out);
+      bulk_commit();
+      if (i + kInSlots < n_items) issue(i + kInSlots, in_ring + slot * kSlotBytes, &full[slot]);
+    }
+    ++outn;
+  }
+  use += n_items;
+}
+
+// Drain this CTA's bulk stores and order them before the generic-proxy release.
+__device__ __forceinline__ void drain_bulk_stores() {
+  if (threadIdx.x == 0) {
+    bulk_wait_all<0>();
+    fence_proxy_async_global();
+  }
+}
+
+template <int K, bool W16, bool SYS>
+__global__ void __launch_bounds__(kThreads, 1)
+tm_exchange_tma_kernel(const __grid_constant__ ExchangeArgs a) {
+  using U = Unit<W16>;
+  constexpr int E = U::kElems;      // elements per 16-byte wire unit
+  constexpr int WB = W16 ? 2 : 4;   // wire bytes per element
+  constexpr int TP = 4096;          // a2 tile: fp32 in 16 KB, wire out <= 16 KB
+  // a4 tile: k sources of TR wire elements fit one 32 KB slot; a multiple of 256
+  // elements keeps every source's smem offset and byte count 16-byte aligned.
+  constexpr int TR_RAW = kSlotBytes / (K * WB) / 256 * 256;
+  constexpr int TR = TR_RAW < 4096 ? TR_RAW : 4096;
+  static_assert(TR >= 256, "a4 tile too small");
+  constexpr int TA = 8192;          // a6 tile: wire in <= 32 KB, fp32 out 32 KB
+  extern __shared__ __align__(128) unsigned char smem[];
+  char* in_ring = reinterpret_cast<char*>(smem);
+  char* out_ring = in_ring + kInSlots * kSlotBytes;
+  __shared__ __align__(8) uint64_t full[kInSlots];
+  __shared__ int s_abort;
+  __shared__ uint32_t s_epoch;
+
+  const int lr = blockIdx.x / a.C;
+  const int c = blockIdx.x - lr * a.C;
+  const int r = a.rank0 + lr;
+  float* __restrict__ x = a.x[lr];
+  const int64_t P = a.P, L = a.L, P4 = P & ~int64_t(3);
+  const int64_t e0 = (int64_t)c * a.Lc;
+  const int64_t e1 = min(e0 + a.Lc, L);
+  const int64_t nel = e1 > e0 ? e1 - e0 : 0;
+  char* const stage_r = reinterpret_cast<char*>(a.stage[r]);
+  const int tid = threadIdx.x;
+
+  if (tid == 0) {
+    s_abort = 0;
+    uint32_t* ctr = a.flags[r] + (size_t)kPhases * TM_MAX_RANKS * a.C + c;  // device epoch
+    s_epoch = *ctr + 1;
+    *ctr = s_epoch;
+    for (int i = 0; i < kInSlots; ++i) mbar_init(&full[i], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  const uint32_t epoch = s_epoch;
+  uint32_t use = 0, outn = 0, st = 0;
+
+  // ---------------- a2: pre-cast x -> own stage (all k segments' chunk c) ----
+  {
+    const int nt = (int)((nel + TP - 1) / TP);
+    auto geom = [&](int i, int64_t& g0, int64_t& n) {
+      const int s = i / nt, t = i - s * nt;
+      g0 = (int64_t)s * L + e0 + (int64_t)t * TP;
+      n = min((int64_t)TP, nel - (int64_t)t * TP);
+    };
+    tile_pipeline(
+        K * nt, use, outn, in_ring, out_ring, full,
+        [&](int i, char* slot, uint64_t* bar) {
+          int64_t g0, n;
+          geom(i, g0, n);
+          const int64_t nb = max((int64_t)0, min(g0 + n, P4) - g0);  // bulk-loadable elements
+          mbar_expect_tx(bar, (uint32_t)(nb * 4));
+          if (nb > 0) bulk_load(slot, x + g0, (uint32_t)(nb * 4), bar);
+        },
+        [&](int i, const char* in, char* out) {
+          int64_t g0, n;
+          geom(i, g0, n);
+          const int64_t nb = max((int64_t)0, min(g0 + n, P4) - g0);
+          const float* fin = reinterpret_cast<const float*>(in);
+          for (int v = tid; v < (int)(n / E); v += kThreads) {
+            float f[E];
+            if ((int64_t)(v + 1) * E <= nb) {
+#pragma unroll
+              for (int q = 0; q < E; q += 4) {
+                const float4 t4 = reinterpret_cast<const float4*>(fin + v * E)[q / 4];
+                f[q] = t4.x; f[q + 1] = t4.y; f[q + 2] = t4.z; f[q + 3] = t4.w;
+              }
+            } else {
+#pragma unroll
+              for (int q = 0; q < E; ++q) {
+                const int64_t e = (int64_t)v * E + q;
+                f[q] = e < nb ? fin[e] : (g0 + e < P ? x[g0 + e] : 0.0f);
+              }
+            }
+            st |= unit_status<W16, E>(f);
+            reinterpret_cast<uint4*>(out)[v] = U::encode(f);
+          }
+        },
+        [&](int i, const char* out) {
+          int64_t g0, n;
+          geom(i, g0, n);
+          bulk_store(stage_r + g0 * WB, out, (uint32_t)(n * WB));
+        });
+  }
+  if (st) atomicOr(a.status, st);
+  drain_bulk_stores();
+  if (!rank_barrier<K, SYS>(a, kPhaseReady, r, c, epoch, &s_abort)) return;
+  if (tid == 0) fence_proxy_async_global();  // peers' staging, acquired above -> bulk loads
+
+  // ---------------- a4: reduce-scatter pull (TMA from every rank's stage) ----
+  {
+    char* const avg_r = reinterpret_cast<char*>(a.avg[r]);
+    const int nt = (int)((nel + TR - 1) / TR);
+    tile_pipeline(
+        nt, use, outn, in_ring, out_ring, full,
+        [&](int i, char* slot, uint64_t* bar) {
+          const int64_t e = e0 + (int64_t)i * TR;
+          const int64_t n = min((int64_t)TR, e1 - e);
+          mbar_expect_tx(bar, (uint32_t)(K * n * WB));
+#pragma unroll
+          for (int j = 0; j < K; ++j)
+            bulk_load(slot + j * TR * WB, reinterpret_cast<const char*>(a.stage[j]) + ((int64_t)r * L + e) * WB,
+                      (uint32_t)(n * WB), bar);
+        },
+        [&](int i, const char* in, char* out) {
+          const int64_t e = e0 + (int64_t)i * TR;
+          const int n = (int)min((int64_t)TR, e1 - e);
+          for (int v = tid; v < n / E; v += kThreads) {
+            uint4 raw[K];
+#pragma unroll
+            for (int j = 0; j < K; ++j) raw[j] = reinterpret_cast<const uint4*>(in + j * TR * WB)[v];
+            float sm[E], t[E];
+            U::decode(raw[0], sm);
+#pragma unroll
+            for (int j = 1; j < K; ++j) {
+              U::decode(raw[j], t);
+#pragma unroll
+              for (int q = 0; q < E; ++q) sm[q] = __fadd_rn(sm[q], t[q]);
+            }
+#pragma unroll
+            for (int q = 0; q < E; ++q) sm[q] = div_k<K>(sm[q]);
+            reinterpret_cast<uint4*>(out)[v] = U::encode(sm);
+          }
+        },
+        [&](int i, const char* out) {
+          const int64_t e = e0 + (int64_t)i * TR;
+          const int64_t n = min((int64_t)TR, e1 - e);
+          bulk_store(avg_r + e * WB, out, (uint32_t)(n * WB));
+        });
+  }
+  drain_bulk_stores();
+  if (!rank_barrier<K, SYS>(a, kPhaseReduced, r, c, epoch, &s_abort)) return;
+  if (tid == 0) fence_proxy_async_global();
+
+  // ---------------- a6: allgather pull (TMA from every rank's avg) ----------
+  {
+    const int nt = (int)((nel + TA - 1) / TA);
+    auto geom = [&](int i, int& j, int64_t& e, int64_t& n) {
+      j = i / nt;
+      const int t = i - j * nt;
+      e = e0 + (int64_t)t * TA;
+      n = min((int64_t)TA, e1 - e);
+    };
+    tile_pipeline(
+        K * nt, use, outn, in_ring, out_ring, full,
+        [&](int i, char* slot, uint64_t* bar) {
+          int j;
+          int64_t e, n;
+          geom(i, j, e, n);
+          mbar_expect_tx(bar, (uint32_t)(n * WB));
+          bulk_load(slot, reinterpret_cast<const char*>(a.avg[j]) + e * WB, (uint32_t)(n * WB), bar);
+        },
+        [&](int i, const char* in, char* out) {
+          int j;
+          int64_t e, n;
+          geom(i, j, e, n);
+          const int64_t g0 = (int64_t)j * L + e;
+          float* fo = reinterpret_cast<float*>(out);
+          for (int v = tid; v < (int)(n / E); v += kThreads) {
+            float f[E];
+            U::decode(reinterpret_cast<const uint4*>(in)[v], f);
+#pragma unroll
+            for (int q = 0; q < E; q += 4)
+              reinterpret_cast<float4*>(fo + v * E)[q / 4] = make_float4(f[q], f[q + 1], f[q + 2], f[q + 3]);
+#pragma unroll
+            for (int q = 0; q < E; ++q) {  // the <= 3 elements in [P & ~3, P)
+              const int64_t g = g0 + (int64_t)v * E + q;
+              if (g >= P4 && g < P) x[g] = f[q];
+            }
+          }
+        },
+        [&](int i, const char* out) {
+          int j;
+          int64_t e, n;
+          geom(i, j, e, n);
+          const int64_t g0 = (int64_t)j * L + e;
+          const int64_t nb = max((int64_t)0, min(g0 + n, P4) - g0);
+          if (nb > 0) bulk_store(x + g0, out, (uint32_t)(nb * 4));
+        });
+  }
+  if (tid == 0) bulk_wait_all<0>();  // kernel exit also waits; explicit for clarity
+}
+
 template <int K, bool W16>
-const void* exchange_fn(bool sys) {
+const void* exchange_fn(bool sys, bool tma) {
+  if (tma)
+    return sys ? reinterpret_cast<const void*>(&tm_exchange_tma_kernel<K, W16, true>)
+               : reinterpret_cast<const void*>(&tm_exchange_tma_kernel<K, W16, false>);
   return sys ? reinterpret_cast<const void*>(&tm_exchange_kernel<K, W16, true>)
              : reinterpret_cast<const void*>(&tm_exchange_kernel<K, W16, false>);
 }
 
-const void* pick_exchange(int k, bool w16, bool sys) {
+const void* pick_exchange(int k, bool w16, bool sys, bool tma) {
   switch (k) {
-    case 2: return w16 ? exchange_fn<2, true>(sys) : exchange_fn<2, false>(sys);
-    case 3: return w16 ? exchange_fn<3, true>(sys) : exchange_fn<3, false>(sys);
-    case 4: return w16 ? exchange_fn<4, true>(sys) : exchange_fn<4, false>(sys);
-    case 5: return w16 ? exchange_fn<5, true>(sys) : exchange_fn<5, false>(sys);
-    case 6: return w16 ? exchange_fn<6, true>(sys) : exchange_fn<6, false>(sys);
-    case 7: return w16 ? exchange_fn<7, true>(sys) : exchange_fn<7, false>(sys);
-    case 8: return w16 ? exchange_fn<8, true>(sys) : exchange_fn<8, false>(sys);
+    case 2: return w16 ? exchange_fn<2, true>(sys, tma) : exchange_fn<2, false>(sys, tma);
+    case 3: return w16 ? exchange_fn<3, true>(sys, tma) : exchange_fn<3, false>(sys, tma);
+    case 4: return w16 ? exchange_fn<4, true>(sys, tma) : exchange_fn<4, false>(sys, tma);
+    case 5: return w16 ? exchange_fn<5, true>(sys, tma) : exchange_fn<5, false>(sys, tma);
+    case 6: return w16 ? exchange_fn<6, true>(sys, tma) : exchange_fn<6, false>(sys, tma);
+    case 7: return w16 ? exchange_fn<7, true>(sys, tma) : exchange_fn<7, false>(sys, tma);
+    case 8: return w16 ? exchange_fn<8, true>(sys, tma) : exchange_fn<8, false>(sys, tma);
     default: return nullptr;
   }
 }
 
+constexpr int kTmaSmem = (kInSlots + kOutSlots) * kSlotBytes;
+
+// Opt every TMA instantiation into its dynamic shared memory (idempotent).
+cudaError_t prepare(const void* fn, bool tma) {
+  if (!tma) return cudaSuccess;
+  return cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, kTmaSmem);
+}
+
 }  // namespace
 
+bool staged_uses_tma() { return env_int("TM_STAGED_LDG", 0) != 1; }
+
 int exchange_max_ctas(int device, bool wire16, int k) {
-  const void* fn = pick_exchange(k, wire16, true);
+  const bool tma = staged_uses_tma();
+  const void* fn = pick_exchange(k, wire16, true, tma);
   if (!fn) return 0;
+  if (prepare(fn, tma) != cudaSuccess) return 0;
   int per_sm = 0;
-  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, kThreads, 0) != cudaSuccess)
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, kThreads, tma ? kTmaSmem : 0) !=
+      cudaSuccess)
     return 0;
   return per_sm * sm_count(device);
 }
@@ -232,12 +503,16 @@ int exchange_max_ctas(int device, bool wire16, int k) {
 cudaError_t launch_exchange(const ExchangeArgs& a, int nlocal, bool wire16, cudaStream_t s) {
   // System-scope flags only when some peer rank lives in another process
   // (another GPU, over NVLink); a single-process group syncs at GPU scope.
-  const void* fn = pick_exchange(a.k, wire16, nlocal != a.k);
+  const bool tma = staged_uses_tma();
+  const void* fn = pick_exchange(a.k, wire16, nlocal != a.k, tma);
   if (!fn) return cudaErrorInvalidValue;
+  cudaError_t e = prepare(fn, tma);
+  if (e != cudaSuccess) return e;
   void* params[] = {const_cast<ExchangeArgs*>(&a)};
   // Cooperative launch: guarantees every CTA is co-resident, which the
   // per-CTA flag barriers need when several ranks share this device.
-  return cudaLaunchCooperativeKernel(fn, dim3(nlocal * a.C), dim3(kThreads), params, 0, s);
+  return cudaLaunchCooperativeKernel(fn, dim3(nlocal * a.C), dim3(kThreads), params,
+                                     tma ? kTmaSmem : 0, s);
 }
 
 }  // namespace tmx
