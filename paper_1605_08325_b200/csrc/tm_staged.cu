@@ -218,6 +218,7 @@ tm_exchange_kernel(const __grid_constant__ ExchangeArgs a) {
 constexpr int kSlotBytes = 32 * 1024;
 constexpr int kInSlots = 4;
 constexpr int kOutSlots = 3;
+constexpr int kTmaThreads = 512;  // 16 warps share the in-smem transform of each tile
 
 __device__ __forceinline__ void fence_proxy_async_global() {
   asm volatile("fence.proxy.async.global;" ::: "memory");
@@ -266,7 +267,7 @@ __device__ __forceinline__ void drain_bulk_stores() {
 }
 
 template <int K, bool W16, bool SYS>
-__global__ void __launch_bounds__(kThreads, 1)
+__global__ void __launch_bounds__(kTmaThreads, 1)
 tm_exchange_tma_kernel(const __grid_constant__ ExchangeArgs a) {
   using U = Unit<W16>;
   constexpr int E = U::kElems;      // elements per 16-byte wire unit
@@ -330,9 +331,10 @@ tm_exchange_tma_kernel(const __grid_constant__ ExchangeArgs a) {
           geom(i, g0, n);
           const int64_t nb = max((int64_t)0, min(g0 + n, P4) - g0);
           const float* fin = reinterpret_cast<const float*>(in);
-          for (int v = tid; v < (int)(n / E); v += kThreads) {
+          const int nbi = (int)nb;
+          for (int v = tid; v < (int)(n / E); v += kTmaThreads) {
             float f[E];
-            if ((int64_t)(v + 1) * E <= nb) {
+            if ((v + 1) * E <= nbi) {
 #pragma unroll
               for (int q = 0; q < E; q += 4) {
                 const float4 t4 = reinterpret_cast<const float4*>(fin + v * E)[q / 4];
@@ -341,8 +343,8 @@ tm_exchange_tma_kernel(const __grid_constant__ ExchangeArgs a) {
             } else {
 #pragma unroll
               for (int q = 0; q < E; ++q) {
-                const int64_t e = (int64_t)v * E + q;
-                f[q] = e < nb ? fin[e] : (g0 + e < P ? x[g0 + e] : 0.0f);
+                const int e = v * E + q;
+                f[q] = e < nbi ? fin[e] : (g0 + e < P ? x[g0 + e] : 0.0f);
               }
             }
             st |= unit_status<W16, E>(f);
@@ -378,7 +380,7 @@ tm_exchange_tma_kernel(const __grid_constant__ ExchangeArgs a) {
         [&](int i, const char* in, char* out) {
           const int64_t e = e0 + (int64_t)i * TR;
           const int n = (int)min((int64_t)TR, e1 - e);
-          for (int v = tid; v < n / E; v += kThreads) {
+          for (int v = tid; v < n / E; v += kTmaThreads) {
             uint4 raw[K];
 #pragma unroll
             for (int j = 0; j < K; ++j) raw[j] = reinterpret_cast<const uint4*>(in + j * TR * WB)[v];
@@ -428,17 +430,21 @@ tm_exchange_tma_kernel(const __grid_constant__ ExchangeArgs a) {
           int64_t e, n;
           geom(i, j, e, n);
           const int64_t g0 = (int64_t)j * L + e;
+          // tile-relative window [lo, hi) of the <= 3 elements in [P & ~3, P):
+          // bulk stores cannot cover them, plain stores do
+          const int lo = (int)max((int64_t)0, min(n, P4 - g0));
+          const int hi = (int)max((int64_t)0, min(n, P - g0));
           float* fo = reinterpret_cast<float*>(out);
-          for (int v = tid; v < (int)(n / E); v += kThreads) {
+          for (int v = tid; v < (int)(n / E); v += kTmaThreads) {
             float f[E];
             U::decode(reinterpret_cast<const uint4*>(in)[v], f);
 #pragma unroll
             for (int q = 0; q < E; q += 4)
               reinterpret_cast<float4*>(fo + v * E)[q / 4] = make_float4(f[q], f[q + 1], f[q + 2], f[q + 3]);
+            if (hi > lo && (v + 1) * E > lo && v * E < hi) {
 #pragma unroll
-            for (int q = 0; q < E; ++q) {  // the <= 3 elements in [P & ~3, P)
-              const int64_t g = g0 + (int64_t)v * E + q;
-              if (g >= P4 && g < P) x[g] = f[q];
+              for (int q = 0; q < E; ++q)
+                if (v * E + q >= lo && v * E + q < hi) x[g0 + v * E + q] = f[q];
             }
           }
         },
@@ -494,7 +500,8 @@ int exchange_max_ctas(int device, bool wire16, int k) {
   if (!fn) return 0;
   if (prepare(fn, tma) != cudaSuccess) return 0;
   int per_sm = 0;
-  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, kThreads, tma ? kTmaSmem : 0) !=
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, tma ? kTmaThreads : kThreads,
+                                                    tma ? kTmaSmem : 0) !=
       cudaSuccess)
     return 0;
   return per_sm * sm_count(device);
@@ -511,7 +518,7 @@ cudaError_t launch_exchange(const ExchangeArgs& a, int nlocal, bool wire16, cuda
   void* params[] = {const_cast<ExchangeArgs*>(&a)};
   // Cooperative launch: guarantees every CTA is co-resident, which the
   // per-CTA flag barriers need when several ranks share this device.
-  return cudaLaunchCooperativeKernel(fn, dim3(nlocal * a.C), dim3(kThreads), params,
+  return cudaLaunchCooperativeKernel(fn, dim3(nlocal * a.C), dim3(tma ? kTmaThreads : kThreads), params,
                                      tma ? kTmaSmem : 0, s);
 }
 
