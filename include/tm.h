@@ -71,6 +71,13 @@ extern "C" {
 #define TM_MAX_RANKS 8      /* one NVSwitch box */
 #define TM_BLOB_BYTES 512   /* size of one bootstrap blob */
 
+/* OR into the strategy of tm_exchange_init: SUBGD, "summing up the parameter
+ * updates from all GPUs before performing gradient descent" (PAPER L384-389,
+ * the mode of the paper's runs, L458-460): the exchange returns the rank-order
+ * fp32 sum instead of the average (no 1/k); ASA16 rounds the sum to binary16
+ * (TM_E_OVERFLOW16 if it leaves the range).  Not valid with TM_EASGD. */
+#define TM_OP_SUM 0x100
+
 typedef enum {
   TM_AR = 0,     /* plain allreduce                     */
   TM_ASA = 1,    /* Alltoall-sum-Allgather, fp32 wire (L237-246)          */

@@ -14,6 +14,8 @@ Paper anchors:
                      boxes), Allgather of the results.
   L262-269           ASA16: transfer at half precision, sum at full precision.
   L377-384 (Sec. 4)  AWAGD: weights are AVERAGED (1/k) after gradient descent.
+  L384-389, L458-460 SUBGD: the parameter UPDATES are SUMMED (no 1/k); the mode of
+                     the paper's convergence runs.  op="sum" below.
 
 Readings of what the paper leaves open ("Readings"):
   Q1/R1  ASA16 quantises every contribution (own one included) and every rank,
@@ -27,7 +29,7 @@ Readings of what the paper leaves open ("Readings"):
 
 Each fp32 step below is ONE numpy float32 ufunc call (correctly rounded IEEE op).
 
-Parity status: asa_average, asa16_average, ar_average, partition/unpartition,
+Parity status: asa_average, asa16_average, ar_average (op avg and sum), partition/unpartition,
 alltoall, allgather, wire_bytes_per_rank are pinned (tests/test_oracle_exchange.py:
 SPEC worked examples, exact-rational brute force of every rounding step,
 exact-arithmetic special cases, identity invariants, error bounds).
@@ -97,17 +99,23 @@ def _check(X):
     return k, P
 
 
-def _sum_then_divide(received, k):
+def _sum_then_divide(received, k, op="avg"):
     """GPU summation step of Fig. 2 on one owner: ascending source rank, starting
-    from the rank-0 term (Q5), then one IEEE division by k (Q3, Q4)."""
+    from the rank-0 term (Q5), then (op="avg", AWAGD) one IEEE division by k (Q3,
+    Q4); op="sum" (SUBGD) stops after the sum."""
     s = received[0].copy()
     for j in range(1, k):
         s = np.add(s, received[j], dtype=np.float32)
+    if op == "sum":
+        return s
+    if op != "avg":
+        raise ValueError(op)
     return np.divide(s, np.float32(k), dtype=np.float32)
 
 
-def asa_average(X):
-    """ASA (fp32): Alltoall -> sum on owner -> Allgather, averaged by 1/k.
+def asa_average(X, op="avg"):
+    """ASA (fp32): Alltoall -> sum on owner -> Allgather, averaged by 1/k
+    (op="sum": the sum, SUBGD).
 
     X: list of k float32[P] worker buffers.  Returns the list of k results
     (identical on every rank)."""
@@ -116,12 +124,12 @@ def asa_average(X):
         return [X[0].copy()]
     send = [partition(x, k) for x in X]          # sub-arrays, Fig. 2
     recv = alltoall(send)                         # rank r gets sub-array r of all ranks
-    avg = [_sum_then_divide(recv[r], k) for r in range(k)]
+    avg = [_sum_then_divide(recv[r], k, op) for r in range(k)]
     gathered = allgather(avg)
     return [unpartition(gathered[r], P) for r in range(k)]
 
 
-def asa16_average(X):
+def asa16_average(X, op="avg"):
     """ASA16 (reading R1): every sub-array is rounded to binary16 before the
     Alltoall (own one included), widened and summed in fp32 on the owner, divided
     by k, rounded to binary16 for the Allgather, and widened by every receiver
@@ -133,13 +141,13 @@ def asa16_average(X):
     recv = alltoall(send)
     avg16 = []
     for r in range(k):
-        a = _sum_then_divide([widen(h) for h in recv[r]], k)   # fp32 summation
+        a = _sum_then_divide([widen(h) for h in recv[r]], k, op)   # fp32 summation
         avg16.append(rn16(a))                                   # fp16 on the wire
     gathered = allgather(avg16)
     return [widen(unpartition(gathered[r], P)) for r in range(k)]
 
 
-def ar_average(X):
+def ar_average(X, op="avg"):
     """AR: the allreduce-average by definition, elementwise
     fl(...fl(fl(x0 + x1) + x2)... + x_{k-1}) / k, on every rank.  Its value equals
     asa_average's; a real Allreduce may sum in another order, so the GPU AR path
@@ -147,22 +155,23 @@ def ar_average(X):
     k, P = _check(X)
     if k == 1:
         return [X[0].copy()]
-    a = _sum_then_divide(X, k)
+    a = _sum_then_divide(X, k, op)
     return [a.copy() for _ in range(k)]
 
 
-def exchange(X, strategy):
-    """Dispatch by strategy name ('ar', 'asa', 'asa16')."""
+def exchange(X, strategy, op="avg"):
+    """Dispatch by strategy name ('ar', 'asa', 'asa16'); op 'avg' (AWAGD) or
+    'sum' (SUBGD)."""
     if strategy == "ar":
-        return ar_average(X)
+        return ar_average(X, op)
     if strategy == "asa":
-        return asa_average(X)
+        return asa_average(X, op)
     if strategy == "asa16":
-        return asa16_average(X)
+        return asa16_average(X, op)
     raise ValueError(f"unknown strategy {strategy!r}")
 
 
-def element_average(values, strategy):
+def element_average(values, strategy, op="avg"):
     """Result of one element given its k per-rank values (1-D float32 array of
     length k, or [k, n] for n independent elements).  Same steps as the
     strategies above restricted to one index; used for sampled checks at full
@@ -172,9 +181,9 @@ def element_average(values, strategy):
     if k == 1:
         return v[0].copy()
     if strategy in ("ar", "asa"):
-        return _sum_then_divide([v[j] for j in range(k)], k)
+        return _sum_then_divide([v[j] for j in range(k)], k, op)
     if strategy == "asa16":
-        a = _sum_then_divide([widen(rn16(v[j])) for j in range(k)], k)
+        a = _sum_then_divide([widen(rn16(v[j])) for j in range(k)], k, op)
         return widen(rn16(a))
     raise ValueError(strategy)
 

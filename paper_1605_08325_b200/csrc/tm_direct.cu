@@ -28,13 +28,14 @@ using namespace dev;
 // ---------------------------------------------------------------------------
 struct LocalBufs {
   float* b[TM_MAX_RANKS];
+  int sum;  // SUBGD sum mode: no 1/k
 };
 
 // The method's arithmetic on 4 elements of k contributions (registers in, one
 // float4 out): rn16 of each contribution (Q16), ascending-rank sum from the
 // rank-0 term, fl(s/k), rn16 of the average.  `st` accumulates status bits.
 template <int K, bool Q16>
-__device__ __forceinline__ float4 average4(const float4 (&in)[K], uint32_t& st) {
+__device__ __forceinline__ float4 average4(const float4 (&in)[K], uint32_t& st, bool sum) {
   // running max of |bits| screens for non-finite / fp16-overflow inputs
   uint32_t m = max(max(__float_as_uint(in[0].x) & 0x7fffffffu, __float_as_uint(in[0].y) & 0x7fffffffu),
                    max(__float_as_uint(in[0].z) & 0x7fffffffu, __float_as_uint(in[0].w) & 0x7fffffffu));
@@ -53,7 +54,12 @@ __device__ __forceinline__ float4 average4(const float4 (&in)[K], uint32_t& st) 
       st |= status_of(in[j].x, Q16) | status_of(in[j].y, Q16) | status_of(in[j].z, Q16) |
             status_of(in[j].w, Q16);
   }
-  s.x = div_k<K>(s.x); s.y = div_k<K>(s.y); s.z = div_k<K>(s.z); s.w = div_k<K>(s.w);
+  if (!sum) {
+    s.x = div_k<K>(s.x); s.y = div_k<K>(s.y); s.z = div_k<K>(s.z); s.w = div_k<K>(s.w);
+  } else if (Q16) {  // a sum (unlike an average) can leave the binary16 range
+    st |= (status_of(s.x, true) | status_of(s.y, true) | status_of(s.z, true) | status_of(s.w, true)) &
+          TM_BIT_OVERFLOW16;
+  }
   if (Q16) s = q16(s);
   return s;
 }
@@ -69,7 +75,8 @@ __device__ __forceinline__ void average1(const LocalBufs& lb, int64_t i, uint32_
   float s = Q16 ? __half2float(__float2half_rn(in[0])) : in[0];
 #pragma unroll
   for (int j = 1; j < K; ++j) s = __fadd_rn(s, Q16 ? __half2float(__float2half_rn(in[j])) : in[j]);
-  s = div_k<K>(s);
+  if (!lb.sum) s = div_k<K>(s);
+  else if (Q16) st |= status_of(s, true) & TM_BIT_OVERFLOW16;
   if (Q16) s = __half2float(__float2half_rn(s));
 #pragma unroll
   for (int j = 0; j < K; ++j) lb.b[j][i] = s;
@@ -87,7 +94,7 @@ tm_direct_kernel(const __grid_constant__ LocalBufs lb, int64_t e_begin, int64_t 
     float4 in[K];
 #pragma unroll
     for (int j = 0; j < K; ++j) in[j] = ld16_f(lb.b[j] + v * 4);
-    const float4 s = average4<K, Q16>(in, st);
+    const float4 s = average4<K, Q16>(in, st, lb.sum != 0);
 #pragma unroll
     for (int j = 0; j < K; ++j) st16_f(lb.b[j] + v * 4, s);
   }
@@ -164,7 +171,7 @@ tm_direct_tma_kernel(const __grid_constant__ LocalBufs lb, int64_t ntiles, int64
 #pragma unroll
       for (int j = 0; j < K; ++j)
         in[j] = reinterpret_cast<const float4*>(ring + ((size_t)s * K + j) * TILE)[tid + u * kThreads];
-      reinterpret_cast<float4*>(out)[tid + u * kThreads] = average4<K, Q16>(in, st);
+      reinterpret_cast<float4*>(out)[tid + u * kThreads] = average4<K, Q16>(in, st, lb.sum != 0);
     }
     fence_proxy_async_smem();  // generic-proxy smem writes -> visible to the bulk store
     if (tid == 0) bulk_wait_read<kOutRing - 2>();  // out slot of tile i+1 is free
@@ -186,7 +193,7 @@ tm_direct_tma_kernel(const __grid_constant__ LocalBufs lb, int64_t ntiles, int64
       float4 in[K];
 #pragma unroll
       for (int j = 0; j < K; ++j) in[j] = ld16_f(lb.b[j] + v * 4);
-      const float4 r = average4<K, Q16>(in, st);
+      const float4 r = average4<K, Q16>(in, st, lb.sum != 0);
 #pragma unroll
       for (int j = 0; j < K; ++j) st16_f(lb.b[j] + v * 4, r);
     }
@@ -251,9 +258,10 @@ cudaError_t direct_k(const LocalBufs& lb, int64_t P, uint32_t* status, bool q16,
   return cudaGetLastError();
 }
 
-cudaError_t launch_direct(float* const* bufs, int k, int64_t P, bool q16, uint32_t* status,
-                          cudaStream_t s) {
+cudaError_t launch_direct(float* const* bufs, int k, int64_t P, bool q16, bool sum,
+                          uint32_t* status, cudaStream_t s) {
   LocalBufs lb{};
+  lb.sum = sum ? 1 : 0;
   for (int j = 0; j < k; ++j) lb.b[j] = bufs[j];
   int dev = 0;
   cudaGetDevice(&dev);

@@ -30,6 +30,7 @@ struct ExchangeArgs {
   uint32_t* status;               // sticky status word (local)
   int64_t P, L, Lc;               // params, segment length, per-CTA chunk length
   int32_t k, rank0, C;            // ranks, first local rank, CTAs per rank
+  int32_t sum;                    // SUBGD: sum, no 1/k
   uint64_t timeout_ns;
 };
 
@@ -42,8 +43,8 @@ cudaError_t launch_exchange(const ExchangeArgs& a, int nlocal, bool wire16, cuda
 // of each element from the k buffers, fused rn16 (q16) / ascending-rank sum /
 // (1/k) / rn16, push the result to all k buffers.  Also AR when all ranks are
 // local (q16 = false).
-cudaError_t launch_direct(float* const* bufs, int k, int64_t P, bool q16, uint32_t* status,
-                          cudaStream_t s);
+cudaError_t launch_direct(float* const* bufs, int k, int64_t P, bool q16, bool sum,
+                          uint32_t* status, cudaStream_t s);
 
 cudaError_t launch_easgd(float* x, float* c, int64_t n, float alpha, bool concurrent,
                          cudaStream_t s);

@@ -77,6 +77,7 @@ struct Ctx {
   char* rank_base[TM_MAX_RANKS] = {};  // per global rank, as mapped on this device
   uint32_t epoch = 0;
   int path = TM_PATH_AUTO;
+  bool sum = false;  // TM_OP_SUM (SUBGD)
   uint64_t timeout_ns = kDefaultTimeoutNs;
   ncclComm_t comm = nullptr;
   ncclUniqueId nccl_id{};
@@ -132,6 +133,7 @@ ExchangeArgs make_args(float* const* bufs) {
   a.k = g.k;
   a.rank0 = g.rank0;
   a.C = g.C;
+  a.sum = g.sum ? 1 : 0;
   a.timeout_ns = g.timeout_ns;
   return a;
 }
@@ -151,12 +153,13 @@ int do_exchange(float* const* bufs, int nbufs, cudaStream_t s) {
   if (g.k == 1) return TM_OK;  // reading Q10: identity, nothing launched
   cudaSetDevice(g.device);
   if (g.nlocal == g.k && (g.strategy == TM_AR || effective_path() == TM_PATH_DIRECT)) {
-    cudaError_t e = tmx::launch_direct(bufs, g.k, g.P, g.strategy == TM_ASA16, g.status, s);
+    cudaError_t e = tmx::launch_direct(bufs, g.k, g.P, g.strategy == TM_ASA16, g.sum, g.status, s);
     return e == cudaSuccess ? TM_OK : cuda_fail("launch_direct", e);
   }
   if (g.strategy == TM_AR) {
     if (!g.comm) return TM_E_NCCL;
-    ncclResult_t r = g_nccl.AllReduce(bufs[0], bufs[0], (size_t)g.P, ncclFloat32, ncclAvg, g.comm, s);
+    ncclResult_t r = g_nccl.AllReduce(bufs[0], bufs[0], (size_t)g.P, ncclFloat32,
+                                      g.sum ? ncclSum : ncclAvg, g.comm, s);
     return r == ncclSuccess ? TM_OK : TM_E_NCCL;
   }
   ExchangeArgs a = make_args(bufs);
@@ -174,7 +177,10 @@ int tm_exchange_init(int64_t nparams, const tm_world* world, int strategy) {
   std::lock_guard<std::mutex> lk(g_mu);
   if (g.inited) return TM_E_STATE;
   if (!world || nparams < 1) return TM_E_ARG;
+  const bool op_sum = (strategy & TM_OP_SUM) != 0;
+  strategy &= ~TM_OP_SUM;
   if (strategy < TM_AR || strategy > TM_EASGD) return TM_E_ARG;
+  if (op_sum && strategy == TM_EASGD) return TM_E_ARG;
   const int k = world->size;
   if (k < 1 || k > TM_MAX_RANKS) return TM_E_ARG;
   if (world->nlocal != 1 && world->nlocal != k) return TM_E_ARG;
@@ -194,6 +200,7 @@ int tm_exchange_init(int64_t nparams, const tm_world* world, int strategy) {
   c.nlocal = world->nlocal;
   c.device = world->device;
   c.strategy = strategy;
+  c.sum = op_sum;
   c.nprocs = k / world->nlocal;
   c.proc = world->rank / world->nlocal;
   c.L = round_up((nparams + k - 1) / k, tmx::kAlign);
@@ -254,7 +261,7 @@ int tm_bootstrap_export(void* blob, size_t* len) {
   b.rank0 = g.rank0;
   b.nlocal = g.nlocal;
   b.size = g.k;
-  b.strategy = g.strategy;
+  b.strategy = g.strategy | (g.sum ? TM_OP_SUM : 0);
   b.C = g.C;
   b.pid = (int32_t)getpid();
   b.P = g.P;
@@ -291,7 +298,8 @@ int tm_bootstrap_import(const void* blobs, size_t len_each) {
     Blob b;
     memcpy(&b, p + (size_t)q * len_each, sizeof(b));
     if (b.magic != kMagic || b.version != kVersion) return TM_E_ARG;
-    if (b.P != g.P || b.size != g.k || b.strategy != g.strategy || b.C != g.C || b.L != g.L ||
+    if (b.P != g.P || b.size != g.k || b.strategy != (g.strategy | (g.sum ? TM_OP_SUM : 0)) ||
+        b.C != g.C || b.L != g.L ||
         b.Lc != g.Lc || b.nlocal != g.nlocal || b.rank_stride != g.rank_stride ||
         b.rank0 != q * g.nlocal)
       return TM_E_MISMATCH;
@@ -422,7 +430,7 @@ int tm_layout(tm_layout_info* out) {
   out->k = g.k;
   out->rank = g.rank0;
   out->nlocal = g.nlocal;
-  out->strategy = g.strategy;
+  out->strategy = g.strategy | (g.sum ? TM_OP_SUM : 0);
   out->ctas_per_rank = g.C;
   out->threads = tmx::kThreads;
   int sms = 0;

@@ -165,11 +165,17 @@ tm_exchange_kernel(const __grid_constant__ ExchangeArgs a) {
 #pragma unroll
         for (int q = 0; q < E; ++q) s[q] = __fadd_rn(s[q], t[q]);
       }
+      if (!a.sum) {
 #pragma unroll
-      for (int q = 0; q < E; ++q) s[q] = div_k<K>(s[q]);
+        for (int q = 0; q < E; ++q) s[q] = div_k<K>(s[q]);
+      } else if (W16) {  // a sum can leave the binary16 range
+#pragma unroll
+        for (int q = 0; q < E; ++q) st |= status_of(s[q], true) & TM_BIT_OVERFLOW16;
+      }
       st16_cg(avg_r + (e0 + v * E) * WB, U::encode(s));
     }
   }
+  if (st) atomicOr(a.status, st);
 
   if (!rank_barrier<K, SYS>(a, kPhaseReduced, r, c, epoch, &s_abort)) return;
 
@@ -392,8 +398,13 @@ tm_exchange_tma_kernel(const __grid_constant__ ExchangeArgs a) {
 #pragma unroll
               for (int q = 0; q < E; ++q) sm[q] = __fadd_rn(sm[q], t[q]);
             }
+            if (!a.sum) {
 #pragma unroll
-            for (int q = 0; q < E; ++q) sm[q] = div_k<K>(sm[q]);
+              for (int q = 0; q < E; ++q) sm[q] = div_k<K>(sm[q]);
+            } else if (W16) {  // a sum can leave the binary16 range
+#pragma unroll
+              for (int q = 0; q < E; ++q) st |= status_of(sm[q], true) & TM_BIT_OVERFLOW16;
+            }
             reinterpret_cast<uint4*>(out)[v] = U::encode(sm);
           }
         },
@@ -403,6 +414,7 @@ tm_exchange_tma_kernel(const __grid_constant__ ExchangeArgs a) {
           bulk_store(avg_r + e * WB, out, (uint32_t)(n * WB));
         });
   }
+  if (st) atomicOr(a.status, st);
   drain_bulk_stores();
   if (!rank_barrier<K, SYS>(a, kPhaseReduced, r, c, epoch, &s_abort)) return;
   if (tid == 0) fence_proxy_async_global();

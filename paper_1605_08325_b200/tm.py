@@ -21,6 +21,7 @@ STRATEGY = {"ar": TM_AR, "asa": TM_ASA, "asa16": TM_ASA16, "easgd": TM_EASGD}
 TM_OK, TM_E_ARG, TM_E_ALIGN, TM_E_STATE, TM_E_CUDA, TM_E_NCCL = 0, 1, 2, 3, 4, 5
 TM_E_MISMATCH, TM_E_TIMEOUT, TM_E_NONFINITE, TM_E_OVERFLOW16 = 6, 7, 8, 9
 TM_BIT_NONFINITE, TM_BIT_OVERFLOW16, TM_BIT_TIMEOUT = 1, 2, 4
+TM_OP_SUM = 0x100  # SUBGD: sum instead of average
 TM_PATH_AUTO, TM_PATH_STAGED, TM_PATH_DIRECT = 0, 1, 2
 PATH = {"auto": TM_PATH_AUTO, "staged": TM_PATH_STAGED, "direct": TM_PATH_DIRECT}
 TM_BLOB_BYTES = 512
@@ -258,14 +259,17 @@ class Exchanger:
     """
 
     def __init__(self, nparams, strategy, rank=0, size=1, device=None, nlocal=None,
-                 group=None, timeout_s=None, path="auto"):
+                 group=None, timeout_s=None, path="auto", op="avg"):
         if device is None:
             device = torch.cuda.current_device()
         nlocal = size if nlocal is None else nlocal
         self.nparams, self.size, self.nlocal, self.rank = int(nparams), size, nlocal, rank
         self.strategy = strategy
         torch.cuda.set_device(device)
-        tm_exchange_init(nparams, rank, size, device, nlocal, STRATEGY[strategy])
+        if op not in ("avg", "sum"):
+            raise ValueError(op)
+        tm_exchange_init(nparams, rank, size, device, nlocal,
+                         STRATEGY[strategy] | (TM_OP_SUM if op == "sum" else 0))
         if timeout_s is not None:
             tm_set_timeout_ns(int(timeout_s * 1e9))
         if path != "auto":

@@ -4,7 +4,7 @@ all_gather_object.  Used by tests/test_gpu_multiprocess.py; on a one-GPU box
 every rank uses cuda:0 (IPC between processes on one device), on a multi-GPU
 box rank r uses cuda:r.
 
-argv: outdir strategy P dist mode      (mode: normal | skip1 | mismatch)
+argv: outdir strategy P dist mode      (mode: normal | sum | skip1 | mismatch)
 """
 
 import json
@@ -34,7 +34,8 @@ def main():
     Pr = P + (1 if (mode == "mismatch" and rank == 1) else 0)
     try:
         ex = tm.Exchanger(Pr, strategy, rank=rank, size=size, device=device, nlocal=1,
-                          timeout_s=(1.0 if mode == "skip1" else 20.0))
+                          timeout_s=(1.0 if mode == "skip1" else 20.0),
+                          op=("sum" if mode == "sum" else "avg"))
     except tm.TmError as e:
         result["init_error"] = e.code
         json.dump(result, open(os.path.join(outdir, f"rank{rank}.json"), "w"))

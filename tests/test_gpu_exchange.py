@@ -252,3 +252,39 @@ def test_cuda_graph_capture_and_replay(strategy, path):
                 assert_bitwise(out[r], want[r], f"{strategy} {path} replay {it} rank {r}")
         code, _ = ex.status()
         assert code == tm.TM_OK
+
+
+@pytest.mark.parametrize("path", PATHS)
+@pytest.mark.parametrize("strategy", ["asa", "asa16", "ar"])
+def test_subgd_sum_mode(strategy, path):
+    """TM_OP_SUM (SUBGD): the rank-order sum, no 1/k."""
+    for k in (2, 3, 8):
+        for P in (7, 4099, 100_003):
+            X = worker_buffers(P, k, "D2", config=80)
+            bufs = to_dev(X)
+            with tm.Exchanger(P, strategy, size=k, nlocal=k, path=path, op="sum") as ex:
+                ex.exchange(bufs)
+                code, _ = ex.status()
+                assert ex.layout()["strategy"] & tm.TM_OP_SUM
+            assert code == tm.TM_OK
+            out = to_host(bufs)
+            want = ox.exchange(X, strategy, op="sum")
+            for r in range(k):
+                assert_bitwise(out[r], want[r], f"sum {strategy} {path} k={k} P={P} rank {r}")
+
+
+@pytest.mark.parametrize("path", PATHS)
+def test_subgd_sum_overflows_binary16(path):
+    """A sum (unlike an average) can leave the binary16 range: 40000 + 40000 ->
+    +inf on the wire, TM_E_OVERFLOW16 reported."""
+    P = 4099
+    X = [np.full(P, 1.0, np.float32), np.full(P, 1.0, np.float32)]
+    X[0][123] = X[1][123] = np.float32(40000.0)
+    X[0][P - 1] = X[1][P - 1] = np.float32(-40000.0)  # scalar tail of the direct path
+    bufs = to_dev(X)
+    with tm.Exchanger(P, "asa16", size=2, nlocal=2, path=path, op="sum") as ex:
+        ex.exchange(bufs)
+        code, bits = ex.status()
+    assert code == tm.TM_E_OVERFLOW16 and bits == tm.TM_BIT_OVERFLOW16
+    out = to_host(bufs)
+    assert np.isposinf(out[0][123]) and np.isneginf(out[1][P - 1]) and out[0][5] == 2.0

@@ -49,14 +49,15 @@ def launch(tmp_path, k, strategy, P, dist, mode="normal", timeout=240):
     return res
 
 
-@pytest.mark.parametrize("strategy,k", [("asa16", 2), ("asa", 2), ("asa16", 3)])
-def test_multiprocess_bitwise(tmp_path, strategy, k):
+@pytest.mark.parametrize("strategy,k,op", [("asa16", 2, "avg"), ("asa", 2, "avg"), ("asa16", 3, "avg"),
+                                           ("asa16", 2, "sum")])
+def test_multiprocess_bitwise(tmp_path, strategy, k, op):
     P = 100_003
-    res = launch(tmp_path, k, strategy, P, "D2")
+    res = launch(tmp_path, k, strategy, P, "D2", mode=("sum" if op == "sum" else "normal"))
     X = [worker_buffer(P, "D2", r, config=50) for r in range(k)]
     want = X
     for _ in range(3):
-        want = ox.exchange(want, strategy)
+        want = ox.exchange(want, strategy, op=op)
     for r in range(k):
         assert res[r]["code"] == 0, res[r]
         got = np.load(os.path.join(tmp_path, f"rank{r}.npy"))

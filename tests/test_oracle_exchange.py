@@ -270,3 +270,60 @@ def test_traffic_accounting_spec():
             assert 2 * ex.wire_bytes_per_rank("asa16", P, k) == ex.wire_bytes_per_rank("asa", P, k)
             assert ex.wire_bytes_per_rank("asa", P, k) == 2 * (k - 1) * (-(-P // k)) * 4
     assert ex.wire_bytes_per_rank("asa16", 123, 1) == 0
+
+
+# ------------------------------------------------------------- SUBGD sum mode
+
+def test_spec_sum_examples():
+    # k=2 [1,2,3,4] + [10,20,30,40] -> sums [11,22,33,44]
+    X = [np.array([1, 2, 3, 4], F32), np.array([10, 20, 30, 40], F32)]
+    for strat in ("ar", "asa", "asa16"):
+        for o in ex.exchange(X, strat, op="sum"):
+            assert o.tolist() == [11.0, 22.0, 33.0, 44.0], strat
+    # k=2, [0.1] + [0.1] in ASA16 -> 0.199951171875
+    X = [np.array([0.1], F32), np.array([0.1], F32)]
+    for o in ex.asa16_average(X, op="sum"):
+        assert float(o[0]) == 0.199951171875
+
+
+def _brute_sum(values, k, q16):
+    h = [exact.to16(v) if q16 else float(v) for v in values]
+    s = h[0]
+    for j in range(1, k):
+        s = exact.add(s, h[j])
+    return exact.to16(s) if q16 else s
+
+
+@pytest.mark.parametrize("dist", DISTS)
+@pytest.mark.parametrize("k", [2, 3, 5, 8])
+def test_sum_brute_force(dist, k):
+    for P in (1, 6):
+        X = worker_buffers(P, k, dist, config=12)
+        o = ex.asa_average(X, op="sum")
+        o16 = ex.asa16_average(X, op="sum")
+        oar = ex.ar_average(X, op="sum")
+        for i in range(P):
+            vals = [float(x[i]) for x in X]
+            assert exact.same_bits32(o[1][i], _brute_sum(vals, k, False))
+            assert exact.same_bits32(oar[0][i], _brute_sum(vals, k, False))
+            assert exact.same_bits32(o16[k - 1][i], _brute_sum(vals, k, True))
+
+
+@pytest.mark.parametrize("k", [2, 4, 8])
+def test_sum_is_k_times_average_for_power_of_two_k(k):
+    """For k = 2^n, fl(s / k) = s / k exactly for normal s, so the SUBGD sum is
+    k times the AWAGD average bitwise (D1: no fp32 subnormal averages)."""
+    X = worker_buffers(20000, k, "D1", config=13)
+    s = ex.asa_average(X, op="sum")[0]
+    a = ex.asa_average(X)[0]
+    assert_bitwise(s, (a.astype(np.float64) * k).astype(F32))
+
+
+@pytest.mark.parametrize("k", [2, 4, 8])
+def test_asa16_sum_exact_on_small_integers(k):
+    """Integers in [-256, 256]: every partial sum is an integer of magnitude <=
+    2048, exact in binary16, so the ASA16 sum is the exact sum."""
+    X = worker_buffers(5001, k, "D5", config=14)
+    exact_sum = np.sum(np.stack(X).astype(np.float64), axis=0).astype(F32)
+    for o in ex.asa16_average(X, op="sum"):
+        assert_bitwise(o, exact_sum)
