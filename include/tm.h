@@ -168,6 +168,19 @@ int tm_exchange(float* dev_buf, void* stream);
  * pairwise disjoint. */
 int tm_exchange_group(float* const* dev_bufs, int nbufs, void* stream);
 
+/* Exchange only elements [offset, offset + count) of the buffer(s): a bucket,
+ * e.g. one layer's parameters, so that buckets can be exchanged while backward
+ * is still producing the next ones -- the overlap the paper leaves as future
+ * work.  Same result as tm_exchange on those
+ * elements (the method is elementwise); the range is partitioned into k
+ * segments of its own.  offset must be a multiple of 4 (16-byte alignment),
+ * 0 <= offset, offset + count <= nparams.  Ranges of one exchanger are
+ * serialised by stream order: issue them on one stream, or order streams with
+ * events; every rank issues the same ranges in the same order. */
+int tm_exchange_range(float* dev_buf, int64_t offset, int64_t count, void* stream);
+int tm_exchange_group_range(float* const* dev_bufs, int nbufs, int64_t offset, int64_t count,
+                            void* stream);
+
 /* North-star call: one elastic update of nparams elements:
  *   d = fl(x - c); e = fl(alpha*d); x = fl(x - e); c = fl(c + e)   (no FMA)
  * worker_buf: this rank's fp32 buffer; center_buf: any fp32 buffer addressable

@@ -29,7 +29,8 @@ struct ExchangeArgs {
   float* x[TM_MAX_RANKS];         // user buffers of the LOCAL ranks (index r - rank0)
   uint32_t* status;               // sticky status word (local)
   int64_t P, L, Lc;               // params, segment length, per-CTA chunk length
-  int32_t k, rank0, C;            // ranks, first local rank, CTAs per rank
+  int32_t k, rank0, C;            // ranks, first local rank, CTAs per rank (this call)
+  int32_t flag_stride;            // C the flag pad was laid out for (>= C)
   int32_t sum;                    // SUBGD: sum, no 1/k
   uint64_t timeout_ns;
 };

@@ -118,21 +118,33 @@ void release() {
   g = Ctx();
 }
 
-ExchangeArgs make_args(float* const* bufs) {
+// Launch arguments for an exchange of elements [off, off + n) of the callers'
+// buffers.  The range gets a segmented layout of its own (a1): L' =
+// roundup(ceil(n/k), 256) <= L, so it fits the staging allocated for P; C' <= C
+// CTAs per rank, and the flag pad keeps the stride C it was laid out with.
+ExchangeArgs make_args(float* const* bufs, int64_t off, int64_t n) {
   ExchangeArgs a{};
   for (int j = 0; j < g.k; ++j) {
     a.stage[j] = g.rank_base[j] + g.off_stage;
     a.avg[j] = g.rank_base[j] + g.off_avg;
     a.flags[j] = reinterpret_cast<uint32_t*>(g.rank_base[j] + g.off_flags);
   }
-  for (int i = 0; i < g.nlocal; ++i) a.x[i] = bufs[i];
+  for (int i = 0; i < g.nlocal; ++i) a.x[i] = bufs[i] + off;
   a.status = g.status;
-  a.P = g.P;
-  a.L = g.L;
-  a.Lc = g.Lc;
+  a.P = n;
+  if (off == 0 && n == g.P) {
+    a.L = g.L;
+    a.Lc = g.Lc;
+    a.C = g.C;
+  } else {
+    a.L = round_up((n + g.k - 1) / g.k, tmx::kAlign);
+    const int64_t want = std::max<int64_t>(1, (a.L + tmx::kMinChunk - 1) / tmx::kMinChunk);
+    a.C = (int)std::min<int64_t>(g.C, want);
+    a.Lc = round_up((a.L + a.C - 1) / a.C, tmx::kAlign);
+  }
+  a.flag_stride = g.C;
   a.k = g.k;
   a.rank0 = g.rank0;
-  a.C = g.C;
   a.sum = g.sum ? 1 : 0;
   a.timeout_ns = g.timeout_ns;
   return a;
@@ -143,26 +155,30 @@ int effective_path() {
   return g.nlocal == g.k ? TM_PATH_DIRECT : TM_PATH_STAGED;
 }
 
-int do_exchange(float* const* bufs, int nbufs, cudaStream_t s) {
+int do_exchange(float* const* bufs, int nbufs, int64_t off, int64_t n, cudaStream_t s) {
   if (!g.inited || !g.ready || g.strategy == TM_EASGD) return TM_E_STATE;
   if (nbufs != g.nlocal || !bufs) return TM_E_ARG;
+  if (off < 0 || n < 0 || off + n > g.P) return TM_E_ARG;
+  if (off % 4) return TM_E_ALIGN;
   for (int i = 0; i < nbufs; ++i) {
     if (!bufs[i]) return TM_E_ARG;
     if (!aligned16(bufs[i])) return TM_E_ALIGN;
   }
-  if (g.k == 1) return TM_OK;  // reading Q10: identity, nothing launched
+  if (g.k == 1 || n == 0) return TM_OK;  // reading Q10: identity, nothing launched
   cudaSetDevice(g.device);
   if (g.nlocal == g.k && (g.strategy == TM_AR || effective_path() == TM_PATH_DIRECT)) {
-    cudaError_t e = tmx::launch_direct(bufs, g.k, g.P, g.strategy == TM_ASA16, g.sum, g.status, s);
+    float* shifted[TM_MAX_RANKS];
+    for (int i = 0; i < nbufs; ++i) shifted[i] = bufs[i] + off;
+    cudaError_t e = tmx::launch_direct(shifted, g.k, n, g.strategy == TM_ASA16, g.sum, g.status, s);
     return e == cudaSuccess ? TM_OK : cuda_fail("launch_direct", e);
   }
   if (g.strategy == TM_AR) {
     if (!g.comm) return TM_E_NCCL;
-    ncclResult_t r = g_nccl.AllReduce(bufs[0], bufs[0], (size_t)g.P, ncclFloat32,
+    ncclResult_t r = g_nccl.AllReduce(bufs[0] + off, bufs[0] + off, (size_t)n, ncclFloat32,
                                       g.sum ? ncclSum : ncclAvg, g.comm, s);
     return r == ncclSuccess ? TM_OK : TM_E_NCCL;
   }
-  ExchangeArgs a = make_args(bufs);
+  ExchangeArgs a = make_args(bufs, off, n);
   cudaError_t e = tmx::launch_exchange(a, g.nlocal, wire16(g.strategy), s);
   if (e != cudaSuccess) return cuda_fail("launch_exchange", e);
   ++g.epoch;  // host-side count for tm_layout; the kernels keep their own
@@ -326,12 +342,25 @@ int tm_exchange(float* dev_buf, void* stream) {
   std::lock_guard<std::mutex> lk(g_mu);
   if (g.inited && g.nlocal != 1) return TM_E_STATE;
   float* bufs[1] = {dev_buf};
-  return do_exchange(bufs, 1, static_cast<cudaStream_t>(stream));
+  return do_exchange(bufs, 1, 0, g.P, static_cast<cudaStream_t>(stream));
 }
 
 int tm_exchange_group(float* const* dev_bufs, int nbufs, void* stream) {
   std::lock_guard<std::mutex> lk(g_mu);
-  return do_exchange(dev_bufs, nbufs, static_cast<cudaStream_t>(stream));
+  return do_exchange(dev_bufs, nbufs, 0, g.P, static_cast<cudaStream_t>(stream));
+}
+
+int tm_exchange_range(float* dev_buf, int64_t offset, int64_t count, void* stream) {
+  std::lock_guard<std::mutex> lk(g_mu);
+  if (g.inited && g.nlocal != 1) return TM_E_STATE;
+  float* bufs[1] = {dev_buf};
+  return do_exchange(bufs, 1, offset, count, static_cast<cudaStream_t>(stream));
+}
+
+int tm_exchange_group_range(float* const* dev_bufs, int nbufs, int64_t offset, int64_t count,
+                            void* stream) {
+  std::lock_guard<std::mutex> lk(g_mu);
+  return do_exchange(dev_bufs, nbufs, offset, count, static_cast<cudaStream_t>(stream));
 }
 
 int tm_easgd_update(float* worker_buf, float* center_buf, float alpha, void* stream) {

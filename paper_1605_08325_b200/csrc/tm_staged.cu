@@ -55,9 +55,9 @@ __device__ __forceinline__ bool rank_barrier(const ExchangeArgs& a, int phase, i
   __syncthreads();
   if (threadIdx.x < K) {
     const int j = threadIdx.x;
-    uint32_t* remote = a.flags[j] + (size_t)(phase * TM_MAX_RANKS + r) * a.C + c;
+    uint32_t* remote = a.flags[j] + (size_t)(phase * TM_MAX_RANKS + r) * a.flag_stride + c;
     st_release<SYS>(remote, epoch);
-    const uint32_t* mine = a.flags[r] + (size_t)(phase * TM_MAX_RANKS + j) * a.C + c;
+    const uint32_t* mine = a.flags[r] + (size_t)(phase * TM_MAX_RANKS + j) * a.flag_stride + c;
     if ((int32_t)(ld_acquire<SYS>(mine) - epoch) < 0) {
       const uint64_t t0 = globaltimer();
       while ((int32_t)(ld_acquire<SYS>(mine) - epoch) < 0) {
@@ -93,7 +93,7 @@ tm_exchange_kernel(const __grid_constant__ ExchangeArgs a) {
   // which makes the exchange capturable in a CUDA graph.
   if (threadIdx.x == 0) {
     s_abort = 0;
-    uint32_t* ctr = a.flags[r] + (size_t)kPhases * TM_MAX_RANKS * a.C + c;
+    uint32_t* ctr = a.flags[r] + (size_t)kPhases * TM_MAX_RANKS * a.flag_stride + c;
     s_epoch = *ctr + 1;
     *ctr = s_epoch;
   }
@@ -305,7 +305,7 @@ tm_exchange_tma_kernel(const __grid_constant__ ExchangeArgs a) {
 
   if (tid == 0) {
     s_abort = 0;
-    uint32_t* ctr = a.flags[r] + (size_t)kPhases * TM_MAX_RANKS * a.C + c;  // device epoch
+    uint32_t* ctr = a.flags[r] + (size_t)kPhases * TM_MAX_RANKS * a.flag_stride + c;  // device epoch
     s_epoch = *ctr + 1;
     *ctr = s_epoch;
     for (int i = 0; i < kInSlots; ++i) mbar_init(&full[i], 1);

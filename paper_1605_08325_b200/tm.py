@@ -58,6 +58,9 @@ _SIGS = {
     "tm_bootstrap_import": (ctypes.c_int, [_P, ctypes.c_size_t]),
     "tm_exchange": (ctypes.c_int, [_P, _P]),
     "tm_exchange_group": (ctypes.c_int, [ctypes.POINTER(_P), ctypes.c_int, _P]),
+    "tm_exchange_range": (ctypes.c_int, [_P, ctypes.c_int64, ctypes.c_int64, _P]),
+    "tm_exchange_group_range": (ctypes.c_int, [ctypes.POINTER(_P), ctypes.c_int, ctypes.c_int64,
+                                               ctypes.c_int64, _P]),
     "tm_easgd_update": (ctypes.c_int, [_P, _P, ctypes.c_float, _P]),
     "tm_easgd_update_ex": (ctypes.c_int, [_P, _P, ctypes.c_int64, ctypes.c_float, ctypes.c_int, _P]),
     "tm_easgd_round": (ctypes.c_int, [ctypes.POINTER(_P), ctypes.c_int, ctypes.POINTER(ctypes.c_int32),
@@ -155,6 +158,17 @@ def tm_exchange(buf, stream=None):
 def tm_exchange_group(bufs, stream=None):
     arr = (ctypes.c_void_p * len(bufs))(*[_fp32_cuda(b).value for b in bufs])
     _check(lib().tm_exchange_group(arr, len(bufs), _stream_handle(stream)), "tm_exchange_group")
+
+
+def tm_exchange_range(buf, offset, count, stream=None):
+    _check(lib().tm_exchange_range(_fp32_cuda(buf), int(offset), int(count), _stream_handle(stream)),
+           "tm_exchange_range")
+
+
+def tm_exchange_group_range(bufs, offset, count, stream=None):
+    arr = (ctypes.c_void_p * len(bufs))(*[_fp32_cuda(b).value for b in bufs])
+    _check(lib().tm_exchange_group_range(arr, len(bufs), int(offset), int(count),
+                                         _stream_handle(stream)), "tm_exchange_group_range")
 
 
 def tm_easgd_update(worker, center, alpha, stream=None):
@@ -282,6 +296,13 @@ class Exchanger:
             tm_exchange(bufs, stream)
         else:
             tm_exchange_group(list(bufs), stream)
+
+    def exchange_range(self, bufs, offset, count, stream=None):
+        """Exchange elements [offset, offset + count) only (one bucket)."""
+        if isinstance(bufs, torch.Tensor):
+            tm_exchange_range(bufs, offset, count, stream)
+        else:
+            tm_exchange_group_range(list(bufs), offset, count, stream)
 
     def status(self, stream=None):
         return tm_exchange_status(stream)

@@ -4,7 +4,7 @@ all_gather_object.  Used by tests/test_gpu_multiprocess.py; on a one-GPU box
 every rank uses cuda:0 (IPC between processes on one device), on a multi-GPU
 box rank r uses cuda:r.
 
-argv: outdir strategy P dist mode      (mode: normal | sum | skip1 | mismatch)
+argv: outdir strategy P dist mode      (mode: normal | sum | range | skip1 | mismatch)
 """
 
 import json
@@ -71,7 +71,13 @@ def main():
     if mode == "skip1" and rank == 1:
         reps = 0  # never arrives: rank 0 must time out, not hang
     for _ in range(reps):
-        ex.exchange(x)
+        if mode == "range":  # three buckets, last first (backward order)
+            b1, b2 = P // 3 // 4 * 4, 2 * P // 3 // 4 * 4
+            ex.exchange_range(x, b2, P - b2)
+            ex.exchange_range(x, b1, b2 - b1)
+            ex.exchange_range(x, 0, b1)
+        else:
+            ex.exchange(x)
         # re-run on fresh inputs so each call is checked
         if _ < reps - 1:
             torch.cuda.synchronize()

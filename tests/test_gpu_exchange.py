@@ -288,3 +288,53 @@ def test_subgd_sum_overflows_binary16(path):
     assert code == tm.TM_E_OVERFLOW16 and bits == tm.TM_BIT_OVERFLOW16
     out = to_host(bufs)
     assert np.isposinf(out[0][123]) and np.isneginf(out[1][P - 1]) and out[0][5] == 2.0
+
+
+# AlexNet per-layer (W + b) parameter counts (PAPER Table 3 total 60,965,224;
+# SURVEY Appendix A1), scaled by 1/32 and rounded to multiples of 4.
+ALEXNET_LAYERS = [34_944, 307_456, 885_120, 663_936, 442_624, 37_752_832, 16_781_312, 4_097_000]
+SCALED_LAYERS = [max(4, (n // 32) // 4 * 4) for n in ALEXNET_LAYERS]
+
+
+@pytest.mark.parametrize("path", PATHS)
+@pytest.mark.parametrize("strategy", ["asa16", "asa", "ar"])
+def test_bucketed_range_exchange_equals_full(strategy, path):
+    """Per-layer buckets exchanged in backward order (fc8 first) with
+    tm_exchange_group_range give exactly the full exchange (elementwise method);
+    elements outside a bucket are untouched by it."""
+    k = 4
+    P = sum(SCALED_LAYERS) + 3  # + a ragged tail bucket
+    sizes = SCALED_LAYERS + [3]
+    offs = np.concatenate([[0], np.cumsum(sizes)[:-1]]).astype(np.int64)
+    X = worker_buffers(P, k, "D2", config=90)
+    bufs = to_dev(X)
+    with tm.Exchanger(P, strategy, size=k, nlocal=k, path=path) as ex:
+        # first bucket alone: the rest of the buffer must be unchanged
+        ex.exchange_range(bufs, int(offs[-2]), sizes[-2])
+        part = to_host(bufs)
+        untouched = np.ones(P, bool)
+        untouched[offs[-2]: offs[-2] + sizes[-2]] = False
+        for r in range(k):
+            assert_bitwise(part[r][untouched], X[r][untouched], "outside the bucket")
+        for off, n in list(zip(offs, sizes))[::-1][2:]:
+            ex.exchange_range(bufs, int(off), int(n))
+        ex.exchange_range(bufs, int(offs[-1]), sizes[-1])
+        code, _ = ex.status()
+    assert code == tm.TM_OK
+    out = to_host(bufs)
+    want = ox.exchange(X, strategy)
+    for r in range(k):
+        assert_bitwise(out[r], want[r], f"bucketed {strategy} {path} rank {r}")
+
+
+def test_range_argument_errors():
+    P = 4096
+    with tm.Exchanger(P, "asa16", size=2, nlocal=2):
+        b = [torch.zeros(P, device="cuda") for _ in range(2)]
+        with pytest.raises(tm.TmError) as e:
+            tm.tm_exchange_group_range(b, 2, 100)  # offset not a multiple of 4
+        assert e.value.code == tm.TM_E_ALIGN
+        with pytest.raises(tm.TmError) as e:
+            tm.tm_exchange_group_range(b, 4000, 100)  # past nparams
+        assert e.value.code == tm.TM_E_ARG
+        tm.tm_exchange_group_range(b, 0, 0)  # empty range: no-op

@@ -50,10 +50,11 @@ def launch(tmp_path, k, strategy, P, dist, mode="normal", timeout=240):
 
 
 @pytest.mark.parametrize("strategy,k,op", [("asa16", 2, "avg"), ("asa", 2, "avg"), ("asa16", 3, "avg"),
-                                           ("asa16", 2, "sum")])
+                                           ("asa16", 2, "sum"), ("asa16", 2, "range")])
 def test_multiprocess_bitwise(tmp_path, strategy, k, op):
     P = 100_003
-    res = launch(tmp_path, k, strategy, P, "D2", mode=("sum" if op == "sum" else "normal"))
+    res = launch(tmp_path, k, strategy, P, "D2", mode=("normal" if op == "avg" else op))
+    op = "sum" if op == "sum" else "avg"  # bucketed ranges give the full exchange
     X = [worker_buffer(P, "D2", r, config=50) for r in range(k)]
     want = X
     for _ in range(3):
