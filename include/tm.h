@@ -220,6 +220,22 @@ int tm_easgd_center(int owner_rank, float** center);
  * scope across processes), no lost updates, order not fixed. */
 int tm_easgd_update_sharded(float* worker_buf, float alpha, int concurrent, void* stream);
 
+/* Per-worker ATOMIC exchange with the sharded centre (the server
+ * never interleaves two half-completed exchanges; workers are
+ * served in arrival order, no Round-Robin): the centre is updated in chunks of
+ * 4096 elements, each under a spin lock (system-scope atomics across
+ * processes), so several workers may call concurrently (any streams, any
+ * processes) and every chunk ends up exactly as the serial EASGD sequence in
+ * that chunk's arrival order.  worker_id is recorded in the order log (test
+ * hook below).  A lock not obtained within the timeout sets TM_E_TIMEOUT. */
+int tm_easgd_update_locked(float* worker_buf, int worker_id, float alpha, void* stream);
+
+/* Test hook: record, for every (shard s, chunk q), the worker_ids of locked
+ * updates in arrival order into dev_log[(s*nchunk + q)*max + t] (int32,
+ * device memory owned by the caller, nchunk = ceil(seg_len/4096)); resets this
+ * process's tickets.  NULL disables. */
+int tm_easgd_set_order_log(int32_t* dev_log, int max_updates_per_chunk);
+
 /* Synchronise `stream`, then return the most severe sticky status
  * (TM_E_TIMEOUT > TM_E_OVERFLOW16 > TM_E_NONFINITE > TM_OK) and clear it.
  * `bits` (optional) receives the TM_BIT_* mask. */

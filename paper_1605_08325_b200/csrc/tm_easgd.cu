@@ -105,6 +105,92 @@ easgd_sharded_kernel(float* __restrict__ x, const __grid_constant__ ShardArgs sa
   }
 }
 
+// Locked (atomic per-chunk) update against the sharded centre.  Work item =
+// one chunk of kLockChunk elements of one shard.  Thread 0 takes the chunk's
+// spin lock (atomicCAS, system scope when peers are other GPUs), fences, and
+// takes a ticket (the arrival position, logged for tests); the CTA applies the
+// exclusive elastic update to the chunk (centre read/written through L2, .cg);
+// every thread fences its writes, the CTA syncs, thread 0 releases the lock.
+// A chunk is thus updated by one worker at a time, in arrival order: bitwise
+// the serial EASGD sequence of that chunk's arrival order.
+template <bool SYS>
+__device__ __forceinline__ uint32_t cas_u32(uint32_t* p, uint32_t cmp, uint32_t val) {
+  if constexpr (SYS) return atomicCAS_system(p, cmp, val);
+  else return atomicCAS(p, cmp, val);
+}
+template <bool SYS>
+__device__ __forceinline__ void fence_scope() {
+  if constexpr (SYS) __threadfence_system();
+  else __threadfence();
+}
+
+template <bool SYS>
+__global__ void __launch_bounds__(kThreads)
+easgd_locked_kernel(float* __restrict__ x, const __grid_constant__ ShardArgs sa, float alpha) {
+  __shared__ int s_go;
+  const int64_t nch = (sa.L + kLockChunk - 1) / kLockChunk;  // chunks per shard
+  const int64_t total = (int64_t)sa.k * nch;
+  for (int64_t it = blockIdx.x; it < total; it += gridDim.x) {
+    const int s = (int)(it / nch);
+    const int64_t q = it - (int64_t)s * nch;
+    const int64_t len_s = min(sa.L, sa.P - (int64_t)s * sa.L);
+    const int64_t c0 = q * kLockChunk;
+    if (c0 >= len_s) continue;  // uniform across the CTA
+    const int64_t n = min(kLockChunk, len_s - c0);
+    if (threadIdx.x == 0) {
+      uint32_t* lock = sa.locks[s] + q;
+      int go = 1;
+      if (cas_u32<SYS>(lock, 0u, 1u) != 0u) {
+        const uint64_t t0 = globaltimer();
+        while (cas_u32<SYS>(lock, 0u, 1u) != 0u) {
+          if (globaltimer() - t0 > sa.timeout_ns) {
+            atomicOr(sa.status, TM_BIT_TIMEOUT);
+            go = 0;
+            break;
+          }
+          __nanosleep(64);
+        }
+      }
+      if (go) {
+        fence_scope<SYS>();  // acquire: the previous holder's centre writes
+        // ticket: the arrival position (an atomic so no stale L1 line is read)
+        const uint32_t t = SYS ? atomicAdd_system(sa.tickets[s] + q, 1u) : atomicAdd(sa.tickets[s] + q, 1u);
+        if (sa.order_log) sa.order_log[((int64_t)s * nch + q) * sa.log_stride + t] = sa.worker_id;
+      }
+      s_go = go;
+    }
+    __syncthreads();
+    if (!s_go) return;
+    float* c = sa.shard[s] + c0;
+    float* xs = x + (int64_t)s * sa.L + c0;
+    for (int64_t v = threadIdx.x; v < n / 4; v += kThreads) {
+      float4 xv = ld16_f(xs + v * 4);
+      float4 cv = __ldcg(reinterpret_cast<const float4*>(c + v * 4));
+      const float ex = elastic_diff(xv.x, cv.x, alpha), ey = elastic_diff(xv.y, cv.y, alpha);
+      const float ez = elastic_diff(xv.z, cv.z, alpha), ew = elastic_diff(xv.w, cv.w, alpha);
+      xv.x = __fsub_rn(xv.x, ex); xv.y = __fsub_rn(xv.y, ey);
+      xv.z = __fsub_rn(xv.z, ez); xv.w = __fsub_rn(xv.w, ew);
+      cv.x = __fadd_rn(cv.x, ex); cv.y = __fadd_rn(cv.y, ey);
+      cv.z = __fadd_rn(cv.z, ez); cv.w = __fadd_rn(cv.w, ew);
+      st16_f(xs + v * 4, xv);
+      __stcg(reinterpret_cast<float4*>(c + v * 4), cv);
+    }
+    for (int64_t i = (n / 4) * 4 + threadIdx.x; i < n; i += kThreads) {
+      const float xi = xs[i];
+      const float ci = __ldcg(c + i);
+      const float e = elastic_diff(xi, ci, alpha);
+      xs[i] = __fsub_rn(xi, e);
+      __stcg(c + i, __fadd_rn(ci, e));
+    }
+    fence_scope<SYS>();  // release: this thread's centre writes before the unlock
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      if (SYS) atomicExch_system(sa.locks[s] + q, 0u);
+      else atomicExch(sa.locks[s] + q, 0u);
+    }
+  }
+}
+
 // A whole server round in arrival order, fused: the centre is read once and
 // written once; worker w's update uses the centre left by the previous one.
 // Bitwise equal to serial updates in `order` (each element is independent).
@@ -265,6 +351,16 @@ cudaError_t launch_easgd_sharded(float* x, const ShardArgs& sa, float alpha, boo
   } else {
     easgd_sharded_kernel<false, false><<<grid, kThreads, 0, s>>>(x, sa, alpha);
   }
+  return cudaGetLastError();
+}
+
+cudaError_t launch_easgd_locked(float* x, const ShardArgs& sa, float alpha, cudaStream_t s) {
+  const int64_t nch = (sa.L + kLockChunk - 1) / kLockChunk;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const int grid = (int)std::min<int64_t>(std::max<int64_t>(sa.k * nch, 1), 4 * sm_count(dev));
+  if (sa.sys) easgd_locked_kernel<true><<<grid, kThreads, 0, s>>>(x, sa, alpha);
+  else easgd_locked_kernel<false><<<grid, kThreads, 0, s>>>(x, sa, alpha);
   return cudaGetLastError();
 }
 

@@ -54,12 +54,24 @@ cudaError_t launch_easgd_round(float* const* w, int nw, const int32_t* order, in
 // EASGD against a centre sharded by segment: shard[s] holds c[s*L, (s+1)*L).
 struct ShardArgs {
   float* shard[TM_MAX_RANKS];
+  uint32_t* locks[TM_MAX_RANKS];    // per-chunk spin locks of shard s (locked mode)
+  uint32_t* tickets[TM_MAX_RANKS];  // per-chunk count of applied updates (locked mode)
+  int32_t* order_log;               // test hook: [s*nchunk + q][log_stride] worker ids
+  int32_t log_stride;
+  int32_t worker_id;
   int32_t k;
   int64_t L, P;
   bool sys;
+  uint32_t* status;
+  uint64_t timeout_ns;
 };
+constexpr int64_t kLockChunk = 4096;  // elements per lock in locked EASGD
 cudaError_t launch_easgd_sharded(float* x, const ShardArgs& sa, float alpha, bool concurrent,
                                  cudaStream_t s);
+// Locked mode: each (shard, chunk) is updated under a spin lock, so every
+// worker's update of an element is one atomic read-modify-write of the centre
+// (per-worker atomic exchange) in arrival order.
+cudaError_t launch_easgd_locked(float* x, const ShardArgs& sa, float alpha, cudaStream_t s);
 cudaError_t launch_cast_rn16(const float* in, uint16_t* out, int64_t n, cudaStream_t s);
 
 // Max co-resident CTAs of the exchange kernel on `device` (occupancy * SMs).

@@ -70,6 +70,9 @@ struct Ctx {
   int k = 0, rank0 = 0, nlocal = 0, device = 0, strategy = 0, C = 0;
   int nprocs = 1, proc = 0;
   int64_t rank_stride = 0, off_stage = 0, off_avg = 0, off_flags = 0, off_center = 0;
+  int64_t off_locks = 0, off_tickets = 0;  // EASGD locked mode
+  int32_t* order_log = nullptr;            // test hook (tm_easgd_set_order_log)
+  int order_log_stride = 0;
   int64_t slab_bytes = 0;
   char* slab = nullptr;
   uint32_t* status = nullptr;
@@ -235,7 +238,10 @@ int tm_exchange_init(int64_t nparams, const tm_world* world, int strategy) {
   } else if (strategy == TM_EASGD) {
     // Centre sharded by segment: rank s hosts c[s*L, min((s+1)*L, P)).
     c.off_center = 0;
-    c.rank_stride = round_up(c.L * 4, 4096);
+    const int64_t nch = (c.L + tmx::kLockChunk - 1) / tmx::kLockChunk;
+    c.off_locks = round_up(c.L * 4, 256);
+    c.off_tickets = round_up(c.off_locks + nch * 4, 256);
+    c.rank_stride = round_up(c.off_tickets + nch * 4, 4096);
   } else {
     c.rank_stride = 0;
   }
@@ -428,6 +434,50 @@ int tm_easgd_update_sharded(float* worker_buf, float alpha, int concurrent, void
   cudaError_t e = tmx::launch_easgd_sharded(worker_buf, sa, alpha, concurrent != 0,
                                             static_cast<cudaStream_t>(stream));
   return e == cudaSuccess ? TM_OK : cuda_fail("easgd_sharded", e);
+}
+
+int tm_easgd_update_locked(float* worker_buf, int worker_id, float alpha, void* stream) {
+  tmx::ShardArgs sa{};
+  {
+    std::lock_guard<std::mutex> lk(g_mu);
+    if (!g.inited || !g.ready || g.strategy != TM_EASGD) return TM_E_STATE;
+    if (!worker_buf) return TM_E_ARG;
+    if (!aligned16(worker_buf)) return TM_E_ALIGN;
+    for (int s = 0; s < g.k; ++s) {
+      sa.shard[s] = reinterpret_cast<float*>(g.rank_base[s] + g.off_center);
+      sa.locks[s] = reinterpret_cast<uint32_t*>(g.rank_base[s] + g.off_locks);
+      sa.tickets[s] = reinterpret_cast<uint32_t*>(g.rank_base[s] + g.off_tickets);
+    }
+    sa.order_log = g.order_log;
+    sa.log_stride = g.order_log_stride;
+    sa.worker_id = worker_id;
+    sa.k = g.k;
+    sa.L = g.L;
+    sa.P = g.P;
+    sa.sys = g.nprocs > 1;
+    sa.status = g.status;
+    sa.timeout_ns = g.timeout_ns;
+    cudaSetDevice(g.device);
+  }
+  cudaError_t e = tmx::launch_easgd_locked(worker_buf, sa, alpha, static_cast<cudaStream_t>(stream));
+  return e == cudaSuccess ? TM_OK : cuda_fail("easgd_locked", e);
+}
+
+int tm_easgd_set_order_log(int32_t* dev_log, int max_updates_per_chunk) {
+  std::lock_guard<std::mutex> lk(g_mu);
+  if (!g.inited || g.strategy != TM_EASGD) return TM_E_STATE;
+  if (dev_log && max_updates_per_chunk < 1) return TM_E_ARG;
+  g.order_log = dev_log;
+  g.order_log_stride = dev_log ? max_updates_per_chunk : 0;
+  if (!dev_log) return TM_OK;
+  // restart the tickets so log positions start at 0
+  cudaSetDevice(g.device);
+  for (int i = 0; i < g.nlocal; ++i) {
+    const int64_t nch = (g.L + tmx::kLockChunk - 1) / tmx::kLockChunk;
+    cudaError_t e = cudaMemset(g.rank_base[g.rank0 + i] + g.off_tickets, 0, nch * 4);
+    if (e != cudaSuccess) return cuda_fail("ticket reset", e);
+  }
+  return TM_OK;
 }
 
 int tm_exchange_status(void* stream, uint32_t* bits) {

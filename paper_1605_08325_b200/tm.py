@@ -67,6 +67,8 @@ _SIGS = {
                                       ctypes.c_int, _P, ctypes.c_int64, ctypes.c_float, _P]),
     "tm_easgd_center": (ctypes.c_int, [ctypes.c_int, ctypes.POINTER(_P)]),
     "tm_easgd_update_sharded": (ctypes.c_int, [_P, ctypes.c_float, ctypes.c_int, _P]),
+    "tm_easgd_update_locked": (ctypes.c_int, [_P, ctypes.c_int, ctypes.c_float, _P]),
+    "tm_easgd_set_order_log": (ctypes.c_int, [_P, ctypes.c_int]),
     "tm_exchange_status": (ctypes.c_int, [_P, ctypes.POINTER(ctypes.c_uint32)]),
     "tm_layout": (ctypes.c_int, [ctypes.POINTER(tm_layout_info)]),
     "tm_set_timeout_ns": (ctypes.c_int, [ctypes.c_uint64]),
@@ -195,6 +197,17 @@ def tm_easgd_update_sharded(worker, alpha, concurrent=False, stream=None):
     _check(lib().tm_easgd_update_sharded(_fp32_cuda(worker), ctypes.c_float(alpha),
                                          int(bool(concurrent)), _stream_handle(stream)),
            "tm_easgd_update_sharded")
+
+
+def tm_easgd_update_locked(worker, worker_id, alpha, stream=None):
+    _check(lib().tm_easgd_update_locked(_fp32_cuda(worker), int(worker_id), ctypes.c_float(alpha),
+                                        _stream_handle(stream)), "tm_easgd_update_locked")
+
+
+def tm_easgd_set_order_log(log, max_updates_per_chunk):
+    """log: int32 CUDA tensor of >= k * nchunk * max entries, or None."""
+    ptr = None if log is None else ctypes.c_void_p(log.data_ptr())
+    _check(lib().tm_easgd_set_order_log(ptr, int(max_updates_per_chunk)), "tm_easgd_set_order_log")
 
 
 def tm_easgd_center(owner_rank):

@@ -182,3 +182,53 @@ def test_sharded_requires_easgd_context():
         with pytest.raises(tm.TmError) as e:
             tm.tm_easgd_update_sharded(x, 0.5)
         assert e.value.code == tm.TM_E_STATE
+
+
+def _check_against_logged_order(W, c0, gW, gc, log, k, P, L, nw, alpha):
+    """Each 4096-element chunk must equal the serial EASGD sequence in the
+    arrival order the kernel logged for that chunk."""
+    nch = -(-L // 4096)
+    for s in range(k):
+        for q in range(nch):
+            lo = s * L + q * 4096
+            hi = min(s * L + min(L, (q + 1) * 4096), P)
+            if lo >= hi:
+                continue
+            order = [int(w) for w in log[(s * nch + q) * nw:(s * nch + q + 1) * nw]]
+            assert sorted(order) == list(range(nw)), (s, q, order)
+            ws, cc = easgd_sequence([w[lo:hi] for w in W], c0[lo:hi], alpha, order)
+            assert_bitwise(gc[lo:hi], cc, f"centre chunk ({s},{q}) order {order}")
+            for r in range(nw):
+                assert_bitwise(gW[r][lo:hi], ws[r], f"worker {r} chunk ({s},{q})")
+
+
+@pytest.mark.parametrize("k,P", [(4, 300_007), (8, 1_000_003)])
+def test_locked_concurrent_updates_follow_logged_arrival_order(k, P):
+    """Per-worker atomic exchange: nw workers update the sharded
+    centre concurrently from nw streams; every chunk is bitwise the serial
+    sequence of its logged arrival order."""
+    nw = 8
+    alpha = 0.5 / nw
+    W = [worker_buffer(P, "D1", r, config=48) for r in range(nw)]
+    c0 = worker_buffer(P, "D1", 99, config=48)
+    with tm.Exchanger(P, "easgd", size=k, nlocal=k) as ex:
+        L = ex.layout()["seg_len"]
+        nch = -(-L // 4096)
+        for s in range(k):
+            sh = ex.center_shard(s)
+            if sh.numel():
+                sh.copy_(torch.from_numpy(c0[s * L: s * L + sh.numel()]))
+        log = torch.full((k * nch * nw,), -1, dtype=torch.int32, device="cuda")
+        tm.tm_easgd_set_order_log(log, nw)
+        Wd = to_dev(W)
+        streams = [torch.cuda.Stream() for _ in range(nw)]
+        torch.cuda.synchronize()
+        for r, (w, st) in enumerate(zip(Wd, streams)):
+            tm.tm_easgd_update_locked(w, r, alpha, stream=st)
+        torch.cuda.synchronize()
+        code, _ = ex.status()
+        assert code == tm.TM_OK
+        gW, gc = to_host(Wd), _read_centre(ex, P, k)
+        logh = log.cpu().numpy()
+        tm.tm_easgd_set_order_log(None, 0)
+    _check_against_logged_order(W, c0, gW, gc, logh, k, P, L, nw, alpha)
