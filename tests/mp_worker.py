@@ -4,7 +4,7 @@ all_gather_object.  Used by tests/test_gpu_multiprocess.py; on a one-GPU box
 every rank uses cuda:0 (IPC between processes on one device), on a multi-GPU
 box rank r uses cuda:r.
 
-argv: outdir strategy P dist mode      (mode: normal | sum | range | skip1 | mismatch)
+argv: outdir strategy P dist mode      (mode: normal | sum | range | locked | skip1 | mismatch)
 """
 
 import json
@@ -51,12 +51,23 @@ def main():
         mine.copy_(torch.from_numpy(c0[rank * L: rank * L + mine.numel()]))
         x = torch.from_numpy(worker_buffer(P, dist_name, rank, config=51)).cuda()
         torch.cuda.synchronize()
-        for w in range(size):
+        log = None
+        if mode == "locked":  # all workers at once; per-chunk locks order them
+            nch = -(-L // 4096)
+            log = torch.full((size * nch * size,), -1, dtype=torch.int32, device="cuda")
+            tm.tm_easgd_set_order_log(log, size)
             dist.barrier()
-            if w == rank:
-                tm.tm_easgd_update_sharded(x, 0.3)
-                torch.cuda.synchronize()
+            tm.tm_easgd_update_locked(x, rank, 0.3)
+            torch.cuda.synchronize()
+        else:
+            for w in range(size):
+                dist.barrier()
+                if w == rank:
+                    tm.tm_easgd_update_sharded(x, 0.3)
+                    torch.cuda.synchronize()
         dist.barrier()
+        if log is not None:
+            np.save(os.path.join(outdir, f"log{rank}.npy"), log.cpu().numpy())
         shard = ex.center_shard(rank).cpu().numpy()
         np.save(os.path.join(outdir, f"rank{rank}.npy"), x.cpu().numpy())
         np.save(os.path.join(outdir, f"shard{rank}.npy"), shard)

@@ -92,3 +92,32 @@ def test_multiprocess_sharded_easgd(tmp_path):
         assert_bitwise(np.load(os.path.join(tmp_path, f"rank{r}.npy")), wW[r], f"worker {r}")
         sh = np.load(os.path.join(tmp_path, f"shard{r}.npy"))
         assert_bitwise(sh, wc[r * L: r * L + sh.shape[0]], f"shard {r}")
+
+
+def test_multiprocess_locked_easgd(tmp_path):
+    """Two processes update the sharded centre at the same time with per-chunk
+    locks over IPC (system-scope atomics); each process logs its own arrival
+    positions; the merged order reproduces every chunk bitwise."""
+    from oracle.easgd import easgd_sequence
+    P, k = 300_007, 2
+    res = launch(tmp_path, k, "easgd", P, "D1", mode="locked")
+    W = [worker_buffer(P, "D1", r, config=51) for r in range(k)]
+    c0 = worker_buffer(P, "D1", 99, config=51)
+    L = res[0]["seg_len"]
+    nch = -(-L // 4096)
+    logs = [np.load(os.path.join(tmp_path, f"log{r}.npy")) for r in range(k)]
+    merged = np.maximum(logs[0], logs[1])
+    gW = [np.load(os.path.join(tmp_path, f"rank{r}.npy")) for r in range(k)]
+    shards = [np.load(os.path.join(tmp_path, f"shard{r}.npy")) for r in range(k)]
+    gc = np.concatenate(shards)[:P]
+    for s in range(k):
+        for q in range(nch):
+            lo, hi = s * L + q * 4096, min(s * L + min(L, (q + 1) * 4096), P)
+            if lo >= hi:
+                continue
+            order = [int(v) for v in merged[(s * nch + q) * k:(s * nch + q + 1) * k]]
+            assert sorted(order) == [0, 1], order
+            ws, cc = easgd_sequence([w[lo:hi] for w in W], c0[lo:hi], 0.3, order)
+            assert_bitwise(gc[lo:hi], cc, f"chunk ({s},{q})")
+            for r in range(k):
+                assert_bitwise(gW[r][lo:hi], ws[r])
