@@ -38,7 +38,8 @@ struct ExchangeArgs {
 // Persistent fused exchange: pre-cast -> ready barrier -> reduce-scatter pull with
 // fused sum/scale/cast -> reduced barrier -> allgather pull with fused widen.
 // wire16: fp16 wire (ASA16) else fp32 (ASA).  grid = nlocal * C, cooperative.
-cudaError_t launch_exchange(const ExchangeArgs& a, int nlocal, bool wire16, cudaStream_t s);
+// tma: the bulk-async (TMA engine) kernel, else the register-staged one.
+cudaError_t launch_exchange(const ExchangeArgs& a, int nlocal, bool wire16, bool tma, cudaStream_t s);
 
 // Single-process group, one pass (the "direct" path): pull the k contributions
 // of each element from the k buffers, fused rn16 (q16) / ascending-rank sum /
@@ -75,6 +76,6 @@ cudaError_t launch_easgd_locked(float* x, const ShardArgs& sa, float alpha, cuda
 cudaError_t launch_cast_rn16(const float* in, uint16_t* out, int64_t n, cudaStream_t s);
 
 // Max co-resident CTAs of the exchange kernel on `device` (occupancy * SMs).
-int exchange_max_ctas(int device, bool wire16, int k);
+int exchange_max_ctas(int device, bool wire16, int k, bool tma);
 
 }  // namespace tmx

@@ -80,6 +80,7 @@ struct Ctx {
   char* rank_base[TM_MAX_RANKS] = {};  // per global rank, as mapped on this device
   uint32_t epoch = 0;
   int path = TM_PATH_AUTO;
+  bool staged_tma = true;  // staged kernel flavour, fixed at init (it sets C)
   bool sum = false;  // TM_OP_SUM (SUBGD)
   uint64_t timeout_ns = kDefaultTimeoutNs;
   ncclComm_t comm = nullptr;
@@ -182,7 +183,7 @@ int do_exchange(float* const* bufs, int nbufs, int64_t off, int64_t n, cudaStrea
     return r == ncclSuccess ? TM_OK : TM_E_NCCL;
   }
   ExchangeArgs a = make_args(bufs, off, n);
-  cudaError_t e = tmx::launch_exchange(a, g.nlocal, wire16(g.strategy), s);
+  cudaError_t e = tmx::launch_exchange(a, g.nlocal, wire16(g.strategy), g.staged_tma, s);
   if (e != cudaSuccess) return cuda_fail("launch_exchange", e);
   ++g.epoch;  // host-side count for tm_layout; the kernels keep their own
   return TM_OK;
@@ -226,7 +227,15 @@ int tm_exchange_init(int64_t nparams, const tm_world* world, int strategy) {
 
   const int wb = wire_bytes(strategy);
   if (strategy == TM_ASA || strategy == TM_ASA16) {
-    int cmax = k >= 2 ? tmx::exchange_max_ctas(c.device, wire16(strategy), k) / c.nlocal : 1;
+    // Staged kernel flavour.  Single-process groups: the TMA-engine kernel
+    // (measured faster).  Across processes the register kernel is the default:
+    // its 16-byte peer loads are the established NVLink P2P pattern, while bulk
+    // copies from IPC-mapped peer memory are validated here only on one device.
+    // TM_STAGED_LDG=1 / TM_STAGED_TMA=1 override.
+    const char* ldg = getenv("TM_STAGED_LDG");
+    const char* tma = getenv("TM_STAGED_TMA");
+    c.staged_tma = c.nprocs == 1 ? !(ldg && ldg[0] == '1') : (tma && tma[0] == '1');
+    int cmax = k >= 2 ? tmx::exchange_max_ctas(c.device, wire16(strategy), k, c.staged_tma) / c.nlocal : 1;
     if (k >= 2 && cmax < 1) return TM_E_CUDA;
     const int64_t want = std::max<int64_t>(1, (c.L + tmx::kMinChunk - 1) / tmx::kMinChunk);
     c.C = (int)std::min<int64_t>(std::max(cmax, 1), want);
@@ -519,6 +528,7 @@ int tm_layout(tm_layout_info* out) {
   out->lib_bytes = g.slab_bytes;
   out->epoch = g.epoch;
   out->path = effective_path();
+  out->staged_tma = g.staged_tma ? 1 : 0;
   return TM_OK;
 }
 

@@ -504,25 +504,20 @@ cudaError_t prepare(const void* fn, bool tma) {
 
 }  // namespace
 
-bool staged_uses_tma() { return env_int("TM_STAGED_LDG", 0) != 1; }
-
-int exchange_max_ctas(int device, bool wire16, int k) {
-  const bool tma = staged_uses_tma();
+int exchange_max_ctas(int device, bool wire16, int k, bool tma) {
   const void* fn = pick_exchange(k, wire16, true, tma);
   if (!fn) return 0;
   if (prepare(fn, tma) != cudaSuccess) return 0;
   int per_sm = 0;
   if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, tma ? kTmaThreads : kThreads,
-                                                    tma ? kTmaSmem : 0) !=
-      cudaSuccess)
+                                                    tma ? kTmaSmem : 0) != cudaSuccess)
     return 0;
   return per_sm * sm_count(device);
 }
 
-cudaError_t launch_exchange(const ExchangeArgs& a, int nlocal, bool wire16, cudaStream_t s) {
+cudaError_t launch_exchange(const ExchangeArgs& a, int nlocal, bool wire16, bool tma, cudaStream_t s) {
   // System-scope flags only when some peer rank lives in another process
   // (another GPU, over NVLink); a single-process group syncs at GPU scope.
-  const bool tma = staged_uses_tma();
   const void* fn = pick_exchange(a.k, wire16, nlocal != a.k, tma);
   if (!fn) return cudaErrorInvalidValue;
   cudaError_t e = prepare(fn, tma);

@@ -29,12 +29,12 @@ def _free_port():
     return p
 
 
-def launch(tmp_path, k, strategy, P, dist, mode="normal", timeout=240):
+def launch(tmp_path, k, strategy, P, dist, mode="normal", timeout=240, extra_env=None):
     port = _free_port()
     procs = []
     for r in range(k):
         env = dict(os.environ, RANK=str(r), WORLD_SIZE=str(k), MASTER_ADDR="127.0.0.1",
-                   MASTER_PORT=str(port), LOCAL_RANK=str(r))
+                   MASTER_PORT=str(port), LOCAL_RANK=str(r), **(extra_env or {}))
         procs.append(subprocess.Popen([sys.executable, os.path.join(HERE, "mp_worker.py"), str(tmp_path),
                                        strategy, str(P), dist, mode], env=env))
     try:
@@ -49,11 +49,16 @@ def launch(tmp_path, k, strategy, P, dist, mode="normal", timeout=240):
     return res
 
 
-@pytest.mark.parametrize("strategy,k,op", [("asa16", 2, "avg"), ("asa", 2, "avg"), ("asa16", 3, "avg"),
-                                           ("asa16", 2, "sum"), ("asa16", 2, "range")])
-def test_multiprocess_bitwise(tmp_path, strategy, k, op):
+@pytest.mark.parametrize("strategy,k,op,kernel", [("asa16", 2, "avg", "ldg"), ("asa", 2, "avg", "ldg"),
+                                                  ("asa16", 3, "avg", "ldg"), ("asa16", 2, "sum", "ldg"),
+                                                  ("asa16", 2, "range", "ldg"), ("asa16", 2, "avg", "tma"),
+                                                  ("asa", 3, "range", "tma")])
+def test_multiprocess_bitwise(tmp_path, strategy, k, op, kernel):
     P = 100_003
-    res = launch(tmp_path, k, strategy, P, "D2", mode=("normal" if op == "avg" else op))
+    env = {"TM_STAGED_TMA": "1"} if kernel == "tma" else None
+    res = launch(tmp_path, k, strategy, P, "D2", mode=("normal" if op == "avg" else op), extra_env=env)
+    for r in range(k):
+        assert res[r]["layout"]["staged_tma"] == (1 if kernel == "tma" else 0)
     op = "sum" if op == "sum" else "avg"  # bucketed ranges give the full exchange
     X = [worker_buffer(P, "D2", r, config=50) for r in range(k)]
     want = X
