@@ -182,6 +182,21 @@ int tm_exchange_range(float* dev_buf, int64_t offset, int64_t count, void* strea
 int tm_exchange_group_range(float* const* dev_bufs, int nbufs, int64_t offset, int64_t count,
                             void* stream);
 
+/* One BSP iteration's update + combine (PAPER L195-212,
+ * L373-384): every rank takes its momentum-SGD step (one IEEE
+ * rounding per operation, no FMA):
+ *     v = fl(fl(mu*v) - fl(lr*grad));   w = fl(w + v)
+ * and then the weights are exchanged (averaged) with the exchanger's strategy;
+ * exchange_momentum != 0 also averages the velocities (PAPER L160-164,
+ * L373-376), else each rank keeps its own.  w, v, grad: fp32[nparams], 16-byte
+ * aligned; w and v are updated in place.  In a single-process group on the
+ * direct path the step and the exchange are ONE fused pass over memory.
+ * Not valid with TM_OP_SUM (exchange the updates with tm_exchange instead). */
+int tm_bsp_step(float* w, float* v, const float* grad, float lr, float mu, int exchange_momentum,
+                void* stream);
+int tm_bsp_step_group(float* const* w, float* const* v, const float* const* grad, int nbufs,
+                      float lr, float mu, int exchange_momentum, void* stream);
+
 /* North-star call: one elastic update of nparams elements:
  *   d = fl(x - c); e = fl(alpha*d); x = fl(x - e); c = fl(c + e)   (no FMA)
  * worker_buf: this rank's fp32 buffer; center_buf: any fp32 buffer addressable

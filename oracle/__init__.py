@@ -17,9 +17,10 @@ Modules
   fp16      -- rn16 (IEEE binary16 round-to-nearest-even) and widen (exact)
   exchange  -- partition / alltoall / allgather / ASA / ASA16 / AR averaging
   easgd     -- elastic-averaging update and arrival-order sequences
+  bsp       -- momentum-SGD step followed by the exchange (one BSP iteration)
 
 Parity status of every function is listed in each module's header and in
 DESIGN.md section "Oracle and pins".
 """
 
-from . import fp16, exchange, easgd  # noqa: F401
+from . import fp16, exchange, easgd, bsp  # noqa: F401

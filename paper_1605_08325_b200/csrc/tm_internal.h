@@ -73,6 +73,18 @@ cudaError_t launch_easgd_sharded(float* x, const ShardArgs& sa, float alpha, boo
 // worker's update of an element is one atomic read-modify-write of the centre
 // (per-worker atomic exchange) in arrival order.
 cudaError_t launch_easgd_locked(float* x, const ShardArgs& sa, float alpha, cudaStream_t s);
+// One BSP iteration (tm_bsp.cu): momentum-SGD step + exchange of the weights
+// (and velocities when mom) for a single-process group, fused in one pass.
+struct BspBufs {
+  float* w[TM_MAX_RANKS];
+  float* v[TM_MAX_RANKS];
+  const float* g[TM_MAX_RANKS];
+  float lr, mu;
+};
+cudaError_t launch_bsp_direct(const BspBufs& bb, int k, int64_t P, bool q16, bool mom,
+                              uint32_t* status, cudaStream_t s);
+cudaError_t launch_sgd(float* w, float* v, const float* g, int64_t n, float lr, float mu,
+                       cudaStream_t s);
 cudaError_t launch_cast_rn16(const float* in, uint16_t* out, int64_t n, cudaStream_t s);
 
 // Max co-resident CTAs of the exchange kernel on `device` (occupancy * SMs).

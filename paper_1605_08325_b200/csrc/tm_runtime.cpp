@@ -189,9 +189,60 @@ int do_exchange(float* const* bufs, int nbufs, int64_t off, int64_t n, cudaStrea
   return TM_OK;
 }
 
+// One BSP iteration: momentum-SGD step of every local rank, then the exchange
+// of the weights (and of the velocities when exchange_momentum).
+int do_bsp(float* const* w, float* const* v, const float* const* gr, int nbufs, float lr, float mu,
+           int mom, cudaStream_t s) {
+  if (!g.inited || !g.ready || g.strategy == TM_EASGD) return TM_E_STATE;
+  if (g.sum) return TM_E_ARG;  // SUBGD sums updates, not weights: exchange deltas instead
+  if (nbufs != g.nlocal || !w || !v || !gr) return TM_E_ARG;
+  for (int i = 0; i < nbufs; ++i) {
+    if (!w[i] || !v[i] || !gr[i]) return TM_E_ARG;
+    if (!aligned16(w[i]) || !aligned16(v[i]) || !aligned16(gr[i])) return TM_E_ALIGN;
+  }
+  cudaSetDevice(g.device);
+  if (g.k > 1 && g.nlocal == g.k && (g.strategy == TM_AR || effective_path() == TM_PATH_DIRECT)) {
+    tmx::BspBufs bb{};
+    for (int i = 0; i < nbufs; ++i) {
+      bb.w[i] = w[i];
+      bb.v[i] = v[i];
+      bb.g[i] = gr[i];
+    }
+    bb.lr = lr;
+    bb.mu = mu;
+    cudaError_t e = tmx::launch_bsp_direct(bb, g.k, g.P, g.strategy == TM_ASA16, mom != 0, g.status, s);
+    return e == cudaSuccess ? TM_OK : cuda_fail("launch_bsp_direct", e);
+  }
+  for (int i = 0; i < nbufs; ++i) {
+    cudaError_t e = tmx::launch_sgd(w[i], v[i], gr[i], g.P, lr, mu, s);
+    if (e != cudaSuccess) return cuda_fail("launch_sgd", e);
+  }
+  int rc = do_exchange(w, nbufs, 0, g.P, s);
+  if (rc != TM_OK || !mom) return rc;
+  return do_exchange(v, nbufs, 0, g.P, s);
+}
+
 }  // namespace
 
 extern "C" {
+
+int tm_bsp_step(float* w, float* v, const float* grad, float lr, float mu,
+                           int exchange_momentum, void* stream) {
+  std::lock_guard<std::mutex> lk(g_mu);
+  if (g.inited && g.nlocal != 1) return TM_E_STATE;
+  float* ws[1] = {w};
+  float* vs[1] = {v};
+  const float* gs[1] = {grad};
+  return do_bsp(ws, vs, gs, 1, lr, mu, exchange_momentum, static_cast<cudaStream_t>(stream));
+}
+
+int tm_bsp_step_group(float* const* w, float* const* v, const float* const* grad,
+                                 int nbufs, float lr, float mu, int exchange_momentum,
+                                 void* stream) {
+  std::lock_guard<std::mutex> lk(g_mu);
+  return do_bsp(w, v, grad, nbufs, lr, mu, exchange_momentum, static_cast<cudaStream_t>(stream));
+}
+
 
 int tm_exchange_init(int64_t nparams, const tm_world* world, int strategy) {
   std::lock_guard<std::mutex> lk(g_mu);

@@ -59,6 +59,9 @@ _SIGS = {
     "tm_exchange": (ctypes.c_int, [_P, _P]),
     "tm_exchange_group": (ctypes.c_int, [ctypes.POINTER(_P), ctypes.c_int, _P]),
     "tm_exchange_range": (ctypes.c_int, [_P, ctypes.c_int64, ctypes.c_int64, _P]),
+    "tm_bsp_step": (ctypes.c_int, [_P, _P, _P, ctypes.c_float, ctypes.c_float, ctypes.c_int, _P]),
+    "tm_bsp_step_group": (ctypes.c_int, [ctypes.POINTER(_P), ctypes.POINTER(_P), ctypes.POINTER(_P),
+                                         ctypes.c_int, ctypes.c_float, ctypes.c_float, ctypes.c_int, _P]),
     "tm_exchange_group_range": (ctypes.c_int, [ctypes.POINTER(_P), ctypes.c_int, ctypes.c_int64,
                                                ctypes.c_int64, _P]),
     "tm_easgd_update": (ctypes.c_int, [_P, _P, ctypes.c_float, _P]),
@@ -171,6 +174,20 @@ def tm_exchange_group_range(bufs, offset, count, stream=None):
     arr = (ctypes.c_void_p * len(bufs))(*[_fp32_cuda(b).value for b in bufs])
     _check(lib().tm_exchange_group_range(arr, len(bufs), int(offset), int(count),
                                          _stream_handle(stream)), "tm_exchange_group_range")
+
+
+def tm_bsp_step(w, v, grad, lr, mu, exchange_momentum=False, stream=None):
+    _check(lib().tm_bsp_step(_fp32_cuda(w), _fp32_cuda(v), _fp32_cuda(grad), ctypes.c_float(lr),
+                             ctypes.c_float(mu), int(bool(exchange_momentum)), _stream_handle(stream)),
+           "tm_bsp_step")
+
+
+def tm_bsp_step_group(ws, vs, grads, lr, mu, exchange_momentum=False, stream=None):
+    n = len(ws)
+    arr = lambda ts: (ctypes.c_void_p * n)(*[_fp32_cuda(t).value for t in ts])  # noqa: E731
+    _check(lib().tm_bsp_step_group(arr(ws), arr(vs), arr(grads), n, ctypes.c_float(lr),
+                                   ctypes.c_float(mu), int(bool(exchange_momentum)),
+                                   _stream_handle(stream)), "tm_bsp_step_group")
 
 
 def tm_easgd_update(worker, center, alpha, stream=None):
@@ -316,6 +333,14 @@ class Exchanger:
             tm_exchange_range(bufs, offset, count, stream)
         else:
             tm_exchange_group_range(list(bufs), offset, count, stream)
+
+    def bsp_step(self, w, v, grad, lr, mu, exchange_momentum=False, stream=None):
+        """Momentum-SGD step of every local rank, then the exchange (fused in
+        one pass for a single-process group on the direct path)."""
+        if isinstance(w, torch.Tensor):
+            tm_bsp_step(w, v, grad, lr, mu, exchange_momentum, stream)
+        else:
+            tm_bsp_step_group(list(w), list(v), list(grad), lr, mu, exchange_momentum, stream)
 
     def status(self, stream=None):
         return tm_exchange_status(stream)
