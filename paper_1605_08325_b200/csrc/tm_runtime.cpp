@@ -201,7 +201,10 @@ int do_bsp(float* const* w, float* const* v, const float* const* gr, int nbufs, 
     if (!aligned16(w[i]) || !aligned16(v[i]) || !aligned16(gr[i])) return TM_E_ALIGN;
   }
   cudaSetDevice(g.device);
-  if (g.k > 1 && g.nlocal == g.k && (g.strategy == TM_AR || effective_path() == TM_PATH_DIRECT)) {
+  const char* unf = getenv("TM_BSP_UNFUSED");  // diagnostics: time the unfused sequence
+  const bool fuse = !(unf && unf[0] == '1');
+  if (fuse && g.k > 1 && g.nlocal == g.k &&
+      (g.strategy == TM_AR || effective_path() == TM_PATH_DIRECT)) {
     tmx::BspBufs bb{};
     for (int i = 0; i < nbufs; ++i) {
       bb.w[i] = w[i];

@@ -132,6 +132,30 @@ def easgd_rows(P, nw, alpha, pk):
     return rows
 
 
+def bsp_rows(P, k, pk):
+    """NEXT-1: momentum-SGD step + exchange of k workers, fused in one pass (direct
+    path) vs the library's unfused sequence (SGD kernel per worker, then the
+    direct exchange; TM_BSP_UNFUSED=1), with and without momentum exchange."""
+    g = torch.Generator(device="cuda").manual_seed(77)
+    W = [torch.randn(P, device="cuda", generator=g) * 0.01 for _ in range(k)]
+    V = [torch.zeros(P, device="cuda") for _ in range(k)]
+    G = [torch.randn(P, device="cuda", generator=g) * 0.01 for _ in range(k)]
+    rows = []
+    for mom in (False, True):
+        for fused in (True, False):
+            os.environ["TM_BSP_UNFUSED"] = "0" if fused else "1"
+            with tm.Exchanger(P, "asa16", size=k, nlocal=k, path="direct") as ex:
+                ms = timeit(lambda: ex.bsp_step(W, V, G, 0.01, 0.9, exchange_momentum=mom), graph=True)
+            # fused: read w, v, g + write w, v = 20 B per element per worker
+            alg = 20.0 * P * k
+            rows.append({"mode": f"{'fused one pass' if fused else 'SGD pass + exchange pass(es)'}"
+                                 f"{', momentum exchanged' if mom else ''}",
+                         "us": ms * 1e3, "hbm_GBps": alg / (ms * 1e-3) / 1e9,
+                         "frac": alg / (ms * 1e-3) / 1e9 / pk, "P": P, "k": k})
+    os.environ.pop("TM_BSP_UNFUSED", None)
+    return rows
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--md", default=None)
@@ -139,7 +163,7 @@ def main():
     a = ap.parse_args()
     torch.cuda.set_device(0)
     pk = peak()
-    out = {"config2": [], "config3": [], "config4": [], "config5": []}
+    out = {"config2": [], "config3": [], "config4": [], "config5": [], "bsp": []}
     ks = (2, 4, 8)
     for strategy in ("asa", "asa16"):
         for k in ks:
@@ -150,6 +174,7 @@ def main():
             for path in (("direct",) if strategy == "ar" else ("direct", "staged")):
                 out["config3"].append(exchange_row(ALEXNET, k, strategy, path, pk))
     out["config4"] = easgd_rows(ALEXNET, 8, 0.5 / 8, pk)
+    out["bsp"] = bsp_rows(ALEXNET, 8, pk)
     sizes = [1 << e for e in range(16, 31, 2 if a.quick else 1)]
     for nbytes in sizes:
         P = nbytes // 4
@@ -179,6 +204,11 @@ def main():
             f.write("## config4 (EASGD, 8 workers + centre, P = 60,965,224, alpha = 0.5/8)\n\n"
                     "| mode | µs | HBM GB/s | frac |\n|---|---|---|---|\n")
             for r in out["config4"]:
+                f.write(f"| {r['mode']} | {r['us']:.1f} | {r['hbm_GBps']:.0f} | {r['frac']:.3f} |\n")
+            f.write("\n## BSP iteration (SGD step + exchange), AlexNet, k = 8, ASA16 "
+                    "(HBM GB/s counts the fused pass's 20 B per element per worker for both rows)\n\n"
+                    "| mode | µs | HBM GB/s | frac |\n|---|---|---|---|\n")
+            for r in out["bsp"]:
                 f.write(f"| {r['mode']} | {r['us']:.1f} | {r['hbm_GBps']:.0f} | {r['frac']:.3f} |\n")
 
 
