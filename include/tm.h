@@ -122,7 +122,7 @@ typedef struct {
   int64_t lib_bytes;     /* device bytes the library owns in this process     */
   uint32_t epoch;        /* number of staged exchanges issued so far          */
   int32_t path;          /* effective tm_path of the next exchange            */
-  int32_t staged_tma;    /* 1: staged kernel on the TMA engine; 0: register   */
+  int32_t staged_kernel; /* staged flavour: 0 register, 1 TMA engine, 2 warp-specialised */
 } tm_layout_info;
 
 /* How an ASA / ASA16 exchange moves data (results are bitwise identical):

@@ -20,7 +20,11 @@ constexpr int64_t kMinChunk = 2048; // smallest per-CTA chunk worth a barrier
 // to CTA c of the owner.
 constexpr int kPhaseReady = 0;    // src finished its pre-cast of chunk c
 constexpr int kPhaseReduced = 1;  // src finished summing its segment's chunk c
-constexpr int kPhases = 2;
+// The warp-specialised staged kernel splits a chunk into kWsSub sub-chunks with
+// one READY phase each (0..kWsSub-1) and REDUCED = kWsSub.  The pad is laid out
+// for kPhases phases; the per-CTA epoch counters follow them.
+constexpr int kWsSub = 4;
+constexpr int kPhases = kWsSub + 1;
 
 struct ExchangeArgs {
   void* stage[TM_MAX_RANKS];      // rank j's staging (k*L wire elems), as mapped here
@@ -38,8 +42,9 @@ struct ExchangeArgs {
 // Persistent fused exchange: pre-cast -> ready barrier -> reduce-scatter pull with
 // fused sum/scale/cast -> reduced barrier -> allgather pull with fused widen.
 // wire16: fp16 wire (ASA16) else fp32 (ASA).  grid = nlocal * C, cooperative.
-// tma: the bulk-async (TMA engine) kernel, else the register-staged one.
-cudaError_t launch_exchange(const ExchangeArgs& a, int nlocal, bool wire16, bool tma, cudaStream_t s);
+// Staged kernel flavours.
+enum StagedKernel { kStagedReg = 0, kStagedTma = 1, kStagedWs = 2 };
+cudaError_t launch_exchange(const ExchangeArgs& a, int nlocal, bool wire16, int flavour, cudaStream_t s);
 
 // Single-process group, one pass (the "direct" path): pull the k contributions
 // of each element from the k buffers, fused rn16 (q16) / ascending-rank sum /
@@ -88,6 +93,6 @@ cudaError_t launch_sgd(float* w, float* v, const float* g, int64_t n, float lr, 
 cudaError_t launch_cast_rn16(const float* in, uint16_t* out, int64_t n, cudaStream_t s);
 
 // Max co-resident CTAs of the exchange kernel on `device` (occupancy * SMs).
-int exchange_max_ctas(int device, bool wire16, int k, bool tma);
+int exchange_max_ctas(int device, bool wire16, int k, int flavour);
 
 }  // namespace tmx

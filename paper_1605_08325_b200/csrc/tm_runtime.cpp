@@ -80,7 +80,7 @@ struct Ctx {
   char* rank_base[TM_MAX_RANKS] = {};  // per global rank, as mapped on this device
   uint32_t epoch = 0;
   int path = TM_PATH_AUTO;
-  bool staged_tma = true;  // staged kernel flavour, fixed at init (it sets C)
+  int staged_kernel = tmx::kStagedTma;  // staged kernel flavour, fixed at init (it sets C)
   bool sum = false;  // TM_OP_SUM (SUBGD)
   uint64_t timeout_ns = kDefaultTimeoutNs;
   ncclComm_t comm = nullptr;
@@ -183,7 +183,7 @@ int do_exchange(float* const* bufs, int nbufs, int64_t off, int64_t n, cudaStrea
     return r == ncclSuccess ? TM_OK : TM_E_NCCL;
   }
   ExchangeArgs a = make_args(bufs, off, n);
-  cudaError_t e = tmx::launch_exchange(a, g.nlocal, wire16(g.strategy), g.staged_tma, s);
+  cudaError_t e = tmx::launch_exchange(a, g.nlocal, wire16(g.strategy), g.staged_kernel, s);
   if (e != cudaSuccess) return cuda_fail("launch_exchange", e);
   ++g.epoch;  // host-side count for tm_layout; the kernels keep their own
   return TM_OK;
@@ -282,14 +282,22 @@ int tm_exchange_init(int64_t nparams, const tm_world* world, int strategy) {
   const int wb = wire_bytes(strategy);
   if (strategy == TM_ASA || strategy == TM_ASA16) {
     // Staged kernel flavour.  Single-process groups: the TMA-engine kernel
-    // (measured faster).  Across processes the register kernel is the default:
-    // its 16-byte peer loads are the established NVLink P2P pattern, while bulk
-    // copies from IPC-mapped peer memory are validated here only on one device.
-    // TM_STAGED_LDG=1 / TM_STAGED_TMA=1 override.
+    // (measured fastest on one GPU).  Across processes: the warp-specialised
+    // register kernel, whose pre-cast (HBM) overlaps the reduce-scatter pull
+    // (NVLink) and whose 16-byte peer loads are the established NVLink P2P
+    // pattern (bulk copies from IPC-mapped peer memory are validated here only
+    // on one device).  TM_STAGED_KERNEL=reg|tma|ws overrides
+    // (TM_STAGED_LDG=1 / TM_STAGED_TMA=1 are accepted too).
+    c.staged_kernel = c.nprocs == 1 ? tmx::kStagedTma : tmx::kStagedWs;
+    const char* sk = getenv("TM_STAGED_KERNEL");
     const char* ldg = getenv("TM_STAGED_LDG");
     const char* tma = getenv("TM_STAGED_TMA");
-    c.staged_tma = c.nprocs == 1 ? !(ldg && ldg[0] == '1') : (tma && tma[0] == '1');
-    int cmax = k >= 2 ? tmx::exchange_max_ctas(c.device, wire16(strategy), k, c.staged_tma) / c.nlocal : 1;
+    if (ldg && ldg[0] == '1') c.staged_kernel = tmx::kStagedReg;
+    if (tma && tma[0] == '1') c.staged_kernel = tmx::kStagedTma;
+    if (sk && !strcmp(sk, "reg")) c.staged_kernel = tmx::kStagedReg;
+    if (sk && !strcmp(sk, "tma")) c.staged_kernel = tmx::kStagedTma;
+    if (sk && !strcmp(sk, "ws")) c.staged_kernel = tmx::kStagedWs;
+    int cmax = k >= 2 ? tmx::exchange_max_ctas(c.device, wire16(strategy), k, c.staged_kernel) / c.nlocal : 1;
     if (k >= 2 && cmax < 1) return TM_E_CUDA;
     const int64_t want = std::max<int64_t>(1, (c.L + tmx::kMinChunk - 1) / tmx::kMinChunk);
     c.C = (int)std::min<int64_t>(std::max(cmax, 1), want);
@@ -582,7 +590,7 @@ int tm_layout(tm_layout_info* out) {
   out->lib_bytes = g.slab_bytes;
   out->epoch = g.epoch;
   out->path = effective_path();
-  out->staged_tma = g.staged_tma ? 1 : 0;
+  out->staged_kernel = g.staged_kernel;
   return TM_OK;
 }
 

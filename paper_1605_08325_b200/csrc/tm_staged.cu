@@ -206,6 +206,174 @@ tm_exchange_kernel(const __grid_constant__ ExchangeArgs a) {
 }
 
 // ---------------------------------------------------------------------------
+// Warp-specialised staged kernel: the pre-cast (HBM-bound) overlaps the
+// reduce-scatter pull (NVLink-bound across GPUs).  512 threads per CTA: warps
+// 0-7 are casters, warps 8-15 reducers.  The CTA's chunk is split into kWsSub
+// sub-chunks; the casters pre-cast sub-chunk t of all k segments, sync among
+// themselves (named barrier 1) and publish READY_t to every rank, then move on
+// to t+1; the reducers wait for READY_t from every rank (named barrier 2) and
+// pull / sum / store sub-chunk t of the own segment while the casters work on
+// t+1.  After the last sub-chunk the whole CTA meets, publishes REDUCED and runs
+// the allgather pull with all 16 warps.  Reuse across exchanges is covered by the
+// same argument as the other kernels (READY_t(n+1) is published after AG(n);
+// stage is rewritten only after REDUCED(n) from every rank).
+// ---------------------------------------------------------------------------
+constexpr int kWsThreads = 512;
+constexpr int kWsGroup = 256;
+
+__device__ __forceinline__ void named_bar(int id, int n) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
+}
+
+template <int K, bool W16, bool SYS>
+__global__ void __launch_bounds__(kWsThreads, 2)
+tm_exchange_ws_kernel(const __grid_constant__ ExchangeArgs a) {
+  using U = Unit<W16>;
+  constexpr int E = U::kElems;
+  constexpr int WB = W16 ? 2 : 4;
+  __shared__ int s_abort;
+  __shared__ uint32_t s_epoch;
+
+  const int lr = blockIdx.x / a.C;
+  const int c = blockIdx.x - lr * a.C;
+  const int r = a.rank0 + lr;
+  if (threadIdx.x == 0) {
+    s_abort = 0;
+    uint32_t* ctr = a.flags[r] + (size_t)kPhases * TM_MAX_RANKS * a.flag_stride + c;
+    s_epoch = *ctr + 1;
+    *ctr = s_epoch;
+  }
+  __syncthreads();
+  const uint32_t epoch = s_epoch;
+  float* __restrict__ x = a.x[lr];
+  const int64_t P = a.P, L = a.L;
+  const int64_t e0 = (int64_t)c * a.Lc;
+  const int64_t e1 = min(e0 + a.Lc, L);
+  const int64_t nel = e1 > e0 ? e1 - e0 : 0;
+  const int64_t Ls = ((nel + kWsSub - 1) / kWsSub + 255) / 256 * 256;  // sub-chunk length
+  char* const stage_r = reinterpret_cast<char*>(a.stage[r]);
+  const int grp = threadIdx.x / kWsGroup;
+  const int tg = threadIdx.x - grp * kWsGroup;
+  uint32_t st = 0;
+
+  if (grp == 0) {
+    // ------------------------------------------------ casters: a2 per sub-chunk
+    constexpr int G = K < 4 ? K : 4;
+    for (int t = 0; t < kWsSub; ++t) {
+      const int64_t s0e = e0 + (int64_t)t * Ls;
+      const int64_t s1e = min(s0e + Ls, e1);
+      const int nu = s1e > s0e ? (int)((s1e - s0e) / E) : 0;
+      for (int v = tg; v < nu; v += kWsGroup) {
+        const int64_t ev = s0e + (int64_t)v * E;
+#pragma unroll
+        for (int sb = 0; sb < K; sb += G) {
+          float f[G][E];
+#pragma unroll
+          for (int u = 0; u < G; ++u) {
+            if (sb + u < K) {
+              const int64_t g = (int64_t)(sb + u) * L + ev;
+              if (g + E <= P) {
+                U::to_floats(U::load_src(x + g), f[u]);
+              } else {
+#pragma unroll
+                for (int q = 0; q < E; ++q) f[u][q] = (g + q < P) ? x[g + q] : 0.0f;
+              }
+            }
+          }
+#pragma unroll
+          for (int u = 0; u < G; ++u) {
+            if (sb + u < K) {
+              const int64_t g = (int64_t)(sb + u) * L + ev;
+              st |= unit_status<W16, E>(f[u]);
+              st16_cg(stage_r + g * WB, U::encode(f[u]));
+            }
+          }
+        }
+      }
+      named_bar(1, kWsGroup);  // every caster's stage writes of sub-chunk t done
+      if (tg < K)
+        st_release<SYS>(a.flags[tg] + (size_t)(t * TM_MAX_RANKS + r) * a.flag_stride + c, epoch);
+    }
+  } else {
+    // ------------------------------------------------ reducers: a4 per sub-chunk
+    const char* src[K];
+#pragma unroll
+    for (int j = 0; j < K; ++j) src[j] = reinterpret_cast<const char*>(a.stage[j]);
+    char* const avg_r = reinterpret_cast<char*>(a.avg[r]);
+    for (int t = 0; t < kWsSub; ++t) {
+      if (tg < K) {  // READY_t from rank tg
+        const uint32_t* mine = a.flags[r] + (size_t)(t * TM_MAX_RANKS + tg) * a.flag_stride + c;
+        if ((int32_t)(ld_acquire<SYS>(mine) - epoch) < 0) {
+          const uint64_t t0 = globaltimer();
+          while ((int32_t)(ld_acquire<SYS>(mine) - epoch) < 0) {
+            if (globaltimer() - t0 > a.timeout_ns) {
+              atomicOr(a.status, TM_BIT_TIMEOUT);
+              s_abort = 1;
+              break;
+            }
+            __nanosleep(32);
+          }
+        }
+      }
+      named_bar(2, kWsGroup);
+      if (s_abort) break;
+      const int64_t s0e = e0 + (int64_t)t * Ls;
+      const int64_t s1e = min(s0e + Ls, e1);
+      const int nu = s1e > s0e ? (int)((s1e - s0e) / E) : 0;
+      for (int v = tg; v < nu; v += kWsGroup) {
+        const int64_t e = s0e + (int64_t)v * E;
+        const int64_t off = ((int64_t)r * L + e) * WB;
+        uint4 raw[K];
+#pragma unroll
+        for (int j = 0; j < K; ++j) raw[j] = ld16_cg(src[j] + off);
+        float sm[E], tt[E];
+        U::decode(raw[0], sm);
+#pragma unroll
+        for (int j = 1; j < K; ++j) {
+          U::decode(raw[j], tt);
+#pragma unroll
+          for (int q = 0; q < E; ++q) sm[q] = __fadd_rn(sm[q], tt[q]);
+        }
+        if (!a.sum) {
+#pragma unroll
+          for (int q = 0; q < E; ++q) sm[q] = div_k<K>(sm[q]);
+        } else if (W16) {
+#pragma unroll
+          for (int q = 0; q < E; ++q) st |= status_of(sm[q], true) & TM_BIT_OVERFLOW16;
+        }
+        st16_cg(avg_r + e * WB, U::encode(sm));
+      }
+    }
+  }
+  if (st) atomicOr(a.status, st);
+  __syncthreads();
+  if (s_abort) return;
+  if (!rank_barrier<K, SYS>(a, kWsSub, r, c, epoch, &s_abort)) return;  // REDUCED
+
+  // ---------------- a6: allgather pull with all 16 warps ----------------------
+  const int nu32 = (int)(nel / E);
+  for (int v = threadIdx.x; v < nu32; v += kWsThreads) {
+    const int64_t ev = e0 + (int64_t)v * E;
+    uint4 raw[K];
+#pragma unroll
+    for (int j = 0; j < K; ++j) raw[j] = ld16_cg(reinterpret_cast<const char*>(a.avg[j]) + ev * WB);
+#pragma unroll
+    for (int j = 0; j < K; ++j) {
+      const int64_t g = (int64_t)j * L + ev;
+      float f[E];
+      U::decode(raw[j], f);
+      if (g + E <= P) {
+        U::store_dst(x + g, f);
+      } else {
+#pragma unroll
+        for (int q = 0; q < E; ++q)
+          if (g + q < P) x[g + q] = f[q];
+      }
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
 // The same three phases on the TMA engine (default staged kernel).
 //
 // One CTA per SM (224 KB of shared memory).  Each phase is a tile pipeline:
@@ -473,60 +641,65 @@ tm_exchange_tma_kernel(const __grid_constant__ ExchangeArgs a) {
 }
 
 template <int K, bool W16>
-const void* exchange_fn(bool sys, bool tma) {
-  if (tma)
+const void* exchange_fn(bool sys, int fl) {
+  if (fl == kStagedTma)
     return sys ? reinterpret_cast<const void*>(&tm_exchange_tma_kernel<K, W16, true>)
                : reinterpret_cast<const void*>(&tm_exchange_tma_kernel<K, W16, false>);
+  if (fl == kStagedWs)
+    return sys ? reinterpret_cast<const void*>(&tm_exchange_ws_kernel<K, W16, true>)
+               : reinterpret_cast<const void*>(&tm_exchange_ws_kernel<K, W16, false>);
   return sys ? reinterpret_cast<const void*>(&tm_exchange_kernel<K, W16, true>)
              : reinterpret_cast<const void*>(&tm_exchange_kernel<K, W16, false>);
 }
 
-const void* pick_exchange(int k, bool w16, bool sys, bool tma) {
+const void* pick_exchange(int k, bool w16, bool sys, int fl) {
   switch (k) {
-    case 2: return w16 ? exchange_fn<2, true>(sys, tma) : exchange_fn<2, false>(sys, tma);
-    case 3: return w16 ? exchange_fn<3, true>(sys, tma) : exchange_fn<3, false>(sys, tma);
-    case 4: return w16 ? exchange_fn<4, true>(sys, tma) : exchange_fn<4, false>(sys, tma);
-    case 5: return w16 ? exchange_fn<5, true>(sys, tma) : exchange_fn<5, false>(sys, tma);
-    case 6: return w16 ? exchange_fn<6, true>(sys, tma) : exchange_fn<6, false>(sys, tma);
-    case 7: return w16 ? exchange_fn<7, true>(sys, tma) : exchange_fn<7, false>(sys, tma);
-    case 8: return w16 ? exchange_fn<8, true>(sys, tma) : exchange_fn<8, false>(sys, tma);
+    case 2: return w16 ? exchange_fn<2, true>(sys, fl) : exchange_fn<2, false>(sys, fl);
+    case 3: return w16 ? exchange_fn<3, true>(sys, fl) : exchange_fn<3, false>(sys, fl);
+    case 4: return w16 ? exchange_fn<4, true>(sys, fl) : exchange_fn<4, false>(sys, fl);
+    case 5: return w16 ? exchange_fn<5, true>(sys, fl) : exchange_fn<5, false>(sys, fl);
+    case 6: return w16 ? exchange_fn<6, true>(sys, fl) : exchange_fn<6, false>(sys, fl);
+    case 7: return w16 ? exchange_fn<7, true>(sys, fl) : exchange_fn<7, false>(sys, fl);
+    case 8: return w16 ? exchange_fn<8, true>(sys, fl) : exchange_fn<8, false>(sys, fl);
     default: return nullptr;
   }
 }
 
+int flavour_threads(int fl) { return fl == kStagedTma ? kTmaThreads : (fl == kStagedWs ? kWsThreads : kThreads); }
+
 constexpr int kTmaSmem = (kInSlots + kOutSlots) * kSlotBytes;
 
 // Opt every TMA instantiation into its dynamic shared memory (idempotent).
-cudaError_t prepare(const void* fn, bool tma) {
-  if (!tma) return cudaSuccess;
+cudaError_t prepare(const void* fn, int fl) {
+  if (fl != kStagedTma) return cudaSuccess;
   return cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, kTmaSmem);
 }
 
 }  // namespace
 
-int exchange_max_ctas(int device, bool wire16, int k, bool tma) {
-  const void* fn = pick_exchange(k, wire16, true, tma);
+int exchange_max_ctas(int device, bool wire16, int k, int fl) {
+  const void* fn = pick_exchange(k, wire16, true, fl);
   if (!fn) return 0;
-  if (prepare(fn, tma) != cudaSuccess) return 0;
+  if (prepare(fn, fl) != cudaSuccess) return 0;
   int per_sm = 0;
-  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, tma ? kTmaThreads : kThreads,
-                                                    tma ? kTmaSmem : 0) != cudaSuccess)
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, flavour_threads(fl),
+                                                    fl == kStagedTma ? kTmaSmem : 0) != cudaSuccess)
     return 0;
   return per_sm * sm_count(device);
 }
 
-cudaError_t launch_exchange(const ExchangeArgs& a, int nlocal, bool wire16, bool tma, cudaStream_t s) {
+cudaError_t launch_exchange(const ExchangeArgs& a, int nlocal, bool wire16, int fl, cudaStream_t s) {
   // System-scope flags only when some peer rank lives in another process
   // (another GPU, over NVLink); a single-process group syncs at GPU scope.
-  const void* fn = pick_exchange(a.k, wire16, nlocal != a.k, tma);
+  const void* fn = pick_exchange(a.k, wire16, nlocal != a.k, fl);
   if (!fn) return cudaErrorInvalidValue;
-  cudaError_t e = prepare(fn, tma);
+  cudaError_t e = prepare(fn, fl);
   if (e != cudaSuccess) return e;
   void* params[] = {const_cast<ExchangeArgs*>(&a)};
   // Cooperative launch: guarantees every CTA is co-resident, which the
   // per-CTA flag barriers need when several ranks share this device.
-  return cudaLaunchCooperativeKernel(fn, dim3(nlocal * a.C), dim3(tma ? kTmaThreads : kThreads), params,
-                                     tma ? kTmaSmem : 0, s);
+  return cudaLaunchCooperativeKernel(fn, dim3(nlocal * a.C), dim3(flavour_threads(fl)), params,
+                                     fl == kStagedTma ? kTmaSmem : 0, s);
 }
 
 }  // namespace tmx

@@ -46,7 +46,7 @@ class tm_layout_info(ctypes.Structure):
                 ("ctas_per_rank", ctypes.c_int32), ("threads", ctypes.c_int32),
                 ("sm_count", ctypes.c_int32), ("wire_bytes", ctypes.c_int32),
                 ("lib_bytes", ctypes.c_int64), ("epoch", ctypes.c_uint32),
-                ("path", ctypes.c_int32), ("staged_tma", ctypes.c_int32)]
+                ("path", ctypes.c_int32), ("staged_kernel", ctypes.c_int32)]
 
 
 _lib = None

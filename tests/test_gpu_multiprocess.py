@@ -49,16 +49,20 @@ def launch(tmp_path, k, strategy, P, dist, mode="normal", timeout=240, extra_env
     return res
 
 
-@pytest.mark.parametrize("strategy,k,op,kernel", [("asa16", 2, "avg", "ldg"), ("asa", 2, "avg", "ldg"),
-                                                  ("asa16", 3, "avg", "ldg"), ("asa16", 2, "sum", "ldg"),
-                                                  ("asa16", 2, "range", "ldg"), ("asa16", 2, "avg", "tma"),
-                                                  ("asa", 3, "range", "tma")])
+KERNEL_ID = {"reg": 0, "tma": 1, "ws": 2}
+
+
+@pytest.mark.parametrize("strategy,k,op,kernel", [("asa16", 2, "avg", "ws"), ("asa", 2, "avg", "ws"),
+                                                  ("asa16", 3, "avg", "ws"), ("asa16", 2, "sum", "ws"),
+                                                  ("asa16", 2, "range", "ws"), ("asa16", 2, "avg", "tma"),
+                                                  ("asa", 3, "range", "tma"), ("asa16", 2, "avg", "reg"),
+                                                  ("asa", 3, "range", "reg")])
 def test_multiprocess_bitwise(tmp_path, strategy, k, op, kernel):
     P = 100_003
-    env = {"TM_STAGED_TMA": "1"} if kernel == "tma" else None
+    env = None if kernel == "ws" else {"TM_STAGED_KERNEL": kernel}
     res = launch(tmp_path, k, strategy, P, "D2", mode=("normal" if op == "avg" else op), extra_env=env)
     for r in range(k):
-        assert res[r]["layout"]["staged_tma"] == (1 if kernel == "tma" else 0)
+        assert res[r]["layout"]["staged_kernel"] == KERNEL_ID[kernel]
     op = "sum" if op == "sum" else "avg"  # bucketed ranges give the full exchange
     X = [worker_buffer(P, "D2", r, config=50) for r in range(k)]
     want = X
