@@ -338,3 +338,30 @@ def test_range_argument_errors():
             tm.tm_exchange_group_range(b, 4000, 100)  # past nparams
         assert e.value.code == tm.TM_E_ARG
         tm.tm_exchange_group_range(b, 0, 0)  # empty range: no-op
+
+
+@pytest.mark.parametrize("path", PATHS)
+@pytest.mark.parametrize("k,P", [(2, (1 << 31) + 4099), (8, (1 << 29) + 77)])
+def test_maximum_sizes_sampled(k, P, path):
+    """Buffers past 2^31 elements (8.6 GB per rank): 64-bit indexing everywhere.
+    Inputs are drawn on the device (timing-free); sampled outputs, the region
+    around element 2^31 and the ragged tail are checked against the oracle's
+    per-element definition."""
+    torch.cuda.empty_cache()
+    gen = torch.Generator(device="cuda").manual_seed(2026)
+    bufs = [(torch.randn(P, device="cuda", generator=gen) * 0.01) for _ in range(k)]
+    g = np.random.default_rng(9)
+    idx = np.unique(np.concatenate([g.integers(0, P, 100_000), np.arange(P - 1000, P),
+                                    np.arange(max(0, (1 << 31) - 300), min(P, (1 << 31) + 300)),
+                                    np.arange(0, 1000)]))
+    ti = torch.from_numpy(idx).cuda()
+    vals = np.stack([b[ti].cpu().numpy() for b in bufs])
+    with tm.Exchanger(P, "asa16", size=k, nlocal=k, path=path) as ex:
+        ex.exchange(bufs)
+        code, _ = ex.status()
+    assert code == tm.TM_OK
+    want = ox.element_average(vals, "asa16")
+    for r in (0, k - 1):
+        assert_bitwise(bufs[r][ti].cpu().numpy(), want, f"P={P} k={k} {path} rank {r}")
+    del bufs
+    torch.cuda.empty_cache()
