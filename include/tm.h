@@ -42,15 +42,19 @@
  *                      CUDA IPC mappings over NVLink/NVSwitch.  Needs the
  *                      bootstrap (export -> all-gather of blobs -> import).
  *   nlocal == size  -- a single-process group: all k ranks' buffers live on one
- *                      device ("k simulated workers"); the same kernels run with
- *                      local pointers in the peer table.  No bootstrap.
+ *                      device ("k simulated workers").  No bootstrap.  By default
+ *                      the one-pass direct path runs (tm_path below); the
+ *                      staged kernels run too (TM_PATH_STAGED), with local
+ *                      pointers in the peer table.
  * Thread safety: one host thread per process calls tm_*.
  *
  * Collective contract: every rank calls tm_exchange the same
- * number of times, in the same order.  Each call carries an epoch; cross-rank
- * synchronisation is by per-CTA epoch flags in peer memory (st.release.sys /
- * ld.acquire.sys).  A rank that never arrives makes its peers' spins time out:
- * they set TM_E_TIMEOUT in the sticky status and exit (no hang).
+ * number of times, in the same order.  Each call carries an epoch (kept on the
+ * device, per CTA, so exchanges can be captured in CUDA graphs); cross-rank
+ * synchronisation is by per-CTA epoch flags in peer memory (st.release /
+ * ld.acquire at system scope across processes, GPU scope within one).  A rank
+ * that never arrives makes its peers' spins time out: they set TM_E_TIMEOUT in
+ * the sticky status and exit (no hang); the exchanger must then be re-created.
  *
  * Errors: argument/state/launch errors are returned synchronously.  Numeric
  * conditions never abort the collective; they set sticky status bits read by
