@@ -3,7 +3,7 @@
 every kernel of libtm.so on small, ragged sizes, checked against the oracle so
 a sanitizer run is also a parity run.
 
-    compute-sanitizer --tool memcheck python tools/sanitize_driver.py
+    compute-sanitizer --tool memcheck python tests/sanitize_driver.py
 """
 
 import os

@@ -16,7 +16,7 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 @pytest.mark.parametrize("env", [{"TM_STAGED_LDG": "1"}, {"TM_STAGED_KERNEL": "ws"},
                                  {"TM_DIRECT_LDG": "1"}, {"TM_TMA_CFG": "8"}, {"TM_TMA_CFG": "3"}])
 def test_kernel_variants_bitwise(env):
-    r = subprocess.run([sys.executable, os.path.join(ROOT, "tools", "sanitize_driver.py")],
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "tests", "sanitize_driver.py")],
                        env=dict(os.environ, **env), capture_output=True, text=True, timeout=600)
     assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]
     assert "all bitwise == oracle" in r.stdout
