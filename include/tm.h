@@ -99,7 +99,8 @@ typedef enum {
   TM_E_MISMATCH = 6,   /* ranks disagree on nparams / strategy / layout           */
   TM_E_TIMEOUT = 7,    /* a peer did not arrive within the timeout (sticky)       */
   TM_E_NONFINITE = 8,  /* a non-finite input element was seen (sticky)             */
-  TM_E_OVERFLOW16 = 9  /* an input rounded to +-inf in binary16 (sticky, ASA16)    */
+  TM_E_OVERFLOW16 = 9, /* an input rounded to +-inf in binary16 (sticky, ASA16)   */
+  TM_E_IO = 10         /* loader: batch file missing, truncated or of wrong shape  */
 } tm_status;
 
 /* Sticky status bits (tm_exchange_status's `bits`). */
@@ -255,6 +256,53 @@ int tm_easgd_update_locked(float* worker_buf, int worker_id, float alpha, void* 
  * device memory owned by the caller, nchunk = ceil(seg_len/4096)); resets this
  * process's tickets.  NULL disables. */
 int tm_easgd_set_order_log(int32_t* dev_log, int max_updates_per_chunk);
+
+/* ----------------------------------------------------------------------------
+ * Parallel loading (Algorithm 1).  A native
+ * loader thread per training process reads batch files into pinned host memory
+ * (hostdata_x), copies the RAW uint8 batch to the GPU, subtracts the mean image,
+ * crops and mirrors there (gpudata_x), and at Alg. 1's synchronisation point
+ * copies gpudata_x into the trainer's input_x and notifies the trainer.
+ *
+ * Batch file: "PXB1" | u32 n | u32 c | u32 h | u32 w (little endian)
+ * | n*c*h*w uint8, NCHW.  Output input_x: fp32 [n][c][crop_h][crop_w],
+ *   input_x[b][k][y][x] = fl(float(raw[b][k][oy+y][ox+xs]) - mean[k][oy+y][ox+xs]),
+ *   xs = mirror ? crop_w-1-x : x.
+ * Crop / mirror: TRAIN mode, per example b of the f-th file loaded since create
+ * (f = 0, 1, ...): z = splitmix64(seed ^ splitmix64((f << 32) | b)),
+ * oy = z % (h-crop_h+1), ox = (z >> 20) % (w-crop_w+1), mirror = (z >> 40) & 1;
+ * VAL mode: centre crop ((h-crop_h)/2, (w-crop_w)/2), no mirror.
+ * splitmix64(z): z += 0x9E3779B97F4A7C15; z = (z ^ z>>30) * 0xBF58476D1CE4E5B9;
+ * z = (z ^ z>>27) * 0x94D049BB133111EB; return z ^ z>>31.
+ *
+ * Protocol (Alg. 1): send TRAIN or VAL, then the first FILE; every later FILE
+ * (sent when training on the last input_x is done) releases the previously
+ * loaded batch into input_x (tm_loader_wait returns once it is there) and
+ * starts loading the new one.  A TRAIN / VAL / STOP message ends the inner loop
+ * (the batch loaded last is not delivered) and is taken as the next mode
+ * (reading Q20).  ------------------------------------------------------------ */
+enum { TM_LOADER_TRAIN = 0, TM_LOADER_VAL = 1, TM_LOADER_STOP = 2, TM_LOADER_FILE = 3 };
+
+typedef struct {
+  int32_t n, c, h, w;      /* batch geometry: examples, channels, height, width   */
+  int32_t crop_h, crop_w;  /* crop window (<= h, w)                                 */
+  int32_t device;          /* CUDA device of input_x                                */
+  uint64_t seed;           /* crop / mirror generator seed                          */
+  const float* mean;       /* HOST fp32 mean image [c][h][w], copied at create      */
+} tm_loader_config;
+
+typedef struct tm_loader tm_loader;
+
+/* input_x: trainer-owned device buffer of n*c*crop_h*crop_w floats. */
+int tm_loader_create(const tm_loader_config* cfg, float* input_x, tm_loader** out);
+/* kind: TM_LOADER_*; filename for TM_LOADER_FILE (copied). Non-blocking. */
+int tm_loader_send(tm_loader* loader, int kind, const char* filename);
+/* Block until the next batch is in input_x (timeout_ms < 0: forever).
+ * TM_E_IO / TM_E_CUDA / TM_E_ARG (protocol) if the loader failed;
+ * TM_E_TIMEOUT; TM_E_STATE if the loader exited without a batch. */
+int tm_loader_wait(tm_loader* loader, int64_t timeout_ms);
+/* Send STOP, join the thread, free everything. */
+int tm_loader_destroy(tm_loader* loader);
 
 /* Synchronise `stream`, then return the most severe sticky status
  * (TM_E_TIMEOUT > TM_E_OVERFLOW16 > TM_E_NONFINITE > TM_OK) and clear it.

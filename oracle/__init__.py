@@ -18,9 +18,10 @@ Modules
   exchange  -- partition / alltoall / allgather / ASA / ASA16 / AR averaging
   easgd     -- elastic-averaging update and arrival-order sequences
   bsp       -- momentum-SGD step followed by the exchange (one BSP iteration)
+  loader    -- Alg. 1 preprocessing (mean, crop, mirror) and delivery sequence
 
 Parity status of every function is listed in each module's header and in
 DESIGN.md section "Oracle and pins".
 """
 
-from . import fp16, exchange, easgd, bsp  # noqa: F401
+from . import fp16, exchange, easgd, bsp, loader  # noqa: F401

@@ -90,6 +90,9 @@ cudaError_t launch_bsp_direct(const BspBufs& bb, int k, int64_t P, bool q16, boo
                               uint32_t* status, cudaStream_t s);
 cudaError_t launch_sgd(float* w, float* v, const float* g, int64_t n, float lr, float mu,
                        cudaStream_t s);
+// Alg. 1 preprocessing (tm_loader_kernels.cu): mean subtraction, crop, mirror.
+cudaError_t launch_preprocess(const uint8_t* raw, const float* mean, const int32_t* crop, float* out,
+                              int n, int c, int h, int w, int ch, int cw, cudaStream_t s);
 cudaError_t launch_cast_rn16(const float* in, uint16_t* out, int64_t n, cudaStream_t s);
 
 // Max co-resident CTAs of the exchange kernel on `device` (occupancy * SMs).

@@ -631,6 +631,7 @@ const char* tm_strerror(int status) {
     case TM_E_TIMEOUT: return "peer did not arrive before the timeout";
     case TM_E_NONFINITE: return "non-finite input element";
     case TM_E_OVERFLOW16: return "input overflows binary16 (|x| >= 65520)";
+    case TM_E_IO: return "batch file missing, truncated or of the wrong shape";
     default: return "unknown status";
   }
 }

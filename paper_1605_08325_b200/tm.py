@@ -79,6 +79,10 @@ _SIGS = {
     "tm_exchange_finalize": (ctypes.c_int, []),
     "tm_strerror": (ctypes.c_char_p, [ctypes.c_int]),
     "tm_cast_rn16": (ctypes.c_int, [_P, _P, ctypes.c_int64, _P]),
+    "tm_loader_create": (ctypes.c_int, [_P, _P, _P]),
+    "tm_loader_send": (ctypes.c_int, [_P, ctypes.c_int, ctypes.c_char_p]),
+    "tm_loader_wait": (ctypes.c_int, [_P, ctypes.c_int64]),
+    "tm_loader_destroy": (ctypes.c_int, [_P]),
 }
 
 
@@ -275,6 +279,71 @@ def device_view(ptr, n, device=None):
                                     "data": (int(ptr), False), "version": 2}
 
     return torch.as_tensor(_Iface(), device=device or torch.cuda.current_device())
+
+
+# ------------------------------------------------------------ parallel loading
+
+TM_LOADER_TRAIN, TM_LOADER_VAL, TM_LOADER_STOP, TM_LOADER_FILE = 0, 1, 2, 3
+TM_E_IO = 10
+
+
+class tm_loader_config(ctypes.Structure):
+    _fields_ = [("n", ctypes.c_int32), ("c", ctypes.c_int32), ("h", ctypes.c_int32),
+                ("w", ctypes.c_int32), ("crop_h", ctypes.c_int32), ("crop_w", ctypes.c_int32),
+                ("device", ctypes.c_int32), ("seed", ctypes.c_uint64),
+                ("mean", ctypes.POINTER(ctypes.c_float))]
+
+
+def write_batch_file(path, raw):
+    """Write a uint8 [n, c, h, w] batch as a PXB1 file."""
+    import struct
+    import numpy as np
+    raw = np.ascontiguousarray(raw, dtype=np.uint8)
+    if raw.ndim != 4:
+        raise ValueError("expected [n, c, h, w]")
+    with open(path, "wb") as f:
+        f.write(b"PXB1" + struct.pack("<4I", *raw.shape))
+        f.write(raw.tobytes())
+
+
+class Loader:
+    """Alg. 1's parallel loading process (tm_loader_*): a native loader thread
+    that reads batch files, preprocesses them on the GPU and hands each batch to
+    `input_x` when the trainer asks for the next file."""
+
+    def __init__(self, n, c, h, w, crop_h, crop_w, mean, input_x, seed=0, device=None):
+        import numpy as np
+        self._mean = np.ascontiguousarray(mean, dtype=np.float32)
+        if self._mean.shape != (c, h, w):
+            raise ValueError("mean image must be [c, h, w]")
+        _fp32_cuda(input_x, n * c * crop_h * crop_w)
+        self.input_x = input_x
+        cfg = tm_loader_config(n, c, h, w, crop_h, crop_w,
+                               input_x.device.index if device is None else device, seed,
+                               self._mean.ctypes.data_as(ctypes.POINTER(ctypes.c_float)))
+        self._h = ctypes.c_void_p()
+        _check(lib().tm_loader_create(ctypes.byref(cfg), ctypes.c_void_p(input_x.data_ptr()),
+                                      ctypes.byref(self._h)), "tm_loader_create")
+
+    def send(self, kind, filename=None):
+        k = {"train": TM_LOADER_TRAIN, "val": TM_LOADER_VAL, "stop": TM_LOADER_STOP,
+             "file": TM_LOADER_FILE}[kind]
+        _check(lib().tm_loader_send(self._h, k, None if filename is None else filename.encode()),
+               "tm_loader_send")
+
+    def wait(self, timeout_ms=-1):
+        _check(lib().tm_loader_wait(self._h, int(timeout_ms)), "tm_loader_wait")
+
+    def close(self):
+        if self._h:
+            lib().tm_loader_destroy(self._h)
+            self._h = ctypes.c_void_p()
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()
 
 
 # ------------------------------------------------------------ convenience
