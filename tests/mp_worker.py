@@ -10,6 +10,7 @@ argv: outdir strategy P dist mode      (mode: normal | sum | range | locked | sk
 import json
 import os
 import sys
+import time
 
 import numpy as np
 import torch
@@ -20,6 +21,8 @@ sys.path.insert(0, ROOT)
 
 from paper_1605_08325_b200 import tm  # noqa: E402
 from paper_1605_08325_b200.inputs import worker_buffer  # noqa: E402
+
+STRESS_ITERS = 60
 
 
 def main():
@@ -78,6 +81,27 @@ def main():
         dist.destroy_process_group()
         return
     x = torch.from_numpy(worker_buffer(P, dist_name, rank, config=50)).cuda()
+    if mode == "stress":
+        # back-to-back exchanges with random host delays between calls on each
+        # rank (exercises the epoch / reuse protocol); each iteration
+        # first adds a deterministic per-rank delta
+        import random
+        rnd = random.Random(1000 + rank)
+        for it in range(STRESS_ITERS):
+            d = np.random.default_rng([1605, rank, it]).standard_normal(P).astype(np.float32) * np.float32(1e-3)
+            x.add_(torch.from_numpy(d).cuda())
+            if rnd.random() < 0.5:
+                torch.cuda.synchronize()
+                time.sleep(rnd.random() * 0.003)
+            ex.exchange(x)
+        code, bits = ex.status()
+        result.update({"code": code, "bits": bits, "layout": ex.layout()})
+        np.save(os.path.join(outdir, f"rank{rank}.npy"), x.cpu().numpy())
+        json.dump(result, open(os.path.join(outdir, f"rank{rank}.json"), "w"))
+        dist.barrier()
+        ex.finalize()
+        dist.destroy_process_group()
+        return
     reps = 3
     if mode == "skip1" and rank == 1:
         reps = 0  # never arrives: rank 0 must time out, not hang

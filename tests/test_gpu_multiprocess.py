@@ -130,3 +130,21 @@ def test_multiprocess_locked_easgd(tmp_path):
             assert_bitwise(gc[lo:hi], cc, f"chunk ({s},{q})")
             for r in range(k):
                 assert_bitwise(gW[r][lo:hi], ws[r])
+
+
+@pytest.mark.parametrize("strategy,kernel", [("asa16", "ws"), ("asa", "reg"), ("asa16", "tma")])
+def test_multiprocess_stress_random_delays(tmp_path, strategy, kernel):
+    """60 back-to-back exchanges per rank, each after a per-rank delta and a random
+    host delay on half of them: every rank ends bitwise at the oracle's sequence."""
+    from mp_worker import STRESS_ITERS
+    P, k = 50_003, 2
+    env = None if kernel == "ws" else {"TM_STAGED_KERNEL": kernel}
+    res = launch(tmp_path, k, strategy, P, "D2", mode="stress", extra_env=env, timeout=600)
+    X = [worker_buffer(P, "D2", r, config=50) for r in range(k)]
+    for it in range(STRESS_ITERS):
+        X = [np.add(X[r], np.random.default_rng([1605, r, it]).standard_normal(P).astype(np.float32)
+                    * np.float32(1e-3), dtype=np.float32) for r in range(k)]
+        X = ox.exchange(X, strategy)
+    for r in range(k):
+        assert res[r]["code"] == 0, res[r]
+        assert_bitwise(np.load(os.path.join(tmp_path, f"rank{r}.npy")), X[r], f"rank {r}")
