@@ -41,27 +41,46 @@ def needs_build():
     if not os.path.exists(LIB):
         return True
     t = os.path.getmtime(LIB)
-    deps = sources() + glob.glob(os.path.join(CSRC, "*.h")) + [os.path.join(ROOT, "include", "tm.h")]
+    deps = (sources() + glob.glob(os.path.join(CSRC, "*.h")) + glob.glob(os.path.join(CSRC, "*.cuh"))
+            + [os.path.join(ROOT, "include", "tm.h")])
     return any(os.path.getmtime(d) > t for d in deps)
 
 
+def _compile_one(nvcc, src, obj, verbose):
+    cmd = [nvcc, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", *NUMERICS,
+           "-Xptxas", "-v" if verbose else "-O3",
+           "-I", os.path.join(ROOT, "include"), "-I", CSRC, "-I", nccl_include(), "-c", src, "-o", obj]
+    r = subprocess.run(cmd, capture_output=True, text=True)
+    return src, r
+
+
 def build(force=False, verbose=False):
+    """Compile every source to an object in parallel, then link libtm.so."""
     if not force and not needs_build():
         return LIB
+    import concurrent.futures
+    import tempfile
     nvcc = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
-    cmd = [nvcc, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-shared", "-Xcompiler", "-fPIC",
-           *NUMERICS, "-Xptxas", "-v" if verbose else "-O3",
-           "-I", os.path.join(ROOT, "include"), "-I", CSRC, "-I", nccl_include(),
-           "-o", LIB + ".tmp", *sources(), "-ldl", "-cudart", "static"]
-    if verbose:
-        print(" ".join(cmd))
-    r = subprocess.run(cmd, capture_output=True, text=True)
+    objdir = tempfile.mkdtemp(prefix="tm_build_")
+    srcs = sources()
+    objs = [os.path.join(objdir, os.path.basename(sname) + ".o") for sname in srcs]
+    with concurrent.futures.ThreadPoolExecutor(max_workers=min(len(srcs), os.cpu_count() or 4)) as pool:
+        results = list(pool.map(lambda so: _compile_one(nvcc, so[0], so[1], verbose), zip(srcs, objs)))
+    for src, r in results:
+        if r.returncode != 0:
+            sys.stderr.write(r.stdout + r.stderr)
+            raise RuntimeError(f"nvcc failed on {os.path.basename(src)}")
+        if verbose:
+            sys.stderr.write(r.stderr)
+    link = [nvcc, *ARCH, "-shared", "-o", LIB + ".tmp", *objs, "-ldl", "-cudart", "static"]
+    r = subprocess.run(link, capture_output=True, text=True)
     if r.returncode != 0:
         sys.stderr.write(r.stdout + r.stderr)
-        raise RuntimeError("nvcc failed building libtm.so")
-    if verbose:
-        sys.stderr.write(r.stderr)
+        raise RuntimeError("nvcc failed linking libtm.so")
     os.replace(LIB + ".tmp", LIB)
+    for o in objs:
+        os.remove(o)
+    os.rmdir(objdir)
     return LIB
 
 
