@@ -316,6 +316,14 @@ int tm_layout(tm_layout_info* out);
  * TM_E_ARG for TM_PATH_DIRECT unless nlocal == size; TM_E_STATE before init. */
 int tm_set_path(int path);
 
+/* Diagnostics: the staged kernels write %globaltimer (ns) of every CTA at its
+ * phase boundaries into dev_buf[cta*8 + slot] (slot 0 start, 1 pre-cast done,
+ * 2 READY acquired, 3 reduce-scatter done, 4 REDUCED acquired, 5 end; the
+ * warp-specialised kernel overlaps pre-cast and reduce-scatter and writes only
+ * 0, 3, 4, 5).  capacity in uint64 slots (>= nlocal*C*8, else ignored); NULL
+ * disables. */
+int tm_set_phase_log(uint64_t* dev_buf, int64_t capacity);
+
 /* Barrier spin timeout in nanoseconds (default 10 s; 0 restores default). */
 int tm_set_timeout_ns(uint64_t ns);
 

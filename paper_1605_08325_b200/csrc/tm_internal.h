@@ -37,11 +37,16 @@ struct ExchangeArgs {
   int32_t flag_stride;            // C the flag pad was laid out for (>= C)
   int32_t sum;                    // SUBGD: sum, no 1/k
   uint64_t timeout_ns;
+  uint64_t* stamps;               // diagnostics: %globaltimer per CTA and phase, or null
 };
 
 // Persistent fused exchange: pre-cast -> ready barrier -> reduce-scatter pull with
 // fused sum/scale/cast -> reduced barrier -> allgather pull with fused widen.
 // wire16: fp16 wire (ASA16) else fp32 (ASA).  grid = nlocal * C, cooperative.
+// Phase stamps (tm_set_phase_log): slot [blockIdx][kStamp*] of the staged kernels.
+constexpr int kStampSlots = 8;
+enum { kStampStart = 0, kStampCast = 1, kStampReady = 2, kStampReduce = 3, kStampReduced = 4,
+       kStampEnd = 5 };
 // Staged kernel flavours.
 enum StagedKernel { kStagedReg = 0, kStagedTma = 1, kStagedWs = 2 };
 cudaError_t launch_exchange(const ExchangeArgs& a, int nlocal, bool wire16, int flavour, cudaStream_t s);

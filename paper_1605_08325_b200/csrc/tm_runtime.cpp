@@ -72,6 +72,8 @@ struct Ctx {
   int64_t rank_stride = 0, off_stage = 0, off_avg = 0, off_flags = 0, off_center = 0;
   int64_t off_locks = 0, off_tickets = 0;  // EASGD locked mode
   int32_t* order_log = nullptr;            // test hook (tm_easgd_set_order_log)
+  uint64_t* stamps = nullptr;              // diagnostics (tm_set_phase_log)
+  int64_t stamps_cap = 0;
   int order_log_stride = 0;
   int64_t slab_bytes = 0;
   char* slab = nullptr;
@@ -151,6 +153,7 @@ ExchangeArgs make_args(float* const* bufs, int64_t off, int64_t n) {
   a.rank0 = g.rank0;
   a.sum = g.sum ? 1 : 0;
   a.timeout_ns = g.timeout_ns;
+  a.stamps = (g.stamps && g.stamps_cap >= (int64_t)g.nlocal * a.C * tmx::kStampSlots) ? g.stamps : nullptr;
   return a;
 }
 
@@ -600,6 +603,15 @@ int tm_set_path(int path) {
   if (path < TM_PATH_AUTO || path > TM_PATH_DIRECT) return TM_E_ARG;
   if (path == TM_PATH_DIRECT && g.nlocal != g.k) return TM_E_ARG;
   g.path = path;
+  return TM_OK;
+}
+
+int tm_set_phase_log(uint64_t* dev_buf, int64_t capacity) {
+  std::lock_guard<std::mutex> lk(g_mu);
+  if (!g.inited) return TM_E_STATE;
+  if (dev_buf && capacity < 1) return TM_E_ARG;
+  g.stamps = dev_buf;
+  g.stamps_cap = dev_buf ? capacity : 0;
   return TM_OK;
 }
 

@@ -47,6 +47,15 @@ namespace tmx {
 namespace {
 using namespace dev;
 
+// Diagnostics: CTA-wide timestamp at a phase boundary (kernel-uniform branch;
+// costs nothing when the log is off).
+__device__ __forceinline__ void stamp(const ExchangeArgs& a, int slot) {
+  if (a.stamps) {
+    __syncthreads();
+    if (threadIdx.x == 0) a.stamps[(size_t)blockIdx.x * kStampSlots + slot] = globaltimer();
+  }
+}
+
 // Cross-rank, per-CTA epoch barrier (see the protocol in the file header).
 // Returns false (whole CTA) if a peer timed out.
 template <int K, bool SYS>
@@ -99,6 +108,7 @@ tm_exchange_kernel(const __grid_constant__ ExchangeArgs a) {
   }
   __syncthreads();
   const uint32_t epoch = s_epoch;
+  stamp(a, kStampStart);
   float* __restrict__ x = a.x[lr];
   const int64_t P = a.P, L = a.L;
   const int64_t e0 = (int64_t)c * a.Lc;
@@ -142,8 +152,10 @@ tm_exchange_kernel(const __grid_constant__ ExchangeArgs a) {
     }
   }
   if (st) atomicOr(a.status, st);  // rare: only threads that saw a bad value
+  stamp(a, kStampCast);
 
   if (!rank_barrier<K, SYS>(a, kPhaseReady, r, c, epoch, &s_abort)) return;
+  stamp(a, kStampReady);
 
   // ---------------- a4: reduce-scatter pull, fused sum / (1/k) / cast -------
   {
@@ -176,8 +188,10 @@ tm_exchange_kernel(const __grid_constant__ ExchangeArgs a) {
     }
   }
   if (st) atomicOr(a.status, st);
+  stamp(a, kStampReduce);
 
   if (!rank_barrier<K, SYS>(a, kPhaseReduced, r, c, epoch, &s_abort)) return;
+  stamp(a, kStampReduced);
 
   // ---------------- a6: allgather pull, fused widen, store to caller ---------
   {
@@ -203,6 +217,7 @@ tm_exchange_kernel(const __grid_constant__ ExchangeArgs a) {
       }
     }
   }
+  stamp(a, kStampEnd);
 }
 
 // ---------------------------------------------------------------------------
@@ -245,6 +260,7 @@ tm_exchange_ws_kernel(const __grid_constant__ ExchangeArgs a) {
   }
   __syncthreads();
   const uint32_t epoch = s_epoch;
+  stamp(a, kStampStart);
   float* __restrict__ x = a.x[lr];
   const int64_t P = a.P, L = a.L;
   const int64_t e0 = (int64_t)c * a.Lc;
@@ -348,7 +364,9 @@ tm_exchange_ws_kernel(const __grid_constant__ ExchangeArgs a) {
   if (st) atomicOr(a.status, st);
   __syncthreads();
   if (s_abort) return;
+  stamp(a, kStampReduce);  // pre-cast and reduce-scatter overlap: one stamp for both
   if (!rank_barrier<K, SYS>(a, kWsSub, r, c, epoch, &s_abort)) return;  // REDUCED
+  stamp(a, kStampReduced);
 
   // ---------------- a6: allgather pull with all 16 warps ----------------------
   const int nu32 = (int)(nel / E);
@@ -371,6 +389,7 @@ tm_exchange_ws_kernel(const __grid_constant__ ExchangeArgs a) {
       }
     }
   }
+  stamp(a, kStampEnd);
 }
 
 // ---------------------------------------------------------------------------
@@ -481,6 +500,7 @@ tm_exchange_tma_kernel(const __grid_constant__ ExchangeArgs a) {
   }
   __syncthreads();
   const uint32_t epoch = s_epoch;
+  stamp(a, kStampStart);
   uint32_t use = 0, outn = 0, st = 0;
 
   // ---------------- a2: pre-cast x -> own stage (all k segments' chunk c) ----
@@ -533,7 +553,9 @@ tm_exchange_tma_kernel(const __grid_constant__ ExchangeArgs a) {
   }
   if (st) atomicOr(a.status, st);
   drain_bulk_stores();
+  stamp(a, kStampCast);
   if (!rank_barrier<K, SYS>(a, kPhaseReady, r, c, epoch, &s_abort)) return;
+  stamp(a, kStampReady);
   if (tid == 0) fence_proxy_async_global();  // peers' staging, acquired above -> bulk loads
 
   // ---------------- a4: reduce-scatter pull (TMA from every rank's stage) ----
@@ -584,7 +606,9 @@ tm_exchange_tma_kernel(const __grid_constant__ ExchangeArgs a) {
   }
   if (st) atomicOr(a.status, st);
   drain_bulk_stores();
+  stamp(a, kStampReduce);
   if (!rank_barrier<K, SYS>(a, kPhaseReduced, r, c, epoch, &s_abort)) return;
+  stamp(a, kStampReduced);
   if (tid == 0) fence_proxy_async_global();
 
   // ---------------- a6: allgather pull (TMA from every rank's avg) ----------
@@ -638,6 +662,7 @@ tm_exchange_tma_kernel(const __grid_constant__ ExchangeArgs a) {
         });
   }
   if (tid == 0) bulk_wait_all<0>();  // kernel exit also waits; explicit for clarity
+  stamp(a, kStampEnd);
 }
 
 template <int K, bool W16>

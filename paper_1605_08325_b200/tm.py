@@ -76,6 +76,7 @@ _SIGS = {
     "tm_layout": (ctypes.c_int, [ctypes.POINTER(tm_layout_info)]),
     "tm_set_timeout_ns": (ctypes.c_int, [ctypes.c_uint64]),
     "tm_set_path": (ctypes.c_int, [ctypes.c_int]),
+    "tm_set_phase_log": (ctypes.c_int, [_P, ctypes.c_int64]),
     "tm_exchange_finalize": (ctypes.c_int, []),
     "tm_strerror": (ctypes.c_char_p, [ctypes.c_int]),
     "tm_cast_rn16": (ctypes.c_int, [_P, _P, ctypes.c_int64, _P]),
@@ -255,6 +256,12 @@ def tm_set_timeout_ns(ns):
 
 def tm_set_path(path):
     _check(lib().tm_set_path(PATH[path] if isinstance(path, str) else int(path)), "tm_set_path")
+
+
+def tm_set_phase_log(buf):
+    """buf: int64 CUDA tensor (>= nlocal*C*8 slots) or None."""
+    _check(lib().tm_set_phase_log(None if buf is None else ctypes.c_void_p(buf.data_ptr()),
+                                  0 if buf is None else buf.numel()), "tm_set_phase_log")
 
 
 def tm_exchange_finalize():

@@ -365,3 +365,25 @@ def test_maximum_sizes_sampled(k, P, path):
         assert_bitwise(bufs[r][ti].cpu().numpy(), want, f"P={P} k={k} {path} rank {r}")
     del bufs
     torch.cuda.empty_cache()
+
+
+@pytest.mark.parametrize("path", PATHS)
+def test_phase_log_does_not_change_results(path):
+    """The diagnostic phase log (tm_set_phase_log) is monotone per CTA and leaves
+    the exchange bitwise unchanged."""
+    k, P = 4, 300_007
+    X = worker_buffers(P, k, "D2", config=95)
+    bufs = to_dev(X)
+    with tm.Exchanger(P, "asa16", size=k, nlocal=k, path=path) as ex:
+        C = ex.layout()["ctas_per_rank"]
+        log = torch.zeros(k * C * 8, dtype=torch.int64, device="cuda")
+        tm.tm_set_phase_log(log)
+        ex.exchange(bufs)
+        tm.tm_set_phase_log(None)
+        out = to_host(bufs)
+    want = ox.asa16_average(X)
+    for r in range(k):
+        assert_bitwise(out[r], want[r])
+    st = log.cpu().numpy().reshape(-1, 8)[:, :6]
+    if path == "staged":
+        assert np.all(st[:, 0] > 0) and np.all(np.diff(st[:, [0, 1, 2, 3, 4, 5]], axis=1) >= 0)
