@@ -465,7 +465,7 @@ tm_exchange_tma_kernel(const __grid_constant__ ExchangeArgs a) {
   using U = Unit<W16>;
   constexpr int E = U::kElems;      // elements per 16-byte wire unit
   constexpr int WB = W16 ? 2 : 4;   // wire bytes per element
-  constexpr int TP = 4096;          // a2 tile: fp32 in 16 KB, wire out <= 16 KB
+  constexpr int TP = 8192;          // a2 tile: fp32 in 32 KB, wire out <= 32 KB
   // a4 tile: k sources of TR wire elements fit one 32 KB slot; a multiple of 256
   // elements keeps every source's smem offset and byte count 16-byte aligned.
   constexpr int TR_RAW = kSlotBytes / (K * WB) / 256 * 256;
