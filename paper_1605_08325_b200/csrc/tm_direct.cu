@@ -130,7 +130,7 @@ struct TmaCfg {
 template <int K, bool Q16, int TILE, int RING_KB, int MINB>
 __global__ void __launch_bounds__(kThreads, MINB)
 tm_direct_tma_kernel(const __grid_constant__ LocalBufs lb, int64_t ntiles, int64_t P,
-                     uint32_t* status) {
+                     uint32_t* status, unsigned long long* tile_ctr) {
   using Cfg = TmaCfg<K, TILE, RING_KB, MINB>;
   constexpr int S = Cfg::kStages;
   constexpr int V = Cfg::kVecPerThread;
@@ -139,14 +139,31 @@ tm_direct_tma_kernel(const __grid_constant__ LocalBufs lb, int64_t ntiles, int64
   float* ring = reinterpret_cast<float*>(smem);                  // [S][K][TILE]
   float* outr = ring + (size_t)S * K * TILE;                     // [kOutRing][TILE]
   __shared__ __align__(8) uint64_t full[S];
+  __shared__ int64_t slot_tile[S];  // tile held by each ring slot, -1 = none left
 
   const int tid = threadIdx.x;
-  // tiles of this CTA: blockIdx.x, blockIdx.x + gridDim.x, ...
-  const int64_t my = blockIdx.x < ntiles ? (ntiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
-  auto tile_of = [&](int64_t i) { return (int64_t)blockIdx.x + i * gridDim.x; };
-  auto issue = [&](int64_t i) {
+  // Tiles are claimed dynamically from a per-launch counter (work stealing), so
+  // a slow SM does not hold back the end of the kernel; without a counter the
+  // static assignment blockIdx.x + i * gridDim.x is used.
+  int64_t next_static = blockIdx.x;
+  auto claim = [&]() -> int64_t {
+    int64_t t;
+    if (tile_ctr) {
+      t = (int64_t)atomicAdd(tile_ctr, 1ull);
+    } else {
+      t = next_static;
+      next_static += gridDim.x;
+    }
+    return t < ntiles ? t : -1;
+  };
+  auto issue = [&](int64_t i) {  // thread 0: fill ring slot i % S with the next tile
     const int s = (int)(i % S);
-    const int64_t t = tile_of(i);
+    const int64_t t = claim();
+    slot_tile[s] = t;  // published to the consumers by the mbarrier arrive below
+    if (t < 0) {
+      mbar_expect_tx(&full[s], 0);
+      return;
+    }
     mbar_expect_tx(&full[s], K * TB);
 #pragma unroll
     for (int j = 0; j < K; ++j)
@@ -156,14 +173,16 @@ tm_direct_tma_kernel(const __grid_constant__ LocalBufs lb, int64_t ntiles, int64
   if (tid == 0) {
     for (int s = 0; s < S; ++s) mbar_init(&full[s], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    for (int64_t i = 0; i < S && i < my; ++i) issue(i);
+    for (int64_t i = 0; i < S; ++i) issue(i);
   }
   __syncthreads();
 
   uint32_t st = 0;
-  for (int64_t i = 0; i < my; ++i) {
+  for (int64_t i = 0;; ++i) {
     const int s = (int)(i % S);
     mbar_wait(&full[s], (uint32_t)((i / S) & 1));
+    const int64_t t = slot_tile[s];
+    if (t < 0) break;  // uniform: every later claim is past the end too
     float* out = outr + (size_t)(i % kOutRing) * TILE;
 #pragma unroll
     for (int u = 0; u < V; ++u) {
@@ -177,11 +196,10 @@ tm_direct_tma_kernel(const __grid_constant__ LocalBufs lb, int64_t ntiles, int64
     if (tid == 0) bulk_wait_read<kOutRing - 2>();  // out slot of tile i+1 is free
     __syncthreads();
     if (tid == 0) {
-      const int64_t t = tile_of(i);
 #pragma unroll
       for (int j = 0; j < K; ++j) bulk_store(lb.b[j] + t * TILE, out, TB);
       bulk_commit();
-      if (i + S < my) issue(i + S);  // every thread has finished reading ring slot s
+      issue(i + S);  // every thread has finished reading ring slot s
     }
   }
   if (tid == 0) bulk_wait_all<0>();
@@ -206,7 +224,8 @@ tm_direct_tma_kernel(const __grid_constant__ LocalBufs lb, int64_t ntiles, int64
 }  // namespace
 
 template <int K, bool Q16, int TILE, int RING_KB, int MINB>
-cudaError_t launch_tma(const LocalBufs& lb, int64_t P, uint32_t* status, int dev, cudaStream_t s) {
+cudaError_t launch_tma(const LocalBufs& lb, int64_t P, uint32_t* status, unsigned long long* ctr,
+                       int dev, cudaStream_t s) {
   using Cfg = TmaCfg<K, TILE, RING_KB, MINB>;
   const int64_t ntiles = P / TILE;
   auto fn = tm_direct_tma_kernel<K, Q16, TILE, RING_KB, MINB>;
@@ -217,39 +236,45 @@ cudaError_t launch_tma(const LocalBufs& lb, int64_t P, uint32_t* status, int dev
     attr_set = true;
   }
   const int grid = (int)std::min<int64_t>(ntiles, (int64_t)MINB * sm_count(dev));
-  fn<<<grid, kThreads, Cfg::kSmem, s>>>(lb, ntiles, P, status);
+  if (ctr) {  // per-launch tile counter (stream-ordered reset; capturable in graphs)
+    cudaError_t e = cudaMemsetAsync(ctr, 0, sizeof(unsigned long long), s);
+    if (e != cudaSuccess) return e;
+  }
+  fn<<<grid, kThreads, Cfg::kSmem, s>>>(lb, ntiles, P, status, ctr);
   return cudaGetLastError();
 }
 
 // Tuning knobs (diagnostics only): TM_TMA_CFG selects the tile / ring / residency
 // of the bulk-async kernel for k = 8; TM_DIRECT_LDG=1 forces the register path.
 template <int K, bool Q16>
-cudaError_t direct_tma(const LocalBufs& lb, int64_t P, uint32_t* status, int dev, cudaStream_t s) {
+cudaError_t direct_tma(const LocalBufs& lb, int64_t P, uint32_t* status, unsigned long long* ctr,
+                       int dev, cudaStream_t s) {
   if constexpr (K == 8) {
     static const int cfg = env_int("TM_TMA_CFG", 0);
     switch (cfg) {
-      case 8: return launch_tma<K, Q16, 1024, 160, 1>(lb, P, status, dev, s);
-      case 1: return launch_tma<K, Q16, 1024, 96, 2>(lb, P, status, dev, s);
-      case 2: return launch_tma<K, Q16, 2048, 192, 1>(lb, P, status, dev, s);
-      case 3: return launch_tma<K, Q16, 1024, 64, 2>(lb, P, status, dev, s);
-      case 4: return launch_tma<K, Q16, 2048, 96, 2>(lb, P, status, dev, s);
-      case 5: return launch_tma<K, Q16, 2048, 96, 1>(lb, P, status, dev, s);
-      case 6: return launch_tma<K, Q16, 2048, 96, 3>(lb, P, status, dev, s);
-      case 7: return launch_tma<K, Q16, 2048, 192, 1>(lb, P, status, dev, s);
+      case 8: return launch_tma<K, Q16, 1024, 160, 1>(lb, P, status, ctr, dev, s);
+      case 1: return launch_tma<K, Q16, 1024, 96, 2>(lb, P, status, ctr, dev, s);
+      case 2: return launch_tma<K, Q16, 2048, 192, 1>(lb, P, status, ctr, dev, s);
+      case 3: return launch_tma<K, Q16, 1024, 64, 2>(lb, P, status, ctr, dev, s);
+      case 4: return launch_tma<K, Q16, 2048, 96, 2>(lb, P, status, ctr, dev, s);
+      case 5: return launch_tma<K, Q16, 2048, 96, 1>(lb, P, status, ctr, dev, s);
+      case 6: return launch_tma<K, Q16, 2048, 96, 3>(lb, P, status, ctr, dev, s);
+      case 7: return launch_tma<K, Q16, 2048, 192, 1>(lb, P, status, ctr, dev, s);
       default: break;
     }
   }
   // Default, from the r01 sweep at k = 8 (profiles/r01/README.md): 8 KB tiles per
   // buffer, a 2-deep ring for k = 8 (128 KB in flight per SM), one CTA per SM.
-  return launch_tma<K, Q16, 2048, 96, 1>(lb, P, status, dev, s);
+  return launch_tma<K, Q16, 2048, 96, 1>(lb, P, status, ctr, dev, s);
 }
 
 template <int K>
-cudaError_t direct_k(const LocalBufs& lb, int64_t P, uint32_t* status, bool q16, int dev,
-                     cudaStream_t s) {
+cudaError_t direct_k(const LocalBufs& lb, int64_t P, uint32_t* status, unsigned long long* ctr,
+                     bool q16, int dev, cudaStream_t s) {
   static const bool force_ldg = env_int("TM_DIRECT_LDG", 0) == 1;
   if (P >= 2048 && !force_ldg)
-    return q16 ? direct_tma<K, true>(lb, P, status, dev, s) : direct_tma<K, false>(lb, P, status, dev, s);
+    return q16 ? direct_tma<K, true>(lb, P, status, ctr, dev, s)
+               : direct_tma<K, false>(lb, P, status, ctr, dev, s);
   const int64_t want = (P / 4 + kThreads - 1) / kThreads;
   const int per_sm = K >= 7 ? 3 : 4;  // = the kernel's __launch_bounds__ residency
   const int grid = (int)std::min<int64_t>(std::max<int64_t>(want, 1), per_sm * sm_count(dev));
@@ -259,20 +284,20 @@ cudaError_t direct_k(const LocalBufs& lb, int64_t P, uint32_t* status, bool q16,
 }
 
 cudaError_t launch_direct(float* const* bufs, int k, int64_t P, bool q16, bool sum,
-                          uint32_t* status, cudaStream_t s) {
+                          uint32_t* status, unsigned long long* tile_ctr, cudaStream_t s) {
   LocalBufs lb{};
   lb.sum = sum ? 1 : 0;
   for (int j = 0; j < k; ++j) lb.b[j] = bufs[j];
   int dev = 0;
   cudaGetDevice(&dev);
   switch (k) {
-    case 2: return direct_k<2>(lb, P, status, q16, dev, s);
-    case 3: return direct_k<3>(lb, P, status, q16, dev, s);
-    case 4: return direct_k<4>(lb, P, status, q16, dev, s);
-    case 5: return direct_k<5>(lb, P, status, q16, dev, s);
-    case 6: return direct_k<6>(lb, P, status, q16, dev, s);
-    case 7: return direct_k<7>(lb, P, status, q16, dev, s);
-    case 8: return direct_k<8>(lb, P, status, q16, dev, s);
+    case 2: return direct_k<2>(lb, P, status, tile_ctr, q16, dev, s);
+    case 3: return direct_k<3>(lb, P, status, tile_ctr, q16, dev, s);
+    case 4: return direct_k<4>(lb, P, status, tile_ctr, q16, dev, s);
+    case 5: return direct_k<5>(lb, P, status, tile_ctr, q16, dev, s);
+    case 6: return direct_k<6>(lb, P, status, tile_ctr, q16, dev, s);
+    case 7: return direct_k<7>(lb, P, status, tile_ctr, q16, dev, s);
+    case 8: return direct_k<8>(lb, P, status, tile_ctr, q16, dev, s);
     default: return cudaErrorInvalidValue;
   }
 }

@@ -55,8 +55,10 @@ cudaError_t launch_exchange(const ExchangeArgs& a, int nlocal, bool wire16, int 
 // of each element from the k buffers, fused rn16 (q16) / ascending-rank sum /
 // (1/k) / rn16, push the result to all k buffers.  Also AR when all ranks are
 // local (q16 = false).
+// tile_ctr: device counter for dynamic tile claiming (reset by the launch), or
+// null for the static tile assignment.
 cudaError_t launch_direct(float* const* bufs, int k, int64_t P, bool q16, bool sum,
-                          uint32_t* status, cudaStream_t s);
+                          uint32_t* status, unsigned long long* tile_ctr, cudaStream_t s);
 
 cudaError_t launch_easgd(float* x, float* c, int64_t n, float alpha, bool concurrent,
                          cudaStream_t s);

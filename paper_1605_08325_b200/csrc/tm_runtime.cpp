@@ -176,7 +176,10 @@ int do_exchange(float* const* bufs, int nbufs, int64_t off, int64_t n, cudaStrea
   if (g.nlocal == g.k && (g.strategy == TM_AR || effective_path() == TM_PATH_DIRECT)) {
     float* shifted[TM_MAX_RANKS];
     for (int i = 0; i < nbufs; ++i) shifted[i] = bufs[i] + off;
-    cudaError_t e = tmx::launch_direct(shifted, g.k, n, g.strategy == TM_ASA16, g.sum, g.status, s);
+    const char* st_env = getenv("TM_DIRECT_STATIC");  // diagnostics: static tile assignment
+    unsigned long long* ctr =
+        (st_env && st_env[0] == '1') ? nullptr : reinterpret_cast<unsigned long long*>(g.status + 16);
+    cudaError_t e = tmx::launch_direct(shifted, g.k, n, g.strategy == TM_ASA16, g.sum, g.status, ctr, s);
     return e == cudaSuccess ? TM_OK : cuda_fail("launch_direct", e);
   }
   if (g.strategy == TM_AR) {
@@ -319,7 +322,7 @@ int tm_exchange_init(int64_t nparams, const tm_world* world, int strategy) {
   } else {
     c.rank_stride = 0;
   }
-  c.slab_bytes = c.rank_stride * c.nlocal + 256;  // + status word
+  c.slab_bytes = c.rank_stride * c.nlocal + 256;  // + status word (+0) and direct tile counter (+64)
   e = cudaMalloc(reinterpret_cast<void**>(&c.slab), c.slab_bytes);
   if (e != cudaSuccess) return cuda_fail("cudaMalloc", e);
   e = cudaMemset(c.slab, 0, c.slab_bytes);
