@@ -240,10 +240,18 @@ def _cpu_model():
     return None
 
 
+STAGED_KERNEL = [1]  # flavour of the staged kernel in use (tm_layout "staged_kernel")
+
+
 def roofline(strategy, P, k, path, ms, peak, peak_src, workload):
     alg = design_hbm_bytes(strategy, P, k, path)
     ach = alg / (ms * 1e-3) / 1e9
-    kernel = "tm_exchange_kernel" if path == "staged" and strategy != "ar" else "tm_direct_kernel"
+    if path == "staged" and strategy != "ar":
+        kernel = {0: "tm_exchange_kernel", 1: "tm_exchange_tma_kernel", 2: "tm_exchange_ws_kernel"}.get(
+            STAGED_KERNEL[0], "tm_exchange_kernel")
+    else:
+        kernel = ("tm_direct_kernel" if os.environ.get("TM_DIRECT_LDG") == "1" or P < 2048
+                  else "tm_direct_tma_kernel")
     return {"bound": "hbm", "achieved": ach, "peak": peak, "unit": "GB/s", "frac": ach / peak,
             "traffic": traffic_from_profiles(f"{workload}_{strategy}_k{k}_{path}"),
             "traffic_unit": "bytes per launch (ncu dram read+write, profiles/ncu_traffic.json)",
@@ -298,6 +306,7 @@ def main():
     ex = tm.Exchanger(P, args.strategy, rank=first, size=k, device=local, nlocal=nlocal,
                       path=args.path)
     path = {0: "auto", 1: "staged", 2: "direct"}[ex.layout()["path"]]
+    STAGED_KERNEL[0] = ex.layout()["staged_kernel"]
     stream = torch.cuda.current_stream()
 
     # L2 hygiene: the inputs one GPU touches per step must exceed the 126 MB L2;
