@@ -311,7 +311,9 @@ int tm_exchange_init(int64_t nparams, const tm_world* world, int strategy) {
     c.off_stage = 0;
     c.off_avg = round_up(c.off_stage + (int64_t)k * c.L * wb, 256);
     c.off_flags = round_up(c.off_avg + c.L * wb, 256);
-    c.rank_stride = round_up(c.off_flags + ((int64_t)tmx::kPhases * TM_MAX_RANKS + 1) * c.C * 4, 4096);
+    // flag pad: [kPhases][TM_MAX_RANKS][C] slots, per-CTA epochs [C], 8 rank-level words
+    c.rank_stride =
+        round_up(c.off_flags + (((int64_t)tmx::kPhases * TM_MAX_RANKS + 1) * c.C + 8) * 4, 4096);
   } else if (strategy == TM_EASGD) {
     // Centre sharded by segment: rank s hosts c[s*L, min((s+1)*L, P)).
     c.off_center = 0;

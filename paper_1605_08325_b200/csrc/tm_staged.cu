@@ -459,6 +459,112 @@ __device__ __forceinline__ void drain_bulk_stores() {
   }
 }
 
+// ---- dynamic work + rank-level barriers (TMA-engine kernel) ----------------
+// The TMA kernel does not tie work to CTA chunks: within a phase every CTA of a
+// rank claims items (tiles) from a per-rank counter until none are left, so no
+// slow SM holds the phase back, and the phase ends with a RANK-level barrier:
+// each CTA, after draining its bulk stores, fences and counts itself done; the
+// rank's last CTA resets the phase's counters and publishes the epoch into
+// every rank's pad slot [phase][r][0]; all CTAs then wait for every rank's slot.
+// The epoch is one counter per rank (pad word kRankEpoch), read by every CTA at
+// the start and advanced by the last CTA at READY -- no CTA can get there before
+// all of them have read it.
+//   READY   resets the pre-cast and allgather claim counters,
+//   REDUCED resets the reduce-scatter claim counter.
+// Reuse across exchanges follows the same argument as the per-CTA protocol with
+// "rank" in place of "CTA c of the rank".
+enum { kRankEpoch = 0, kDoneReady = 1, kDoneReduced = 2, kClaimCast = 3, kClaimReduce = 4,
+       kClaimGather = 5 };
+
+template <bool SYS>
+__device__ __forceinline__ void fence_scope_sys() {
+  if constexpr (SYS) __threadfence_system();
+  else __threadfence();
+}
+
+// Streams claimed items through the rings until claim() returns -1.  Slot item
+// ids live in smem (published to the consumers by the mbarrier arrive).
+template <class ClaimF, class IssueF, class ComputeF, class StoreF>
+__device__ __forceinline__ void dyn_tile_pipeline(uint32_t& use, uint32_t& outn, char* in_ring,
+                                                  char* out_ring, uint64_t* full, int* slot_item,
+                                                  ClaimF claim, IssueF issue, ComputeF compute,
+                                                  StoreF store) {
+  const int tid = threadIdx.x;
+  auto fill = [&](uint32_t u) {  // thread 0: claim an item for ring use u
+    const uint32_t slot = u % kInSlots;
+    const int it = claim();
+    slot_item[slot] = it;
+    if (it < 0) mbar_expect_tx(&full[slot], 0);
+    else issue(it, in_ring + slot * kSlotBytes, &full[slot]);
+  };
+  if (tid == 0)
+    for (int q = 0; q < kInSlots; ++q) fill(use + q);
+  uint32_t q = 0;
+  for (;; ++q) {
+    const uint32_t u = use + q;
+    const uint32_t slot = u % kInSlots;
+    mbar_wait(&full[slot], (u / kInSlots) & 1);
+    const int it = slot_item[slot];
+    if (it < 0) break;  // claims are monotone: every later slot is empty too
+    char* out = out_ring + (outn % kOutSlots) * kSlotBytes;
+    compute(it, in_ring + slot * kSlotBytes, out);
+    fence_proxy_async_smem();
+    if (tid == 0) bulk_wait_read<kOutSlots - 2>();
+    __syncthreads();
+    if (tid == 0) {
+      store(it, out);
+      bulk_commit();
+      fill(u + kInSlots);
+    }
+    ++outn;
+  }
+  // consume the remaining (empty, already completed) prefetched slots so every
+  // slot's phase parity stays in step for the next phase
+  for (uint32_t r = 1; r < kInSlots; ++r) {
+    const uint32_t u = use + q + r;
+    mbar_wait(&full[u % kInSlots], (u / kInSlots) & 1);
+  }
+  __syncthreads();  // nobody still reads slot_item before the next phase refills it
+  use += q + kInSlots;
+}
+
+template <int K, bool SYS>
+__device__ __forceinline__ bool rank_level_barrier(const ExchangeArgs& a, int phase, int r,
+                                                   uint32_t* rk, uint32_t epoch, int done_idx,
+                                                   int reset0, int reset1, int* s_abort) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    fence_scope_sys<SYS>();  // this CTA's writes (all threads, via bar.sync) before the count
+    const uint32_t old = atomicAdd(rk + done_idx, 1u);
+    if (old == (uint32_t)a.C - 1) {  // the rank's last CTA for this phase
+      fence_scope_sys<SYS>();
+      rk[done_idx] = 0;
+      rk[reset0] = 0;
+      if (reset1 >= 0) rk[reset1] = 0;
+      if (phase == kPhaseReady) rk[kRankEpoch] = epoch;
+      __threadfence();
+      for (int j = 0; j < a.k; ++j)
+        st_release<SYS>(a.flags[j] + (size_t)(phase * TM_MAX_RANKS + r) * a.flag_stride, epoch);
+    }
+  }
+  if (threadIdx.x < K) {
+    const uint32_t* mine = a.flags[r] + (size_t)(phase * TM_MAX_RANKS + threadIdx.x) * a.flag_stride;
+    if ((int32_t)(ld_acquire<SYS>(mine) - epoch) < 0) {
+      const uint64_t t0 = globaltimer();
+      while ((int32_t)(ld_acquire<SYS>(mine) - epoch) < 0) {
+        if (globaltimer() - t0 > a.timeout_ns) {
+          atomicOr(a.status, TM_BIT_TIMEOUT);
+          *s_abort = 1;
+          break;
+        }
+        __nanosleep(32);
+      }
+    }
+  }
+  __syncthreads();
+  return *s_abort == 0;
+}
+
 template <int K, bool W16, bool SYS>
 __global__ void __launch_bounds__(kTmaThreads, 1)
 tm_exchange_tma_kernel(const __grid_constant__ ExchangeArgs a) {
@@ -476,25 +582,22 @@ tm_exchange_tma_kernel(const __grid_constant__ ExchangeArgs a) {
   char* in_ring = reinterpret_cast<char*>(smem);
   char* out_ring = in_ring + kInSlots * kSlotBytes;
   __shared__ __align__(8) uint64_t full[kInSlots];
+  __shared__ int slot_item[kInSlots];
   __shared__ int s_abort;
   __shared__ uint32_t s_epoch;
 
   const int lr = blockIdx.x / a.C;
-  const int c = blockIdx.x - lr * a.C;
   const int r = a.rank0 + lr;
   float* __restrict__ x = a.x[lr];
   const int64_t P = a.P, L = a.L, P4 = P & ~int64_t(3);
-  const int64_t e0 = (int64_t)c * a.Lc;
-  const int64_t e1 = min(e0 + a.Lc, L);
-  const int64_t nel = e1 > e0 ? e1 - e0 : 0;
   char* const stage_r = reinterpret_cast<char*>(a.stage[r]);
+  // rank-level words after the per-CTA counters of the pad
+  uint32_t* const rk = a.flags[r] + (size_t)kPhases * TM_MAX_RANKS * a.flag_stride + a.flag_stride;
   const int tid = threadIdx.x;
 
   if (tid == 0) {
     s_abort = 0;
-    uint32_t* ctr = a.flags[r] + (size_t)kPhases * TM_MAX_RANKS * a.flag_stride + c;  // device epoch
-    s_epoch = *ctr + 1;
-    *ctr = s_epoch;
+    s_epoch = *reinterpret_cast<volatile uint32_t*>(rk + kRankEpoch) + 1;
     for (int i = 0; i < kInSlots; ++i) mbar_init(&full[i], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -502,17 +605,23 @@ tm_exchange_tma_kernel(const __grid_constant__ ExchangeArgs a) {
   const uint32_t epoch = s_epoch;
   stamp(a, kStampStart);
   uint32_t use = 0, outn = 0, st = 0;
-
-  // ---------------- a2: pre-cast x -> own stage (all k segments' chunk c) ----
-  {
-    const int nt = (int)((nel + TP - 1) / TP);
-    auto geom = [&](int i, int64_t& g0, int64_t& n) {
-      const int s = i / nt, t = i - s * nt;
-      g0 = (int64_t)s * L + e0 + (int64_t)t * TP;
-      n = min((int64_t)TP, nel - (int64_t)t * TP);
+  auto claimer = [&](int idx, int limit) {
+    return [=]() -> int {
+      const int t = (int)atomicAdd(rk + idx, 1u);
+      return t < limit ? t : -1;
     };
-    tile_pipeline(
-        K * nt, use, outn, in_ring, out_ring, full,
+  };
+
+  // ---------------- a2: pre-cast x -> own stage (every segment, tile by tile) --
+  {
+    const int nt = (int)((L + TP - 1) / TP);  // tiles per segment
+    auto geom = [&](int i, int64_t& g0, int64_t& n) {
+      const int sg = i / nt, t = i - sg * nt;
+      g0 = (int64_t)sg * L + (int64_t)t * TP;
+      n = min((int64_t)TP, L - (int64_t)t * TP);
+    };
+    dyn_tile_pipeline(
+        use, outn, in_ring, out_ring, full, slot_item, claimer(kClaimCast, K * nt),
         [&](int i, char* slot, uint64_t* bar) {
           int64_t g0, n;
           geom(i, g0, n);
@@ -523,9 +632,8 @@ tm_exchange_tma_kernel(const __grid_constant__ ExchangeArgs a) {
         [&](int i, const char* in, char* out) {
           int64_t g0, n;
           geom(i, g0, n);
-          const int64_t nb = max((int64_t)0, min(g0 + n, P4) - g0);
+          const int nbi = (int)max((int64_t)0, min(g0 + n, P4) - g0);
           const float* fin = reinterpret_cast<const float*>(in);
-          const int nbi = (int)nb;
           for (int v = tid; v < (int)(n / E); v += kTmaThreads) {
             float f[E];
             if ((v + 1) * E <= nbi) {
@@ -554,19 +662,21 @@ tm_exchange_tma_kernel(const __grid_constant__ ExchangeArgs a) {
   if (st) atomicOr(a.status, st);
   drain_bulk_stores();
   stamp(a, kStampCast);
-  if (!rank_barrier<K, SYS>(a, kPhaseReady, r, c, epoch, &s_abort)) return;
+  if (!rank_level_barrier<K, SYS>(a, kPhaseReady, r, rk, epoch, kDoneReady, kClaimCast, kClaimGather,
+                                  &s_abort))
+    return;
   stamp(a, kStampReady);
   if (tid == 0) fence_proxy_async_global();  // peers' staging, acquired above -> bulk loads
 
   // ---------------- a4: reduce-scatter pull (TMA from every rank's stage) ----
   {
     char* const avg_r = reinterpret_cast<char*>(a.avg[r]);
-    const int nt = (int)((nel + TR - 1) / TR);
-    tile_pipeline(
-        nt, use, outn, in_ring, out_ring, full,
+    const int nt = (int)((L + TR - 1) / TR);
+    dyn_tile_pipeline(
+        use, outn, in_ring, out_ring, full, slot_item, claimer(kClaimReduce, nt),
         [&](int i, char* slot, uint64_t* bar) {
-          const int64_t e = e0 + (int64_t)i * TR;
-          const int64_t n = min((int64_t)TR, e1 - e);
+          const int64_t e = (int64_t)i * TR;
+          const int64_t n = min((int64_t)TR, L - e);
           mbar_expect_tx(bar, (uint32_t)(K * n * WB));
 #pragma unroll
           for (int j = 0; j < K; ++j)
@@ -574,8 +684,8 @@ tm_exchange_tma_kernel(const __grid_constant__ ExchangeArgs a) {
                       (uint32_t)(n * WB), bar);
         },
         [&](int i, const char* in, char* out) {
-          const int64_t e = e0 + (int64_t)i * TR;
-          const int n = (int)min((int64_t)TR, e1 - e);
+          const int64_t e = (int64_t)i * TR;
+          const int n = (int)min((int64_t)TR, L - e);
           for (int v = tid; v < n / E; v += kTmaThreads) {
             uint4 raw[K];
 #pragma unroll
@@ -599,29 +709,31 @@ tm_exchange_tma_kernel(const __grid_constant__ ExchangeArgs a) {
           }
         },
         [&](int i, const char* out) {
-          const int64_t e = e0 + (int64_t)i * TR;
-          const int64_t n = min((int64_t)TR, e1 - e);
+          const int64_t e = (int64_t)i * TR;
+          const int64_t n = min((int64_t)TR, L - e);
           bulk_store(avg_r + e * WB, out, (uint32_t)(n * WB));
         });
   }
   if (st) atomicOr(a.status, st);
   drain_bulk_stores();
   stamp(a, kStampReduce);
-  if (!rank_barrier<K, SYS>(a, kPhaseReduced, r, c, epoch, &s_abort)) return;
+  if (!rank_level_barrier<K, SYS>(a, kPhaseReduced, r, rk, epoch, kDoneReduced, kClaimReduce, -1,
+                                  &s_abort))
+    return;
   stamp(a, kStampReduced);
   if (tid == 0) fence_proxy_async_global();
 
   // ---------------- a6: allgather pull (TMA from every rank's avg) ----------
   {
-    const int nt = (int)((nel + TA - 1) / TA);
+    const int nt = (int)((L + TA - 1) / TA);
     auto geom = [&](int i, int& j, int64_t& e, int64_t& n) {
       j = i / nt;
       const int t = i - j * nt;
-      e = e0 + (int64_t)t * TA;
-      n = min((int64_t)TA, e1 - e);
+      e = (int64_t)t * TA;
+      n = min((int64_t)TA, L - e);
     };
-    tile_pipeline(
-        K * nt, use, outn, in_ring, out_ring, full,
+    dyn_tile_pipeline(
+        use, outn, in_ring, out_ring, full, slot_item, claimer(kClaimGather, K * nt),
         [&](int i, char* slot, uint64_t* bar) {
           int j;
           int64_t e, n;
