@@ -195,7 +195,11 @@ int tm_exchange_group_range(float* const* dev_bufs, int nbufs, int64_t offset, i
  * exchange_momentum != 0 also averages the velocities (PAPER L160-164,
  * L373-376), else each rank keeps its own.  w, v, grad: fp32[nparams], 16-byte
  * aligned; w and v are updated in place.  In a single-process group on the
- * direct path the step and the exchange are ONE fused pass over memory.
+ * direct path the step and the exchange are ONE fused pass over memory; on the
+ * staged path (across processes / GPUs) the step is fused into the exchange
+ * kernel's pre-cast: it reads w, v, grad, writes v' and the wire staging of
+ * w' = w + v' (w' itself is only written by the allgather).  On a timeout
+ * (TM_E_TIMEOUT) w is left unspecified.
  * Not valid with TM_OP_SUM (exchange the updates with tm_exchange instead). */
 int tm_bsp_step(float* w, float* v, const float* grad, float lr, float mu, int exchange_momentum,
                 void* stream);

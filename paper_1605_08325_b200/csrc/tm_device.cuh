@@ -193,6 +193,21 @@ __device__ __forceinline__ float4 q16(float4 v) {
   return make_float4(lo.x, lo.y, hi.x, hi.y);
 }
 
+// Momentum-SGD step of 4 elements (one IEEE rounding per operation,
+// no FMA): v' = fl(fl(mu*v) - fl(lr*g)); the weights then take w' = fl(w + v').
+__device__ __forceinline__ float4 sgd_v(float4 v, float4 g, float lr, float mu) {
+  return make_float4(__fsub_rn(__fmul_rn(mu, v.x), __fmul_rn(lr, g.x)),
+                     __fsub_rn(__fmul_rn(mu, v.y), __fmul_rn(lr, g.y)),
+                     __fsub_rn(__fmul_rn(mu, v.z), __fmul_rn(lr, g.z)),
+                     __fsub_rn(__fmul_rn(mu, v.w), __fmul_rn(lr, g.w)));
+}
+__device__ __forceinline__ float sgd_v1(float v, float g, float lr, float mu) {
+  return __fsub_rn(__fmul_rn(mu, v), __fmul_rn(lr, g));
+}
+__device__ __forceinline__ float4 add4(float4 a, float4 b) {
+  return make_float4(__fadd_rn(a.x, b.x), __fadd_rn(a.y, b.y), __fadd_rn(a.z, b.z), __fadd_rn(a.w, b.w));
+}
+
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }

@@ -38,6 +38,14 @@ struct ExchangeArgs {
   int32_t sum;                    // SUBGD: sum, no 1/k
   uint64_t timeout_ns;
   uint64_t* stamps;               // diagnostics: %globaltimer per CTA and phase, or null
+  // Fused BSP step (tm_bsp_step on the staged path): when sgd != 0
+  // the pre-cast source of local rank lr is w' = fl(x + v'), with
+  // v' = fl(fl(mu*v) - fl(lr*g)) from v[lr], g[lr]; v' is written back, w' is
+  // not (the allgather overwrites every element of x).  Full range only.
+  float* v[TM_MAX_RANKS];
+  const float* g[TM_MAX_RANKS];
+  float lr, mu;
+  int32_t sgd;
 };
 
 // Persistent fused exchange: pre-cast -> ready barrier -> reduce-scatter pull with
@@ -93,8 +101,10 @@ struct BspBufs {
   const float* g[TM_MAX_RANKS];
   float lr, mu;
 };
+// tile_ctr: device counter for the TMA kernel's dynamic tile claiming (reset
+// by the launch); null selects the register kernel.
 cudaError_t launch_bsp_direct(const BspBufs& bb, int k, int64_t P, bool q16, bool mom,
-                              uint32_t* status, cudaStream_t s);
+                              uint32_t* status, unsigned long long* tile_ctr, cudaStream_t s);
 cudaError_t launch_sgd(float* w, float* v, const float* g, int64_t n, float lr, float mu,
                        cudaStream_t s);
 // Alg. 1 preprocessing (tm_loader_kernels.cu): mean subtraction, crop, mirror.

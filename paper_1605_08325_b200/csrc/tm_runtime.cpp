@@ -219,14 +219,34 @@ int do_bsp(float* const* w, float* const* v, const float* const* gr, int nbufs, 
     }
     bb.lr = lr;
     bb.mu = mu;
-    cudaError_t e = tmx::launch_bsp_direct(bb, g.k, g.P, g.strategy == TM_ASA16, mom != 0, g.status, s);
+    cudaError_t e = tmx::launch_bsp_direct(bb, g.k, g.P, g.strategy == TM_ASA16, mom != 0, g.status,
+                                           reinterpret_cast<unsigned long long*>(g.status + 16), s);
     return e == cudaSuccess ? TM_OK : cuda_fail("launch_bsp_direct", e);
   }
-  for (int i = 0; i < nbufs; ++i) {
-    cudaError_t e = tmx::launch_sgd(w[i], v[i], gr[i], g.P, lr, mu, s);
-    if (e != cudaSuccess) return cuda_fail("launch_sgd", e);
+  int rc = TM_OK;
+  if (fuse && g.k > 1 && g.strategy != TM_AR) {
+    // Staged path: the step is fused into the exchange's pre-cast (a2), which
+    // reads w, v, g, writes v' and the wire staging of w' = w + v'; w' itself is
+    // never written (the allgather overwrites every element of w).
+    ExchangeArgs a = make_args(w, 0, g.P);
+    for (int i = 0; i < nbufs; ++i) {
+      a.v[i] = v[i];
+      a.g[i] = gr[i];
+    }
+    a.lr = lr;
+    a.mu = mu;
+    a.sgd = 1;
+    cudaError_t e = tmx::launch_exchange(a, g.nlocal, wire16(g.strategy), g.staged_kernel, s);
+    if (e != cudaSuccess) return cuda_fail("launch_exchange", e);
+    ++g.epoch;
+  } else {
+    for (int i = 0; i < nbufs; ++i) {
+      cudaError_t e = tmx::launch_sgd(w[i], v[i], gr[i], g.P, lr, mu, s);
+      if (e != cudaSuccess) return cuda_fail("launch_sgd", e);
+    }
+    if (g.k == 1) return TM_OK;  // reading Q10: the exchange is the identity
+    rc = do_exchange(w, nbufs, 0, g.P, s);
   }
-  int rc = do_exchange(w, nbufs, 0, g.P, s);
   if (rc != TM_OK || !mom) return rc;
   return do_exchange(v, nbufs, 0, g.P, s);
 }
@@ -311,9 +331,7 @@ int tm_exchange_init(int64_t nparams, const tm_world* world, int strategy) {
     c.off_stage = 0;
     c.off_avg = round_up(c.off_stage + (int64_t)k * c.L * wb, 256);
     c.off_flags = round_up(c.off_avg + c.L * wb, 256);
-    // flag pad: [kPhases][TM_MAX_RANKS][C] slots, per-CTA epochs [C], 8 rank-level words
-    c.rank_stride =
-        round_up(c.off_flags + (((int64_t)tmx::kPhases * TM_MAX_RANKS + 1) * c.C + 8) * 4, 4096);
+    c.rank_stride = round_up(c.off_flags + ((int64_t)tmx::kPhases * TM_MAX_RANKS + 1) * c.C * 4, 4096);
   } else if (strategy == TM_EASGD) {
     // Centre sharded by segment: rank s hosts c[s*L, min((s+1)*L, P)).
     c.off_center = 0;

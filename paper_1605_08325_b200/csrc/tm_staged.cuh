@@ -1,0 +1,779 @@
+// Kernel templates of the staged exchange, shared by tm_staged.cu (plain
+// exchange) and tm_staged_sgd.cu (the exchange with the momentum-SGD step fused
+// into its pre-cast, SGD = true): two translation units so each kernel's
+// register allocation is its own and the two sets compile in parallel.  Every
+// definition is internal to the including translation unit.
+// sm_100a kernels of the Theano-MPI parameter exchange (arXiv 1605.08325).
+//
+//   tm_exchange_kernel  -- ASA / ASA16: one persistent,
+//                          cooperative launch per exchange, three phases per CTA
+//                          separated by cross-rank per-CTA epoch flags:
+//        a2 pre-cast   x (fp32, caller's buffer) -> stage (wire type), all k
+//                      segments of this CTA's chunk; rn16 for ASA16 (reading R1:
+//                      the own segment is rounded too); non-finite / fp16
+//                      overflow detection fused.
+//        a3 ready barrier.
+//        a4 reduce-scatter PULL: for the own segment r, load the chunk from every
+//                      rank's stage (peer pointers: NVLink P2P loads on a real box,
+//                      local HBM in a single-process group), widen, sum in
+//                      ascending rank from the rank-0 term, one IEEE division by
+//                      k, round to the wire type, store to the own `avg`.
+//        a5 reduced barrier.
+//        a6 allgather PULL: load every rank's `avg` chunk, widen, store into the
+//                      caller's buffer (truncated at P).
+//
+// Numerics: every fp32 op is an explicit round-to-nearest intrinsic
+// (__fadd_rn/__fsub_rn/__fmul_rn/__fdiv_rn: no FMA contraction, IEEE division);
+// the library is compiled without --use_fast_math (no FTZ).  The binary16
+// conversions are cvt.rn.f16(x2).f32 (RNE, gradual subnormals, overflow to inf)
+// and the exact cvt.f32.f16.
+//
+// Memory-ordering protocol (a3/a5): after __syncthreads(), thread j < k writes
+// the epoch into rank j's flag slot [phase][r][c] with st.release.sys and then
+// spins with ld.acquire.sys on its own slot [phase][j][c]; a second
+// __syncthreads() publishes the acquisition to the CTA.  Flags only couple CTA
+// c of every rank, so no grid-wide barrier is needed.  Reuse of stage/avg across
+// back-to-back exchanges is safe without a trailing barrier:
+//   stage_j(n+1) is written only after rank j saw REDUCED(n) from every rank,
+//     i.e. after every rank finished reading stage_j(n);
+//   avg_j(n+1) is written only after rank j saw READY(n+1) from every rank, which
+//     each rank signals after its AG(n) reads of avg_j(n).
+
+#pragma once
+
+#include <cuda_fp16.h>
+#include <stdint.h>
+#include <stdlib.h>
+
+#include <algorithm>
+
+#include "tm_device.cuh"
+#include "tm_internal.h"
+
+namespace tmx {
+namespace {
+using namespace dev;
+
+// Diagnostics: CTA-wide timestamp at a phase boundary (kernel-uniform branch;
+// costs nothing when the log is off).
+__device__ __forceinline__ void stamp(const ExchangeArgs& a, int slot) {
+  if (a.stamps) {
+    __syncthreads();
+    if (threadIdx.x == 0) a.stamps[(size_t)blockIdx.x * kStampSlots + slot] = globaltimer();
+  }
+}
+
+// Cross-rank, per-CTA epoch barrier (see the protocol in the file header).
+// Returns false (whole CTA) if a peer timed out.
+template <int K, bool SYS>
+__device__ __forceinline__ bool rank_barrier(const ExchangeArgs& a, int phase, int r, int c,
+                                             uint32_t epoch, int* s_abort) {
+  __syncthreads();
+  if (threadIdx.x < K) {
+    const int j = threadIdx.x;
+    uint32_t* remote = a.flags[j] + (size_t)(phase * TM_MAX_RANKS + r) * a.flag_stride + c;
+    st_release<SYS>(remote, epoch);
+    const uint32_t* mine = a.flags[r] + (size_t)(phase * TM_MAX_RANKS + j) * a.flag_stride + c;
+    if ((int32_t)(ld_acquire<SYS>(mine) - epoch) < 0) {
+      const uint64_t t0 = globaltimer();
+      while ((int32_t)(ld_acquire<SYS>(mine) - epoch) < 0) {
+        if (globaltimer() - t0 > a.timeout_ns) {
+          atomicOr(a.status, TM_BIT_TIMEOUT);
+          *s_abort = 1;
+          break;
+        }
+        __nanosleep(32);
+      }
+    }
+  }
+  __syncthreads();
+  return *s_abort == 0;
+}
+
+// a2 for one wire unit (E elements at segment offset ev) of all K segments:
+// load the fp32 source -- or, for the fused BSP step (a.sgd), compute it:
+// v' = fl(fl(mu v) - fl(lr g)) is written back to v, the source is w' = fl(w + v')
+// -- screen it and store its wire encoding into the own stage.  G segments per
+// batch, all loads of a batch issued before any store (memory-level parallelism).
+template <bool W16, int K, bool SGD>
+__device__ __forceinline__ void precast_unit(const ExchangeArgs& a, int lr, int64_t ev,
+                                             char* stage_r, uint32_t& st) {
+  using U = Unit<W16>;
+  constexpr int E = U::kElems;
+  constexpr int WB = W16 ? 2 : 4;
+  constexpr int G0 = SGD ? 1 : 4;  // SGD: 3 sources per unit; keep the register budget of the plain cast
+  constexpr int G = K < G0 ? K : G0;
+  const float* __restrict__ x = a.x[lr];
+  const int64_t P = a.P, L = a.L;
+#pragma unroll
+  for (int s0 = 0; s0 < K; s0 += G) {
+    float f[G][E];
+    float fv[SGD ? G : 1][E], fg[SGD ? G : 1][E];
+#pragma unroll
+    for (int u = 0; u < G; ++u) {
+      if (s0 + u < K) {
+        const int64_t g = (int64_t)(s0 + u) * L + ev;
+        if (g + E <= P) {
+#pragma unroll
+          for (int q = 0; q < E; q += 4) {
+            const float4 t = ld16_f(x + g + q);
+            f[u][q] = t.x; f[u][q + 1] = t.y; f[u][q + 2] = t.z; f[u][q + 3] = t.w;
+            if constexpr (SGD) {
+              const float4 tv = ld16_f(a.v[lr] + g + q), tg = ld16_f(a.g[lr] + g + q);
+              fv[u][q] = tv.x; fv[u][q + 1] = tv.y; fv[u][q + 2] = tv.z; fv[u][q + 3] = tv.w;
+              fg[u][q] = tg.x; fg[u][q + 1] = tg.y; fg[u][q + 2] = tg.z; fg[u][q + 3] = tg.w;
+            }
+          }
+        } else {
+#pragma unroll
+          for (int q = 0; q < E; ++q) {
+            const bool in = g + q < P;
+            f[u][q] = in ? x[g + q] : 0.0f;
+            if constexpr (SGD) {
+              fv[u][q] = in ? a.v[lr][g + q] : 0.0f;
+              fg[u][q] = in ? a.g[lr][g + q] : 0.0f;
+            }
+          }
+        }
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < G; ++u) {
+      if (s0 + u < K) {
+        const int64_t g = (int64_t)(s0 + u) * L + ev;
+        if constexpr (SGD) {
+#pragma unroll
+          for (int q = 0; q < E; ++q) {
+            fv[u][q] = sgd_v1(fv[u][q], fg[u][q], a.lr, a.mu);
+            f[u][q] = g + q < P ? __fadd_rn(f[u][q], fv[u][q]) : 0.0f;
+          }
+          if (g + E <= P) {
+#pragma unroll
+            for (int q = 0; q < E; q += 4)
+              st16_f(a.v[lr] + g + q, make_float4(fv[u][q], fv[u][q + 1], fv[u][q + 2], fv[u][q + 3]));
+          } else {
+#pragma unroll
+            for (int q = 0; q < E; ++q)
+              if (g + q < P) a.v[lr][g + q] = fv[u][q];
+          }
+        }
+        st |= unit_status<W16, E>(f[u]);
+        st16_cg(stage_r + g * WB, U::encode(f[u]));
+      }
+    }
+  }
+}
+
+template <int K, bool W16, bool SYS, bool SGD>
+__global__ void __launch_bounds__(kThreads, K == 6 ? 3 : 4)
+tm_exchange_kernel(const __grid_constant__ ExchangeArgs a) {
+  using U = Unit<W16>;
+  constexpr int E = U::kElems;
+  constexpr int WB = W16 ? 2 : 4;  // wire bytes per element
+  __shared__ int s_abort;
+  __shared__ uint32_t s_epoch;
+
+  const int lr = blockIdx.x / a.C;
+  const int c = blockIdx.x - lr * a.C;
+  const int r = a.rank0 + lr;
+  // Device-side epoch: CTA c of rank r owns counter ctr[c] in its own flag pad
+  // (after the [kPhases][TM_MAX_RANKS][C] slots).  Every rank performs the same
+  // sequence of exchanges, so the counters advance in lockstep; keeping the
+  // epoch on the device leaves the launch parameters constant across calls,
+  // which makes the exchange capturable in a CUDA graph.
+  if (threadIdx.x == 0) {
+    s_abort = 0;
+    uint32_t* ctr = a.flags[r] + (size_t)kPhases * TM_MAX_RANKS * a.flag_stride + c;
+    s_epoch = *ctr + 1;
+    *ctr = s_epoch;
+  }
+  __syncthreads();
+  const uint32_t epoch = s_epoch;
+  stamp(a, kStampStart);
+  float* __restrict__ x = a.x[lr];
+  const int64_t P = a.P, L = a.L;
+  const int64_t e0 = (int64_t)c * a.Lc;
+  const int64_t e1 = min(e0 + a.Lc, L);
+  const int64_t nu = e1 > e0 ? (e1 - e0) / E : 0;  // wire units per segment chunk
+  char* const stage_r = reinterpret_cast<char*>(a.stage[r]);
+
+  // ---------------- a2: pre-cast all k segments' chunk c into own stage -------
+  // Thread-contiguous units within a segment (coalesced); G segments per batch
+  // so G independent 32-byte (ASA16) / 16-byte (ASA) loads are in flight.
+  const int nu32 = (int)nu;
+  uint32_t st = 0;
+  for (int v = threadIdx.x; v < nu32; v += kThreads) {
+    const int64_t ev = e0 + (int64_t)v * E;
+    precast_unit<W16, K, SGD>(a, lr, ev, stage_r, st);
+  }
+  if (st) atomicOr(a.status, st);  // rare: only threads that saw a bad value
+  stamp(a, kStampCast);
+
+  if (!rank_barrier<K, SYS>(a, kPhaseReady, r, c, epoch, &s_abort)) return;
+  stamp(a, kStampReady);
+
+  // ---------------- a4: reduce-scatter pull, fused sum / (1/k) / cast -------
+  {
+    const char* src[K];
+#pragma unroll
+    for (int j = 0; j < K; ++j) src[j] = reinterpret_cast<const char*>(a.stage[j]);
+    char* const avg_r = reinterpret_cast<char*>(a.avg[r]);
+    const int64_t seg0 = (int64_t)r * L + e0;
+    for (int64_t v = threadIdx.x; v < nu; v += kThreads) {
+      const int64_t off = (seg0 + v * E) * WB;
+      uint4 raw[K];
+#pragma unroll
+      for (int j = 0; j < K; ++j) raw[j] = ld16_cg(src[j] + off);
+      float s[E], t[E];
+      U::decode(raw[0], s);
+#pragma unroll
+      for (int j = 1; j < K; ++j) {
+        U::decode(raw[j], t);
+#pragma unroll
+        for (int q = 0; q < E; ++q) s[q] = __fadd_rn(s[q], t[q]);
+      }
+      if (!a.sum) {
+#pragma unroll
+        for (int q = 0; q < E; ++q) s[q] = div_k<K>(s[q]);
+      } else if (W16) {  // a sum can leave the binary16 range
+#pragma unroll
+        for (int q = 0; q < E; ++q) st |= status_of(s[q], true) & TM_BIT_OVERFLOW16;
+      }
+      st16_cg(avg_r + (e0 + v * E) * WB, U::encode(s));
+    }
+  }
+  if (st) atomicOr(a.status, st);
+  stamp(a, kStampReduce);
+
+  if (!rank_barrier<K, SYS>(a, kPhaseReduced, r, c, epoch, &s_abort)) return;
+  stamp(a, kStampReduced);
+
+  // ---------------- a6: allgather pull, fused widen, store to caller ---------
+  {
+    constexpr int G = K;  // all k owners' units in flight at once
+    for (int v = threadIdx.x; v < nu32; v += kThreads) {
+      const int64_t ev = e0 + (int64_t)v * E;
+      uint4 raw[G];
+#pragma unroll
+      for (int j = 0; j < G; ++j)
+        raw[j] = ld16_cg(reinterpret_cast<const char*>(a.avg[j]) + ev * WB);
+#pragma unroll
+      for (int j = 0; j < G; ++j) {
+        const int64_t g = (int64_t)j * L + ev;
+        float f[E];
+        U::decode(raw[j], f);
+        if (g + E <= P) {
+          U::store_dst(x + g, f);
+        } else {
+#pragma unroll
+          for (int q = 0; q < E; ++q)
+            if (g + q < P) x[g + q] = f[q];
+        }
+      }
+    }
+  }
+  stamp(a, kStampEnd);
+}
+
+// ---------------------------------------------------------------------------
+// Warp-specialised staged kernel: the pre-cast (HBM-bound) overlaps the
+// reduce-scatter pull (NVLink-bound across GPUs).  512 threads per CTA: warps
+// 0-7 are casters, warps 8-15 reducers.  The CTA's chunk is split into kWsSub
+// sub-chunks; the casters pre-cast sub-chunk t of all k segments, sync among
+// themselves (named barrier 1) and publish READY_t to every rank, then move on
+// to t+1; the reducers wait for READY_t from every rank (named barrier 2) and
+// pull / sum / store sub-chunk t of the own segment while the casters work on
+// t+1.  After the last sub-chunk the whole CTA meets, publishes REDUCED and runs
+// the allgather pull with all 16 warps.  Reuse across exchanges is covered by the
+// same argument as the other kernels (READY_t(n+1) is published after AG(n);
+// stage is rewritten only after REDUCED(n) from every rank).
+// ---------------------------------------------------------------------------
+constexpr int kWsThreads = 512;
+constexpr int kWsGroup = 256;
+
+__device__ __forceinline__ void named_bar(int id, int n) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
+}
+
+template <int K, bool W16, bool SYS, bool SGD>
+__global__ void __launch_bounds__(kWsThreads, 2)
+tm_exchange_ws_kernel(const __grid_constant__ ExchangeArgs a) {
+  using U = Unit<W16>;
+  constexpr int E = U::kElems;
+  constexpr int WB = W16 ? 2 : 4;
+  __shared__ int s_abort;
+  __shared__ uint32_t s_epoch;
+
+  const int lr = blockIdx.x / a.C;
+  const int c = blockIdx.x - lr * a.C;
+  const int r = a.rank0 + lr;
+  if (threadIdx.x == 0) {
+    s_abort = 0;
+    uint32_t* ctr = a.flags[r] + (size_t)kPhases * TM_MAX_RANKS * a.flag_stride + c;
+    s_epoch = *ctr + 1;
+    *ctr = s_epoch;
+  }
+  __syncthreads();
+  const uint32_t epoch = s_epoch;
+  stamp(a, kStampStart);
+  float* __restrict__ x = a.x[lr];
+  const int64_t P = a.P, L = a.L;
+  const int64_t e0 = (int64_t)c * a.Lc;
+  const int64_t e1 = min(e0 + a.Lc, L);
+  const int64_t nel = e1 > e0 ? e1 - e0 : 0;
+  const int64_t Ls = ((nel + kWsSub - 1) / kWsSub + 255) / 256 * 256;  // sub-chunk length
+  char* const stage_r = reinterpret_cast<char*>(a.stage[r]);
+  const int grp = threadIdx.x / kWsGroup;
+  const int tg = threadIdx.x - grp * kWsGroup;
+  uint32_t st = 0;
+
+  if (grp == 0) {
+    // ------------------------------------------------ casters: a2 per sub-chunk
+    for (int t = 0; t < kWsSub; ++t) {
+      const int64_t s0e = e0 + (int64_t)t * Ls;
+      const int64_t s1e = min(s0e + Ls, e1);
+      const int nu = s1e > s0e ? (int)((s1e - s0e) / E) : 0;
+      for (int v = tg; v < nu; v += kWsGroup) {
+        const int64_t ev = s0e + (int64_t)v * E;
+        precast_unit<W16, K, SGD>(a, lr, ev, stage_r, st);
+      }
+      named_bar(1, kWsGroup);  // every caster's stage writes of sub-chunk t done
+      if (tg < K)
+        st_release<SYS>(a.flags[tg] + (size_t)(t * TM_MAX_RANKS + r) * a.flag_stride + c, epoch);
+    }
+  } else {
+    // ------------------------------------------------ reducers: a4 per sub-chunk
+    const char* src[K];
+#pragma unroll
+    for (int j = 0; j < K; ++j) src[j] = reinterpret_cast<const char*>(a.stage[j]);
+    char* const avg_r = reinterpret_cast<char*>(a.avg[r]);
+    for (int t = 0; t < kWsSub; ++t) {
+      if (tg < K) {  // READY_t from rank tg
+        const uint32_t* mine = a.flags[r] + (size_t)(t * TM_MAX_RANKS + tg) * a.flag_stride + c;
+        if ((int32_t)(ld_acquire<SYS>(mine) - epoch) < 0) {
+          const uint64_t t0 = globaltimer();
+          while ((int32_t)(ld_acquire<SYS>(mine) - epoch) < 0) {
+            if (globaltimer() - t0 > a.timeout_ns) {
+              atomicOr(a.status, TM_BIT_TIMEOUT);
+              s_abort = 1;
+              break;
+            }
+            __nanosleep(32);
+          }
+        }
+      }
+      named_bar(2, kWsGroup);
+      if (s_abort) break;
+      const int64_t s0e = e0 + (int64_t)t * Ls;
+      const int64_t s1e = min(s0e + Ls, e1);
+      const int nu = s1e > s0e ? (int)((s1e - s0e) / E) : 0;
+      for (int v = tg; v < nu; v += kWsGroup) {
+        const int64_t e = s0e + (int64_t)v * E;
+        const int64_t off = ((int64_t)r * L + e) * WB;
+        uint4 raw[K];
+#pragma unroll
+        for (int j = 0; j < K; ++j) raw[j] = ld16_cg(src[j] + off);
+        float sm[E], tt[E];
+        U::decode(raw[0], sm);
+#pragma unroll
+        for (int j = 1; j < K; ++j) {
+          U::decode(raw[j], tt);
+#pragma unroll
+          for (int q = 0; q < E; ++q) sm[q] = __fadd_rn(sm[q], tt[q]);
+        }
+        if (!a.sum) {
+#pragma unroll
+          for (int q = 0; q < E; ++q) sm[q] = div_k<K>(sm[q]);
+        } else if (W16) {
+#pragma unroll
+          for (int q = 0; q < E; ++q) st |= status_of(sm[q], true) & TM_BIT_OVERFLOW16;
+        }
+        st16_cg(avg_r + e * WB, U::encode(sm));
+      }
+    }
+  }
+  if (st) atomicOr(a.status, st);
+  __syncthreads();
+  if (s_abort) return;
+  stamp(a, kStampReduce);  // pre-cast and reduce-scatter overlap: one stamp for both
+  if (!rank_barrier<K, SYS>(a, kWsSub, r, c, epoch, &s_abort)) return;  // REDUCED
+  stamp(a, kStampReduced);
+
+  // ---------------- a6: allgather pull with all 16 warps ----------------------
+  const int nu32 = (int)(nel / E);
+  for (int v = threadIdx.x; v < nu32; v += kWsThreads) {
+    const int64_t ev = e0 + (int64_t)v * E;
+    uint4 raw[K];
+#pragma unroll
+    for (int j = 0; j < K; ++j) raw[j] = ld16_cg(reinterpret_cast<const char*>(a.avg[j]) + ev * WB);
+#pragma unroll
+    for (int j = 0; j < K; ++j) {
+      const int64_t g = (int64_t)j * L + ev;
+      float f[E];
+      U::decode(raw[j], f);
+      if (g + E <= P) {
+        U::store_dst(x + g, f);
+      } else {
+#pragma unroll
+        for (int q = 0; q < E; ++q)
+          if (g + q < P) x[g + q] = f[q];
+      }
+    }
+  }
+  stamp(a, kStampEnd);
+}
+
+// ---------------------------------------------------------------------------
+// The same three phases on the TMA engine (default staged kernel).
+//
+// One CTA per SM (224 KB of shared memory).  Each phase is a tile pipeline:
+// thread 0 issues 1-D bulk copies (cp.async.bulk, completing on an mbarrier)
+// of the phase's source tiles into a 4-slot x 32 KB input ring -- for a4 the k
+// sources are peer staging buffers, i.e. the TMA engine pulls over NVLink --
+// all threads transform the tile in shared memory into a 3-slot x 32 KB output
+// ring, and thread 0 bulk-stores it.  Bytes in flight are set by the rings, not
+// by registers or LSU queue depth (the register kernel above was lg_throttle-
+// bound).  Cross-proxy ordering: before a phase's flags are released, thread 0
+// waits for its bulk stores to complete and issues fence.proxy.async.global;
+// after a barrier it fences again before issuing bulk loads of peer data.
+// Elements in [P & ~3, P) (at most 3, in the last segment) are read / written
+// with plain accesses; elements >= P are zero on the wire and never stored.
+// ---------------------------------------------------------------------------
+constexpr int kSlotBytes = 32 * 1024;
+constexpr int kInSlots = 4;
+constexpr int kOutSlots = 3;
+constexpr int kTmaThreads = 512;  // 16 warps share the in-smem transform of each tile
+
+__device__ __forceinline__ void fence_proxy_async_global() {
+  asm volatile("fence.proxy.async.global;" ::: "memory");
+}
+
+// Runs n_items through the rings.  issue(i, slot, bar) [thread 0] starts the
+// bulk loads of item i and arms `bar` with their byte count; compute(i, in, out)
+// [all threads] transforms; store(i, out) [thread 0] issues the bulk stores.
+// `use` / `outn` continue across phases so slot parities stay consistent.
+template <class IssueF, class ComputeF, class StoreF>
+__device__ __forceinline__ void tile_pipeline(int n_items, uint32_t& use, uint32_t& outn,
+                                              char* in_ring, char* out_ring, uint64_t* full,
+                                              IssueF issue, ComputeF compute, StoreF store) {
+  const int tid = threadIdx.x;
+  if (tid == 0) {
+    for (int i = 0; i < kInSlots && i < n_items; ++i) {
+      const uint32_t slot = (use + i) % kInSlots;
+      issue(i, in_ring + slot * kSlotBytes, &full[slot]);
+    }
+  }
+  for (int i = 0; i < n_items; ++i) {
+    const uint32_t u = use + i;
+    const uint32_t slot = u % kInSlots;
+    mbar_wait(&full[slot], (u / kInSlots) & 1);
+    char* out = out_ring + (outn % kOutSlots) * kSlotBytes;
+    compute(i, in_ring + slot * kSlotBytes, out);
+    fence_proxy_async_smem();                      // generic smem writes -> bulk store
+    if (tid == 0) bulk_wait_read<kOutSlots - 2>();  // out slot of item i+1 is free
+    __syncthreads();                               // every thread is done with slot / out
+    if (tid == 0) {
+      store(i, out);
+      bulk_commit();
+      if (i + kInSlots < n_items) issue(i + kInSlots, in_ring + slot * kSlotBytes, &full[slot]);
+    }
+    ++outn;
+  }
+  use += n_items;
+}
+
+// Drain this CTA's bulk stores and order them before the generic-proxy release.
+__device__ __forceinline__ void drain_bulk_stores() {
+  if (threadIdx.x == 0) {
+    bulk_wait_all<0>();
+    fence_proxy_async_global();
+  }
+}
+
+template <int K, bool W16, bool SYS, bool SGD>
+__global__ void __launch_bounds__(kTmaThreads, 1)
+tm_exchange_tma_kernel(const __grid_constant__ ExchangeArgs a) {
+  using U = Unit<W16>;
+  constexpr int E = U::kElems;      // elements per 16-byte wire unit
+  constexpr int WB = W16 ? 2 : 4;   // wire bytes per element
+  constexpr int TP = 8192;          // a2 tile: fp32 in 32 KB, wire out <= 32 KB
+  // a4 tile: k sources of TR wire elements fit one 32 KB slot; a multiple of 256
+  // elements keeps every source's smem offset and byte count 16-byte aligned.
+  constexpr int TR_RAW = kSlotBytes / (K * WB) / 256 * 256;
+  constexpr int TR = TR_RAW < 4096 ? TR_RAW : 4096;
+  static_assert(TR >= 256, "a4 tile too small");
+  constexpr int TA = 8192;          // a6 tile: wire in <= 32 KB, fp32 out 32 KB
+  extern __shared__ __align__(128) unsigned char smem[];
+  char* in_ring = reinterpret_cast<char*>(smem);
+  char* out_ring = in_ring + kInSlots * kSlotBytes;
+  __shared__ __align__(8) uint64_t full[kInSlots];
+  __shared__ int s_abort;
+  __shared__ uint32_t s_epoch;
+
+  const int lr = blockIdx.x / a.C;
+  const int c = blockIdx.x - lr * a.C;
+  const int r = a.rank0 + lr;
+  float* __restrict__ x = a.x[lr];
+  const int64_t P = a.P, L = a.L, P4 = P & ~int64_t(3);
+  const int64_t e0 = (int64_t)c * a.Lc;
+  const int64_t e1 = min(e0 + a.Lc, L);
+  const int64_t nel = e1 > e0 ? e1 - e0 : 0;
+  char* const stage_r = reinterpret_cast<char*>(a.stage[r]);
+  const int tid = threadIdx.x;
+
+  if (tid == 0) {
+    s_abort = 0;
+    uint32_t* ctr = a.flags[r] + (size_t)kPhases * TM_MAX_RANKS * a.flag_stride + c;  // device epoch
+    s_epoch = *ctr + 1;
+    *ctr = s_epoch;
+    for (int i = 0; i < kInSlots; ++i) mbar_init(&full[i], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  const uint32_t epoch = s_epoch;
+  stamp(a, kStampStart);
+  uint32_t use = 0, outn = 0, st = 0;
+
+  // ---------------- a2: pre-cast x -> own stage (all k segments' chunk c) ----
+  // Fused BSP step (SGD): the tile is TPS elements of w, v and g (three bulk
+  // loads into one slot); the output slot holds the wire tile and v' (fp32, at
+  // byte offset TPS*WB), stored with two bulk stores.
+  {
+    constexpr int TPS = 2048;
+    constexpr bool sgd = SGD;
+    const int tp = sgd ? TPS : TP;
+    float* const vr = a.v[lr];
+    const float* const gr = a.g[lr];
+    const int nt = (int)((nel + tp - 1) / tp);
+    auto geom = [&](int i, int64_t& g0, int64_t& n) {
+      const int sg = i / nt, t = i - sg * nt;
+      g0 = (int64_t)sg * L + e0 + (int64_t)t * tp;
+      n = min((int64_t)tp, nel - (int64_t)t * tp);
+    };
+    tile_pipeline(
+        K * nt, use, outn, in_ring, out_ring, full,
+        [&](int i, char* slot, uint64_t* bar) {
+          int64_t g0, n;
+          geom(i, g0, n);
+          const int64_t nb = max((int64_t)0, min(g0 + n, P4) - g0);  // bulk-loadable elements
+          mbar_expect_tx(bar, (uint32_t)(nb * 4 * (sgd ? 3 : 1)));
+          if (nb > 0) {
+            bulk_load(slot, x + g0, (uint32_t)(nb * 4), bar);
+            if (sgd) {
+              bulk_load(slot + TPS * 4, vr + g0, (uint32_t)(nb * 4), bar);
+              bulk_load(slot + 2 * TPS * 4, gr + g0, (uint32_t)(nb * 4), bar);
+            }
+          }
+        },
+        [&](int i, const char* in, char* out) {
+          int64_t g0, n;
+          geom(i, g0, n);
+          const int nbi = (int)max((int64_t)0, min(g0 + n, P4) - g0);
+          const float* fin = reinterpret_cast<const float*>(in);
+          const float* fvin = fin + TPS;
+          const float* fgin = fin + 2 * TPS;
+          float* fvout = reinterpret_cast<float*>(out + TPS * WB);
+          for (int v = tid; v < (int)(n / E); v += kTmaThreads) {
+            float f[E];
+            if ((v + 1) * E <= nbi) {
+#pragma unroll
+              for (int q = 0; q < E; q += 4) {
+                float4 t4 = reinterpret_cast<const float4*>(fin + v * E)[q / 4];
+                if (sgd) {
+                  const float4 vn = sgd_v(reinterpret_cast<const float4*>(fvin + v * E)[q / 4],
+                                          reinterpret_cast<const float4*>(fgin + v * E)[q / 4], a.lr, a.mu);
+                  reinterpret_cast<float4*>(fvout + v * E)[q / 4] = vn;
+                  t4 = add4(t4, vn);
+                }
+                f[q] = t4.x; f[q + 1] = t4.y; f[q + 2] = t4.z; f[q + 3] = t4.w;
+              }
+            } else {
+#pragma unroll
+              for (int q = 0; q < E; ++q) {
+                const int e = v * E + q;
+                if (e < nbi) {
+                  f[q] = fin[e];
+                  if (sgd) {
+                    const float vn = sgd_v1(fvin[e], fgin[e], a.lr, a.mu);
+                    fvout[e] = vn;
+                    f[q] = __fadd_rn(f[q], vn);
+                  }
+                } else if (g0 + e < P) {  // the <= 3 elements in [P & ~3, P): plain accesses
+                  f[q] = x[g0 + e];
+                  if (sgd) {
+                    const float vn = sgd_v1(vr[g0 + e], gr[g0 + e], a.lr, a.mu);
+                    vr[g0 + e] = vn;
+                    f[q] = __fadd_rn(f[q], vn);
+                  }
+                } else {
+                  f[q] = 0.0f;
+                }
+              }
+            }
+            st |= unit_status<W16, E>(f);
+            reinterpret_cast<uint4*>(out)[v] = U::encode(f);
+          }
+        },
+        [&](int i, const char* out) {
+          int64_t g0, n;
+          geom(i, g0, n);
+          bulk_store(stage_r + g0 * WB, out, (uint32_t)(n * WB));
+          if (sgd) {
+            const int64_t nb = max((int64_t)0, min(g0 + n, P4) - g0);
+            if (nb > 0) bulk_store(vr + g0, out + TPS * WB, (uint32_t)(nb * 4));
+          }
+        });
+  }
+  if (st) atomicOr(a.status, st);
+  drain_bulk_stores();
+  stamp(a, kStampCast);
+  if (!rank_barrier<K, SYS>(a, kPhaseReady, r, c, epoch, &s_abort)) return;
+  stamp(a, kStampReady);
+  if (tid == 0) fence_proxy_async_global();  // peers' staging, acquired above -> bulk loads
+
+  // ---------------- a4: reduce-scatter pull (TMA from every rank's stage) ----
+  {
+    char* const avg_r = reinterpret_cast<char*>(a.avg[r]);
+    const int nt = (int)((nel + TR - 1) / TR);
+    tile_pipeline(
+        nt, use, outn, in_ring, out_ring, full,
+        [&](int i, char* slot, uint64_t* bar) {
+          const int64_t e = e0 + (int64_t)i * TR;
+          const int64_t n = min((int64_t)TR, e1 - e);
+          mbar_expect_tx(bar, (uint32_t)(K * n * WB));
+#pragma unroll
+          for (int j = 0; j < K; ++j)
+            bulk_load(slot + j * TR * WB, reinterpret_cast<const char*>(a.stage[j]) + ((int64_t)r * L + e) * WB,
+                      (uint32_t)(n * WB), bar);
+        },
+        [&](int i, const char* in, char* out) {
+          const int64_t e = e0 + (int64_t)i * TR;
+          const int n = (int)min((int64_t)TR, e1 - e);
+          for (int v = tid; v < n / E; v += kTmaThreads) {
+            uint4 raw[K];
+#pragma unroll
+            for (int j = 0; j < K; ++j) raw[j] = reinterpret_cast<const uint4*>(in + j * TR * WB)[v];
+            float sm[E], t[E];
+            U::decode(raw[0], sm);
+#pragma unroll
+            for (int j = 1; j < K; ++j) {
+              U::decode(raw[j], t);
+#pragma unroll
+              for (int q = 0; q < E; ++q) sm[q] = __fadd_rn(sm[q], t[q]);
+            }
+            if (!a.sum) {
+#pragma unroll
+              for (int q = 0; q < E; ++q) sm[q] = div_k<K>(sm[q]);
+            } else if (W16) {  // a sum can leave the binary16 range
+#pragma unroll
+              for (int q = 0; q < E; ++q) st |= status_of(sm[q], true) & TM_BIT_OVERFLOW16;
+            }
+            reinterpret_cast<uint4*>(out)[v] = U::encode(sm);
+          }
+        },
+        [&](int i, const char* out) {
+          const int64_t e = e0 + (int64_t)i * TR;
+          const int64_t n = min((int64_t)TR, e1 - e);
+          bulk_store(avg_r + e * WB, out, (uint32_t)(n * WB));
+        });
+  }
+  if (st) atomicOr(a.status, st);
+  drain_bulk_stores();
+  stamp(a, kStampReduce);
+  if (!rank_barrier<K, SYS>(a, kPhaseReduced, r, c, epoch, &s_abort)) return;
+  stamp(a, kStampReduced);
+  if (tid == 0) fence_proxy_async_global();
+
+  // ---------------- a6: allgather pull (TMA from every rank's avg) ----------
+  {
+    const int nt = (int)((nel + TA - 1) / TA);
+    auto geom = [&](int i, int& j, int64_t& e, int64_t& n) {
+      j = i / nt;
+      const int t = i - j * nt;
+      e = e0 + (int64_t)t * TA;
+      n = min((int64_t)TA, e1 - e);
+    };
+    tile_pipeline(
+        K * nt, use, outn, in_ring, out_ring, full,
+        [&](int i, char* slot, uint64_t* bar) {
+          int j;
+          int64_t e, n;
+          geom(i, j, e, n);
+          mbar_expect_tx(bar, (uint32_t)(n * WB));
+          bulk_load(slot, reinterpret_cast<const char*>(a.avg[j]) + e * WB, (uint32_t)(n * WB), bar);
+        },
+        [&](int i, const char* in, char* out) {
+          int j;
+          int64_t e, n;
+          geom(i, j, e, n);
+          const int64_t g0 = (int64_t)j * L + e;
+          // tile-relative window [lo, hi) of the <= 3 elements in [P & ~3, P):
+          // bulk stores cannot cover them, plain stores do
+          const int lo = (int)max((int64_t)0, min(n, P4 - g0));
+          const int hi = (int)max((int64_t)0, min(n, P - g0));
+          float* fo = reinterpret_cast<float*>(out);
+          for (int v = tid; v < (int)(n / E); v += kTmaThreads) {
+            float f[E];
+            U::decode(reinterpret_cast<const uint4*>(in)[v], f);
+#pragma unroll
+            for (int q = 0; q < E; q += 4)
+              reinterpret_cast<float4*>(fo + v * E)[q / 4] = make_float4(f[q], f[q + 1], f[q + 2], f[q + 3]);
+            if (hi > lo && (v + 1) * E > lo && v * E < hi) {
+#pragma unroll
+              for (int q = 0; q < E; ++q)
+                if (v * E + q >= lo && v * E + q < hi) x[g0 + v * E + q] = f[q];
+            }
+          }
+        },
+        [&](int i, const char* out) {
+          int j;
+          int64_t e, n;
+          geom(i, j, e, n);
+          const int64_t g0 = (int64_t)j * L + e;
+          const int64_t nb = max((int64_t)0, min(g0 + n, P4) - g0);
+          if (nb > 0) bulk_store(x + g0, out, (uint32_t)(nb * 4));
+        });
+  }
+  if (tid == 0) bulk_wait_all<0>();  // kernel exit also waits; explicit for clarity
+  stamp(a, kStampEnd);
+}
+
+template <int K, bool W16, bool SGD>
+const void* exchange_fn(bool sys, int fl) {
+  if (fl == kStagedTma)
+    return sys ? reinterpret_cast<const void*>(&tm_exchange_tma_kernel<K, W16, true, SGD>)
+               : reinterpret_cast<const void*>(&tm_exchange_tma_kernel<K, W16, false, SGD>);
+  if (fl == kStagedWs)
+    return sys ? reinterpret_cast<const void*>(&tm_exchange_ws_kernel<K, W16, true, SGD>)
+               : reinterpret_cast<const void*>(&tm_exchange_ws_kernel<K, W16, false, SGD>);
+  return sys ? reinterpret_cast<const void*>(&tm_exchange_kernel<K, W16, true, SGD>)
+             : reinterpret_cast<const void*>(&tm_exchange_kernel<K, W16, false, SGD>);
+}
+
+// Kernel of k ranks, wire type, flag scope and flavour (SGD: the fused BSP step).
+template <bool SGD>
+const void* pick_exchange(int k, bool w16, bool sys, int fl) {
+  switch (k) {
+    case 2: return w16 ? exchange_fn<2, true, SGD>(sys, fl) : exchange_fn<2, false, SGD>(sys, fl);
+    case 3: return w16 ? exchange_fn<3, true, SGD>(sys, fl) : exchange_fn<3, false, SGD>(sys, fl);
+    case 4: return w16 ? exchange_fn<4, true, SGD>(sys, fl) : exchange_fn<4, false, SGD>(sys, fl);
+    case 5: return w16 ? exchange_fn<5, true, SGD>(sys, fl) : exchange_fn<5, false, SGD>(sys, fl);
+    case 6: return w16 ? exchange_fn<6, true, SGD>(sys, fl) : exchange_fn<6, false, SGD>(sys, fl);
+    case 7: return w16 ? exchange_fn<7, true, SGD>(sys, fl) : exchange_fn<7, false, SGD>(sys, fl);
+    case 8: return w16 ? exchange_fn<8, true, SGD>(sys, fl) : exchange_fn<8, false, SGD>(sys, fl);
+    default: return nullptr;
+  }
+}
+
+int flavour_threads(int fl) { return fl == kStagedTma ? kTmaThreads : (fl == kStagedWs ? kWsThreads : kThreads); }
+
+constexpr int kTmaSmem = (kInSlots + kOutSlots) * kSlotBytes;
+
+// Opt every TMA instantiation into its dynamic shared memory (idempotent).
+cudaError_t prepare(const void* fn, int fl) {
+  if (fl != kStagedTma) return cudaSuccess;
+  return cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, kTmaSmem);
+}
+
+}  // namespace
+}  // namespace tmx

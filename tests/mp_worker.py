@@ -4,7 +4,7 @@ all_gather_object.  Used by tests/test_gpu_multiprocess.py; on a one-GPU box
 every rank uses cuda:0 (IPC between processes on one device), on a multi-GPU
 box rank r uses cuda:r.
 
-argv: outdir strategy P dist mode      (mode: normal | sum | range | locked | skip1 | mismatch)
+argv: outdir strategy P dist mode      (mode: normal | sum | range | locked | skip1 | mismatch | stress | bsp | bspmom)
 """
 
 import json
@@ -81,6 +81,22 @@ def main():
         dist.destroy_process_group()
         return
     x = torch.from_numpy(worker_buffer(P, dist_name, rank, config=50)).cuda()
+    if mode in ("bsp", "bspmom"):
+        # two BSP iterations (momentum SGD fused into the staged pre-cast, then
+        # the exchange of w, and of v for bspmom)
+        v = torch.from_numpy(worker_buffer(P, "D4", rank, config=52)).cuda()
+        g = torch.from_numpy(worker_buffer(P, dist_name, rank, config=53)).cuda()
+        for _ in range(2):
+            ex.bsp_step(x, v, g, 0.01, 0.9, exchange_momentum=(mode == "bspmom"))
+        code, bits = ex.status()
+        result.update({"code": code, "bits": bits, "layout": ex.layout()})
+        np.save(os.path.join(outdir, f"rank{rank}.npy"), x.cpu().numpy())
+        np.save(os.path.join(outdir, f"vel{rank}.npy"), v.cpu().numpy())
+        json.dump(result, open(os.path.join(outdir, f"rank{rank}.json"), "w"))
+        dist.barrier()
+        ex.finalize()
+        dist.destroy_process_group()
+        return
     if mode == "stress":
         # back-to-back exchanges with random host delays between calls on each
         # rank (exercises the epoch / reuse protocol); each iteration

@@ -44,3 +44,48 @@ def test_bsp_step_rejects_sum_mode():
         with pytest.raises(tm.TmError) as e:
             tm.tm_bsp_step_group(b, b, b, 0.1, 0.9)
         assert e.value.code == tm.TM_E_ARG
+
+
+@pytest.mark.parametrize("kernel", ["reg", "tma", "ws"])
+@pytest.mark.parametrize("unfused", ["0", "1"])
+def test_bsp_staged_flavours_bitwise(monkeypatch, kernel, unfused):
+    """Single-process group on the staged path, every staged kernel flavour, with
+    the step fused into the pre-cast (default) and as a separate SGD kernel
+    (TM_BSP_UNFUSED=1): ragged P (P % 4 = 3, several tiles), both strategies."""
+    monkeypatch.setenv("TM_STAGED_KERNEL", kernel)
+    monkeypatch.setenv("TM_BSP_UNFUSED", unfused)
+    lr, mu = 0.05, 0.9
+    for strategy, mom, k, P in (("asa16", False, 4, 1_000_003), ("asa", True, 3, 70_003),
+                                ("asa16", True, 8, 20_483)):
+        W = worker_buffers(P, k, "D1", config=110)
+        V = worker_buffers(P, k, "D4", config=111)
+        G = worker_buffers(P, k, "D2", config=112)
+        Wd, Vd, Gd = to_dev(W), to_dev(V), to_dev(G)
+        with tm.Exchanger(P, strategy, size=k, nlocal=k, path="staged") as ex:
+            assert ex.layout()["staged_kernel"] == {"reg": 0, "tma": 1, "ws": 2}[kernel]
+            for _ in range(3):
+                ex.bsp_step(Wd, Vd, Gd, lr, mu, exchange_momentum=mom)
+            code, _ = ex.status()
+        assert code == tm.TM_OK
+        ww, vv = W, V
+        for _ in range(3):
+            ww, vv = bsp_iteration(ww, vv, G, lr, mu, strategy, exchange_momentum=mom)
+        gW, gV = to_host(Wd), to_host(Vd)
+        for r in range(k):
+            assert_bitwise(gW[r], ww[r], f"w {kernel} {strategy} k={k} P={P} r={r}")
+            assert_bitwise(gV[r], vv[r], f"v {kernel} {strategy} k={k} P={P} r={r}")
+
+
+def test_bsp_staged_status_overflow(monkeypatch):
+    """The fused pre-cast screens w' = w + v' (not w): a step that pushes a weight
+    past the binary16 range sets TM_BIT_OVERFLOW16."""
+    P, k = 4096, 2
+    W = [np.zeros(P, np.float32) for _ in range(k)]
+    V = [np.zeros(P, np.float32) for _ in range(k)]
+    G = [np.zeros(P, np.float32) for _ in range(k)]
+    G[1][777] = np.float32(-1e6)  # v' = 0.1 * 1e6 -> w' = 1e5 > 65504
+    Wd, Vd, Gd = to_dev(W), to_dev(V), to_dev(G)
+    with tm.Exchanger(P, "asa16", size=k, nlocal=k, path="staged") as ex:
+        ex.bsp_step(Wd, Vd, Gd, 0.1, 0.9)
+        code, bits = ex.status()
+    assert bits & tm.TM_BIT_OVERFLOW16, (code, bits)

@@ -74,6 +74,28 @@ def test_multiprocess_bitwise(tmp_path, strategy, k, op, kernel):
         assert_bitwise(got, want[r], f"{strategy} rank {r}")
 
 
+@pytest.mark.parametrize("strategy,k,mode,kernel", [("asa16", 2, "bsp", "ws"), ("asa16", 3, "bspmom", "ws"),
+                                                    ("asa", 2, "bsp", "tma"), ("asa16", 3, "bspmom", "tma"),
+                                                    ("asa16", 2, "bsp", "reg"), ("asa", 3, "bspmom", "reg")])
+def test_multiprocess_bsp_fused_bitwise(tmp_path, strategy, k, mode, kernel):
+    """tm_bsp_step across processes: the momentum-SGD step is fused into the
+    staged kernel's pre-cast; two iterations vs oracle/bsp.py."""
+    from oracle.bsp import bsp_iteration
+    P = 100_003
+    env = None if kernel == "ws" else {"TM_STAGED_KERNEL": kernel}
+    res = launch(tmp_path, k, strategy, P, "D2", mode=mode, extra_env=env)
+    W = [worker_buffer(P, "D2", r, config=50) for r in range(k)]
+    V = [worker_buffer(P, "D4", r, config=52) for r in range(k)]
+    G = [worker_buffer(P, "D2", r, config=53) for r in range(k)]
+    for _ in range(2):
+        W, V = bsp_iteration(W, V, G, 0.01, 0.9, strategy, exchange_momentum=(mode == "bspmom"))
+    for r in range(k):
+        assert res[r]["code"] == 0, res[r]
+        assert res[r]["layout"]["staged_kernel"] == KERNEL_ID[kernel]
+        assert_bitwise(np.load(os.path.join(tmp_path, f"rank{r}.npy")), W[r], f"w rank {r}")
+        assert_bitwise(np.load(os.path.join(tmp_path, f"vel{r}.npy")), V[r], f"v rank {r}")
+
+
 def test_multiprocess_timeout_instead_of_hang(tmp_path):
     """Fault injection: rank 1 never calls tm_exchange; rank 0's
     kernel times out, sets TM_E_TIMEOUT and exits."""

@@ -141,17 +141,19 @@ def bsp_rows(P, k, pk):
     V = [torch.zeros(P, device="cuda") for _ in range(k)]
     G = [torch.randn(P, device="cuda", generator=g) * 0.01 for _ in range(k)]
     rows = []
-    for mom in (False, True):
-        for fused in (True, False):
-            os.environ["TM_BSP_UNFUSED"] = "0" if fused else "1"
-            with tm.Exchanger(P, "asa16", size=k, nlocal=k, path="direct") as ex:
-                ms = timeit(lambda: ex.bsp_step(W, V, G, 0.01, 0.9, exchange_momentum=mom), graph=True)
-            # fused: read w, v, g + write w, v = 20 B per element per worker
-            alg = 20.0 * P * k
-            rows.append({"mode": f"{'fused one pass' if fused else 'SGD pass + exchange pass(es)'}"
-                                 f"{', momentum exchanged' if mom else ''}",
-                         "us": ms * 1e3, "hbm_GBps": alg / (ms * 1e-3) / 1e9,
-                         "frac": alg / (ms * 1e-3) / 1e9 / pk, "P": P, "k": k})
+    for path in ("direct", "staged"):
+        for mom in (False, True):
+            for fused in (True, False):
+                os.environ["TM_BSP_UNFUSED"] = "0" if fused else "1"
+                with tm.Exchanger(P, "asa16", size=k, nlocal=k, path=path) as ex:
+                    ms = timeit(lambda: ex.bsp_step(W, V, G, 0.01, 0.9, exchange_momentum=mom), graph=True)
+                # irreducible: read w, v, g + write w, v = 20 B per element per worker
+                alg = 20.0 * P * k
+                how = ("fused one pass" if path == "direct" else "step fused into the pre-cast") if fused \
+                    else "SGD pass + exchange pass(es)"
+                rows.append({"mode": f"{path}: {how}{', momentum exchanged' if mom else ''}",
+                             "us": ms * 1e3, "hbm_GBps": alg / (ms * 1e-3) / 1e9,
+                             "frac": alg / (ms * 1e-3) / 1e9 / pk, "P": P, "k": k})
     os.environ.pop("TM_BSP_UNFUSED", None)
     return rows
 
@@ -160,9 +162,14 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--md", default=None)
     ap.add_argument("--quick", action="store_true")
+    ap.add_argument("--bsp-only", action="store_true")
     a = ap.parse_args()
     torch.cuda.set_device(0)
     pk = peak()
+    if a.bsp_only:
+        for r in bsp_rows(ALEXNET, 8, pk):
+            print(json.dumps({"config": "bsp", **r}))
+        return
     out = {"config2": [], "config3": [], "config4": [], "config5": [], "bsp": []}
     ks = (2, 4, 8)
     for strategy in ("asa", "asa16"):
