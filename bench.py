@@ -50,6 +50,8 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=5)
+    ap.add_argument("--e2e-chunks", type=int, default=16,
+                    help="element ranges the e2e leg pipelines H2D / exchange / D2H over (1 = none)")
     ap.add_argument("--path", choices=["auto", "staged", "direct"], default="auto",
                     help="data path of the exchange (auto: direct for a one-GPU group)")
     ap.add_argument("--no-staged", action="store_true",
@@ -84,6 +86,35 @@ def design_hbm_bytes(strategy, P, k, path):
 def nvlink_roof_us(strategy, P, k):
     s = 2 if strategy == "asa16" else 4
     return 2 * (k - 1) / k * P * s / (NVLINK_GBS * 1e3) if k > 1 else 0.0
+
+
+class NvlinkCounters:
+    """NVML NVLink data-throughput counters (KiB, cumulative) of one GPU, read
+    before and after the timed region of a multi-GPU run (the bytes
+    should be about steps * 2(k-1)/k * P * s per direction).  None where NVML
+    does not expose them."""
+
+    def __init__(self, device):
+        self.ok = False
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(device)
+            self.fields = [pynvml.NVML_FI_DEV_NVLINK_THROUGHPUT_DATA_TX,
+                           pynvml.NVML_FI_DEV_NVLINK_THROUGHPUT_DATA_RX]
+            self.ok = self.read() is not None
+        except Exception:
+            self.ok = False
+
+    def read(self):
+        try:
+            vals = self.nv.nvmlDeviceGetFieldValues(self.h, self.fields)
+            if any(v.nvmlReturn != 0 for v in vals):
+                return None
+            return [int(v.value.ullVal) * 1024 for v in vals]
+        except Exception:
+            return None
 
 
 class ClockSampler:
@@ -339,6 +370,8 @@ def main():
         dist.barrier()
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    nvl = NvlinkCounters(local) if multi else None
+    nvl0 = nvl.read() if nvl and nvl.ok else None
     with ClockSampler(local) as clk:
         e0.record(stream)
         for _ in range(args.steps):
@@ -346,6 +379,15 @@ def main():
         e1.record(stream)
         torch.cuda.synchronize()
     ms = e0.elapsed_time(e1) / args.steps
+    nvlink = None
+    if nvl0 is not None:
+        nvl1 = nvl.read()
+        if nvl1 is not None:
+            wire = 2 if args.strategy == "asa16" else 4
+            nvlink = {"tx_bytes_per_step": (nvl1[0] - nvl0[0]) / args.steps,
+                      "rx_bytes_per_step": (nvl1[1] - nvl0[1]) / args.steps,
+                      "expected_bytes_per_step_per_direction": 2 * (k - 1) / k * P * wire,
+                      "source": "NVML NVLINK_THROUGHPUT_DATA_TX/RX, rank 0's GPU"}
     if multi:
         ms = reduce_max(ms, dev if backend == "nccl" else "cpu")
     code, bits = ex.status()
@@ -389,20 +431,54 @@ def main():
         torch.cuda.synchronize()
         if multi:
             dist.barrier()
+        # Pipelined over nch element ranges (the bucketed range exchange of the
+        # public API): H2D of range c+1 on one copy stream overlaps the exchange
+        # of range c on the compute stream and the D2H of range c-1 on another
+        # (PCIe is full duplex).  Range c of step n+1 is overwritten only after
+        # its D2H of step n.
+        nch = max(1, min(args.e2e_chunks, P // 4096))
+        edges = [(P * c // nch) // 4 * 4 for c in range(nch)] + [P]
+        s_in, s_out = torch.cuda.Stream(dev), torch.cuda.Stream(dev)
+        ev_in = [torch.cuda.Event() for _ in range(nch)]
+        ev_x = [torch.cuda.Event() for _ in range(nch)]
+        ev_out = [torch.cuda.Event() for _ in range(nch)]
         f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         f0.record(stream)
-        for _ in range(args.e2e_steps):
-            for b, h in zip(bufs, hpin):
-                b.copy_(h, non_blocking=True)
-            step()
-            out_h.copy_(bufs[0], non_blocking=True)
+        s_in.wait_event(f0)
+        for n in range(args.e2e_steps):
+            for c in range(nch):
+                lo, hi = edges[c], edges[c + 1]
+                with torch.cuda.stream(s_in):
+                    if n > 0:
+                        s_in.wait_event(ev_out[c])
+                    for b, h in zip(bufs, hpin):
+                        b[lo:hi].copy_(h[lo:hi], non_blocking=True)
+                    ev_in[c].record(s_in)
+                stream.wait_event(ev_in[c])
+                if nch == 1:
+                    ex.exchange(bufs[0] if multi else bufs, stream)
+                else:
+                    ex.exchange_range(bufs[0] if multi else bufs, lo, hi - lo, stream)
+                ev_x[c].record(stream)
+                with torch.cuda.stream(s_out):
+                    s_out.wait_event(ev_x[c])
+                    out_h[lo:hi].copy_(bufs[0][lo:hi], non_blocking=True)
+                    ev_out[c].record(s_out)
+        stream.wait_stream(s_out)
         f1.record(stream)
         torch.cuda.synchronize()
         e2e_ms = f0.elapsed_time(f1) / args.e2e_steps
         if multi:
             e2e_ms = reduce_max(e2e_ms, dev if backend == "nccl" else "cpu")
+        # every e2e step reloads the same host inputs, so its result is the first
+        # exchange's: compare the sampled outputs (rank k-1 there, rank 0 here --
+        # all ranks hold the same average)
+        ok = None if sample_idx is None else bool(np.array_equal(
+            out_h.numpy()[sample_idx].view(np.uint32), sample_got.view(np.uint32)))
         e2e = {"value": bytes_alg / (e2e_ms * 1e-3) / 1e9, "unit": "GB/s", "ms_per_step": e2e_ms,
-               "h2d_bytes_per_step": 4 * P * nlocal, "d2h_bytes_per_step": 4 * P}
+               "h2d_bytes_per_step": 4 * P * nlocal, "d2h_bytes_per_step": 4 * P,
+               "pipeline": f"{nch} ranges (tm_exchange_group_range), H2D / exchange / D2H on 3 streams",
+               "sampled_result_equals_first_exchange": ok}
 
     if rank == 0:
         lay = ex.layout()
@@ -422,6 +498,7 @@ def main():
             "roofline": roof,
             "gpu_launches": args.steps,
             "staged_path_one_gpu": staged,
+            "nvlink_counters": nvlink,
             "clocks": clk.summary(),
             "e2e": e2e,
             "status": code,
