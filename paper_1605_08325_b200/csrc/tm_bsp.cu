@@ -148,6 +148,9 @@ tm_bsp_direct_kernel(const __grid_constant__ BspBufs bb, int64_t P, uint32_t* st
 // TMA-engine kernel.  Ring slot = the tile's 3K source tiles [w_0..w_{K-1} |
 // v_0.. | g_0..]; output slot = [avg w | avg v (MOM) or v'_0..v'_{K-1}].
 // ---------------------------------------------------------------------------
+// Thread 0 issues every bulk copy of a tile (measured faster than one copy per
+// lane of warp 0: 1.65 vs 1.86-1.91 ms at AlexNet k = 8).  Three output slots:
+// the stores of tile i-2 must have read their slot before tile i+1 is written.
 template <int K, bool MOM>
 struct BspTma {
   static constexpr int kTile = 512;                   // elements per buffer per tile
@@ -157,7 +160,7 @@ struct BspTma {
   static constexpr int kRaw = (144 * 1024) / kInBytes;
   static constexpr int kStages = kRaw > 8 ? 8 : (kRaw < 2 ? 2 : kRaw);
   static constexpr int kOutTiles = MOM ? 2 : K + 1;
-  static constexpr int kOutSlots = 2;
+  static constexpr int kOutSlots = 3;
   static constexpr int kSmem = kStages * kInBytes + kOutSlots * kOutTiles * (int)kTB;
 };
 
@@ -197,9 +200,10 @@ tm_bsp_tma_kernel(const __grid_constant__ BspBufs bb, int64_t ntiles, int64_t P,
   if (tid == 0) {
     for (int s = 0; s < S; ++s) mbar_init(&full[s], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    for (int64_t i = 0; i < S; ++i) issue(i);
   }
   __syncthreads();
+  if (tid == 0)
+    for (int64_t i = 0; i < S; ++i) issue(i);
 
   uint32_t st = 0;
   for (int64_t i = 0;; ++i) {
@@ -226,7 +230,7 @@ tm_bsp_tma_kernel(const __grid_constant__ BspBufs bb, int64_t ntiles, int64_t P,
       for (int j = 0; j < K; ++j) reinterpret_cast<float4*>(out + (size_t)(1 + j) * T)[tid] = v[j];
     }
     fence_proxy_async_smem();  // generic-proxy smem writes -> visible to the bulk stores
-    if (tid == 0) bulk_wait_read<C::kOutSlots - 2>();  // out slot of tile i+1 is free
+    if (tid == 0) bulk_wait_read<C::kOutSlots - 2>();  // the out slot of tile i+1 is free
     __syncthreads();  // every thread is done with ring slot s and wrote its outputs
     if (tid == 0) {
 #pragma unroll
@@ -273,14 +277,11 @@ cudaError_t bsp_launch(const BspBufs& bb, int64_t P, uint32_t* status, unsigned 
   const int64_t ntiles = P / C::kTile;
   if (ctr && ntiles > 0) {
     auto fn = tm_bsp_tma_kernel<K, Q16, MOM>;
-    static bool attr_set = false;
-    if (!attr_set) {
-      cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmem);
-      if (e != cudaSuccess) return e;
-      attr_set = true;
-    }
+    static std::atomic<uint64_t> optin{0};
+    cudaError_t e = smem_optin(reinterpret_cast<const void*>(fn), C::kSmem, dev, optin);
+    if (e != cudaSuccess) return e;
     // per-launch tile counter: stream-ordered reset, capturable in graphs
-    cudaError_t e = cudaMemsetAsync(ctr, 0, sizeof(unsigned long long), s);
+    e = cudaMemsetAsync(ctr, 0, sizeof(unsigned long long), s);
     if (e != cudaSuccess) return e;
     const int grid = (int)std::min<int64_t>(ntiles, sm_count(dev));
     fn<<<grid, C::kThr, C::kSmem, s>>>(bb, ntiles, P, status, ctr);

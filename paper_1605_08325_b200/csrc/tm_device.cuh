@@ -10,6 +10,7 @@
 #include <stdlib.h>
 
 #include <algorithm>
+#include <atomic>
 
 #include "tm_internal.h"
 
@@ -25,6 +26,16 @@ inline int sm_count(int device) {
 inline int env_int(const char* name, int dflt) {
   const char* v = getenv(name);
   return (v && *v) ? atoi(v) : dflt;
+}
+
+// Opt kernel `fn` into `bytes` of dynamic shared memory on device `dev`, once
+// per (kernel, device): `done` is the caller's per-kernel bit set of devices.
+inline cudaError_t smem_optin(const void* fn, int bytes, int dev, std::atomic<uint64_t>& done) {
+  const uint64_t bit = 1ull << (dev & 63);
+  if (done.load(std::memory_order_acquire) & bit) return cudaSuccess;
+  cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  if (e == cudaSuccess) done.fetch_or(bit, std::memory_order_release);
+  return e;
 }
 
 // grid for a grid-stride streaming kernel over `work_items` thread-items

@@ -229,12 +229,9 @@ cudaError_t launch_tma(const LocalBufs& lb, int64_t P, uint32_t* status, unsigne
   using Cfg = TmaCfg<K, TILE, RING_KB, MINB>;
   const int64_t ntiles = P / TILE;
   auto fn = tm_direct_tma_kernel<K, Q16, TILE, RING_KB, MINB>;
-  static bool attr_set = false;
-  if (!attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::kSmem);
-    if (e != cudaSuccess) return e;
-    attr_set = true;
-  }
+  static std::atomic<uint64_t> optin{0};
+  cudaError_t e0 = smem_optin(reinterpret_cast<const void*>(fn), Cfg::kSmem, dev, optin);
+  if (e0 != cudaSuccess) return e0;
   const int grid = (int)std::min<int64_t>(ntiles, (int64_t)MINB * sm_count(dev));
   if (ctr) {  // per-launch tile counter (stream-ordered reset; capturable in graphs)
     cudaError_t e = cudaMemsetAsync(ctr, 0, sizeof(unsigned long long), s);

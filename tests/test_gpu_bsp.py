@@ -89,3 +89,31 @@ def test_bsp_staged_status_overflow(monkeypatch):
         ex.bsp_step(Wd, Vd, Gd, 0.1, 0.9)
         code, bits = ex.status()
     assert bits & tm.TM_BIT_OVERFLOW16, (code, bits)
+
+
+@pytest.mark.parametrize("path", ["direct", "staged"])
+def test_bsp_full_size_sampled(path):
+    """AlexNet size, k = 8 (the launch configuration the BSP sweep times): sampled
+    elements and the tail against oracle/bsp.py (elementwise, so the oracle runs
+    on the sampled columns)."""
+    from paper_1605_08325_b200.inputs import WORKLOADS
+    P, k = WORKLOADS["alexnet"], 8
+    W = worker_buffers(P, k, "D2", config=120)
+    V = worker_buffers(P, k, "D4", config=121)
+    G = worker_buffers(P, k, "D2", config=122)
+    idx = np.unique(np.concatenate([np.random.default_rng(9).integers(0, P, 100_000),
+                                    np.arange(P - 300, P)]))
+    want_w, want_v = bsp_iteration([w[idx] for w in W], [v[idx] for v in V], [g[idx] for g in G],
+                                   0.01, 0.9, "asa16")
+    Wd, Vd, Gd = to_dev(W), to_dev(V), to_dev(G)
+    del W, V, G
+    with tm.Exchanger(P, "asa16", size=k, nlocal=k, path=path) as ex:
+        ex.bsp_step(Wd, Vd, Gd, 0.01, 0.9)
+        code, _ = ex.status()
+    assert code == tm.TM_OK
+    ti = torch.from_numpy(idx).cuda()
+    for r in (0, 5, 7):
+        assert_bitwise(Wd[r][ti].cpu().numpy(), want_w[r], f"w {path} rank {r}")
+        assert_bitwise(Vd[r][ti].cpu().numpy(), want_v[r], f"v {path} rank {r}")
+    del Wd, Vd, Gd
+    torch.cuda.empty_cache()

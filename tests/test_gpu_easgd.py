@@ -67,9 +67,11 @@ def test_concurrent_mode_serial_stream_equals_exclusive():
     assert_bitwise(gc, wc)
 
 
-@pytest.mark.parametrize("order", [[0, 1, 2, 3, 4, 5, 6, 7], [7, 2, 5, 0, 2, 1], [3]])
-def test_fused_round_equals_arrival_order_sequence(order):
-    n = 1_000_003
+@pytest.mark.parametrize("n", [1_000_003, 5_123, 1_027])
+@pytest.mark.parametrize("order", [[0, 1, 2, 3, 4, 5, 6, 7], [7, 2, 5, 0, 2, 1], [3], [4, 0, 6, 1, 2]])
+def test_fused_round_equals_arrival_order_sequence(order, n):
+    """Distinct arrival orders run the TMA-engine round kernel (whole 1024-element
+    tiles + register tail), repeated workers the generic kernel."""
     nw = 8
     W = [worker_buffer(n, "D3", r, config=44) for r in range(nw)]
     c = worker_buffer(n, "D3", 99, config=44)
@@ -232,3 +234,25 @@ def test_locked_concurrent_updates_follow_logged_arrival_order(k, P):
         logh = log.cpu().numpy()
         tm.tm_easgd_set_order_log(None, 0)
     _check_against_logged_order(W, c0, gW, gc, logh, k, P, L, nw, alpha)
+
+
+def test_fused_round_full_size_sampled():
+    """Config 4 (8 workers + centre, AlexNet size, alpha = 0.5/8), the TMA-engine
+    round in arrival order: sampled elements and the tail vs easgd_sequence."""
+    import torch
+    from paper_1605_08325_b200.inputs import WORKLOADS
+    P, nw = WORKLOADS["alexnet"], 8
+    order = [5, 2, 7, 0, 1, 6, 3, 4]
+    W = [worker_buffer(P, "D3", r, config=45) for r in range(nw)]
+    c = worker_buffer(P, "D3", 99, config=45)
+    idx = np.unique(np.concatenate([np.random.default_rng(11).integers(0, P, 100_000),
+                                    np.arange(P - 300, P)]))
+    wW, wc = easgd_sequence([w[idx] for w in W], c[idx], 0.5 / 8, order)
+    Wd = to_dev(W)
+    cd = to_dev([c])[0]
+    del W, c
+    tm.tm_easgd_round(Wd, order, cd, 0.5 / 8)
+    ti = torch.from_numpy(idx).cuda()
+    assert_bitwise(cd[ti].cpu().numpy(), wc, "centre")
+    for r in range(nw):
+        assert_bitwise(Wd[r][ti].cpu().numpy(), wW[r], f"worker {r}")

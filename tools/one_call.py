@@ -1,0 +1,47 @@
+#!/usr/bin/env python
+"""A few calls of one library entry point at AlexNet size, k = 8 ranks on one GPU
+(a short target for ncu captures; no timing).
+
+    python tools/one_call.py exchange-direct|exchange-staged|bsp-direct|bsp-staged|easgd-round [n]
+"""
+
+import os
+import sys
+
+import torch
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+from paper_1605_08325_b200 import tm  # noqa: E402
+
+P, K = 60_965_224, 8
+
+
+def main():
+    what = sys.argv[1]
+    n = int(sys.argv[2]) if len(sys.argv) > 2 else 3
+    torch.cuda.set_device(0)
+    g = torch.Generator(device="cuda").manual_seed(1)
+    W = [torch.randn(P, device="cuda", generator=g) * 0.01 for _ in range(K)]
+    if what.startswith("exchange"):
+        with tm.Exchanger(P, "asa16", size=K, nlocal=K, path=what.split("-")[1]) as ex:
+            for _ in range(n):
+                ex.exchange(W)
+    elif what.startswith("bsp"):
+        V = [torch.zeros(P, device="cuda") for _ in range(K)]
+        G = [torch.randn(P, device="cuda", generator=g) * 0.01 for _ in range(K)]
+        with tm.Exchanger(P, "asa16", size=K, nlocal=K, path=what.split("-")[1]) as ex:
+            for _ in range(n):
+                ex.bsp_step(W, V, G, 0.01, 0.9)
+    elif what == "easgd-round":
+        c = torch.randn(P, device="cuda", generator=g) * 0.01
+        for _ in range(n):
+            tm.tm_easgd_round(W, list(range(K)), c, 0.5 / K)
+    else:
+        raise SystemExit(f"unknown call {what}")
+    torch.cuda.synchronize()
+
+
+if __name__ == "__main__":
+    main()

@@ -162,13 +162,15 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--md", default=None)
     ap.add_argument("--quick", action="store_true")
-    ap.add_argument("--bsp-only", action="store_true")
+    ap.add_argument("--only", choices=["bsp", "easgd"], default=None,
+                    help="time only the BSP rows or only the EASGD (config 4) rows")
     a = ap.parse_args()
     torch.cuda.set_device(0)
     pk = peak()
-    if a.bsp_only:
-        for r in bsp_rows(ALEXNET, 8, pk):
-            print(json.dumps({"config": "bsp", **r}))
+    if a.only:
+        rows = bsp_rows(ALEXNET, 8, pk) if a.only == "bsp" else easgd_rows(ALEXNET, 8, 0.5 / 8, pk)
+        for r in rows:
+            print(json.dumps({"config": a.only if a.only == "bsp" else "config4", **r}))
         return
     out = {"config2": [], "config3": [], "config4": [], "config5": [], "bsp": []}
     ks = (2, 4, 8)
