@@ -128,6 +128,7 @@ typedef struct {
   uint32_t epoch;        /* number of staged exchanges issued so far          */
   int32_t path;          /* effective tm_path of the next exchange            */
   int32_t staged_kernel; /* staged flavour: 0 register, 1 TMA engine, 2 warp-specialised */
+  int32_t allgather;     /* tm_allgather mode of the staged path                */
 } tm_layout_info;
 
 /* How an ASA / ASA16 exchange moves data (results are bitwise identical):
@@ -144,6 +145,23 @@ typedef struct {
  *                   result to all k buffers: no staging, no flags.
  *   TM_PATH_AUTO    DIRECT when nlocal == size, else STAGED (default). */
 typedef enum { TM_PATH_AUTO = 0, TM_PATH_STAGED = 1, TM_PATH_DIRECT = 2 } tm_path;
+
+/* How the staged path's allgather ("Allgather
+ * ... do[es] not involve any arithmetic") moves the averaged segments; results
+ * are bitwise identical in every mode:
+ *   TM_AG_SM    (default) the exchange kernel's CTAs pull every rank's averaged
+ *               segment over NVLink and widen it into the caller's buffer, fused.
+ *   TM_AG_CE    the kernel stops after the reduced barrier; the COPY ENGINES
+ *               gather the k averaged segments (cudaMemcpyAsync from the peer
+ *               mappings into the library's staging, k copies per rank), then a
+ *               widen kernel writes the caller's buffer (ASA: the copies land in
+ *               the caller's buffer directly).  Frees the SMs during the gather.
+ *   TM_AG_NCCL  as TM_AG_CE with ncclAllGather of the segments (the north
+ *               star's "falling back to NCCL allgather over NVLink only where it
+ *               measures faster").  Needs an NCCL communicator: processes that
+ *               set TM_ALLGATHER=nccl in the environment before tm_exchange_init
+ *               get one at bootstrap (one process per GPU, nlocal == 1). */
+typedef enum { TM_AG_SM = 0, TM_AG_CE = 1, TM_AG_NCCL = 2 } tm_allgather;
 
 /* Create the process-global exchanger.  nparams >= 1; world as above; strategy
  * a tm_strategy.  Allocates the library-owned buffers on world->device.  For
@@ -319,6 +337,12 @@ int tm_layout(tm_layout_info* out);
 /* Select the data path (tm_path) for later exchanges of this exchanger.
  * TM_E_ARG for TM_PATH_DIRECT unless nlocal == size; TM_E_STATE before init. */
 int tm_set_path(int path);
+
+/* Select the allgather mode (tm_allgather) of later staged exchanges.  Every
+ * rank must select the same mode before the same exchange.  TM_E_ARG for an
+ * unknown mode; TM_E_NCCL for TM_AG_NCCL without a communicator; TM_E_STATE
+ * before init. */
+int tm_set_allgather(int mode);
 
 /* Diagnostics: the staged kernels write %globaltimer (ns) of every CTA at its
  * phase boundaries into dev_buf[cta*8 + slot] (slot 0 start, 1 pre-cast done,

@@ -46,6 +46,9 @@ struct ExchangeArgs {
   const float* g[TM_MAX_RANKS];
   float lr, mu;
   int32_t sgd;
+  // Allgather outside the kernel (TM_AG_CE / TM_AG_NCCL): the kernel returns
+  // after the REDUCED barrier and skips a6.
+  int32_t ag_external;
 };
 
 // Persistent fused exchange: pre-cast -> ready barrier -> reduce-scatter pull with
@@ -111,6 +114,10 @@ cudaError_t launch_sgd(float* w, float* v, const float* g, int64_t n, float lr, 
 cudaError_t launch_preprocess(const uint8_t* raw, const float* mean, const int32_t* crop, float* out,
                               int n, int c, int h, int w, int ch, int cw, cudaStream_t s);
 cudaError_t launch_cast_rn16(const float* in, uint16_t* out, int64_t n, cudaStream_t s);
+
+// After an external allgather into `gather` (k*L wire elements in segment
+// order): x[i] = widen(gather[i]) for i < P (fp16 wire).
+cudaError_t launch_widen16(const void* gather, float* x, int64_t P, cudaStream_t s);
 
 // Max co-resident CTAs of the exchange kernel on `device` (occupancy * SMs).
 int exchange_max_ctas(int device, bool wire16, int k, int flavour);

@@ -51,6 +51,8 @@ struct Nccl {
   ncclResult_t (*AllReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
                             cudaStream_t) = nullptr;
   ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+  ncclResult_t (*AllGather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t,
+                            cudaStream_t) = nullptr;
   bool load() {
     if (lib) return true;
     const char* path = getenv("TM_NCCL_LIB");
@@ -60,7 +62,8 @@ struct Nccl {
     CommInitRank = (decltype(CommInitRank))dlsym(lib, "ncclCommInitRank");
     AllReduce = (decltype(AllReduce))dlsym(lib, "ncclAllReduce");
     CommDestroy = (decltype(CommDestroy))dlsym(lib, "ncclCommDestroy");
-    return GetUniqueId && CommInitRank && AllReduce && CommDestroy;
+    AllGather = (decltype(AllGather))dlsym(lib, "ncclAllGather");
+    return GetUniqueId && CommInitRank && AllReduce && CommDestroy && AllGather;
   }
 };
 
@@ -83,6 +86,8 @@ struct Ctx {
   uint32_t epoch = 0;
   int path = TM_PATH_AUTO;
   int staged_kernel = tmx::kStagedTma;  // staged kernel flavour, fixed at init (it sets C)
+  int ag_mode = TM_AG_SM;               // tm_allgather of the staged path
+  bool want_nccl_ag = false;            // TM_ALLGATHER=nccl at init: build a communicator
   bool sum = false;  // TM_OP_SUM (SUBGD)
   uint64_t timeout_ns = kDefaultTimeoutNs;
   ncclComm_t comm = nullptr;
@@ -157,6 +162,60 @@ ExchangeArgs make_args(float* const* bufs, int64_t off, int64_t n) {
   return a;
 }
 
+// a6 outside the kernel (TM_AG_CE / TM_AG_NCCL), after the kernel's REDUCED
+// barrier: gather the k averaged segments (a.L wire elements each) of every local
+// rank into its own staging (free: every rank has finished its reduce-scatter
+// reads of it), then widen into the caller's buffer.  ASA on the copy engines
+// copies straight into the caller's buffer (no widening).  Reuse: the next
+// exchange overwrites staging (pre-cast) and avg (reduce-scatter, after READY
+// from every rank) only after this stream-ordered work, and NCCL has consumed
+// its send buffer when its kernel completes.
+int external_allgather(const ExchangeArgs& a, cudaStream_t s) {
+  const int wb = wire_bytes(g.strategy);
+  for (int i = 0; i < g.nlocal; ++i) {
+    const int r = g.rank0 + i;
+    char* gather = static_cast<char*>(a.stage[r]);
+    float* x = a.x[i];
+    if (g.ag_mode == TM_AG_NCCL) {
+      if (!g.comm) return TM_E_NCCL;
+      ncclResult_t nr = g_nccl.AllGather(a.avg[r], gather, (size_t)a.L,
+                                         wb == 2 ? ncclFloat16 : ncclFloat32, g.comm, s);
+      if (nr != ncclSuccess) return TM_E_NCCL;
+    }
+    for (int j = 0; j < g.k; ++j) {
+      const int64_t n = std::min(a.L, a.P - (int64_t)j * a.L);  // elements of segment j < P
+      if (g.ag_mode == TM_AG_CE) {
+        cudaError_t e;
+        if (wb == 4) {
+          if (n <= 0) break;
+          e = cudaMemcpyAsync(x + (int64_t)j * a.L, a.avg[j], (size_t)n * 4, cudaMemcpyDefault, s);
+        } else {
+          e = cudaMemcpyAsync(gather + (int64_t)j * a.L * wb, a.avg[j], (size_t)a.L * wb,
+                              cudaMemcpyDefault, s);
+        }
+        if (e != cudaSuccess) return cuda_fail("allgather copy", e);
+      } else if (wb == 4 && n > 0) {  // NCCL, fp32: segment j of the gather -> caller
+        cudaError_t e = cudaMemcpyAsync(x + (int64_t)j * a.L, gather + (int64_t)j * a.L * wb,
+                                        (size_t)n * 4, cudaMemcpyDeviceToDevice, s);
+        if (e != cudaSuccess) return cuda_fail("allgather copy", e);
+      }
+    }
+    if (wb == 2) {
+      cudaError_t e = tmx::launch_widen16(gather, x, a.P, s);
+      if (e != cudaSuccess) return cuda_fail("launch_widen16", e);
+    }
+  }
+  return TM_OK;
+}
+
+int launch_staged(ExchangeArgs& a, cudaStream_t s) {
+  a.ag_external = g.ag_mode != TM_AG_SM;
+  cudaError_t e = tmx::launch_exchange(a, g.nlocal, wire16(g.strategy), g.staged_kernel, s);
+  if (e != cudaSuccess) return cuda_fail("launch_exchange", e);
+  ++g.epoch;  // host-side count for tm_layout; the kernels keep their own
+  return a.ag_external ? external_allgather(a, s) : TM_OK;
+}
+
 int effective_path() {
   if (g.path != TM_PATH_AUTO) return g.path;
   return g.nlocal == g.k ? TM_PATH_DIRECT : TM_PATH_STAGED;
@@ -189,10 +248,7 @@ int do_exchange(float* const* bufs, int nbufs, int64_t off, int64_t n, cudaStrea
     return r == ncclSuccess ? TM_OK : TM_E_NCCL;
   }
   ExchangeArgs a = make_args(bufs, off, n);
-  cudaError_t e = tmx::launch_exchange(a, g.nlocal, wire16(g.strategy), g.staged_kernel, s);
-  if (e != cudaSuccess) return cuda_fail("launch_exchange", e);
-  ++g.epoch;  // host-side count for tm_layout; the kernels keep their own
-  return TM_OK;
+  return launch_staged(a, s);
 }
 
 // One BSP iteration: momentum-SGD step of every local rank, then the exchange
@@ -236,9 +292,7 @@ int do_bsp(float* const* w, float* const* v, const float* const* gr, int nbufs, 
     a.lr = lr;
     a.mu = mu;
     a.sgd = 1;
-    cudaError_t e = tmx::launch_exchange(a, g.nlocal, wire16(g.strategy), g.staged_kernel, s);
-    if (e != cudaSuccess) return cuda_fail("launch_exchange", e);
-    ++g.epoch;
+    rc = launch_staged(a, s);
   } else {
     for (int i = 0; i < nbufs; ++i) {
       cudaError_t e = tmx::launch_sgd(w[i], v[i], gr[i], g.P, lr, mu, s);
@@ -323,6 +377,10 @@ int tm_exchange_init(int64_t nparams, const tm_world* world, int strategy) {
     if (sk && !strcmp(sk, "reg")) c.staged_kernel = tmx::kStagedReg;
     if (sk && !strcmp(sk, "tma")) c.staged_kernel = tmx::kStagedTma;
     if (sk && !strcmp(sk, "ws")) c.staged_kernel = tmx::kStagedWs;
+    const char* ag = getenv("TM_ALLGATHER");  // sm | ce | nccl
+    if (ag && !strcmp(ag, "ce")) c.ag_mode = TM_AG_CE;
+    c.want_nccl_ag = ag && !strcmp(ag, "nccl") && c.nprocs > 1;
+    if (c.want_nccl_ag) c.ag_mode = TM_AG_NCCL;
     int cmax = k >= 2 ? tmx::exchange_max_ctas(c.device, wire16(strategy), k, c.staged_kernel) / c.nlocal : 1;
     if (k >= 2 && cmax < 1) return TM_E_CUDA;
     const int64_t want = std::max<int64_t>(1, (c.L + tmx::kMinChunk - 1) / tmx::kMinChunk);
@@ -355,7 +413,7 @@ int tm_exchange_init(int64_t nparams, const tm_world* world, int strategy) {
   c.ready = (c.nprocs == 1);
   g = c;
   fill_rank_bases_local();
-  if (g.strategy == TM_AR && g.nprocs > 1 && g.proc == 0) {
+  if ((g.strategy == TM_AR || g.want_nccl_ag) && g.nprocs > 1 && g.proc == 0) {
     if (!g_nccl.load()) {
       release();
       return TM_E_NCCL;
@@ -431,7 +489,7 @@ int tm_bootstrap_import(const void* blobs, size_t len_each) {
     for (int i = 0; i < b.nlocal; ++i)
       g.rank_base[b.rank0 + i] = static_cast<char*>(base) + (int64_t)i * b.rank_stride;
   }
-  if (g.strategy == TM_AR && g.nprocs > 1) {
+  if ((g.strategy == TM_AR || g.want_nccl_ag) && g.nprocs > 1) {
     if (!nccl_blob || !g_nccl.load()) return TM_E_NCCL;
     Blob nb;
     memcpy(&nb, nccl_blob, sizeof(nb));
@@ -617,6 +675,16 @@ int tm_layout(tm_layout_info* out) {
   out->epoch = g.epoch;
   out->path = effective_path();
   out->staged_kernel = g.staged_kernel;
+  out->allgather = g.ag_mode;
+  return TM_OK;
+}
+
+int tm_set_allgather(int mode) {
+  std::lock_guard<std::mutex> lk(g_mu);
+  if (!g.inited) return TM_E_STATE;
+  if (mode < TM_AG_SM || mode > TM_AG_NCCL) return TM_E_ARG;
+  if (mode == TM_AG_NCCL && !g.comm) return TM_E_NCCL;
+  g.ag_mode = mode;
   return TM_OK;
 }
 

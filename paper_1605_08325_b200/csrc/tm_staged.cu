@@ -8,6 +8,28 @@ namespace tmx {
 const void* pick_exchange_sgd(int k, bool w16, bool sys, int fl);
 
 
+namespace {
+// x[i] = widen(gather[i]) for i < P: 8 elements (16 bytes of fp16) per thread-step.
+__global__ void __launch_bounds__(kThreads)
+widen16_kernel(const uint4* __restrict__ g, float* __restrict__ x, int64_t P) {
+  const int64_t stride = (int64_t)gridDim.x * kThreads;
+  const int64_t n8 = P / 8;
+  for (int64_t v = (int64_t)blockIdx.x * kThreads + threadIdx.x; v < n8; v += stride) {
+    float f[8];
+    Unit<true>::decode(__ldcs(g + v), f);
+    Unit<true>::store_dst(x + v * 8, f);
+  }
+  const int64_t i = n8 * 8 + (int64_t)blockIdx.x * kThreads + threadIdx.x;
+  if (blockIdx.x == 0 && i < P)
+    x[i] = __half2float(reinterpret_cast<const __half*>(g)[i]);
+}
+}  // namespace
+
+cudaError_t launch_widen16(const void* gather, float* x, int64_t P, cudaStream_t s) {
+  widen16_kernel<<<streaming_grid(P / 8 + 8), kThreads, 0, s>>>(static_cast<const uint4*>(gather), x, P);
+  return cudaGetLastError();
+}
+
 int exchange_max_ctas(int device, bool wire16, int k, int fl) {
   const void* fn = pick_exchange<false>(k, wire16, true, fl);
   if (!fn) return 0;

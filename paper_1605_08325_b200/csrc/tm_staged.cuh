@@ -247,6 +247,7 @@ tm_exchange_kernel(const __grid_constant__ ExchangeArgs a) {
 
   if (!rank_barrier<K, SYS>(a, kPhaseReduced, r, c, epoch, &s_abort)) return;
   stamp(a, kStampReduced);
+  if (a.ag_external) return;  // a6 by the copy engines / NCCL (tm_allgather)
 
   // ---------------- a6: allgather pull, fused widen, store to caller ---------
   {
@@ -398,6 +399,7 @@ tm_exchange_ws_kernel(const __grid_constant__ ExchangeArgs a) {
   stamp(a, kStampReduce);  // pre-cast and reduce-scatter overlap: one stamp for both
   if (!rank_barrier<K, SYS>(a, kWsSub, r, c, epoch, &s_abort)) return;  // REDUCED
   stamp(a, kStampReduced);
+  if (a.ag_external) return;  // a6 by the copy engines / NCCL (tm_allgather)
 
   // ---------------- a6: allgather pull with all 16 warps ----------------------
   const int nu32 = (int)(nel / E);
@@ -682,6 +684,7 @@ tm_exchange_tma_kernel(const __grid_constant__ ExchangeArgs a) {
   stamp(a, kStampReduce);
   if (!rank_barrier<K, SYS>(a, kPhaseReduced, r, c, epoch, &s_abort)) return;
   stamp(a, kStampReduced);
+  if (a.ag_external) return;  // a6 by the copy engines / NCCL (tm_allgather)
   if (tid == 0) fence_proxy_async_global();
 
   // ---------------- a6: allgather pull (TMA from every rank's avg) ----------

@@ -24,6 +24,8 @@ TM_BIT_NONFINITE, TM_BIT_OVERFLOW16, TM_BIT_TIMEOUT = 1, 2, 4
 TM_OP_SUM = 0x100  # SUBGD: sum instead of average
 TM_PATH_AUTO, TM_PATH_STAGED, TM_PATH_DIRECT = 0, 1, 2
 PATH = {"auto": TM_PATH_AUTO, "staged": TM_PATH_STAGED, "direct": TM_PATH_DIRECT}
+TM_AG_SM, TM_AG_CE, TM_AG_NCCL = 0, 1, 2
+ALLGATHER = {"sm": TM_AG_SM, "ce": TM_AG_CE, "nccl": TM_AG_NCCL}
 TM_BLOB_BYTES = 512
 TM_MAX_RANKS = 8
 
@@ -46,7 +48,8 @@ class tm_layout_info(ctypes.Structure):
                 ("ctas_per_rank", ctypes.c_int32), ("threads", ctypes.c_int32),
                 ("sm_count", ctypes.c_int32), ("wire_bytes", ctypes.c_int32),
                 ("lib_bytes", ctypes.c_int64), ("epoch", ctypes.c_uint32),
-                ("path", ctypes.c_int32), ("staged_kernel", ctypes.c_int32)]
+                ("path", ctypes.c_int32), ("staged_kernel", ctypes.c_int32),
+                ("allgather", ctypes.c_int32)]
 
 
 _lib = None
@@ -76,6 +79,7 @@ _SIGS = {
     "tm_layout": (ctypes.c_int, [ctypes.POINTER(tm_layout_info)]),
     "tm_set_timeout_ns": (ctypes.c_int, [ctypes.c_uint64]),
     "tm_set_path": (ctypes.c_int, [ctypes.c_int]),
+    "tm_set_allgather": (ctypes.c_int, [ctypes.c_int]),
     "tm_set_phase_log": (ctypes.c_int, [_P, ctypes.c_int64]),
     "tm_exchange_finalize": (ctypes.c_int, []),
     "tm_strerror": (ctypes.c_char_p, [ctypes.c_int]),
@@ -258,6 +262,11 @@ def tm_set_path(path):
     _check(lib().tm_set_path(PATH[path] if isinstance(path, str) else int(path)), "tm_set_path")
 
 
+def tm_set_allgather(mode):
+    _check(lib().tm_set_allgather(ALLGATHER[mode] if isinstance(mode, str) else int(mode)),
+           "tm_set_allgather")
+
+
 def tm_set_phase_log(buf):
     """buf: int64 CUDA tensor (>= nlocal*C*8 slots) or None."""
     _check(lib().tm_set_phase_log(None if buf is None else ctypes.c_void_p(buf.data_ptr()),
@@ -379,7 +388,7 @@ class Exchanger:
     """
 
     def __init__(self, nparams, strategy, rank=0, size=1, device=None, nlocal=None,
-                 group=None, timeout_s=None, path="auto", op="avg"):
+                 group=None, timeout_s=None, path="auto", op="avg", allgather=None):
         if device is None:
             device = torch.cuda.current_device()
         nlocal = size if nlocal is None else nlocal
@@ -396,6 +405,8 @@ class Exchanger:
             tm_set_path(path)
         if nlocal != size:
             tm_bootstrap_import(gather_blobs(tm_bootstrap_export(), size // nlocal, group))
+        if allgather is not None:
+            tm_set_allgather(allgather)
 
     def exchange(self, bufs, stream=None):
         if isinstance(bufs, torch.Tensor):

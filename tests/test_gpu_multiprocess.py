@@ -96,6 +96,49 @@ def test_multiprocess_bsp_fused_bitwise(tmp_path, strategy, k, mode, kernel):
         assert_bitwise(np.load(os.path.join(tmp_path, f"vel{r}.npy")), V[r], f"v rank {r}")
 
 
+@pytest.mark.parametrize("strategy,k,mode,kernel", [("asa16", 2, "normal", "ws"), ("asa", 3, "range", "tma"),
+                                                    ("asa16", 3, "bspmom", "reg")])
+def test_multiprocess_copy_engine_allgather(tmp_path, strategy, k, mode, kernel):
+    """TM_ALLGATHER=ce across processes: the copy engines pull the peers' averaged
+    segments through the IPC mappings (the NVLink copy path on a multi-GPU box)."""
+    P = 100_003
+    env = {"TM_ALLGATHER": "ce"}
+    if kernel != "ws":
+        env["TM_STAGED_KERNEL"] = kernel
+    res = launch(tmp_path, k, strategy, P, "D2", mode=mode, extra_env=env)
+    for r in range(k):
+        assert res[r]["code"] == 0, res[r]
+        assert res[r]["layout"]["allgather"] == 1
+    if mode.startswith("bsp"):
+        from oracle.bsp import bsp_iteration
+        W = [worker_buffer(P, "D2", r, config=50) for r in range(k)]
+        V = [worker_buffer(P, "D4", r, config=52) for r in range(k)]
+        G = [worker_buffer(P, "D2", r, config=53) for r in range(k)]
+        for _ in range(2):
+            W, V = bsp_iteration(W, V, G, 0.01, 0.9, strategy, exchange_momentum=True)
+        want = W
+    else:
+        want = [worker_buffer(P, "D2", r, config=50) for r in range(k)]
+        for _ in range(3):
+            want = ox.exchange(want, strategy)
+    for r in range(k):
+        assert_bitwise(np.load(os.path.join(tmp_path, f"rank{r}.npy")), want[r], f"rank {r}")
+
+
+@pytest.mark.skipif(__import__("torch").cuda.device_count() < 2,
+                    reason="NCCL needs one GPU per rank (multi-GPU box)")
+def test_multiprocess_nccl_allgather(tmp_path):
+    """TM_ALLGATHER=nccl: ncclAllGather of the averaged segments (one process per GPU)."""
+    P, k = 100_003, 2
+    res = launch(tmp_path, k, "asa16", P, "D2", extra_env={"TM_ALLGATHER": "nccl"})
+    want = [worker_buffer(P, "D2", r, config=50) for r in range(k)]
+    for _ in range(3):
+        want = ox.exchange(want, "asa16")
+    for r in range(k):
+        assert res[r]["code"] == 0 and res[r]["layout"]["allgather"] == 2, res[r]
+        assert_bitwise(np.load(os.path.join(tmp_path, f"rank{r}.npy")), want[r], f"rank {r}")
+
+
 def test_multiprocess_timeout_instead_of_hang(tmp_path):
     """Fault injection: rank 1 never calls tm_exchange; rank 0's
     kernel times out, sets TM_E_TIMEOUT and exits."""

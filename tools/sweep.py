@@ -158,19 +158,41 @@ def bsp_rows(P, k, pk):
     return rows
 
 
+def allgather_rows(P, k, pk):
+    """a6 modes on the staged path (tm_allgather): the fused SM pull vs the copy
+    engines + widen kernel, every staged flavour, ASA16."""
+    rows = []
+    for fl in ("tma", "ws", "reg"):
+        for ag in ("sm", "ce"):
+            os.environ["TM_STAGED_KERNEL"] = fl
+            g = torch.Generator(device="cuda").manual_seed(1605)
+            bufs = [torch.randn(P, device="cuda", generator=g) * 0.01 for _ in range(k)]
+            with tm.Exchanger(P, "asa16", size=k, nlocal=k, path="staged", allgather=ag) as ex:
+                ms = timeit(lambda: ex.exchange(bufs), graph=True)
+            alg = hbm_bytes("asa16", P, k, "staged")
+            rows.append({"mode": f"staged/{fl} allgather={ag}", "us": ms * 1e3,
+                         "hbm_GBps": alg / (ms * 1e-3) / 1e9, "frac": alg / (ms * 1e-3) / 1e9 / pk,
+                         "P": P, "k": k})
+            del bufs
+            torch.cuda.empty_cache()
+    os.environ.pop("TM_STAGED_KERNEL", None)
+    return rows
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--md", default=None)
     ap.add_argument("--quick", action="store_true")
-    ap.add_argument("--only", choices=["bsp", "easgd"], default=None,
-                    help="time only the BSP rows or only the EASGD (config 4) rows")
+    ap.add_argument("--only", choices=["bsp", "easgd", "ag"], default=None,
+                    help="time only the BSP rows, the EASGD (config 4) rows or the allgather modes")
     a = ap.parse_args()
     torch.cuda.set_device(0)
     pk = peak()
     if a.only:
-        rows = bsp_rows(ALEXNET, 8, pk) if a.only == "bsp" else easgd_rows(ALEXNET, 8, 0.5 / 8, pk)
+        rows = {"bsp": lambda: bsp_rows(ALEXNET, 8, pk), "easgd": lambda: easgd_rows(ALEXNET, 8, 0.5 / 8, pk),
+                "ag": lambda: allgather_rows(ALEXNET, 8, pk)}[a.only]()
         for r in rows:
-            print(json.dumps({"config": a.only if a.only == "bsp" else "config4", **r}))
+            print(json.dumps({"config": "config4" if a.only == "easgd" else a.only, **r}))
         return
     out = {"config2": [], "config3": [], "config4": [], "config5": [], "bsp": []}
     ks = (2, 4, 8)
