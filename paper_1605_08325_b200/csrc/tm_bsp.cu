@@ -11,9 +11,9 @@
 //                         step of 4 elements of every worker and averages the
 //                         new weights (and velocities) with the exchange's
 //                         arithmetic (rn16 of each contribution for ASA16,
-//                         rank-order sum, fl(s/k), rn16); thread 0 bulk-stores
-//                         the average into all k workers (and each worker's own
-//                         v' when the velocities are not exchanged):
+//                         rank-order sum, fl(s/k), rn16) and stores the average
+//                         into all k workers (and each worker's own v' when the
+//                         velocities are not exchanged) from registers:
 //                         12 B read + 8 B written per element per worker,
 //                         instead of 20 B for the step plus 8 B (16 B with
 //                         momentum) for a separate exchange.
@@ -148,20 +148,21 @@ tm_bsp_direct_kernel(const __grid_constant__ BspBufs bb, int64_t P, uint32_t* st
 // TMA-engine kernel.  Ring slot = the tile's 3K source tiles [w_0..w_{K-1} |
 // v_0.. | g_0..]; output slot = [avg w | avg v (MOM) or v'_0..v'_{K-1}].
 // ---------------------------------------------------------------------------
-// Thread 0 issues every bulk copy of a tile (measured faster than one copy per
-// lane of warp 0: 1.65 vs 1.86-1.91 ms at AlexNet k = 8).  Three output slots:
-// the stores of tile i-2 must have read their slot before tile i+1 is written.
+// Loads: thread 0 issues every bulk copy of a tile (measured faster than one
+// copy per lane of warp 0: 1.65 vs 1.86-1.91 ms at AlexNet k = 8).  Stores: each
+// thread writes its results with 16-byte register stores (128 threads x 16 B =
+// one coalesced 2 KB row per buffer), measured 1.48 ms against 1.60 ms for bulk
+// stores from an output ring (whose smem reads queue behind the ring's loads) and
+// 1.57 ms for register stores with an "empty" mbarrier in place of __syncthreads.
 template <int K, bool MOM>
 struct BspTma {
   static constexpr int kTile = 512;                   // elements per buffer per tile
   static constexpr int kThr = kTile / 4;              // one float4 per thread
   static constexpr uint32_t kTB = kTile * 4;          // bytes per buffer tile
   static constexpr int kInBytes = 3 * K * kTB;        // one ring slot
-  static constexpr int kRaw = (144 * 1024) / kInBytes;
+  static constexpr int kRaw = (200 * 1024) / kInBytes;
   static constexpr int kStages = kRaw > 8 ? 8 : (kRaw < 2 ? 2 : kRaw);
-  static constexpr int kOutTiles = MOM ? 2 : K + 1;
-  static constexpr int kOutSlots = 3;
-  static constexpr int kSmem = kStages * kInBytes + kOutSlots * kOutTiles * (int)kTB;
+  static constexpr int kSmem = kStages * kInBytes;
 };
 
 template <int K, bool Q16, bool MOM>
@@ -173,7 +174,6 @@ tm_bsp_tma_kernel(const __grid_constant__ BspBufs bb, int64_t ntiles, int64_t P,
   constexpr int T = C::kTile;
   extern __shared__ __align__(128) unsigned char smem[];
   float* ring = reinterpret_cast<float*>(smem);              // [S][3][K][T]
-  float* outr = ring + (size_t)S * 3 * K * T;                 // [kOutSlots][kOutTiles][T]
   __shared__ __align__(8) uint64_t full[S];
   __shared__ int64_t slot_tile[S];
   const int tid = threadIdx.x;
@@ -212,7 +212,6 @@ tm_bsp_tma_kernel(const __grid_constant__ BspBufs bb, int64_t ntiles, int64_t P,
     const int64_t t = slot_tile[s];
     if (t < 0) break;  // uniform: every later claim is past the end too
     const float* src = ring + (size_t)s * 3 * K * T;
-    float* out = outr + (size_t)(i % C::kOutSlots) * C::kOutTiles * T;
     float4 w[K], v[K], g[K];
 #pragma unroll
     for (int j = 0; j < K; ++j) {
@@ -222,28 +221,14 @@ tm_bsp_tma_kernel(const __grid_constant__ BspBufs bb, int64_t ntiles, int64_t P,
     }
     float4 sw, sv;
     bsp_core<K, Q16, MOM>(w, v, g, bb.lr, bb.mu, sw, sv, st);
-    reinterpret_cast<float4*>(out)[tid] = sw;
-    if (MOM) {
-      reinterpret_cast<float4*>(out + T)[tid] = sv;
-    } else {
 #pragma unroll
-      for (int j = 0; j < K; ++j) reinterpret_cast<float4*>(out + (size_t)(1 + j) * T)[tid] = v[j];
+    for (int j = 0; j < K; ++j) {
+      st16_f(bb.w[j] + t * T + tid * 4, sw);
+      st16_f(bb.v[j] + t * T + tid * 4, MOM ? sv : v[j]);
     }
-    fence_proxy_async_smem();  // generic-proxy smem writes -> visible to the bulk stores
-    if (tid == 0) bulk_wait_read<C::kOutSlots - 2>();  // the out slot of tile i+1 is free
-    __syncthreads();  // every thread is done with ring slot s and wrote its outputs
-    if (tid == 0) {
-#pragma unroll
-      for (int j = 0; j < K; ++j) {
-        bulk_store(bb.w[j] + t * T, out, C::kTB);
-        bulk_store(bb.v[j] + t * T, MOM ? out + T : out + (size_t)(1 + j) * T, C::kTB);
-      }
-      bulk_commit();
-      issue(i + S);
-    }
+    __syncthreads();  // every thread is done with ring slot s
+    if (tid == 0) issue(i + S);
   }
-  if (tid == 0) bulk_wait_all<0>();
-
   // elements past the last whole tile: register path (last CTA)
   if (blockIdx.x == gridDim.x - 1) {
     for (int64_t v = ntiles * T / 4 + tid; v < P / 4; v += C::kThr) bsp_vec<K, Q16, MOM>(bb, v, st);

@@ -262,6 +262,8 @@ cudaError_t direct_tma(const LocalBufs& lb, int64_t P, uint32_t* status, unsigne
   }
   // Default, from the r01 sweep at k = 8 (profiles/r01/README.md): 8 KB tiles per
   // buffer, a 2-deep ring for k = 8 (128 KB in flight per SM), one CTA per SM.
+  // (With dynamic tiles every TM_TMA_CFG measures 0.570-0.572 ms; register stores
+  // in place of the bulk stores measured 0.574 ms.)
   return launch_tma<K, Q16, 2048, 96, 1>(lb, P, status, ctr, dev, s);
 }
 
