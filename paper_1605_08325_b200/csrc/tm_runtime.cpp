@@ -29,7 +29,7 @@ namespace {
 using tmx::ExchangeArgs;
 
 constexpr uint32_t kMagic = 0x544d4558u;  // "TMEX"
-constexpr uint32_t kVersion = 1;
+constexpr uint32_t kVersion = 2;
 constexpr uint64_t kDefaultTimeoutNs = 10ull * 1000 * 1000 * 1000;
 
 struct Blob {
@@ -38,6 +38,7 @@ struct Blob {
   int64_t P, L, Lc, rank_stride;
   int64_t off_stage, off_avg, off_flags, off_center;
   int32_t has_nccl, device_ordinal;
+  int32_t ag_nccl;  // TM_ALLGATHER=nccl at init: every rank must agree (a collective)
   cudaIpcMemHandle_t handle;
   ncclUniqueId nccl_id;
 };
@@ -450,6 +451,7 @@ int tm_bootstrap_export(void* blob, size_t* len) {
   b.off_flags = g.off_flags;
   b.off_center = g.off_center;
   b.device_ordinal = g.device;
+  b.ag_nccl = g.want_nccl_ag ? 1 : 0;
   cudaSetDevice(g.device);
   cudaError_t e = cudaIpcGetMemHandle(&b.handle, g.slab);
   if (e != cudaSuccess) return cuda_fail("cudaIpcGetMemHandle", e);
@@ -478,6 +480,7 @@ int tm_bootstrap_import(const void* blobs, size_t len_each) {
     if (b.P != g.P || b.size != g.k || b.strategy != (g.strategy | (g.sum ? TM_OP_SUM : 0)) ||
         b.C != g.C || b.L != g.L ||
         b.Lc != g.Lc || b.nlocal != g.nlocal || b.rank_stride != g.rank_stride ||
+        b.ag_nccl != (g.want_nccl_ag ? 1 : 0) ||
         b.rank0 != q * g.nlocal)
       return TM_E_MISMATCH;
     if (b.has_nccl) nccl_blob = reinterpret_cast<const Blob*>(p + (size_t)q * len_each);
