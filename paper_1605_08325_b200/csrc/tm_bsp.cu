@@ -229,6 +229,7 @@ tm_bsp_tma_kernel(const __grid_constant__ BspBufs bb, int64_t ntiles, int64_t P,
     __syncthreads();  // every thread is done with ring slot s
     if (tid == 0) issue(i + S);
   }
+  if (tid == 0) tile_ctr_retire(tile_ctr);
   // elements past the last whole tile: register path (last CTA)
   if (blockIdx.x == gridDim.x - 1) {
     for (int64_t v = ntiles * T / 4 + tid; v < P / 4; v += C::kThr) bsp_vec<K, Q16, MOM>(bb, v, st);
@@ -264,9 +265,6 @@ cudaError_t bsp_launch(const BspBufs& bb, int64_t P, uint32_t* status, unsigned 
     auto fn = tm_bsp_tma_kernel<K, Q16, MOM>;
     static std::atomic<uint64_t> optin{0};
     cudaError_t e = smem_optin(reinterpret_cast<const void*>(fn), C::kSmem, dev, optin);
-    if (e != cudaSuccess) return e;
-    // per-launch tile counter: stream-ordered reset, capturable in graphs
-    e = cudaMemsetAsync(ctr, 0, sizeof(unsigned long long), s);
     if (e != cudaSuccess) return e;
     const int grid = (int)std::min<int64_t>(ntiles, sm_count(dev));
     fn<<<grid, C::kThr, C::kSmem, s>>>(bb, ntiles, P, status, ctr);

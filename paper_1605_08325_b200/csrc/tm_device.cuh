@@ -229,6 +229,19 @@ __device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
                : "memory");
 }
+// Dynamic tile claiming without a host-side reset: ctr[0] is the claim counter
+// of the launch, ctr[1] counts CTAs that have made their last claim.  Thread 0
+// calls this once its CTA will claim no more; the last CTA to retire resets both
+// words for the next launch (the kernel boundary orders the reset before it).
+// Both words start at zero (the library's slab is zeroed at init).
+__device__ __forceinline__ void tile_ctr_retire(unsigned long long* ctr) {
+  __threadfence();  // this CTA's claims precede its retirement
+  if (atomicAdd(ctr + 1, 1ull) == (unsigned long long)gridDim.x - 1) {
+    ctr[0] = 0;
+    ctr[1] = 0;
+  }
+}
+
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }

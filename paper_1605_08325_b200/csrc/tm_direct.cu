@@ -202,7 +202,10 @@ tm_direct_tma_kernel(const __grid_constant__ LocalBufs lb, int64_t ntiles, int64
       issue(i + S);  // every thread has finished reading ring slot s
     }
   }
-  if (tid == 0) bulk_wait_all<0>();
+  if (tid == 0) {
+    if (tile_ctr) tile_ctr_retire(tile_ctr);
+    bulk_wait_all<0>();
+  }
 
   // elements past the last whole tile: register path (one CTA)
   if (blockIdx.x == gridDim.x - 1) {
@@ -233,10 +236,6 @@ cudaError_t launch_tma(const LocalBufs& lb, int64_t P, uint32_t* status, unsigne
   cudaError_t e0 = smem_optin(reinterpret_cast<const void*>(fn), Cfg::kSmem, dev, optin);
   if (e0 != cudaSuccess) return e0;
   const int grid = (int)std::min<int64_t>(ntiles, (int64_t)MINB * sm_count(dev));
-  if (ctr) {  // per-launch tile counter (stream-ordered reset; capturable in graphs)
-    cudaError_t e = cudaMemsetAsync(ctr, 0, sizeof(unsigned long long), s);
-    if (e != cudaSuccess) return e;
-  }
   fn<<<grid, kThreads, Cfg::kSmem, s>>>(lb, ntiles, P, status, ctr);
   return cudaGetLastError();
 }

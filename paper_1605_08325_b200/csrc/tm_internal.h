@@ -66,8 +66,9 @@ cudaError_t launch_exchange(const ExchangeArgs& a, int nlocal, bool wire16, int 
 // of each element from the k buffers, fused rn16 (q16) / ascending-rank sum /
 // (1/k) / rn16, push the result to all k buffers.  Also AR when all ranks are
 // local (q16 = false).
-// tile_ctr: device counter for dynamic tile claiming (reset by the launch), or
-// null for the static tile assignment.
+// tile_ctr: two zero-initialised device words for dynamic tile claiming (the
+// kernel's last CTA resets them: no memset node per launch), or null for the
+// static tile assignment.
 cudaError_t launch_direct(float* const* bufs, int k, int64_t P, bool q16, bool sum,
                           uint32_t* status, unsigned long long* tile_ctr, cudaStream_t s);
 
@@ -104,8 +105,8 @@ struct BspBufs {
   const float* g[TM_MAX_RANKS];
   float lr, mu;
 };
-// tile_ctr: device counter for the TMA kernel's dynamic tile claiming (reset
-// by the launch); null selects the register kernel.
+// tile_ctr: as for launch_direct (two self-resetting words); null selects the
+// register kernel.
 cudaError_t launch_bsp_direct(const BspBufs& bb, int k, int64_t P, bool q16, bool mom,
                               uint32_t* status, unsigned long long* tile_ctr, cudaStream_t s);
 cudaError_t launch_sgd(float* w, float* v, const float* g, int64_t n, float lr, float mu,

@@ -369,7 +369,11 @@ int tm_exchange_init(int64_t nparams, const tm_world* world, int strategy) {
     // pattern (bulk copies from IPC-mapped peer memory are validated here only
     // on one device).  TM_STAGED_KERNEL=reg|tma|ws overrides
     // (TM_STAGED_LDG=1 / TM_STAGED_TMA=1 are accepted too).
-    c.staged_kernel = c.nprocs == 1 ? tmx::kStagedTma : tmx::kStagedWs;
+    // Small segments (L <= 64 Ki elements): the register kernel, whose phases
+    // have no bulk-copy round trips to drain (measured 6-16 us vs 15-22 us for the
+    // TMA / warp-specialised kernels at k = 8, P <= 256 Ki; profiles/r01/latency_flavours.txt).
+    c.staged_kernel = c.L <= (int64_t)1 << 16 ? tmx::kStagedReg
+                      : (c.nprocs == 1 ? tmx::kStagedTma : tmx::kStagedWs);
     const char* sk = getenv("TM_STAGED_KERNEL");
     const char* ldg = getenv("TM_STAGED_LDG");
     const char* tma = getenv("TM_STAGED_TMA");
@@ -401,7 +405,7 @@ int tm_exchange_init(int64_t nparams, const tm_world* world, int strategy) {
   } else {
     c.rank_stride = 0;
   }
-  c.slab_bytes = c.rank_stride * c.nlocal + 256;  // + status word (+0) and direct tile counter (+64)
+  c.slab_bytes = c.rank_stride * c.nlocal + 256;  // + status word (+0), tile claim / retire counters (+64, +72)
   e = cudaMalloc(reinterpret_cast<void**>(&c.slab), c.slab_bytes);
   if (e != cudaSuccess) return cuda_fail("cudaMalloc", e);
   e = cudaMemset(c.slab, 0, c.slab_bytes);

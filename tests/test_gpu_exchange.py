@@ -387,3 +387,13 @@ def test_phase_log_does_not_change_results(path):
     st = log.cpu().numpy().reshape(-1, 8)[:, :6]
     if path == "staged":
         assert np.all(st[:, 0] > 0) and np.all(np.diff(st[:, [0, 1, 2, 3, 4, 5]], axis=1) >= 0)
+
+
+def test_default_staged_flavour_by_segment_length(monkeypatch):
+    """Without TM_STAGED_KERNEL: the register kernel for segments of <= 64 Ki
+    elements (latency-bound), the TMA-engine kernel above that in a
+    single-process group."""
+    monkeypatch.delenv("TM_STAGED_KERNEL", raising=False)
+    for P, k, want in ((100_003, 2, 0), (131_072 * 8, 8, 1), (65_536 * 4, 4, 0), (1_000_003, 2, 1)):
+        with tm.Exchanger(P, "asa16", size=k, nlocal=k, path="staged") as ex:
+            assert ex.layout()["staged_kernel"] == want, (P, k)

@@ -59,7 +59,7 @@ KERNEL_ID = {"reg": 0, "tma": 1, "ws": 2}
                                                   ("asa", 3, "range", "reg")])
 def test_multiprocess_bitwise(tmp_path, strategy, k, op, kernel):
     P = 100_003
-    env = None if kernel == "ws" else {"TM_STAGED_KERNEL": kernel}
+    env = {"TM_STAGED_KERNEL": kernel}
     res = launch(tmp_path, k, strategy, P, "D2", mode=("normal" if op == "avg" else op), extra_env=env)
     for r in range(k):
         assert res[r]["layout"]["staged_kernel"] == KERNEL_ID[kernel]
@@ -82,7 +82,7 @@ def test_multiprocess_bsp_fused_bitwise(tmp_path, strategy, k, mode, kernel):
     staged kernel's pre-cast; two iterations vs oracle/bsp.py."""
     from oracle.bsp import bsp_iteration
     P = 100_003
-    env = None if kernel == "ws" else {"TM_STAGED_KERNEL": kernel}
+    env = {"TM_STAGED_KERNEL": kernel}
     res = launch(tmp_path, k, strategy, P, "D2", mode=mode, extra_env=env)
     W = [worker_buffer(P, "D2", r, config=50) for r in range(k)]
     V = [worker_buffer(P, "D4", r, config=52) for r in range(k)]
@@ -102,9 +102,7 @@ def test_multiprocess_copy_engine_allgather(tmp_path, strategy, k, mode, kernel)
     """TM_ALLGATHER=ce across processes: the copy engines pull the peers' averaged
     segments through the IPC mappings (the NVLink copy path on a multi-GPU box)."""
     P = 100_003
-    env = {"TM_ALLGATHER": "ce"}
-    if kernel != "ws":
-        env["TM_STAGED_KERNEL"] = kernel
+    env = {"TM_ALLGATHER": "ce", "TM_STAGED_KERNEL": kernel}
     res = launch(tmp_path, k, strategy, P, "D2", mode=mode, extra_env=env)
     for r in range(k):
         assert res[r]["code"] == 0, res[r]
@@ -203,7 +201,7 @@ def test_multiprocess_stress_random_delays(tmp_path, strategy, kernel):
     host delay on half of them: every rank ends bitwise at the oracle's sequence."""
     from mp_worker import STRESS_ITERS
     P, k = 50_003, 2
-    env = None if kernel == "ws" else {"TM_STAGED_KERNEL": kernel}
+    env = {"TM_STAGED_KERNEL": kernel}
     res = launch(tmp_path, k, strategy, P, "D2", mode="stress", extra_env=env, timeout=600)
     X = [worker_buffer(P, "D2", r, config=50) for r in range(k)]
     for it in range(STRESS_ITERS):

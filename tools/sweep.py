@@ -41,10 +41,20 @@ def timeit(fn, min_ms=60.0, warmup=5, graph=False):
     for _ in range(warmup):
         fn()
     torch.cuda.synchronize()
+    inner = 1
     if graph:  # replay a captured call: no host launch overhead in the timing
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        fn()
+        e1.record()
+        torch.cuda.synchronize()
+        # short calls: capture `inner` back-to-back calls per graph, so the GPU is
+        # never starved by the host's replay rate (~2 us per replay)
+        inner = 64 if e0.elapsed_time(e1) < 0.2 else 1
         g = torch.cuda.CUDAGraph()
         with torch.cuda.graph(g):
-            fn()
+            for _ in range(inner):
+                fn()
         fn = g.replay
         fn()
         torch.cuda.synchronize()
@@ -60,7 +70,7 @@ def timeit(fn, min_ms=60.0, warmup=5, graph=False):
         fn()
     e1.record()
     torch.cuda.synchronize()
-    return e0.elapsed_time(e1) / n
+    return e0.elapsed_time(e1) / (n * inner)
 
 
 def hbm_bytes(strategy, P, k, path):
