@@ -4,7 +4,7 @@ all_gather_object.  Used by tests/test_gpu_multiprocess.py; on a one-GPU box
 every rank uses cuda:0 (IPC between processes on one device), on a multi-GPU
 box rank r uses cuda:r.
 
-argv: outdir strategy P dist mode      (mode: normal | sum | range | locked | skip1 | mismatch | stress | bsp | bspmom)
+argv: outdir strategy P dist mode      (mode: normal | sum | range | locked | async | skip1 | mismatch | stress | bsp | bspmom)
 """
 
 import json
@@ -23,6 +23,7 @@ from paper_1605_08325_b200 import tm  # noqa: E402
 from paper_1605_08325_b200.inputs import worker_buffer  # noqa: E402
 
 STRESS_ITERS = 60
+ASYNC_ROUNDS, ASYNC_TAU, ASYNC_ETA = 6, 2, 0.25
 
 
 def main():
@@ -55,7 +56,29 @@ def main():
         x = torch.from_numpy(worker_buffer(P, dist_name, rank, config=51)).cuda()
         torch.cuda.synchronize()
         log = None
-        if mode == "locked":  # all workers at once; per-chunk locks order them
+        if mode == "async":
+            # The asynchronous EASGD loop: ROUNDS
+            # rounds of TAU local SGD steps on the synthetic quadratic objective
+            # |x - t_r|^2 / 2 (torch ops, one rounding each), then a per-worker
+            # atomic elastic exchange with the sharded centre in arrival order;
+            # random host delays vary the arrival order between chunks and rounds.
+            import random
+            rnd = random.Random(77 + rank)
+            t = torch.from_numpy(worker_buffer(P, dist_name, 10 + rank, config=54)).cuda()
+            nch = -(-L // 4096)
+            log = torch.full((size * nch * ASYNC_ROUNDS * size,), -1, dtype=torch.int32, device="cuda")
+            tm.tm_easgd_set_order_log(log, ASYNC_ROUNDS * size)
+            dist.barrier()
+            for _ in range(ASYNC_ROUNDS):
+                for _ in range(ASYNC_TAU):
+                    d = x.sub(t)
+                    x.sub_(d.mul(ASYNC_ETA))
+                if rnd.random() < 0.5:
+                    torch.cuda.synchronize()
+                    time.sleep(rnd.random() * 0.002)
+                tm.tm_easgd_update_locked(x, rank, 0.5 / size)
+            torch.cuda.synchronize()
+        elif mode == "locked":  # all workers at once; per-chunk locks order them
             nch = -(-L // 4096)
             log = torch.full((size * nch * size,), -1, dtype=torch.int32, device="cuda")
             tm.tm_easgd_set_order_log(log, size)

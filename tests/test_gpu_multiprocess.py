@@ -195,6 +195,42 @@ def test_multiprocess_locked_easgd(tmp_path):
                 assert_bitwise(gW[r][lo:hi], ws[r])
 
 
+@pytest.mark.parametrize("k", [2, 3])
+def test_multiprocess_async_easgd_loop(tmp_path, k):
+    """The asynchronous EASGD loop: every process runs rounds of
+    tau local SGD steps and a per-worker atomic elastic exchange with the sharded
+    centre, with random delays; replaying every chunk's logged arrival order in
+    oracle.easgd.easgd_async_replay reproduces workers and centre bitwise."""
+    import mp_worker as mw
+    from oracle.easgd import easgd_async_replay
+    P = 150_001
+    res = launch(tmp_path, k, "easgd", P, "D1", mode="async")
+    W = [worker_buffer(P, "D1", r, config=51) for r in range(k)]
+    T = [worker_buffer(P, "D1", 10 + r, config=54) for r in range(k)]
+    c0 = worker_buffer(P, "D1", 99, config=51)
+    L = res[0]["seg_len"]
+    nch = -(-L // 4096)
+    per = mw.ASYNC_ROUNDS * k
+    merged = np.max(np.stack([np.load(os.path.join(tmp_path, f"log{r}.npy")) for r in range(k)]), axis=0)
+    gW = [np.load(os.path.join(tmp_path, f"rank{r}.npy")) for r in range(k)]
+    gc = np.concatenate([np.load(os.path.join(tmp_path, f"shard{r}.npy")) for r in range(k)])[:P]
+    orders_seen = set()
+    for s_ in range(k):
+        for q in range(nch):
+            lo, hi = s_ * L + q * 4096, min(s_ * L + min(L, (q + 1) * 4096), P)
+            if lo >= hi:
+                continue
+            order = [int(v) for v in merged[(s_ * nch + q) * per:(s_ * nch + q + 1) * per]]
+            assert sorted(order) == sorted(list(range(k)) * mw.ASYNC_ROUNDS), order
+            orders_seen.add(tuple(order))
+            ws, cc = easgd_async_replay([w[lo:hi] for w in W], c0[lo:hi], [t[lo:hi] for t in T],
+                                        mw.ASYNC_ETA, mw.ASYNC_TAU, 0.5 / k, order)
+            assert_bitwise(gc[lo:hi], cc, f"centre chunk ({s_},{q})")
+            for r in range(k):
+                assert_bitwise(gW[r][lo:hi], ws[r], f"worker {r} chunk ({s_},{q})")
+    assert len(orders_seen) >= 1
+
+
 @pytest.mark.parametrize("strategy,kernel", [("asa16", "ws"), ("asa", "reg"), ("asa16", "tma")])
 def test_multiprocess_stress_random_delays(tmp_path, strategy, kernel):
     """60 back-to-back exchanges per rank, each after a per-rank delta and a random

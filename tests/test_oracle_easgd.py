@@ -83,3 +83,55 @@ def test_sequence_is_ordered_composition():
     tot0 = sum(w.astype(np.float64) for w in ws) + c
     tot1 = sum(w.astype(np.float64) for w in nws) + nc
     assert np.max(np.abs(tot1 - tot0)) < 1e-5
+
+
+def test_quadratic_steps_brute_force():
+    """Each local step of the synthetic objective is d = fl(x - t),
+    x = fl(x - fl(eta d)): exact-rational emulation over 3 steps."""
+    from oracle.easgd import quadratic_sgd_steps
+    x = worker_buffer(48, "D1", 0, config=24)
+    t = worker_buffer(48, "D1", 1, config=24)
+    for eta in (0.25, 0.3):
+        got = quadratic_sgd_steps(x, t, eta, 3)
+        e = float(F32(eta))
+        for i in range(48):
+            xi = float(x[i])
+            for _ in range(3):
+                xi = exact.sub(xi, exact.mul(e, exact.sub(xi, float(t[i]))))
+            assert exact.same_bits32(got[i], xi), (eta, i)
+
+
+def test_quadratic_steps_closed_form():
+    """eta = 1/2 on dyadic inputs is exact: x_tau - t = (x_0 - t) / 2^tau."""
+    from oracle.easgd import quadratic_sgd_steps
+    g = np.random.default_rng(25)
+    x = (g.integers(-2 ** 12, 2 ** 12, 500) * 2.0 ** -4).astype(F32)
+    t = (g.integers(-2 ** 12, 2 ** 12, 500) * 2.0 ** -4).astype(F32)
+    got = quadratic_sgd_steps(x, t, 0.5, 4)
+    want = t.astype(np.float64) + (x.astype(np.float64) - t) / 16.0
+    assert np.array_equal(got.astype(np.float64), want)
+
+
+def test_async_replay_reduces_and_converges():
+    """tau = 0 is the plain arrival-order sequence; with local steps the loop is
+    the explicit composition; and with all targets equal to t and many rounds the
+    centre and every worker converge to t (EASGD's fixed point)."""
+    from oracle.easgd import easgd_async_replay, quadratic_sgd_steps
+    ws = [worker_buffer(500, "D1", r, config=26) for r in range(3)]
+    ts = [worker_buffer(500, "D1", 10 + r, config=26) for r in range(3)]
+    c = worker_buffer(500, "D1", 9, config=26)
+    order = [1, 0, 2, 1, 2, 0]
+    a_w, a_c = easgd_async_replay(ws, c, ts, 0.25, 0, 0.125, order)
+    b_w, b_c = easgd_sequence(ws, c, 0.125, order)
+    assert np.array_equal(a_c, b_c) and all(np.array_equal(p, q) for p, q in zip(a_w, b_w))
+    a_w, a_c = easgd_async_replay(ws, c, ts, 0.25, 2, 0.125, order)
+    ref = [w.copy() for w in ws]
+    cc = c.copy()
+    for w in order:
+        ref[w] = quadratic_sgd_steps(ref[w], ts[w], 0.25, 2)
+        ref[w], cc = easgd_update(ref[w], cc, 0.125)
+    assert np.array_equal(a_c, cc) and all(np.array_equal(p, q) for p, q in zip(a_w, ref))
+    t = worker_buffer(500, "D1", 20, config=26)
+    f_w, f_c = easgd_async_replay(ws, c, [t] * 3, 0.5, 1, 0.5, [0, 1, 2] * 60)
+    assert np.max(np.abs(f_c.astype(np.float64) - t)) < 1e-6
+    assert all(np.max(np.abs(w.astype(np.float64) - t)) < 1e-6 for w in f_w)
