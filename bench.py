@@ -48,6 +48,8 @@ def parse():
     ap.add_argument("--k", type=int, default=8, help="ranks simulated on one GPU when --gpus 1")
     ap.add_argument("--dist", default="D2")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-nccl-compare", action="store_true",
+                    help="multi-GPU: skip timing NCCL's allreduce of the same buffer")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=5)
     ap.add_argument("--e2e-chunks", type=int, default=16,
@@ -423,6 +425,29 @@ def main():
                   "roofline": roofline(args.strategy, P, k, "staged", sms, peak, peak_src, args.workload)}
         tm.tm_set_path(path)
 
+    # context on a multi-GPU run: NCCL's own fp32 allreduce (the paper's AR
+    # baseline) of the same buffer, same timing method
+    nccl_ar = None
+    if multi and backend == "nccl" and not args.no_nccl_compare:
+        try:
+            ref = bufs[0].clone()
+            for _ in range(args.warmup):
+                dist.all_reduce(ref)
+            dist.barrier()
+            torch.cuda.synchronize()
+            h0, h1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            h0.record(stream)
+            for _ in range(args.steps):
+                dist.all_reduce(ref)
+            h1.record(stream)
+            torch.cuda.synchronize()
+            ams = reduce_max(h0.elapsed_time(h1) / args.steps, dev)
+            nccl_ar = {"ms_per_step": ams, "algbw_GBps": 4.0 * P / (ams * 1e-3) / 1e9,
+                       "what": "torch.distributed.all_reduce (NCCL, fp32 sum) of the same P floats"}
+            del ref
+        except Exception as e:  # context only: never fail the bench line
+            nccl_ar = {"error": str(e)[:200]}
+
     # end to end through the public API with host buffers
     e2e = None
     if not args.no_e2e:
@@ -499,6 +524,7 @@ def main():
             "gpu_launches": args.steps,
             "staged_path_one_gpu": staged,
             "nvlink_counters": nvlink,
+            "nccl_allreduce_same_buffer": nccl_ar,
             "clocks": clk.summary(),
             "e2e": e2e,
             "status": code,
