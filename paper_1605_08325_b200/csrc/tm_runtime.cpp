@@ -13,6 +13,7 @@
 #include <cuda_runtime.h>
 #include <dlfcn.h>
 #include <nccl.h>
+#include <nvtx3/nvToolsExt.h>  // header-only; ranges are no-ops unless a tool (nsys) is attached
 #include <stdio.h>
 #include <stdlib.h>
 #include <string.h>
@@ -27,6 +28,13 @@
 namespace {
 
 using tmx::ExchangeArgs;
+
+// Host-side NVTX range around each enqueueing call (the exchange
+// appears as a named range on nsys timelines next to its kernels).
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+};
 
 constexpr uint32_t kMagic = 0x544d4558u;  // "TMEX"
 constexpr uint32_t kVersion = 2;
@@ -312,6 +320,7 @@ extern "C" {
 
 int tm_bsp_step(float* w, float* v, const float* grad, float lr, float mu,
                            int exchange_momentum, void* stream) {
+  NvtxRange nvtx("tm_bsp_step");
   std::lock_guard<std::mutex> lk(g_mu);
   if (g.inited && g.nlocal != 1) return TM_E_STATE;
   float* ws[1] = {w};
@@ -323,6 +332,7 @@ int tm_bsp_step(float* w, float* v, const float* grad, float lr, float mu,
 int tm_bsp_step_group(float* const* w, float* const* v, const float* const* grad,
                                  int nbufs, float lr, float mu, int exchange_momentum,
                                  void* stream) {
+  NvtxRange nvtx("tm_bsp_step_group");
   std::lock_guard<std::mutex> lk(g_mu);
   return do_bsp(w, v, grad, nbufs, lr, mu, exchange_momentum, static_cast<cudaStream_t>(stream));
 }
@@ -507,6 +517,7 @@ int tm_bootstrap_import(const void* blobs, size_t len_each) {
 }
 
 int tm_exchange(float* dev_buf, void* stream) {
+  NvtxRange nvtx("tm_exchange");
   std::lock_guard<std::mutex> lk(g_mu);
   if (g.inited && g.nlocal != 1) return TM_E_STATE;
   float* bufs[1] = {dev_buf};
@@ -514,11 +525,13 @@ int tm_exchange(float* dev_buf, void* stream) {
 }
 
 int tm_exchange_group(float* const* dev_bufs, int nbufs, void* stream) {
+  NvtxRange nvtx("tm_exchange_group");
   std::lock_guard<std::mutex> lk(g_mu);
   return do_exchange(dev_bufs, nbufs, 0, g.P, static_cast<cudaStream_t>(stream));
 }
 
 int tm_exchange_range(float* dev_buf, int64_t offset, int64_t count, void* stream) {
+  NvtxRange nvtx("tm_exchange_range");
   std::lock_guard<std::mutex> lk(g_mu);
   if (g.inited && g.nlocal != 1) return TM_E_STATE;
   float* bufs[1] = {dev_buf};
@@ -527,6 +540,7 @@ int tm_exchange_range(float* dev_buf, int64_t offset, int64_t count, void* strea
 
 int tm_exchange_group_range(float* const* dev_bufs, int nbufs, int64_t offset, int64_t count,
                             void* stream) {
+  NvtxRange nvtx("tm_exchange_group_range");
   std::lock_guard<std::mutex> lk(g_mu);
   return do_exchange(dev_bufs, nbufs, offset, count, static_cast<cudaStream_t>(stream));
 }
@@ -543,6 +557,7 @@ int tm_easgd_update(float* worker_buf, float* center_buf, float alpha, void* str
 
 int tm_easgd_update_ex(float* worker_buf, float* center_buf, int64_t n, float alpha,
                        int concurrent, void* stream) {
+  NvtxRange nvtx("tm_easgd_update_ex");
   if (!worker_buf || !center_buf || n < 0) return TM_E_ARG;
   if (n == 0) return TM_OK;
   if ((reinterpret_cast<uintptr_t>(worker_buf) | reinterpret_cast<uintptr_t>(center_buf)) & 3)
@@ -554,6 +569,7 @@ int tm_easgd_update_ex(float* worker_buf, float* center_buf, int64_t n, float al
 
 int tm_easgd_round(float* const* workers, int nworkers, const int32_t* order, int norder,
                    float* center_buf, int64_t n, float alpha, void* stream) {
+  NvtxRange nvtx("tm_easgd_round");
   if (!workers || !order || !center_buf || n < 0 || nworkers < 1 || nworkers > 16 ||
       norder < 0 || norder > 64)
     return TM_E_ARG;
@@ -578,6 +594,7 @@ int tm_easgd_center(int owner_rank, float** center) {
 }
 
 int tm_easgd_update_sharded(float* worker_buf, float alpha, int concurrent, void* stream) {
+  NvtxRange nvtx("tm_easgd_update_sharded");
   tmx::ShardArgs sa{};
   {
     std::lock_guard<std::mutex> lk(g_mu);
@@ -599,6 +616,7 @@ int tm_easgd_update_sharded(float* worker_buf, float alpha, int concurrent, void
 }
 
 int tm_easgd_update_locked(float* worker_buf, int worker_id, float alpha, void* stream) {
+  NvtxRange nvtx("tm_easgd_update_locked");
   tmx::ShardArgs sa{};
   {
     std::lock_guard<std::mutex> lk(g_mu);
