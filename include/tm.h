@@ -235,6 +235,8 @@ int tm_easgd_update(float* worker_buf, float* center_buf, float alpha, void* str
 /* Extended form: explicit length n, and concurrent != 0 applies the centre
  * update with an atomic add (red.global.add.f32, system scope) so several
  * workers may update one centre at once (no lost updates; order not fixed).
+ * The float atomic flushes fp32-subnormal operands and results of the centre's
+ * add to signed zero (hardware semantics), unlike the exclusive update.
  * Does not need tm_exchange_init. */
 int tm_easgd_update_ex(float* worker_buf, float* center_buf, int64_t n, float alpha,
                        int concurrent, void* stream);

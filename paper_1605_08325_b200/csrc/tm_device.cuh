@@ -293,5 +293,18 @@ __device__ __forceinline__ void red_add_gpu(float* p, float v) {
   asm volatile("red.relaxed.gpu.global.add.f32 [%0], %1;" ::"l"(p), "f"(v) : "memory");
 }
 
+// Four independent fp32 atomic adds in one instruction (sm_90+ vector red; each
+// element's add is atomic on its own, exactly as four scalar reds).  p 16-B aligned.
+__device__ __forceinline__ void red_add4_sys(float* p, float4 v) {
+  asm volatile("red.relaxed.sys.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(p), "f"(v.x), "f"(v.y),
+               "f"(v.z), "f"(v.w)
+               : "memory");
+}
+__device__ __forceinline__ void red_add4_gpu(float* p, float4 v) {
+  asm volatile("red.relaxed.gpu.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(p), "f"(v.x), "f"(v.y),
+               "f"(v.z), "f"(v.w)
+               : "memory");
+}
+
 }  // namespace dev
 }  // namespace tmx

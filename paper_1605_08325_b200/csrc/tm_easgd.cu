@@ -38,9 +38,7 @@ easgd_kernel(float* __restrict__ x, float* c, int64_t n, float alpha, int vec) {
       xv.z = __fsub_rn(xv.z, ez); xv.w = __fsub_rn(xv.w, ew);
       st16_f(x + v * 4, xv);
       if (Concurrent) {
-        float* cp = c + v * 4;
-        red_add_sys(cp, ex); red_add_sys(cp + 1, ey);
-        red_add_sys(cp + 2, ez); red_add_sys(cp + 3, ew);
+        red_add4_sys(c + v * 4, make_float4(ex, ey, ez, ew));
       } else {
         cv.x = __fadd_rn(cv.x, ex); cv.y = __fadd_rn(cv.y, ey);
         cv.z = __fadd_rn(cv.z, ez); cv.w = __fadd_rn(cv.w, ew);
@@ -85,9 +83,8 @@ easgd_sharded_kernel(float* __restrict__ x, const __grid_constant__ ShardArgs sa
       xv.z = __fsub_rn(xv.z, ez); xv.w = __fsub_rn(xv.w, ew);
       st16_f(xs + v * 4, xv);
       if (Concurrent) {
-        float* cp = c + v * 4;
-        if (SYS) { red_add_sys(cp, ex); red_add_sys(cp + 1, ey); red_add_sys(cp + 2, ez); red_add_sys(cp + 3, ew); }
-        else { red_add_gpu(cp, ex); red_add_gpu(cp + 1, ey); red_add_gpu(cp + 2, ez); red_add_gpu(cp + 3, ew); }
+        if (SYS) red_add4_sys(c + v * 4, make_float4(ex, ey, ez, ew));
+        else red_add4_gpu(c + v * 4, make_float4(ex, ey, ez, ew));
       } else {
         cv.x = __fadd_rn(cv.x, ex); cv.y = __fadd_rn(cv.y, ey);
         cv.z = __fadd_rn(cv.z, ez); cv.w = __fadd_rn(cv.w, ew);

@@ -256,3 +256,23 @@ def test_fused_round_full_size_sampled():
     assert_bitwise(cd[ti].cpu().numpy(), wc, "centre")
     for r in range(nw):
         assert_bitwise(Wd[r][ti].cpu().numpy(), wW[r], f"worker {r}")
+
+
+def test_concurrent_mode_flushes_subnormals():
+    """Concurrent mode adds e to the centre with the hardware float atomic
+    (red.add.f32), which flushes subnormal inputs and results to signed zero (PTX
+    ISA, atom/red .add.f32).  Exclusive mode keeps gradual underflow (reading Q6).
+    Pinned so the documented difference stays true: elements whose e or c' is an
+    fp32 subnormal differ; everything else is bitwise the exclusive update."""
+    n = 4096
+    x = worker_buffer(n, "D1", 0, config=46)
+    c = worker_buffer(n, "D1", 1, config=46)
+    x[:8] = np.float32(1e-39)  # d, e subnormal; c' = 0 + e subnormal
+    c[:8] = np.float32(0.0)
+    xd, cd = to_dev([x, c])
+    tm.tm_easgd_update_ex(xd, cd, 0.5, concurrent=True)
+    gx, gc = to_host([xd, cd])
+    wx, wc = easgd_update(x, c, 0.5)
+    assert_bitwise(gx, wx)  # the worker side is plain IEEE arithmetic
+    assert np.all(gc[:8] == 0) and np.all(wc[:8] != 0)
+    assert_bitwise(gc[8:], wc[8:])
