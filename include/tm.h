@@ -127,7 +127,8 @@ typedef struct {
   int64_t lib_bytes;     /* device bytes the library owns in this process     */
   uint32_t epoch;        /* number of staged exchanges issued so far          */
   int32_t path;          /* effective tm_path of the next exchange            */
-  int32_t staged_kernel; /* staged flavour: 0 register, 1 TMA engine, 2 warp-specialised */
+  int32_t staged_kernel; /* staged flavour: 0 register, 1 TMA engine, 2 warp-specialised,
+                            3 warp-specialised on the TMA engine */
   int32_t allgather;     /* tm_allgather mode of the staged path                */
 } tm_layout_info;
 

@@ -174,8 +174,9 @@ tm_bsp_tma_kernel(const __grid_constant__ BspBufs bb, int64_t ntiles, int64_t P,
   constexpr int T = C::kTile;
   extern __shared__ __align__(128) unsigned char smem[];
   float* ring = reinterpret_cast<float*>(smem);              // [S][3][K][T]
-  __shared__ __align__(8) uint64_t full[S];
-  __shared__ int64_t slot_tile[S];
+  __shared__ __align__(16) uint64_t full[kMaxStages];
+  __shared__ int64_t slot_tile[kMaxStages];
+  static_assert(S <= kMaxStages, "ring depth");
   const int tid = threadIdx.x;
 
   auto issue = [&](int64_t i) {  // thread 0: claim a tile for ring use i

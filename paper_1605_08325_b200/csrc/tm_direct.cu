@@ -138,8 +138,9 @@ tm_direct_tma_kernel(const __grid_constant__ LocalBufs lb, int64_t ntiles, int64
   extern __shared__ __align__(128) unsigned char smem[];
   float* ring = reinterpret_cast<float*>(smem);                  // [S][K][TILE]
   float* outr = ring + (size_t)S * K * TILE;                     // [kOutRing][TILE]
-  __shared__ __align__(8) uint64_t full[S];
-  __shared__ int64_t slot_tile[S];  // tile held by each ring slot, -1 = none left
+  __shared__ __align__(16) uint64_t full[kMaxStages];
+  __shared__ int64_t slot_tile[kMaxStages];  // tile held by each ring slot, -1 = none left
+  static_assert(S <= kMaxStages, "ring depth");
 
   const int tid = threadIdx.x;
   // Tiles are claimed dynamically from a per-launch counter (work stealing), so

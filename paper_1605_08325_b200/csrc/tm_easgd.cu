@@ -302,12 +302,16 @@ easgd_round_distinct_kernel(const __grid_constant__ OrderedWorkers ow, float* c,
 // thread runs the chain on one float4; the N + 1 result tiles go to an output
 // slot and are bulk-stored.  72 B per element for N = 8, each byte once.
 constexpr int kRoundTile = 4 * kThreads;  // one float4 per thread
+// Ring depth: the largest power of two (<= 8) whose slots fit 216 KB beside the
+// two output slots.  Non-power-of-two depths (3, 5, 7) ran correctly but every
+// mbarrier wait was reported "missing init" by compute-sanitizer synccheck (with
+// racecheck hazards following from it); power-of-two depths are clean.
 template <int N>
 struct RoundTma {
   static constexpr uint32_t kTB = kRoundTile * 4;
   static constexpr int kIn = (N + 1) * (int)kTB;
-  static constexpr int kRaw = (112 * 1024) / kIn;
-  static constexpr int kStages = kRaw > 8 ? 8 : (kRaw < 2 ? 2 : kRaw);
+  static constexpr int kFit = (216 * 1024 - 2 * kIn) / kIn;
+  static constexpr int kStages = kFit >= 8 ? 8 : kFit >= 4 ? 4 : 2;
   static constexpr int kOutSlots = 2;
   static constexpr int kSmem = kStages * kIn + kOutSlots * kIn;
 };
@@ -323,6 +327,7 @@ easgd_round_tma_kernel(const __grid_constant__ OrderedWorkers ow, float* c, int6
   float* ring = reinterpret_cast<float*>(smem);            // [S][N + 1][T]: centre, workers
   float* outr = ring + (size_t)S * (N + 1) * T;             // [kOutSlots][N + 1][T]
   __shared__ __align__(8) uint64_t full[S];
+  const uint32_t fb = smem_u32(&full[0]);  // one address computation for every barrier op
   const int tid = threadIdx.x;
   const int64_t my = ntiles > blockIdx.x ? (ntiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
   // thread 0 issues the N + 1 copies of a tile (measured 0.705 ms vs 0.711 ms with
@@ -331,14 +336,14 @@ easgd_round_tma_kernel(const __grid_constant__ OrderedWorkers ow, float* c, int6
   auto issue = [&](int64_t i) {
     const int s = (int)(i % S);
     const int64_t t = blockIdx.x + i * gridDim.x;
-    mbar_expect_tx(&full[s], (N + 1) * R::kTB);
+    mbar_expect_tx_a(fb + 8 * s, (N + 1) * R::kTB);
 #pragma unroll
     for (int q = 0; q <= N; ++q)
-      bulk_load(ring + ((size_t)s * (N + 1) + q) * T, (q == 0 ? c : ow.wo[q - 1]) + t * T, R::kTB,
-                &full[s]);
+      bulk_load_a(ring + ((size_t)s * (N + 1) + q) * T, (q == 0 ? c : ow.wo[q - 1]) + t * T, R::kTB,
+                  fb + 8 * s);
   };
   if (tid == 0) {
-    for (int s = 0; s < S; ++s) mbar_init(&full[s], 1);
+    for (int s = 0; s < S; ++s) mbar_init_a(fb + 8 * s, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
@@ -347,7 +352,7 @@ easgd_round_tma_kernel(const __grid_constant__ OrderedWorkers ow, float* c, int6
   for (int64_t i = 0; i < my; ++i) {
     const int s = (int)(i % S);
     const int64_t t = blockIdx.x + i * gridDim.x;
-    mbar_wait(&full[s], (uint32_t)((i / S) & 1));
+    mbar_wait_a(fb + 8 * s, (uint32_t)((i / S) & 1));
     const float* src = ring + (size_t)s * (N + 1) * T;
     float* out = outr + (size_t)(i % R::kOutSlots) * (N + 1) * T;
     float4 cv = reinterpret_cast<const float4*>(src)[tid];
@@ -376,21 +381,27 @@ easgd_round_tma_kernel(const __grid_constant__ OrderedWorkers ow, float* c, int6
 }
 
 template <int N>
+cudaError_t launch_round_tma(const OrderedWorkers& ow, float* c, int64_t n, int64_t ntiles, float alpha,
+                             cudaStream_t s) {
+  using R = RoundTma<N>;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  auto fn = easgd_round_tma_kernel<N>;
+  static std::atomic<uint64_t> optin{0};
+  cudaError_t e = smem_optin(reinterpret_cast<const void*>(fn), R::kSmem, dev, optin);
+  if (e != cudaSuccess) return e;
+  const int grid = (int)std::min<int64_t>(ntiles, sm_count(dev));
+  fn<<<grid, kThreads, R::kSmem, s>>>(ow, c, ntiles, n, alpha);
+  return cudaGetLastError();
+}
+
+template <int N>
 cudaError_t launch_round_distinct(const OrderedWorkers& ow, float* c, int64_t n, float alpha,
                                   cudaStream_t s) {
   static const bool force_ldg = env_int("TM_DIRECT_LDG", 0) == 1;  // diagnostics: register kernel
   const int64_t ntiles = n / kRoundTile;
   if (ntiles > 0 && !force_ldg) {
-    using R = RoundTma<N>;
-    int dev = 0;
-    cudaGetDevice(&dev);
-    auto fn = easgd_round_tma_kernel<N>;
-    static std::atomic<uint64_t> optin{0};
-    cudaError_t e = smem_optin(reinterpret_cast<const void*>(fn), R::kSmem, dev, optin);
-    if (e != cudaSuccess) return e;
-    const int grid = (int)std::min<int64_t>(ntiles, sm_count(dev));
-    fn<<<grid, kThreads, R::kSmem, s>>>(ow, c, ntiles, n, alpha);
-    return cudaGetLastError();
+    return launch_round_tma<N>(ow, c, n, ntiles, alpha, s);
   }
   easgd_round_distinct_kernel<N><<<streaming_grid(n / 4 + 4), kThreads, 0, s>>>(ow, c, n, alpha);
   return cudaGetLastError();

@@ -59,7 +59,7 @@ constexpr int kStampSlots = 8;
 enum { kStampStart = 0, kStampCast = 1, kStampReady = 2, kStampReduce = 3, kStampReduced = 4,
        kStampEnd = 5 };
 // Staged kernel flavours.
-enum StagedKernel { kStagedReg = 0, kStagedTma = 1, kStagedWs = 2 };
+enum StagedKernel { kStagedReg = 0, kStagedTma = 1, kStagedWs = 2, kStagedTmaWs = 3 };
 cudaError_t launch_exchange(const ExchangeArgs& a, int nlocal, bool wire16, int flavour, cudaStream_t s);
 
 // Single-process group, one pass (the "direct" path): pull the k contributions

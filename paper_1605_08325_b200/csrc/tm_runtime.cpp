@@ -374,16 +374,17 @@ int tm_exchange_init(int64_t nparams, const tm_world* world, int strategy) {
   if (strategy == TM_ASA || strategy == TM_ASA16) {
     // Staged kernel flavour.  Single-process groups: the TMA-engine kernel
     // (measured fastest on one GPU).  Across processes: the warp-specialised
-    // register kernel, whose pre-cast (HBM) overlaps the reduce-scatter pull
-    // (NVLink) and whose 16-byte peer loads are the established NVLink P2P
-    // pattern (bulk copies from IPC-mapped peer memory are validated here only
-    // on one device).  TM_STAGED_KERNEL=reg|tma|ws overrides
-    // (TM_STAGED_LDG=1 / TM_STAGED_TMA=1 are accepted too).
+    // TMA-engine kernel, whose pre-cast (HBM) overlaps the reduce-scatter pull
+    // (NVLink) sub-chunk by sub-chunk, both fed by bulk copies; on one GPU it
+    // measures as the TMA kernel (0.982 vs 0.984 ms at AlexNet k = 8) and ahead
+    // of the register warp-specialised kernel (1.248 ms).
+    // TM_STAGED_KERNEL=reg|tma|ws|tmaws overrides (TM_STAGED_LDG=1 /
+    // TM_STAGED_TMA=1 are accepted too).
     // Small segments (L <= 64 Ki elements): the register kernel, whose phases
     // have no bulk-copy round trips to drain (measured 6-16 us vs 15-22 us for the
     // TMA / warp-specialised kernels at k = 8, P <= 256 Ki; profiles/r01/latency_flavours.txt).
     c.staged_kernel = c.L <= (int64_t)1 << 16 ? tmx::kStagedReg
-                      : (c.nprocs == 1 ? tmx::kStagedTma : tmx::kStagedWs);
+                      : (c.nprocs == 1 ? tmx::kStagedTma : tmx::kStagedTmaWs);
     const char* sk = getenv("TM_STAGED_KERNEL");
     const char* ldg = getenv("TM_STAGED_LDG");
     const char* tma = getenv("TM_STAGED_TMA");
@@ -392,6 +393,7 @@ int tm_exchange_init(int64_t nparams, const tm_world* world, int strategy) {
     if (sk && !strcmp(sk, "reg")) c.staged_kernel = tmx::kStagedReg;
     if (sk && !strcmp(sk, "tma")) c.staged_kernel = tmx::kStagedTma;
     if (sk && !strcmp(sk, "ws")) c.staged_kernel = tmx::kStagedWs;
+    if (sk && !strcmp(sk, "tmaws")) c.staged_kernel = tmx::kStagedTmaWs;
     const char* ag = getenv("TM_ALLGATHER");  // sm | ce | nccl
     if (ag && !strcmp(ag, "ce")) c.ag_mode = TM_AG_CE;
     c.want_nccl_ag = ag && !strcmp(ag, "nccl") && c.nprocs > 1;

@@ -36,7 +36,7 @@ int exchange_max_ctas(int device, bool wire16, int k, int fl) {
   if (prepare(fn, fl) != cudaSuccess) return 0;
   int per_sm = 0;
   if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, flavour_threads(fl),
-                                                    fl == kStagedTma ? kTmaSmem : 0) != cudaSuccess)
+                                                    flavour_smem(fl)) != cudaSuccess)
     return 0;
   return per_sm * sm_count(device);
 }
@@ -53,7 +53,7 @@ cudaError_t launch_exchange(const ExchangeArgs& a, int nlocal, bool wire16, int 
   // Cooperative launch: guarantees every CTA is co-resident, which the
   // per-CTA flag barriers need when several ranks share this device.
   return cudaLaunchCooperativeKernel(fn, dim3(nlocal * a.C), dim3(flavour_threads(fl)), params,
-                                     fl == kStagedTma ? kTmaSmem : 0, s);
+                                     flavour_smem(fl), s);
 }
 
 }  // namespace tmx

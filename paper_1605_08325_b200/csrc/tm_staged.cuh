@@ -450,61 +450,295 @@ __device__ __forceinline__ void fence_proxy_async_global() {
   asm volatile("fence.proxy.async.global;" ::: "memory");
 }
 
-// Runs n_items through the rings.  issue(i, slot, bar) [thread 0] starts the
-// bulk loads of item i and arms `bar` with their byte count; compute(i, in, out)
-// [all threads] transforms; store(i, out) [thread 0] issues the bulk stores.
-// `use` / `outn` continue across phases so slot parities stay consistent.
-template <class IssueF, class ComputeF, class StoreF>
-__device__ __forceinline__ void tile_pipeline(int n_items, uint32_t& use, uint32_t& outn,
+// A group of NT threads that runs tile pipelines together: the whole CTA
+// (BAR = 0, __syncthreads) or half of it (named barrier BAR), with NIN input
+// slots of INB bytes and NOUT output slots of OUTB bytes.
+template <int NT, int BAR, int NIN, int NOUT, int INB, int OUTB>
+struct Grp {
+  static constexpr int kNT = NT, kNin = NIN, kNout = NOUT, kInB = INB, kOutB = OUTB;
+  __device__ static void sync() {
+    if constexpr (BAR == 0) __syncthreads();
+    else named_bar(BAR, NT);
+  }
+};
+using FullGrp = Grp<kTmaThreads, 0, kInSlots, kOutSlots, kSlotBytes, kSlotBytes>;
+
+// Runs n_items through the group's rings.  issue(i, slot, bar) [group thread 0]
+// starts the bulk loads of item i and arms `bar` with their byte count;
+// compute(i, in, out) [all group threads] transforms; store(i, out) [group
+// thread 0] issues the bulk stores.  `use` / `outn` continue across calls so
+// slot parities stay consistent.
+template <class G, class IssueF, class ComputeF, class StoreF>
+__device__ __forceinline__ void tile_pipeline(int gtid, int n_items, uint32_t& use, uint32_t& outn,
                                               char* in_ring, char* out_ring, uint64_t* full,
                                               IssueF issue, ComputeF compute, StoreF store) {
-  const int tid = threadIdx.x;
-  if (tid == 0) {
-    for (int i = 0; i < kInSlots && i < n_items; ++i) {
-      const uint32_t slot = (use + i) % kInSlots;
-      issue(i, in_ring + slot * kSlotBytes, &full[slot]);
+  if (gtid == 0) {
+    for (int i = 0; i < G::kNin && i < n_items; ++i) {
+      const uint32_t slot = (use + i) % G::kNin;
+      issue(i, in_ring + slot * G::kInB, &full[slot]);
     }
   }
   for (int i = 0; i < n_items; ++i) {
     const uint32_t u = use + i;
-    const uint32_t slot = u % kInSlots;
-    mbar_wait(&full[slot], (u / kInSlots) & 1);
-    char* out = out_ring + (outn % kOutSlots) * kSlotBytes;
-    compute(i, in_ring + slot * kSlotBytes, out);
-    fence_proxy_async_smem();                      // generic smem writes -> bulk store
-    if (tid == 0) bulk_wait_read<kOutSlots - 2>();  // out slot of item i+1 is free
-    __syncthreads();                               // every thread is done with slot / out
-    if (tid == 0) {
+    const uint32_t slot = u % G::kNin;
+    mbar_wait(&full[slot], (u / G::kNin) & 1);
+    char* out = out_ring + (outn % G::kNout) * G::kOutB;
+    compute(i, in_ring + slot * G::kInB, out);
+    fence_proxy_async_smem();                             // generic smem writes -> bulk store
+    if (gtid == 0) bulk_wait_read<G::kNout - 2>();        // out slot of item i+1 is free
+    G::sync();                                            // every thread is done with slot / out
+    if (gtid == 0) {
       store(i, out);
       bulk_commit();
-      if (i + kInSlots < n_items) issue(i + kInSlots, in_ring + slot * kSlotBytes, &full[slot]);
+      if (i + G::kNin < n_items) issue(i + G::kNin, in_ring + slot * G::kInB, &full[slot]);
     }
     ++outn;
   }
   use += n_items;
 }
 
-// Drain this CTA's bulk stores and order them before the generic-proxy release.
-__device__ __forceinline__ void drain_bulk_stores() {
-  if (threadIdx.x == 0) {
-    bulk_wait_all<0>();
-    fence_proxy_async_global();
-  }
+// Wait for this thread's bulk stores and order them before a generic-proxy release.
+__device__ __forceinline__ void drain_bulk_stores_thread() {
+  bulk_wait_all<0>();
+  fence_proxy_async_global();
+}
+
+// What the phases of one CTA need to know.
+struct PhaseCtx {
+  const ExchangeArgs* a;
+  int lr, r;
+  float* x;
+  int64_t P, L, P4;
+  char* stage_r;
+};
+
+// a2 on the TMA engine: pre-cast the chunk range [s0, s1) of all K segments into
+// the own stage.  Fused BSP step (SGD): the tile is TPS elements of w, v and g
+// (three bulk loads into one slot); v' goes back to v with register stores
+// (1.819 vs 1.835 ms for a second bulk store from the output slot), the wire
+// tile of w' = w + v' is bulk-stored as in the plain pre-cast.
+template <class G, int K, bool W16, bool SGD>
+__device__ __forceinline__ void precast_phase(const PhaseCtx& pc, int gtid, int64_t s0, int64_t s1,
+                                              uint32_t& use, uint32_t& outn, char* in_ring,
+                                              char* out_ring, uint64_t* full, uint32_t& st) {
+  using U = Unit<W16>;
+  constexpr int E = U::kElems;
+  constexpr int WB = W16 ? 2 : 4;
+  constexpr int TP = G::kInB / 4;                 // plain tile: fp32 in one input slot
+  constexpr int TPS = G::kInB / 12 / 256 * 256;   // SGD tile: w, v, g in one input slot
+  static_assert(TP * WB <= G::kOutB && TPS >= 256, "pre-cast tiles");
+  const ExchangeArgs& a = *pc.a;
+  const int tp = SGD ? TPS : TP;
+  float* const x = pc.x;
+  float* const vr = a.v[pc.lr];
+  const float* const gr = a.g[pc.lr];
+  const int64_t P = pc.P, L = pc.L, P4 = pc.P4;
+  const int64_t nel = s1 > s0 ? s1 - s0 : 0;
+  const int nt = (int)((nel + tp - 1) / tp);
+  auto geom = [&](int i, int64_t& g0, int64_t& n) {
+    const int sg = i / nt, t = i - sg * nt;
+    g0 = (int64_t)sg * L + s0 + (int64_t)t * tp;
+    n = min((int64_t)tp, nel - (int64_t)t * tp);
+  };
+  tile_pipeline<G>(
+      gtid, K * nt, use, outn, in_ring, out_ring, full,
+      [&](int i, char* slot, uint64_t* bar) {
+        int64_t g0, n;
+        geom(i, g0, n);
+        const int64_t nb = max((int64_t)0, min(g0 + n, P4) - g0);  // bulk-loadable elements
+        mbar_expect_tx(bar, (uint32_t)(nb * 4 * (SGD ? 3 : 1)));
+        if (nb > 0) {
+          bulk_load(slot, x + g0, (uint32_t)(nb * 4), bar);
+          if (SGD) {
+            bulk_load(slot + TPS * 4, vr + g0, (uint32_t)(nb * 4), bar);
+            bulk_load(slot + 2 * TPS * 4, gr + g0, (uint32_t)(nb * 4), bar);
+          }
+        }
+      },
+      [&](int i, const char* in, char* out) {
+        int64_t g0, n;
+        geom(i, g0, n);
+        const int nbi = (int)max((int64_t)0, min(g0 + n, P4) - g0);
+        const float* fin = reinterpret_cast<const float*>(in);
+        const float* fvin = fin + TPS;
+        const float* fgin = fin + 2 * TPS;
+        for (int v = gtid; v < (int)(n / E); v += G::kNT) {
+          float f[E];
+          if ((v + 1) * E <= nbi) {
+#pragma unroll
+            for (int q = 0; q < E; q += 4) {
+              float4 t4 = reinterpret_cast<const float4*>(fin + v * E)[q / 4];
+              if (SGD) {
+                const float4 vn = sgd_v(reinterpret_cast<const float4*>(fvin + v * E)[q / 4],
+                                        reinterpret_cast<const float4*>(fgin + v * E)[q / 4], a.lr, a.mu);
+                st16_f(vr + g0 + v * E + q, vn);
+                t4 = add4(t4, vn);
+              }
+              f[q] = t4.x; f[q + 1] = t4.y; f[q + 2] = t4.z; f[q + 3] = t4.w;
+            }
+          } else {
+#pragma unroll
+            for (int q = 0; q < E; ++q) {
+              const int e = v * E + q;
+              if (e < nbi) {
+                f[q] = fin[e];
+                if (SGD) {
+                  const float vn = sgd_v1(fvin[e], fgin[e], a.lr, a.mu);
+                  vr[g0 + e] = vn;
+                  f[q] = __fadd_rn(f[q], vn);
+                }
+              } else if (g0 + e < P) {  // the <= 3 elements in [P & ~3, P): plain accesses
+                f[q] = x[g0 + e];
+                if (SGD) {
+                  const float vn = sgd_v1(vr[g0 + e], gr[g0 + e], a.lr, a.mu);
+                  vr[g0 + e] = vn;
+                  f[q] = __fadd_rn(f[q], vn);
+                }
+              } else {
+                f[q] = 0.0f;
+              }
+            }
+          }
+          st |= unit_status<W16, E>(f);
+          reinterpret_cast<uint4*>(out)[v] = U::encode(f);
+        }
+      },
+      [&](int i, const char* out) {
+        int64_t g0, n;
+        geom(i, g0, n);
+        bulk_store(pc.stage_r + g0 * WB, out, (uint32_t)(n * WB));
+      });
+}
+
+// a4 on the TMA engine: pull [s0, s1) of the own segment from every rank's
+// stage (peer memory), ascending-rank fp32 sum, 1/k, round, store into own avg.
+template <class G, int K, bool W16>
+__device__ __forceinline__ void reduce_phase(const PhaseCtx& pc, int gtid, int64_t s0, int64_t s1,
+                                             uint32_t& use, uint32_t& outn, char* in_ring,
+                                             char* out_ring, uint64_t* full, uint32_t& st) {
+  using U = Unit<W16>;
+  constexpr int E = U::kElems;
+  constexpr int WB = W16 ? 2 : 4;
+  // k sources of TR wire elements fit one input slot; a multiple of 256 elements
+  // keeps every source's smem offset and byte count 16-byte aligned.
+  constexpr int TR_RAW = G::kInB / (K * WB) / 256 * 256;
+  constexpr int TR = TR_RAW < 4096 ? TR_RAW : 4096;
+  static_assert(TR >= 256 && TR * WB <= G::kOutB, "a4 tile");
+  const ExchangeArgs& a = *pc.a;
+  const int r = pc.r;
+  const int64_t L = pc.L;
+  char* const avg_r = reinterpret_cast<char*>(a.avg[r]);
+  const int nt = (int)((max((int64_t)0, s1 - s0) + TR - 1) / TR);
+  tile_pipeline<G>(
+      gtid, nt, use, outn, in_ring, out_ring, full,
+      [&](int i, char* slot, uint64_t* bar) {
+        const int64_t e = s0 + (int64_t)i * TR;
+        const int64_t n = min((int64_t)TR, s1 - e);
+        mbar_expect_tx(bar, (uint32_t)(K * n * WB));
+#pragma unroll
+        for (int j = 0; j < K; ++j)
+          bulk_load(slot + j * TR * WB, reinterpret_cast<const char*>(a.stage[j]) + ((int64_t)r * L + e) * WB,
+                    (uint32_t)(n * WB), bar);
+      },
+      [&](int i, const char* in, char* out) {
+        const int64_t e = s0 + (int64_t)i * TR;
+        const int n = (int)min((int64_t)TR, s1 - e);
+        for (int v = gtid; v < n / E; v += G::kNT) {
+          uint4 raw[K];
+#pragma unroll
+          for (int j = 0; j < K; ++j) raw[j] = reinterpret_cast<const uint4*>(in + j * TR * WB)[v];
+          float sm[E], t[E];
+          U::decode(raw[0], sm);
+#pragma unroll
+          for (int j = 1; j < K; ++j) {
+            U::decode(raw[j], t);
+#pragma unroll
+            for (int q = 0; q < E; ++q) sm[q] = __fadd_rn(sm[q], t[q]);
+          }
+          if (!a.sum) {
+#pragma unroll
+            for (int q = 0; q < E; ++q) sm[q] = div_k<K>(sm[q]);
+          } else if (W16) {  // a sum can leave the binary16 range
+#pragma unroll
+            for (int q = 0; q < E; ++q) st |= status_of(sm[q], true) & TM_BIT_OVERFLOW16;
+          }
+          reinterpret_cast<uint4*>(out)[v] = U::encode(sm);
+        }
+      },
+      [&](int i, const char* out) {
+        const int64_t e = s0 + (int64_t)i * TR;
+        const int64_t n = min((int64_t)TR, s1 - e);
+        bulk_store(avg_r + e * WB, out, (uint32_t)(n * WB));
+      });
+}
+
+// a6 on the TMA engine: pull chunk [e0, e1) of every rank's avg, widen, store
+// into the caller's buffer (truncated at P).
+template <class G, int K, bool W16>
+__device__ __forceinline__ void gather_phase(const PhaseCtx& pc, int gtid, int64_t e0, int64_t e1,
+                                             uint32_t& use, uint32_t& outn, char* in_ring,
+                                             char* out_ring, uint64_t* full) {
+  using U = Unit<W16>;
+  constexpr int E = U::kElems;
+  constexpr int WB = W16 ? 2 : 4;
+  constexpr int TA = G::kOutB / 4;  // fp32 out tile fills one output slot
+  static_assert(TA * WB <= G::kInB, "a6 tile");
+  const ExchangeArgs& a = *pc.a;
+  float* const x = pc.x;
+  const int64_t P = pc.P, L = pc.L, P4 = pc.P4;
+  const int64_t nel = e1 > e0 ? e1 - e0 : 0;
+  const int nt = (int)((nel + TA - 1) / TA);
+  auto geom = [&](int i, int& j, int64_t& e, int64_t& n) {
+    j = i / nt;
+    const int t = i - j * nt;
+    e = e0 + (int64_t)t * TA;
+    n = min((int64_t)TA, e1 - e);
+  };
+  tile_pipeline<G>(
+      gtid, K * nt, use, outn, in_ring, out_ring, full,
+      [&](int i, char* slot, uint64_t* bar) {
+        int j;
+        int64_t e, n;
+        geom(i, j, e, n);
+        mbar_expect_tx(bar, (uint32_t)(n * WB));
+        bulk_load(slot, reinterpret_cast<const char*>(a.avg[j]) + e * WB, (uint32_t)(n * WB), bar);
+      },
+      [&](int i, const char* in, char* out) {
+        int j;
+        int64_t e, n;
+        geom(i, j, e, n);
+        const int64_t g0 = (int64_t)j * L + e;
+        // tile-relative window [lo, hi) of the <= 3 elements in [P & ~3, P):
+        // bulk stores cannot cover them, plain stores do
+        const int lo = (int)max((int64_t)0, min(n, P4 - g0));
+        const int hi = (int)max((int64_t)0, min(n, P - g0));
+        float* fo = reinterpret_cast<float*>(out);
+        for (int v = gtid; v < (int)(n / E); v += G::kNT) {
+          float f[E];
+          U::decode(reinterpret_cast<const uint4*>(in)[v], f);
+#pragma unroll
+          for (int q = 0; q < E; q += 4)
+            reinterpret_cast<float4*>(fo + v * E)[q / 4] = make_float4(f[q], f[q + 1], f[q + 2], f[q + 3]);
+          if (hi > lo && (v + 1) * E > lo && v * E < hi) {
+#pragma unroll
+            for (int q = 0; q < E; ++q)
+              if (v * E + q >= lo && v * E + q < hi) x[g0 + v * E + q] = f[q];
+          }
+        }
+      },
+      [&](int i, const char* out) {
+        int j;
+        int64_t e, n;
+        geom(i, j, e, n);
+        const int64_t g0 = (int64_t)j * L + e;
+        const int64_t nb = max((int64_t)0, min(g0 + n, P4) - g0);
+        if (nb > 0) bulk_store(x + g0, out, (uint32_t)(nb * 4));
+      });
 }
 
 template <int K, bool W16, bool SYS, bool SGD>
 __global__ void __launch_bounds__(kTmaThreads, 1)
 tm_exchange_tma_kernel(const __grid_constant__ ExchangeArgs a) {
-  using U = Unit<W16>;
-  constexpr int E = U::kElems;      // elements per 16-byte wire unit
-  constexpr int WB = W16 ? 2 : 4;   // wire bytes per element
-  constexpr int TP = 8192;          // a2 tile: fp32 in 32 KB, wire out <= 32 KB
-  // a4 tile: k sources of TR wire elements fit one 32 KB slot; a multiple of 256
-  // elements keeps every source's smem offset and byte count 16-byte aligned.
-  constexpr int TR_RAW = kSlotBytes / (K * WB) / 256 * 256;
-  constexpr int TR = TR_RAW < 4096 ? TR_RAW : 4096;
-  static_assert(TR >= 256, "a4 tile too small");
-  constexpr int TA = 8192;          // a6 tile: wire in <= 32 KB, fp32 out 32 KB
   extern __shared__ __align__(128) unsigned char smem[];
   char* in_ring = reinterpret_cast<char*>(smem);
   char* out_ring = in_ring + kInSlots * kSlotBytes;
@@ -515,12 +749,9 @@ tm_exchange_tma_kernel(const __grid_constant__ ExchangeArgs a) {
   const int lr = blockIdx.x / a.C;
   const int c = blockIdx.x - lr * a.C;
   const int r = a.rank0 + lr;
-  float* __restrict__ x = a.x[lr];
-  const int64_t P = a.P, L = a.L, P4 = P & ~int64_t(3);
+  const PhaseCtx pc{&a, lr, r, a.x[lr], a.P, a.L, a.P & ~int64_t(3), reinterpret_cast<char*>(a.stage[r])};
   const int64_t e0 = (int64_t)c * a.Lc;
-  const int64_t e1 = min(e0 + a.Lc, L);
-  const int64_t nel = e1 > e0 ? e1 - e0 : 0;
-  char* const stage_r = reinterpret_cast<char*>(a.stage[r]);
+  const int64_t e1 = min(e0 + a.Lc, a.L);
   const int tid = threadIdx.x;
 
   if (tid == 0) {
@@ -536,204 +767,141 @@ tm_exchange_tma_kernel(const __grid_constant__ ExchangeArgs a) {
   stamp(a, kStampStart);
   uint32_t use = 0, outn = 0, st = 0;
 
-  // ---------------- a2: pre-cast x -> own stage (all k segments' chunk c) ----
-  // Fused BSP step (SGD): the tile is TPS elements of w, v and g (three bulk
-  // loads into one slot); v' goes back to v with register stores (1.819 vs
-  // 1.835 ms for a second bulk store from the output slot), the wire tile of
-  // w' = w + v' is bulk-stored as in the plain pre-cast.
-  {
-    constexpr int TPS = 2048;
-    constexpr bool sgd = SGD;
-    const int tp = sgd ? TPS : TP;
-    float* const vr = a.v[lr];
-    const float* const gr = a.g[lr];
-    const int nt = (int)((nel + tp - 1) / tp);
-    auto geom = [&](int i, int64_t& g0, int64_t& n) {
-      const int sg = i / nt, t = i - sg * nt;
-      g0 = (int64_t)sg * L + e0 + (int64_t)t * tp;
-      n = min((int64_t)tp, nel - (int64_t)t * tp);
-    };
-    tile_pipeline(
-        K * nt, use, outn, in_ring, out_ring, full,
-        [&](int i, char* slot, uint64_t* bar) {
-          int64_t g0, n;
-          geom(i, g0, n);
-          const int64_t nb = max((int64_t)0, min(g0 + n, P4) - g0);  // bulk-loadable elements
-          mbar_expect_tx(bar, (uint32_t)(nb * 4 * (sgd ? 3 : 1)));
-          if (nb > 0) {
-            bulk_load(slot, x + g0, (uint32_t)(nb * 4), bar);
-            if (sgd) {
-              bulk_load(slot + TPS * 4, vr + g0, (uint32_t)(nb * 4), bar);
-              bulk_load(slot + 2 * TPS * 4, gr + g0, (uint32_t)(nb * 4), bar);
-            }
-          }
-        },
-        [&](int i, const char* in, char* out) {
-          int64_t g0, n;
-          geom(i, g0, n);
-          const int nbi = (int)max((int64_t)0, min(g0 + n, P4) - g0);
-          const float* fin = reinterpret_cast<const float*>(in);
-          const float* fvin = fin + TPS;
-          const float* fgin = fin + 2 * TPS;
-          for (int v = tid; v < (int)(n / E); v += kTmaThreads) {
-            float f[E];
-            if ((v + 1) * E <= nbi) {
-#pragma unroll
-              for (int q = 0; q < E; q += 4) {
-                float4 t4 = reinterpret_cast<const float4*>(fin + v * E)[q / 4];
-                if (sgd) {
-                  const float4 vn = sgd_v(reinterpret_cast<const float4*>(fvin + v * E)[q / 4],
-                                          reinterpret_cast<const float4*>(fgin + v * E)[q / 4], a.lr, a.mu);
-                  st16_f(vr + g0 + v * E + q, vn);
-                  t4 = add4(t4, vn);
-                }
-                f[q] = t4.x; f[q + 1] = t4.y; f[q + 2] = t4.z; f[q + 3] = t4.w;
-              }
-            } else {
-#pragma unroll
-              for (int q = 0; q < E; ++q) {
-                const int e = v * E + q;
-                if (e < nbi) {
-                  f[q] = fin[e];
-                  if (sgd) {
-                    const float vn = sgd_v1(fvin[e], fgin[e], a.lr, a.mu);
-                    vr[g0 + e] = vn;
-                    f[q] = __fadd_rn(f[q], vn);
-                  }
-                } else if (g0 + e < P) {  // the <= 3 elements in [P & ~3, P): plain accesses
-                  f[q] = x[g0 + e];
-                  if (sgd) {
-                    const float vn = sgd_v1(vr[g0 + e], gr[g0 + e], a.lr, a.mu);
-                    vr[g0 + e] = vn;
-                    f[q] = __fadd_rn(f[q], vn);
-                  }
-                } else {
-                  f[q] = 0.0f;
-                }
-              }
-            }
-            st |= unit_status<W16, E>(f);
-            reinterpret_cast<uint4*>(out)[v] = U::encode(f);
-          }
-        },
-        [&](int i, const char* out) {
-          int64_t g0, n;
-          geom(i, g0, n);
-          bulk_store(stage_r + g0 * WB, out, (uint32_t)(n * WB));
-        });
-  }
+  precast_phase<FullGrp, K, W16, SGD>(pc, tid, e0, e1, use, outn, in_ring, out_ring, full, st);
   if (st) atomicOr(a.status, st);
-  drain_bulk_stores();
+  st = 0;
+  if (tid == 0) drain_bulk_stores_thread();
   stamp(a, kStampCast);
   if (!rank_barrier<K, SYS>(a, kPhaseReady, r, c, epoch, &s_abort)) return;
   stamp(a, kStampReady);
   if (tid == 0) fence_proxy_async_global();  // peers' staging, acquired above -> bulk loads
 
-  // ---------------- a4: reduce-scatter pull (TMA from every rank's stage) ----
-  {
-    char* const avg_r = reinterpret_cast<char*>(a.avg[r]);
-    const int nt = (int)((nel + TR - 1) / TR);
-    tile_pipeline(
-        nt, use, outn, in_ring, out_ring, full,
-        [&](int i, char* slot, uint64_t* bar) {
-          const int64_t e = e0 + (int64_t)i * TR;
-          const int64_t n = min((int64_t)TR, e1 - e);
-          mbar_expect_tx(bar, (uint32_t)(K * n * WB));
-#pragma unroll
-          for (int j = 0; j < K; ++j)
-            bulk_load(slot + j * TR * WB, reinterpret_cast<const char*>(a.stage[j]) + ((int64_t)r * L + e) * WB,
-                      (uint32_t)(n * WB), bar);
-        },
-        [&](int i, const char* in, char* out) {
-          const int64_t e = e0 + (int64_t)i * TR;
-          const int n = (int)min((int64_t)TR, e1 - e);
-          for (int v = tid; v < n / E; v += kTmaThreads) {
-            uint4 raw[K];
-#pragma unroll
-            for (int j = 0; j < K; ++j) raw[j] = reinterpret_cast<const uint4*>(in + j * TR * WB)[v];
-            float sm[E], t[E];
-            U::decode(raw[0], sm);
-#pragma unroll
-            for (int j = 1; j < K; ++j) {
-              U::decode(raw[j], t);
-#pragma unroll
-              for (int q = 0; q < E; ++q) sm[q] = __fadd_rn(sm[q], t[q]);
-            }
-            if (!a.sum) {
-#pragma unroll
-              for (int q = 0; q < E; ++q) sm[q] = div_k<K>(sm[q]);
-            } else if (W16) {  // a sum can leave the binary16 range
-#pragma unroll
-              for (int q = 0; q < E; ++q) st |= status_of(sm[q], true) & TM_BIT_OVERFLOW16;
-            }
-            reinterpret_cast<uint4*>(out)[v] = U::encode(sm);
-          }
-        },
-        [&](int i, const char* out) {
-          const int64_t e = e0 + (int64_t)i * TR;
-          const int64_t n = min((int64_t)TR, e1 - e);
-          bulk_store(avg_r + e * WB, out, (uint32_t)(n * WB));
-        });
-  }
+  reduce_phase<FullGrp, K, W16>(pc, tid, e0, e1, use, outn, in_ring, out_ring, full, st);
   if (st) atomicOr(a.status, st);
-  drain_bulk_stores();
+  if (tid == 0) drain_bulk_stores_thread();
   stamp(a, kStampReduce);
   if (!rank_barrier<K, SYS>(a, kPhaseReduced, r, c, epoch, &s_abort)) return;
   stamp(a, kStampReduced);
   if (a.ag_external) return;  // a6 by the copy engines / NCCL (tm_allgather)
   if (tid == 0) fence_proxy_async_global();
 
-  // ---------------- a6: allgather pull (TMA from every rank's avg) ----------
-  {
-    const int nt = (int)((nel + TA - 1) / TA);
-    auto geom = [&](int i, int& j, int64_t& e, int64_t& n) {
-      j = i / nt;
-      const int t = i - j * nt;
-      e = e0 + (int64_t)t * TA;
-      n = min((int64_t)TA, e1 - e);
-    };
-    tile_pipeline(
-        K * nt, use, outn, in_ring, out_ring, full,
-        [&](int i, char* slot, uint64_t* bar) {
-          int j;
-          int64_t e, n;
-          geom(i, j, e, n);
-          mbar_expect_tx(bar, (uint32_t)(n * WB));
-          bulk_load(slot, reinterpret_cast<const char*>(a.avg[j]) + e * WB, (uint32_t)(n * WB), bar);
-        },
-        [&](int i, const char* in, char* out) {
-          int j;
-          int64_t e, n;
-          geom(i, j, e, n);
-          const int64_t g0 = (int64_t)j * L + e;
-          // tile-relative window [lo, hi) of the <= 3 elements in [P & ~3, P):
-          // bulk stores cannot cover them, plain stores do
-          const int lo = (int)max((int64_t)0, min(n, P4 - g0));
-          const int hi = (int)max((int64_t)0, min(n, P - g0));
-          float* fo = reinterpret_cast<float*>(out);
-          for (int v = tid; v < (int)(n / E); v += kTmaThreads) {
-            float f[E];
-            U::decode(reinterpret_cast<const uint4*>(in)[v], f);
-#pragma unroll
-            for (int q = 0; q < E; q += 4)
-              reinterpret_cast<float4*>(fo + v * E)[q / 4] = make_float4(f[q], f[q + 1], f[q + 2], f[q + 3]);
-            if (hi > lo && (v + 1) * E > lo && v * E < hi) {
-#pragma unroll
-              for (int q = 0; q < E; ++q)
-                if (v * E + q >= lo && v * E + q < hi) x[g0 + v * E + q] = f[q];
-            }
-          }
-        },
-        [&](int i, const char* out) {
-          int j;
-          int64_t e, n;
-          geom(i, j, e, n);
-          const int64_t g0 = (int64_t)j * L + e;
-          const int64_t nb = max((int64_t)0, min(g0 + n, P4) - g0);
-          if (nb > 0) bulk_store(x + g0, out, (uint32_t)(nb * 4));
-        });
-  }
+  gather_phase<FullGrp, K, W16>(pc, tid, e0, e1, use, outn, in_ring, out_ring, full);
   if (tid == 0) bulk_wait_all<0>();  // kernel exit also waits; explicit for clarity
+  stamp(a, kStampEnd);
+}
+
+// ---------------------------------------------------------------------------
+// Warp-specialised staged kernel on the TMA engine: warps 0-7 (casters) run the
+// pre-cast pipeline sub-chunk by sub-chunk and publish READY_t to every rank;
+// warps 8-15 (reducers) pull sub-chunk t of the own segment from every rank's
+// staging as soon as READY_t is in from all of them.  The HBM-bound pre-cast and
+// the NVLink-bound reduce-scatter overlap, both fed by bulk copies (the register
+// warp-specialised kernel above does the same with 16-byte loads).  Then the
+// whole CTA meets at REDUCED and runs the allgather pipeline.  Same flag phases
+// as that kernel (READY_0..3, REDUCED = kWsSub).
+// Shared memory (224 KB): phase 1 casters [0, 128 KB) = 2 input + 2 output slots
+// of 32 KB, reducers [128, 224 KB) = 2 input slots of 32 KB + 2 output slots of
+// 16 KB; the allgather reuses all of it as the full-CTA rings.
+// ---------------------------------------------------------------------------
+using CastGrp = Grp<kTmaThreads / 2, 1, 2, 2, kSlotBytes, kSlotBytes>;
+using RedGrp = Grp<kTmaThreads / 2, 2, 2, 2, kSlotBytes, kSlotBytes / 2>;
+
+template <int K, bool W16, bool SYS, bool SGD>
+__global__ void __launch_bounds__(kTmaThreads, 1)
+tm_exchange_tmaws_kernel(const __grid_constant__ ExchangeArgs a) {
+  extern __shared__ __align__(128) unsigned char smem[];
+  char* const base = reinterpret_cast<char*>(smem);
+  __shared__ __align__(8) uint64_t full_c[CastGrp::kNin];
+  __shared__ __align__(8) uint64_t full_r[RedGrp::kNin];
+  __shared__ __align__(8) uint64_t full[kInSlots];
+  __shared__ int s_abort;
+  __shared__ uint32_t s_epoch;
+
+  const int lr = blockIdx.x / a.C;
+  const int c = blockIdx.x - lr * a.C;
+  const int r = a.rank0 + lr;
+  const PhaseCtx pc{&a, lr, r, a.x[lr], a.P, a.L, a.P & ~int64_t(3), reinterpret_cast<char*>(a.stage[r])};
+  const int64_t e0 = (int64_t)c * a.Lc;
+  const int64_t e1 = min(e0 + a.Lc, a.L);
+  const int64_t nel = e1 > e0 ? e1 - e0 : 0;
+  const int64_t Ls = ((nel + kWsSub - 1) / kWsSub + 255) / 256 * 256;  // sub-chunk length
+  const int tid = threadIdx.x;
+  constexpr int NT = CastGrp::kNT;
+  const int grp = tid / NT;
+  const int gtid = tid - grp * NT;
+
+  if (tid == 0) {
+    s_abort = 0;
+    uint32_t* ctr = a.flags[r] + (size_t)kPhases * TM_MAX_RANKS * a.flag_stride + c;  // device epoch
+    s_epoch = *ctr + 1;
+    *ctr = s_epoch;
+    for (int i = 0; i < CastGrp::kNin; ++i) mbar_init(&full_c[i], 1);
+    for (int i = 0; i < RedGrp::kNin; ++i) mbar_init(&full_r[i], 1);
+    for (int i = 0; i < kInSlots; ++i) mbar_init(&full[i], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  const uint32_t epoch = s_epoch;
+  stamp(a, kStampStart);
+  uint32_t st = 0;
+
+  if (grp == 0) {
+    // ------------------------------------------------ casters: a2 per sub-chunk
+    uint32_t use = 0, outn = 0;
+    char* const in_ring = base;
+    char* const out_ring = base + CastGrp::kNin * CastGrp::kInB;
+    for (int t = 0; t < kWsSub; ++t) {
+      const int64_t s0 = e0 + (int64_t)t * Ls;
+      const int64_t s1 = min(s0 + Ls, e1);
+      if (s1 > s0)
+        precast_phase<CastGrp, K, W16, SGD>(pc, gtid, s0, s1, use, outn, in_ring, out_ring, full_c, st);
+      if (gtid == 0) drain_bulk_stores_thread();  // this sub-chunk's staging is in memory
+      named_bar(1, NT);
+      if (gtid < K)
+        st_release<SYS>(a.flags[gtid] + (size_t)(t * TM_MAX_RANKS + r) * a.flag_stride + c, epoch);
+    }
+  } else {
+    // ------------------------------------------------ reducers: a4 per sub-chunk
+    uint32_t use = 0, outn = 0;
+    char* const in_ring = base + 2 * CastGrp::kNin * CastGrp::kInB;
+    char* const out_ring = in_ring + RedGrp::kNin * RedGrp::kInB;
+    for (int t = 0; t < kWsSub; ++t) {
+      if (gtid < K) {  // READY_t from rank gtid
+        const uint32_t* mine = a.flags[r] + (size_t)(t * TM_MAX_RANKS + gtid) * a.flag_stride + c;
+        if ((int32_t)(ld_acquire<SYS>(mine) - epoch) < 0) {
+          const uint64_t t0 = globaltimer();
+          while ((int32_t)(ld_acquire<SYS>(mine) - epoch) < 0) {
+            if (globaltimer() - t0 > a.timeout_ns) {
+              atomicOr(a.status, TM_BIT_TIMEOUT);
+              s_abort = 1;
+              break;
+            }
+            __nanosleep(32);
+          }
+        }
+      }
+      named_bar(2, NT);
+      if (s_abort) break;
+      if (gtid == 0) fence_proxy_async_global();  // acquired peers' staging -> bulk loads
+      const int64_t s0 = e0 + (int64_t)t * Ls;
+      const int64_t s1 = min(s0 + Ls, e1);
+      if (s1 > s0) reduce_phase<RedGrp, K, W16>(pc, gtid, s0, s1, use, outn, in_ring, out_ring, full_r, st);
+    }
+    if (gtid == 0) drain_bulk_stores_thread();  // avg in memory before REDUCED
+  }
+  if (st) atomicOr(a.status, st);
+  __syncthreads();
+  if (s_abort) return;
+  stamp(a, kStampReduce);  // pre-cast and reduce-scatter overlap: one stamp for both
+  if (!rank_barrier<K, SYS>(a, kWsSub, r, c, epoch, &s_abort)) return;  // REDUCED
+  stamp(a, kStampReduced);
+  if (a.ag_external) return;  // a6 by the copy engines / NCCL (tm_allgather)
+  if (tid == 0) fence_proxy_async_global();
+
+  // ---------------- a6: allgather pull with the whole CTA ---------------------
+  uint32_t use = 0, outn = 0;
+  gather_phase<FullGrp, K, W16>(pc, tid, e0, e1, use, outn, base, base + kInSlots * kSlotBytes, full);
+  if (tid == 0) bulk_wait_all<0>();
   stamp(a, kStampEnd);
 }
 
@@ -745,6 +913,9 @@ const void* exchange_fn(bool sys, int fl) {
   if (fl == kStagedWs)
     return sys ? reinterpret_cast<const void*>(&tm_exchange_ws_kernel<K, W16, true, SGD>)
                : reinterpret_cast<const void*>(&tm_exchange_ws_kernel<K, W16, false, SGD>);
+  if (fl == kStagedTmaWs)
+    return sys ? reinterpret_cast<const void*>(&tm_exchange_tmaws_kernel<K, W16, true, SGD>)
+               : reinterpret_cast<const void*>(&tm_exchange_tmaws_kernel<K, W16, false, SGD>);
   return sys ? reinterpret_cast<const void*>(&tm_exchange_kernel<K, W16, true, SGD>)
              : reinterpret_cast<const void*>(&tm_exchange_kernel<K, W16, false, SGD>);
 }
@@ -764,13 +935,17 @@ const void* pick_exchange(int k, bool w16, bool sys, int fl) {
   }
 }
 
-int flavour_threads(int fl) { return fl == kStagedTma ? kTmaThreads : (fl == kStagedWs ? kWsThreads : kThreads); }
+bool uses_tma(int fl) { return fl == kStagedTma || fl == kStagedTmaWs; }
+int flavour_threads(int fl) { return uses_tma(fl) ? kTmaThreads : (fl == kStagedWs ? kWsThreads : kThreads); }
 
 constexpr int kTmaSmem = (kInSlots + kOutSlots) * kSlotBytes;
+static_assert(2 * CastGrp::kNin * CastGrp::kInB + RedGrp::kNin * RedGrp::kInB +
+                  RedGrp::kNout * RedGrp::kOutB <= kTmaSmem, "tmaws phase-1 rings");
+int flavour_smem(int fl) { return uses_tma(fl) ? kTmaSmem : 0; }
 
 // Opt every TMA instantiation into its dynamic shared memory (idempotent).
 cudaError_t prepare(const void* fn, int fl) {
-  if (fl != kStagedTma) return cudaSuccess;
+  if (!uses_tma(fl)) return cudaSuccess;
   return cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, kTmaSmem);
 }
 

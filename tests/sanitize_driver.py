@@ -58,6 +58,20 @@ def main():
     check(cd.cpu().numpy(), cc, "easgd centre")
     for r in range(4):
         check(Wd[r].cpu().numpy(), ws[r], f"easgd worker {r}")
+    from oracle.bsp import bsp_iteration
+    for path in ("direct", "staged"):  # BSP step: TMA-engine one pass / step fused into the pre-cast
+        k, P = 3, 20011
+        Wb = worker_buffers(P, k, "D2", config=73)
+        Vb = worker_buffers(P, k, "D4", config=74)
+        Gb = worker_buffers(P, k, "D2", config=75)
+        Wt, Vt, Gt = ([torch.from_numpy(a).cuda() for a in arrs] for arrs in (Wb, Vb, Gb))
+        with tm.Exchanger(P, "asa16", size=k, nlocal=k, path=path) as ex:
+            ex.bsp_step(Wt, Vt, Gt, 0.01, 0.9, exchange_momentum=True)
+        ww, vv = bsp_iteration(Wb, Vb, Gb, 0.01, 0.9, "asa16", exchange_momentum=True)
+        for r in range(k):
+            check(Wt[r].cpu().numpy(), ww[r], f"bsp w {path}")
+            check(Vt[r].cpu().numpy(), vv[r], f"bsp v {path}")
+        n_ok += 1
     x = torch.randn(100003, device="cuda")
     h = tm.tm_cast_rn16(x)
     torch.cuda.synchronize()

@@ -18,7 +18,7 @@ from paper_1605_08325_b200.inputs import worker_buffers
 pytestmark = pytest.mark.gpu
 
 
-@pytest.mark.parametrize("kernel", ["tma", "ws", "reg"])
+@pytest.mark.parametrize("kernel", ["tma", "ws", "reg", "tmaws"])
 @pytest.mark.parametrize("strategy", ["asa16", "asa"])
 def test_copy_engine_allgather_bitwise(monkeypatch, kernel, strategy):
     monkeypatch.setenv("TM_STAGED_KERNEL", kernel)

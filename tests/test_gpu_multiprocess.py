@@ -49,14 +49,15 @@ def launch(tmp_path, k, strategy, P, dist, mode="normal", timeout=240, extra_env
     return res
 
 
-KERNEL_ID = {"reg": 0, "tma": 1, "ws": 2}
+KERNEL_ID = {"reg": 0, "tma": 1, "ws": 2, "tmaws": 3}
 
 
 @pytest.mark.parametrize("strategy,k,op,kernel", [("asa16", 2, "avg", "ws"), ("asa", 2, "avg", "ws"),
                                                   ("asa16", 3, "avg", "ws"), ("asa16", 2, "sum", "ws"),
                                                   ("asa16", 2, "range", "ws"), ("asa16", 2, "avg", "tma"),
                                                   ("asa", 3, "range", "tma"), ("asa16", 2, "avg", "reg"),
-                                                  ("asa", 3, "range", "reg")])
+                                                  ("asa", 3, "range", "reg"), ("asa16", 2, "avg", "tmaws"),
+                                                  ("asa", 3, "range", "tmaws"), ("asa16", 3, "sum", "tmaws")])
 def test_multiprocess_bitwise(tmp_path, strategy, k, op, kernel):
     P = 100_003
     env = {"TM_STAGED_KERNEL": kernel}
@@ -76,7 +77,8 @@ def test_multiprocess_bitwise(tmp_path, strategy, k, op, kernel):
 
 @pytest.mark.parametrize("strategy,k,mode,kernel", [("asa16", 2, "bsp", "ws"), ("asa16", 3, "bspmom", "ws"),
                                                     ("asa", 2, "bsp", "tma"), ("asa16", 3, "bspmom", "tma"),
-                                                    ("asa16", 2, "bsp", "reg"), ("asa", 3, "bspmom", "reg")])
+                                                    ("asa16", 2, "bsp", "reg"), ("asa", 3, "bspmom", "reg"),
+                                                    ("asa16", 3, "bspmom", "tmaws")])
 def test_multiprocess_bsp_fused_bitwise(tmp_path, strategy, k, mode, kernel):
     """tm_bsp_step across processes: the momentum-SGD step is fused into the
     staged kernel's pre-cast; two iterations vs oracle/bsp.py."""
@@ -231,7 +233,8 @@ def test_multiprocess_async_easgd_loop(tmp_path, k):
     assert len(orders_seen) >= 1
 
 
-@pytest.mark.parametrize("strategy,kernel", [("asa16", "ws"), ("asa", "reg"), ("asa16", "tma")])
+@pytest.mark.parametrize("strategy,kernel", [("asa16", "ws"), ("asa", "reg"), ("asa16", "tma"),
+                                             ("asa16", "tmaws")])
 def test_multiprocess_stress_random_delays(tmp_path, strategy, kernel):
     """60 back-to-back exchanges per rank, each after a per-rank delta and a random
     host delay on half of them: every rank ends bitwise at the oracle's sequence."""

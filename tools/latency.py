@@ -17,7 +17,7 @@ from sweep import timeit  # noqa: E402
 def main():
     torch.cuda.set_device(0)
     # staged: every kernel flavour (TM_STAGED_KERNEL is read at init)
-    variants = [("direct", None), ("staged", "tma"), ("staged", "ws"), ("staged", "reg")]
+    variants = [("direct", None), ("staged", "tma"), ("staged", "tmaws"), ("staged", "ws"), ("staged", "reg")]
     for P in (2048, 16384, 65536, 262144, 1 << 20, 1 << 22):
         for k in (2, 8):
             for path, fl in variants:

@@ -1,7 +1,7 @@
 #!/usr/bin/env python
 """Phase breakdown of the staged exchange kernels (tm_set_phase_log), one GPU.
 
-For each staged kernel flavour (TM_STAGED_KERNEL=tma|reg|ws, one subprocess
+For each staged kernel flavour (TM_STAGED_KERNEL=tma|tmaws|reg|ws, one subprocess
 each), k = 8 ranks in one process, AlexNet-sized ASA16, path=staged: the
 per-CTA %globaltimer stamps of one exchange (after warm-up) are reduced to the
 median over CTAs of each phase's duration and to the span from the first CTA
@@ -37,7 +37,7 @@ def child():
         tm.tm_set_phase_log(None)
         st = log.cpu().numpy().reshape(k * C, 8)[:, :6].astype(np.int64)
     t0 = st[:, 0].min()
-    res = {"kernel": ["reg", "tma", "ws"][lay["staged_kernel"]], "ctas": int(k * C),
+    res = {"kernel": ["reg", "tma", "ws", "tmaws"][lay["staged_kernel"]], "ctas": int(k * C),
            "span_us": round((st[:, 5].max() - t0) / 1e3, 1)}
     for i in range(1, 6):
         if st[:, i].max() == 0:
@@ -54,7 +54,7 @@ def child():
 def main():
     if len(sys.argv) > 1 and sys.argv[1] == "--child":
         return child()
-    for kern in ("tma", "reg", "ws"):
+    for kern in ("tma", "tmaws", "reg", "ws"):
         env = dict(os.environ, TM_STAGED_KERNEL=kern)
         r = subprocess.run([sys.executable, __file__, "--child"], env=env, capture_output=True, text=True)
         print(r.stdout.strip() or r.stderr[-2000:])

@@ -172,7 +172,7 @@ def allgather_rows(P, k, pk):
     """a6 modes on the staged path (tm_allgather): the fused SM pull vs the copy
     engines + widen kernel, every staged flavour, ASA16."""
     rows = []
-    for fl in ("tma", "ws", "reg"):
+    for fl in ("tma", "tmaws", "ws", "reg"):
         for ag in ("sm", "ce"):
             os.environ["TM_STAGED_KERNEL"] = fl
             g = torch.Generator(device="cuda").manual_seed(1605)
