@@ -280,7 +280,8 @@ def roofline(strategy, P, k, path, ms, peak, peak_src, workload):
     alg = design_hbm_bytes(strategy, P, k, path)
     ach = alg / (ms * 1e-3) / 1e9
     if path == "staged" and strategy != "ar":
-        kernel = {0: "tm_exchange_kernel", 1: "tm_exchange_tma_kernel", 2: "tm_exchange_ws_kernel"}.get(
+        kernel = {0: "tm_exchange_kernel", 1: "tm_exchange_tma_kernel", 2: "tm_exchange_ws_kernel",
+                  3: "tm_exchange_tmaws_kernel"}.get(
             STAGED_KERNEL[0], "tm_exchange_kernel")
     else:
         kernel = ("tm_direct_kernel" if os.environ.get("TM_DIRECT_LDG") == "1" or P < 2048
