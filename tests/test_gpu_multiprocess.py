@@ -139,6 +139,29 @@ def test_multiprocess_nccl_allgather(tmp_path):
         assert_bitwise(np.load(os.path.join(tmp_path, f"rank{r}.npy")), want[r], f"rank {r}")
 
 
+@pytest.mark.skipif(__import__("torch").cuda.device_count() < 2,
+                    reason="NCCL needs one GPU per rank (multi-GPU box)")
+@pytest.mark.parametrize("k", [2, 4, 8])
+def test_multiprocess_ar_nccl_within_q11(tmp_path, k):
+    """AR across processes is NCCL's allreduce (ncclAvg): its summation order is
+    NCCL's, so it is checked against the oracle within reading Q11."""
+    import torch
+    from gpu_helpers import q11_bound
+    if torch.cuda.device_count() < k:
+        pytest.skip(f"needs {k} GPUs")
+    P = 100_003
+    res = launch(tmp_path, k, "ar", P, "D2")
+    X = [worker_buffer(P, "D2", r, config=50) for r in range(k)]
+    want = X
+    for _ in range(3):
+        bound = q11_bound(want)
+        want = ox.exchange(want, "ar")
+    got = [np.load(os.path.join(tmp_path, f"rank{r}.npy")) for r in range(k)]
+    for r in range(k):
+        assert res[r]["code"] == 0, res[r]
+        assert np.all(np.abs(got[r].astype(np.float64) - want[r]) <= 3 * bound), f"rank {r}"
+
+
 def test_multiprocess_timeout_instead_of_hang(tmp_path):
     """Fault injection: rank 1 never calls tm_exchange; rank 0's
     kernel times out, sets TM_E_TIMEOUT and exits."""
