@@ -44,7 +44,8 @@ def parse():
     ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--strategy", choices=["asa16", "asa", "ar"], default="asa16")
-    ap.add_argument("--workload", default="alexnet")
+    ap.add_argument("--workload", default="alexnet",
+                    help="alexnet | googlenet | googlenet_aux | vggnet | 1m | 1m_tail, or a parameter count")
     ap.add_argument("--k", type=int, default=8, help="ranks simulated on one GPU when --gpus 1")
     ap.add_argument("--dist", default="D2")
     ap.add_argument("--no-e2e", action="store_true")
@@ -197,7 +198,7 @@ def run_reference(args):
         return
     from oracle import exchange as ox
     from paper_1605_08325_b200.inputs import WORKLOADS, worker_buffers
-    P = WORKLOADS[args.workload]
+    P = WORKLOADS[args.workload] if args.workload in WORKLOADS else int(args.workload)
     multi = args.gpus > 1
     k = args.gpus if multi else args.k
     budget = float(os.environ.get("REF_BUDGET_S", "120"))
@@ -332,7 +333,7 @@ def main():
         rank, local = 0, 0
         torch.cuda.set_device(0)
         k, nlocal, first = args.k, args.k, 0
-    P = WORKLOADS[args.workload]
+    P = WORKLOADS[args.workload] if args.workload in WORKLOADS else int(args.workload)
     dev = torch.device("cuda", local)
 
     host = [worker_buffer(P, args.dist, first + i, config=3) for i in range(nlocal)]
