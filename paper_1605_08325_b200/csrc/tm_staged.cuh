@@ -1,9 +1,22 @@
-// Kernel templates of the staged exchange, shared by tm_staged.cu (plain
-// exchange) and tm_staged_sgd.cu (the exchange with the momentum-SGD step fused
-// into its pre-cast, SGD = true): two translation units so each kernel's
-// register allocation is its own and the two sets compile in parallel.  Every
-// definition is internal to the including translation unit.
-// sm_100a kernels of the Theano-MPI parameter exchange (arXiv 1605.08325).
+// sm_100a kernels of the Theano-MPI parameter exchange (arXiv 1605.08325):
+// the staged path, one persistent cooperative launch per exchange.  Kernel
+// templates shared by tm_staged.cu (plain exchange) and tm_staged_sgd.cu (the
+// exchange with the momentum-SGD step fused into its pre-cast, SGD = true): two
+// translation units, so each kernel's register allocation is its own and the two
+// sets compile in parallel.  Every definition is internal to the including
+// translation unit.
+//
+// Four flavours of the same protocol (results bitwise identical):
+//   tm_exchange_kernel        phases in sequence, 16-byte register loads/stores
+//                             (default for segments <= 64 Ki elements);
+//   tm_exchange_ws_kernel     caster warps / reducer warps overlap a2 and a4 per
+//                             sub-chunk, register loads;
+//   tm_exchange_tma_kernel    phases in sequence as bulk-copy (TMA engine) tile
+//                             pipelines (single-process default);
+//   tm_exchange_tmaws_kernel  the ws overlap with TMA pipelines in both warp
+//                             groups (multi-process default).
+// The TMA phases (precast_phase / reduce_phase / gather_phase) are written once
+// and parameterised by the thread group that runs them (Grp: whole CTA or half).
 //
 //   tm_exchange_kernel  -- ASA / ASA16: one persistent,
 //                          cooperative launch per exchange, three phases per CTA
