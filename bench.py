@@ -507,8 +507,40 @@ def main():
                "pipeline": f"{nch} ranges (tm_exchange_group_range), H2D / exchange / D2H on 3 streams",
                "sampled_result_equals_first_exchange": ok}
 
+    lay = ex.layout()
+    # secondary: the multi-process default staged kernel (warp-specialised, TMA
+    # engine), k ranks in this process on this GPU; the flavour is fixed at init,
+    # so a second exchanger (the library holds one at a time)
+    mp_kernel = None
+    if not multi and not args.no_staged and args.strategy != "ar":
+        ex.finalize()
+        prev = os.environ.get("TM_STAGED_KERNEL")
+        os.environ["TM_STAGED_KERNEL"] = "tmaws"
+        try:
+            ex = tm.Exchanger(P, args.strategy, rank=first, size=k, device=local, nlocal=nlocal, path="staged")
+            for _ in range(args.warmup):
+                step()
+            torch.cuda.synchronize()
+            m0, m1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            m0.record(stream)
+            for _ in range(args.steps):
+                step()
+            m1.record(stream)
+            torch.cuda.synchronize()
+            mms = m0.elapsed_time(m1) / args.steps
+            mp_kernel = {"kernel": "tm_exchange_tmaws_kernel", "ms_per_step": mms,
+                         "value": bytes_alg / (mms * 1e-3) / 1e9, "unit": "GB/s",
+                         "roofline": roofline(args.strategy, P, k, "staged", mms, peak, peak_src, args.workload)}
+            mp_kernel["roofline"]["kernel"] = "tm_exchange_tmaws_kernel"
+            mp_kernel["roofline"]["traffic"] = traffic_from_profiles(
+                f"{args.workload}_{args.strategy}_k{k}_staged_tmaws")
+        finally:
+            if prev is None:
+                os.environ.pop("TM_STAGED_KERNEL", None)
+            else:
+                os.environ["TM_STAGED_KERNEL"] = prev
+
     if rank == 0:
-        lay = ex.layout()
         line = {
             "metric": METRIC, "value": value, "unit": "GB/s", "n_gpus": N, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
@@ -525,6 +557,7 @@ def main():
             "roofline": roof,
             "gpu_launches": args.steps,
             "staged_path_one_gpu": staged,
+            "multiprocess_default_kernel_one_gpu": mp_kernel,
             "nvlink_counters": nvlink,
             "nccl_allreduce_same_buffer": nccl_ar,
             "clocks": clk.summary(),
