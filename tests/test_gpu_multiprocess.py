@@ -162,6 +162,24 @@ def test_multiprocess_ar_nccl_within_q11(tmp_path, k):
         assert np.all(np.abs(got[r].astype(np.float64) - want[r]) <= 3 * bound), f"rank {r}"
 
 
+@pytest.mark.parametrize("k,kernel", [(4, "tmaws"), (8, "tmaws"), (8, "reg")])
+def test_multiprocess_k4_k8_cross_rank_identity(tmp_path, k, kernel):
+    """k = 4 and 8 processes (on a one-GPU box they share cuda:0,
+    time-sliced): bitwise parity with the oracle and every rank's buffer
+    bitwise identical (cross-rank identity)."""
+    P = 60_001 if kernel == "reg" else 300_007
+    res = launch(tmp_path, k, "asa16", P, "D2", extra_env={"TM_STAGED_KERNEL": kernel}, timeout=600)
+    want = [worker_buffer(P, "D2", r, config=50) for r in range(k)]
+    for _ in range(3):
+        want = ox.exchange(want, "asa16")
+    got = [np.load(os.path.join(tmp_path, f"rank{r}.npy")) for r in range(k)]
+    for r in range(k):
+        assert res[r]["code"] == 0, res[r]
+        assert res[r]["layout"]["staged_kernel"] == KERNEL_ID[kernel]
+        assert_bitwise(got[r], want[r], f"rank {r}")
+        assert_bitwise(got[r], got[0], f"rank {r} vs rank 0")
+
+
 def test_multiprocess_timeout_instead_of_hang(tmp_path):
     """Fault injection: rank 1 never calls tm_exchange; rank 0's
     kernel times out, sets TM_E_TIMEOUT and exits."""
