@@ -398,7 +398,12 @@ int tm_exchange_init(int64_t nparams, const tm_world* world, int strategy) {
     if (ag && !strcmp(ag, "ce")) c.ag_mode = TM_AG_CE;
     c.want_nccl_ag = ag && !strcmp(ag, "nccl") && c.nprocs > 1;
     if (c.want_nccl_ag) c.ag_mode = TM_AG_NCCL;
-    int cmax = k >= 2 ? tmx::exchange_max_ctas(c.device, wire16(strategy), k, c.staged_kernel) / c.nlocal : 1;
+    // TM_PROCS_PER_GPU=n: n processes share this GPU concurrently (CUDA MPS), so
+    // each may keep only 1/n of the co-resident CTAs (every rank's CTA c must be
+    // resident at once for the per-CTA flag barriers).
+    const int share = std::max(1, getenv("TM_PROCS_PER_GPU") ? atoi(getenv("TM_PROCS_PER_GPU")) : 1);
+    int cmax = k >= 2 ? tmx::exchange_max_ctas(c.device, wire16(strategy), k, c.staged_kernel) / c.nlocal / share
+                      : 1;
     if (k >= 2 && cmax < 1) return TM_E_CUDA;
     const int64_t want = std::max<int64_t>(1, (c.L + tmx::kMinChunk - 1) / tmx::kMinChunk);
     c.C = (int)std::min<int64_t>(std::max(cmax, 1), want);
