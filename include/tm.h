@@ -48,6 +48,22 @@
  *                      pointers in the peer table.
  * Thread safety: one host thread per process calls tm_*.
  *
+ * Environment (read at tm_exchange_init unless noted; every rank of a group must
+ * use the same values):
+ *   TM_STAGED_KERNEL=reg|tma|ws|tmaws  staged kernel flavour (default: reg for
+ *                      segments <= 64 Ki elements, else tma in a single-process
+ *                      group and tmaws across processes).
+ *   TM_ALLGATHER=sm|ce|nccl            allgather mode (tm_set_allgather); nccl
+ *                      also creates the NCCL communicator at bootstrap.
+ *   TM_PROCS_PER_GPU=n                 n processes share this GPU concurrently
+ *                      (CUDA MPS): each keeps 1/n of the co-resident CTAs.
+ *   TM_NCCL_LIB=path                   libnccl.so.2 to dlopen (the binding sets
+ *                      torch's); TM_DEBUG=1 prints CUDA errors to stderr.
+ *   Diagnostics (read at first use): TM_DIRECT_LDG=1 register kernels instead of
+ *   the TMA ones on the direct / BSP / EASGD-round paths; TM_DIRECT_STATIC=1
+ *   static tile assignment; TM_TMA_CFG=n direct-kernel tile/ring variant;
+ *   TM_BSP_UNFUSED=1 SGD pass + exchange instead of the fused kernels.
+ *
  * Collective contract: every rank calls tm_exchange the same
  * number of times, in the same order.  Each call carries an epoch (kept on the
  * device, per CTA, so exchanges can be captured in CUDA graphs); cross-rank
