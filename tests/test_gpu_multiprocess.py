@@ -1,7 +1,9 @@
 """Multi-process exchange: one process per rank (nlocal = 1), peers reached through
 CUDA IPC mappings, flags in peer memory -- the north-star deployment.  On the
 one-GPU test box all processes share cuda:0 (IPC across processes on one device;
-the kernels are time-sliced, so this checks correctness, not speed)."""
+the kernels are time-sliced, so this checks correctness, not speed).  With
+TM_TEST_MPS=1 and a CUDA MPS daemon running, the processes' kernels run
+concurrently instead (real cross-process races on the flags and data)."""
 
 import json
 import os
@@ -32,9 +34,14 @@ def _free_port():
 def launch(tmp_path, k, strategy, P, dist, mode="normal", timeout=240, extra_env=None):
     port = _free_port()
     procs = []
+    extra = dict(extra_env or {})
+    if os.environ.get("TM_TEST_MPS") == "1":
+        # the processes run concurrently under a CUDA MPS daemon started by the
+        # caller: each keeps 1/k of the co-resident CTAs
+        extra.setdefault("TM_PROCS_PER_GPU", str(k))
     for r in range(k):
         env = dict(os.environ, RANK=str(r), WORLD_SIZE=str(k), MASTER_ADDR="127.0.0.1",
-                   MASTER_PORT=str(port), LOCAL_RANK=str(r), **(extra_env or {}))
+                   MASTER_PORT=str(port), LOCAL_RANK=str(r), **extra)
         procs.append(subprocess.Popen([sys.executable, os.path.join(HERE, "mp_worker.py"), str(tmp_path),
                                        strategy, str(P), dist, mode], env=env))
     try:
