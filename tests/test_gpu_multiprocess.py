@@ -187,10 +187,13 @@ def test_multiprocess_k4_k8_cross_rank_identity(tmp_path, k, kernel):
         assert_bitwise(got[r], got[0], f"rank {r} vs rank 0")
 
 
-def test_multiprocess_timeout_instead_of_hang(tmp_path):
+@pytest.mark.parametrize("kernel", ["reg", "tma", "ws", "tmaws"])
+def test_multiprocess_timeout_instead_of_hang(tmp_path, kernel):
     """Fault injection: rank 1 never calls tm_exchange; rank 0's
-    kernel times out, sets TM_E_TIMEOUT and exits."""
-    res = launch(tmp_path, 2, "asa16", 4096, "D1", mode="skip1")
+    kernel times out in its first barrier, sets TM_E_TIMEOUT and exits -- every
+    staged flavour (the warp-specialised ones time out in the reducer group)."""
+    P = 4096 if kernel == "reg" else 300_007
+    res = launch(tmp_path, 2, "asa16", P, "D1", mode="skip1", extra_env={"TM_STAGED_KERNEL": kernel})
     assert res[0]["code"] == 7 and res[0]["bits"] & 4  # TM_E_TIMEOUT
 
 
