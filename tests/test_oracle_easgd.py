@@ -135,3 +135,26 @@ def test_async_replay_reduces_and_converges():
     f_w, f_c = easgd_async_replay(ws, c, [t] * 3, 0.5, 1, 0.5, [0, 1, 2] * 60)
     assert np.max(np.abs(f_c.astype(np.float64) - t)) < 1e-6
     assert all(np.max(np.abs(w.astype(np.float64) - t)) < 1e-6 for w in f_w)
+
+
+from hypothesis import given, settings, strategies as st  # noqa: E402
+
+_F32_1E37 = float(np.float32(1e37))
+
+
+@settings(max_examples=300, deadline=None)
+@given(x=st.lists(st.floats(width=32, min_value=-_F32_1E37, max_value=_F32_1E37), min_size=1, max_size=6),
+       c=st.floats(width=32, min_value=-_F32_1E37, max_value=_F32_1E37),
+       alpha=st.sampled_from([0.5, 0.0625, 0.3, 1.0, 0.125]))
+def test_property_update_vs_brute_force(x, c, alpha):
+    """Any finite fp32 worker / centre values (subnormals, mixed magnitudes):
+    each of the four steps is one correctly rounded operation."""
+    xs = np.array(x, dtype=F32)
+    cs = np.full(len(x), c, dtype=F32)
+    x2, c2 = easgd_update(xs, cs, alpha)
+    a = float(F32(alpha))
+    for i in range(len(x)):
+        d = exact.sub(float(xs[i]), float(cs[i]))
+        e = exact.mul(a, d)
+        assert exact.same_bits32(x2[i], exact.sub(float(xs[i]), e))
+        assert exact.same_bits32(c2[i], exact.add(float(cs[i]), e))

@@ -327,3 +327,39 @@ def test_asa16_sum_exact_on_small_integers(k):
     exact_sum = np.sum(np.stack(X).astype(np.float64), axis=0).astype(F32)
     for o in ex.asa16_average(X, op="sum"):
         assert_bitwise(o, exact_sum)
+
+
+# Property-based pin (hypothesis): fp32 values drawn over the whole finite range
+# the arithmetic stays finite in -- fp32 subnormals, binary16 subnormals and
+# ties, values up to the binary16 limit (ASA16) or 1e37 (ASA), mixed magnitudes
+# and signs -- against the exact-rational brute force of the same steps.
+from hypothesis import given, settings, strategies as st  # noqa: E402
+
+_F32_1E37 = float(np.float32(1e37))
+_F16_LIM = float(np.float32(65519.99))  # largest fp32 below the binary16 overflow threshold 65520
+_f32_asa = st.floats(width=32, min_value=-_F32_1E37, max_value=_F32_1E37)
+_f32_asa16 = st.floats(width=32, min_value=-_F16_LIM, max_value=_F16_LIM)
+
+
+def _cols(elem):
+    return st.lists(st.lists(elem, min_size=8, max_size=8), min_size=1, max_size=3)
+
+
+@settings(max_examples=300, deadline=None)
+@given(k=st.integers(2, 8), cols=_cols(_f32_asa))
+def test_property_asa_vs_brute_force(k, cols):
+    X = [np.array([c[j] for c in cols], dtype=F32) for j in range(k)]
+    o = ex.asa_average(X)
+    for i in range(len(cols)):
+        vals = [float(x[i]) for x in X]
+        assert exact.same_bits32(o[0][i], _brute_asa(vals, k)), (k, vals)
+
+
+@settings(max_examples=300, deadline=None)
+@given(k=st.integers(2, 8), cols=_cols(_f32_asa16))
+def test_property_asa16_vs_brute_force(k, cols):
+    X = [np.array([c[j] for c in cols], dtype=F32) for j in range(k)]
+    o = ex.asa16_average(X)
+    for i in range(len(cols)):
+        vals = [float(x[i]) for x in X]
+        assert exact.same_bits32(o[0][i], _brute_asa16(vals, k)), (k, vals)
