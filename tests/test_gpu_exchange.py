@@ -397,3 +397,32 @@ def test_default_staged_flavour_by_segment_length(monkeypatch):
     for P, k, want in ((100_003, 2, 0), (131_072 * 8, 8, 1), (65_536 * 4, 4, 0), (1_000_003, 2, 1)):
         with tm.Exchanger(P, "asa16", size=k, nlocal=k, path="staged") as ex:
             assert ex.layout()["staged_kernel"] == want, (P, k)
+
+
+@pytest.mark.parametrize("path", PATHS)
+@pytest.mark.parametrize("strategy", ["asa", "asa16"])
+def test_random_bit_patterns(path, strategy):
+    """Uniformly random finite fp32 bit patterns (every exponent: fp32
+    subnormals, values far beyond the binary16 range, huge magnitudes whose sums
+    overflow to inf): bitwise against the oracle, NaN where the oracle has NaN
+    (inf - inf; payloads are outside the contract, Q8).  Status reports the
+    non-finite / overflow conditions."""
+    g = np.random.default_rng(1605)
+    for k in (2, 3, 8):
+        P = 50_003
+        X = []
+        for _ in range(k):
+            u = g.integers(0, 2 ** 32, P, dtype=np.uint64).astype(np.uint32)
+            u[(u & 0x7F800000) == 0x7F800000] &= 0xBF7FFFFF  # finite inputs only
+            X.append(u.view(np.float32))
+        bufs = to_dev(X)
+        with tm.Exchanger(P, strategy, size=k, nlocal=k, path=path) as ex:
+            ex.exchange(bufs)
+            code, bits_ = ex.status()
+        with np.errstate(over="ignore", invalid="ignore"):
+            want = ox.exchange(X, strategy)
+        got = to_host(bufs)
+        for r in range(k):
+            assert_bitwise(got[r], want[r], f"{strategy} {path} k={k} rank {r}")
+        if strategy == "asa16":
+            assert bits_ & tm.TM_BIT_OVERFLOW16
