@@ -6,6 +6,8 @@ single-process kernel whose order is ascending rank, bitwise); every rank's
 result bitwise identical.
 """
 
+import os
+
 import numpy as np
 import pytest
 import torch
@@ -212,19 +214,33 @@ def test_device_rn16_exhaustive():
     numpy's binary16 conversion, which the opt-in CPU test pins to the oracle's
     integer emulation on all 2^32 inputs; plus the oracle itself on a dense
     stratified subset.  NaN payloads are outside the contract (Q8)."""
+    from concurrent.futures import ThreadPoolExecutor
+
     from oracle.fp16 import rn16
     step = 1 << 28
-    for start in range(0, 1 << 32, step):
-        b = torch.arange(start, start + step, dtype=torch.int64, device="cuda").to(torch.int32)
-        x = b.view(torch.float32)
-        h = tm.tm_cast_rn16(x).cpu().numpy().view(np.uint16)
-        xn = x.cpu().numpy()
-        ref = xn.astype(np.float16).view(np.uint16)
-        nan = np.isnan(xn)
-        assert np.array_equal(h[~nan], ref[~nan]), start
-        assert np.all((h[nan] & 0x7C00) == 0x7C00) and np.all((h[nan] & 0x3FF) != 0)
-        sub = slice(None, None, 4099)
-        assert np.array_equal(h[sub][~nan[sub]], rn16(xn[sub])[~nan[sub]]), start
+    nthr = max(1, min(16, os.cpu_count() or 1))
+
+    def check_slice(xn, h, lo, hi):  # numpy releases the GIL in astype / compares
+        xs, hs = xn[lo:hi], h[lo:hi]
+        with np.errstate(over="ignore"):
+            ref = xs.astype(np.float16).view(np.uint16)
+        nan = np.isnan(xs)
+        ok = np.array_equal(hs[~nan], ref[~nan])
+        return ok and bool(np.all((hs[nan] & 0x7C00) == 0x7C00) and np.all((hs[nan] & 0x3FF) != 0))
+
+    with ThreadPoolExecutor(nthr) as pool:
+        for start in range(0, 1 << 32, step):
+            b = torch.arange(start, start + step, dtype=torch.int64, device="cuda").to(torch.int32)
+            x = b.view(torch.float32)
+            h = tm.tm_cast_rn16(x).cpu().numpy().view(np.uint16)
+            xn = x.cpu().numpy()
+            part = step // nthr
+            futs = [pool.submit(check_slice, xn, h, i * part, step if i == nthr - 1 else (i + 1) * part)
+                    for i in range(nthr)]
+            assert all(f.result() for f in futs), start
+            sub = slice(None, None, 4099)
+            nan = np.isnan(xn[sub])
+            assert np.array_equal(h[sub][~nan], rn16(xn[sub])[~nan]), start
 
 
 @pytest.mark.parametrize("strategy", ["asa16", "asa", "ar"])
