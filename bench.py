@@ -376,13 +376,23 @@ def main():
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     nvl = NvlinkCounters(local) if multi else None
     nvl0 = nvl.read() if nvl and nvl.ok else None
+    # five sub-loops marked inside the one timed region (median / min
+    # of 5 loops), without changing what is timed
+    nsub = 5 if args.steps >= 5 else 1
+    marks = [args.steps * i // nsub for i in range(1, nsub)]
+    sub_ev = [torch.cuda.Event(enable_timing=True) for _ in marks]
     with ClockSampler(local) as clk:
         e0.record(stream)
-        for _ in range(args.steps):
+        for i in range(args.steps):
             step()
+            if i + 1 in marks:
+                sub_ev[marks.index(i + 1)].record(stream)
         e1.record(stream)
         torch.cuda.synchronize()
     ms = e0.elapsed_time(e1) / args.steps
+    bounds = [e0] + sub_ev + [e1]
+    counts = [b - a for a, b in zip([0] + marks, marks + [args.steps])]
+    loop_ms = [bounds[i].elapsed_time(bounds[i + 1]) / counts[i] for i in range(len(counts))]
     nvlink = None
     if nvl0 is not None:
         nvl1 = nvl.read()
@@ -564,6 +574,9 @@ def main():
             "e2e": e2e,
             "status": code,
             "exchange_us": ms * 1e3,
+            "ms_per_step_loops": {"n": len(loop_ms), "median": float(np.median(loop_ms)),
+                                  "min": float(np.min(loop_ms)), "max": float(np.max(loop_ms)),
+                                  "note": "rank 0's sub-loops of the one timed region"},
             "nvlink_roof_us_if_distributed": nvlink_roof_us(args.strategy, P, k),
             "paper_context": "paper ASA16 AlexNet k=8: 91.5-94 ms per exchange on K20m/IB QDR (Table 2)",
         }
