@@ -232,6 +232,11 @@ cudaError_t launch_tma(const LocalBufs& lb, int64_t P, uint32_t* status, unsigne
                        int dev, cudaStream_t s) {
   using Cfg = TmaCfg<K, TILE, RING_KB, MINB>;
   const int64_t ntiles = P / TILE;
+  if (ntiles == 0) {  // smaller than one tile: the register kernel
+    tm_direct_kernel<K, Q16><<<(int)std::max<int64_t>(1, (P / 4 + kThreads - 1) / kThreads), kThreads, 0, s>>>(
+        lb, 0, P, status);
+    return cudaGetLastError();
+  }
   auto fn = tm_direct_tma_kernel<K, Q16, TILE, RING_KB, MINB>;
   static std::atomic<uint64_t> optin{0};
   cudaError_t e0 = smem_optin(reinterpret_cast<const void*>(fn), Cfg::kSmem, dev, optin);
@@ -260,6 +265,19 @@ cudaError_t direct_tma(const LocalBufs& lb, int64_t P, uint32_t* status, unsigne
       default: break;
     }
   }
+  if constexpr (K <= 4) {  // A/B for small k: larger tiles / deeper rings
+    static const int cfg = env_int("TM_TMA_CFG", 0);
+    switch (cfg) {
+      case 9: return launch_tma<K, Q16, 4096, 128, 1>(lb, P, status, ctr, dev, s);
+      case 10: return launch_tma<K, Q16, 2048, 128, 1>(lb, P, status, ctr, dev, s);
+      case 11: return launch_tma<K, Q16, 4096, 96, 1>(lb, P, status, ctr, dev, s);
+      case 12: return launch_tma<K, Q16, 2048, 160, 1>(lb, P, status, ctr, dev, s);
+      default: break;
+    }
+  }
+  // k = 2: 16 KB tiles per buffer, 3-deep ring: 0.146 vs 0.160 ms at AlexNet size
+  // (profiles/r01/direct_small_k_cfg.txt; k = 4 measures the same either way).
+  if constexpr (K == 2) return launch_tma<K, Q16, 4096, 96, 1>(lb, P, status, ctr, dev, s);
   // Default, from the r01 sweep at k = 8 (profiles/r01/README.md): 8 KB tiles per
   // buffer, a 2-deep ring for k = 8 (128 KB in flight per SM), one CTA per SM.
   // (With dynamic tiles every TM_TMA_CFG measures 0.570-0.572 ms; register stores

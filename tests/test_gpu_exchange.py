@@ -19,7 +19,7 @@ from paper_1605_08325_b200.inputs import DISTS, WORKLOADS, worker_buffers
 
 pytestmark = pytest.mark.gpu
 
-SIZES = [1, 7, 8, 9, 255, 1024, 100003, 1_000_003]
+SIZES = [1, 7, 8, 9, 255, 1024, 3001, 4099, 8195, 100003, 1_000_003]  # 3001: < one k=2 direct tile
 
 
 PATHS = ["staged", "direct"]
