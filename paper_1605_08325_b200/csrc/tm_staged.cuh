@@ -538,7 +538,7 @@ __device__ __forceinline__ void precast_phase(const PhaseCtx& pc, int gtid, int6
   constexpr int E = U::kElems;
   constexpr int WB = W16 ? 2 : 4;
   constexpr int TP = G::kInB / 4;                 // plain tile: fp32 in one input slot
-  constexpr int TPS = G::kInB / 12 / 256 * 256;   // SGD tile: w, v, g in one input slot
+  constexpr int TPS = G::kInB / 16;               // SGD tile: w, v, g in one input slot (2048 for 32 KB: 1.82 ms vs 1.87 for 2560)
   static_assert(TP * WB <= G::kOutB && TPS >= 256, "pre-cast tiles");
   const ExchangeArgs& a = *pc.a;
   const int tp = SGD ? TPS : TP;
