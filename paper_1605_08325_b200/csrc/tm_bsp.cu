@@ -149,14 +149,14 @@ tm_bsp_direct_kernel(const __grid_constant__ BspBufs bb, int64_t P, uint32_t* st
 // v_0.. | g_0..]; output slot = [avg w | avg v (MOM) or v'_0..v'_{K-1}].
 // ---------------------------------------------------------------------------
 // Loads: thread 0 issues every bulk copy of a tile (measured faster than one
-// copy per lane of warp 0: 1.65 vs 1.86-1.91 ms at AlexNet k = 8).  Stores: each
+// copy per lane of warp 0: 1.65 vs 1.86-1.91 ms at AlexNet k = 8, 512-element tiles).  Stores: each
 // thread writes its results with 16-byte register stores (128 threads x 16 B =
 // one coalesced 2 KB row per buffer), measured 1.48 ms against 1.60 ms for bulk
 // stores from an output ring (whose smem reads queue behind the ring's loads) and
 // 1.57 ms for register stores with an "empty" mbarrier in place of __syncthreads.
-template <int K, bool MOM>
+template <int K, bool MOM, int TILE = 512>
 struct BspTma {
-  static constexpr int kTile = 512;                   // elements per buffer per tile
+  static constexpr int kTile = TILE;                  // elements per buffer per tile
   static constexpr int kThr = kTile / 4;              // one float4 per thread
   static constexpr uint32_t kTB = kTile * 4;          // bytes per buffer tile
   static constexpr int kInBytes = 3 * K * kTB;        // one ring slot
@@ -165,11 +165,11 @@ struct BspTma {
   static constexpr int kSmem = kStages * kInBytes;
 };
 
-template <int K, bool Q16, bool MOM>
-__global__ void __launch_bounds__(BspTma<K, MOM>::kThr, 1)
+template <int K, bool Q16, bool MOM, int TILE>
+__global__ void __launch_bounds__(BspTma<K, MOM, TILE>::kThr, 1)
 tm_bsp_tma_kernel(const __grid_constant__ BspBufs bb, int64_t ntiles, int64_t P, uint32_t* status,
                   unsigned long long* tile_ctr) {
-  using C = BspTma<K, MOM>;
+  using C = BspTma<K, MOM, TILE>;
   constexpr int S = C::kStages;
   constexpr int T = C::kTile;
   extern __shared__ __align__(128) unsigned char smem[];
@@ -257,19 +257,33 @@ sgd_kernel(float* __restrict__ w, float* __restrict__ v, const float* __restrict
   }
 }
 
+template <int K, bool Q16, bool MOM, int TILE>
+cudaError_t bsp_tma_launch(const BspBufs& bb, int64_t P, uint32_t* status, unsigned long long* ctr,
+                           int dev, cudaStream_t s) {
+  using C = BspTma<K, MOM, TILE>;
+  const int64_t ntiles = P / C::kTile;
+  auto fn = tm_bsp_tma_kernel<K, Q16, MOM, TILE>;
+  static std::atomic<uint64_t> optin{0};
+  cudaError_t e = smem_optin(reinterpret_cast<const void*>(fn), C::kSmem, dev, optin);
+  if (e != cudaSuccess) return e;
+  const int grid = (int)std::min<int64_t>(ntiles, sm_count(dev));
+  fn<<<grid, C::kThr, C::kSmem, s>>>(bb, ntiles, P, status, ctr);
+  return cudaGetLastError();
+}
+
 template <int K, bool Q16, bool MOM>
 cudaError_t bsp_launch(const BspBufs& bb, int64_t P, uint32_t* status, unsigned long long* ctr,
                        int dev, cudaStream_t s) {
-  using C = BspTma<K, MOM>;
-  const int64_t ntiles = P / C::kTile;
-  if (ctr && ntiles > 0) {
-    auto fn = tm_bsp_tma_kernel<K, Q16, MOM>;
-    static std::atomic<uint64_t> optin{0};
-    cudaError_t e = smem_optin(reinterpret_cast<const void*>(fn), C::kSmem, dev, optin);
-    if (e != cudaSuccess) return e;
-    const int grid = (int)std::min<int64_t>(ntiles, sm_count(dev));
-    fn<<<grid, C::kThr, C::kSmem, s>>>(bb, ntiles, P, status, ctr);
-    return cudaGetLastError();
+  if (ctr) {
+    // Tile per buffer: 2048 elements for k <= 4, 1024 above (AlexNet size: k = 2 / 4 /
+    // 8 at 355 / 707 / 1421 us = 1.05 of the copy peak, vs 578 / 876 / 1478 us with
+    // 512-element tiles, whose per-tile overhead dominated at small k;
+    // profiles/r01/bsp_tile_ab.txt).  TM_BSP_TILE = 512 | 1024 | 2048 overrides.
+    static const int tile = env_int("TM_BSP_TILE", K <= 4 ? 2048 : 1024);
+    if constexpr (K <= 4)
+      if (tile == 2048 && P >= 2048) return bsp_tma_launch<K, Q16, MOM, 2048>(bb, P, status, ctr, dev, s);
+    if (tile == 1024 && P >= 1024) return bsp_tma_launch<K, Q16, MOM, 1024>(bb, P, status, ctr, dev, s);
+    if (P >= 512) return bsp_tma_launch<K, Q16, MOM, 512>(bb, P, status, ctr, dev, s);
   }
   const int64_t want = (P / 4 + kThreads - 1) / kThreads;
   const int grid = (int)std::min<int64_t>(std::max<int64_t>(want, 1), 2 * sm_count(dev));
