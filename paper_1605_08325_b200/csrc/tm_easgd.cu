@@ -5,6 +5,7 @@
 #include <stdlib.h>
 
 #include <algorithm>
+#include <mutex>
 
 #include "tm_device.cuh"
 #include "tm_internal.h"
@@ -319,7 +320,7 @@ struct RoundTma {
 template <int N>
 __global__ void __launch_bounds__(kThreads, 1)
 easgd_round_tma_kernel(const __grid_constant__ OrderedWorkers ow, float* c, int64_t ntiles, int64_t n,
-                       float alpha) {
+                       float alpha, unsigned long long* tile_ctr) {
   using R = RoundTma<N>;
   constexpr int S = R::kStages;
   constexpr int T = kRoundTile;
@@ -327,15 +328,33 @@ easgd_round_tma_kernel(const __grid_constant__ OrderedWorkers ow, float* c, int6
   float* ring = reinterpret_cast<float*>(smem);            // [S][N + 1][T]: centre, workers
   float* outr = ring + (size_t)S * (N + 1) * T;             // [kOutSlots][N + 1][T]
   __shared__ __align__(8) uint64_t full[S];
+  __shared__ int64_t slot_tile[S];
   const uint32_t fb = smem_u32(&full[0]);  // one address computation for every barrier op
   const int tid = threadIdx.x;
-  const int64_t my = ntiles > blockIdx.x ? (ntiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+  // tiles claimed from a per-launch counter (work stealing; self-resetting), or
+  // the static assignment blockIdx + i * gridDim without one
+  int64_t next_static = blockIdx.x;
+  auto claim = [&]() -> int64_t {
+    int64_t t;
+    if (tile_ctr) {
+      t = (int64_t)atomicAdd(tile_ctr, 1ull);
+    } else {
+      t = next_static;
+      next_static += gridDim.x;
+    }
+    return t < ntiles ? t : -1;
+  };
   // thread 0 issues the N + 1 copies of a tile (measured 0.705 ms vs 0.711 ms with
   // one copy per lane of warp 0 at AlexNet size, N = 8; register stores in place
   // of the bulk stores: 0.710 vs 0.709 ms, no gain)
-  auto issue = [&](int64_t i) {
+  auto issue = [&](int64_t i) {  // thread 0: claim a tile for ring use i
     const int s = (int)(i % S);
-    const int64_t t = blockIdx.x + i * gridDim.x;
+    const int64_t t = claim();
+    slot_tile[s] = t;  // published to the consumers by the mbarrier arrive
+    if (t < 0) {
+      mbar_expect_tx_a(fb + 8 * s, 0);
+      return;
+    }
     mbar_expect_tx_a(fb + 8 * s, (N + 1) * R::kTB);
 #pragma unroll
     for (int q = 0; q <= N; ++q)
@@ -348,11 +367,12 @@ easgd_round_tma_kernel(const __grid_constant__ OrderedWorkers ow, float* c, int6
   }
   __syncthreads();
   if (tid == 0)
-    for (int64_t i = 0; i < S && i < my; ++i) issue(i);
-  for (int64_t i = 0; i < my; ++i) {
+    for (int64_t i = 0; i < S; ++i) issue(i);
+  for (int64_t i = 0;; ++i) {
     const int s = (int)(i % S);
-    const int64_t t = blockIdx.x + i * gridDim.x;
     mbar_wait_a(fb + 8 * s, (uint32_t)((i / S) & 1));
+    const int64_t t = slot_tile[s];
+    if (t < 0) break;  // uniform: every later claim is past the end too
     const float* src = ring + (size_t)s * (N + 1) * T;
     float* out = outr + (size_t)(i % R::kOutSlots) * (N + 1) * T;
     float4 cv = reinterpret_cast<const float4*>(src)[tid];
@@ -370,14 +390,38 @@ easgd_round_tma_kernel(const __grid_constant__ OrderedWorkers ow, float* c, int6
 #pragma unroll
       for (int q = 0; q <= N; ++q) bulk_store((q == 0 ? c : ow.wo[q - 1]) + t * T, out + (size_t)q * T, R::kTB);
       bulk_commit();
-      if (i + S < my) issue(i + S);
+      issue(i + S);
     }
   }
-  if (tid == 0) bulk_wait_all<0>();
+  if (tid == 0) {
+    if (tile_ctr) tile_ctr_retire(tile_ctr);
+    bulk_wait_all<0>();
+  }
   if (blockIdx.x == gridDim.x - 1) {  // past the last whole tile: register path
     for (int64_t v = ntiles * T / 4 + tid; v < n / 4; v += kThreads) round_vec<N>(ow, c, v, alpha);
     for (int64_t i = (n / 4) * 4 + tid; i < n; i += kThreads) round_scalar<N>(ow, c, i, alpha);
   }
+}
+
+// Per-device claim / retire words for the round kernel's dynamic tiles (the
+// round needs no exchanger context): allocated and zeroed on first use, reset
+// by each launch's last CTA; null if the allocation failed (static tiles then).
+unsigned long long* round_tile_ctr(int dev, bool may_allocate) {
+  static std::mutex mu;
+  static unsigned long long* ctr[64] = {};
+  std::lock_guard<std::mutex> lk(mu);
+  if (dev < 0 || dev >= 64) return nullptr;
+  if (!ctr[dev]) {
+    if (!may_allocate) return nullptr;
+    void* p = nullptr;
+    if (cudaMalloc(&p, 2 * sizeof(unsigned long long)) != cudaSuccess) return nullptr;
+    if (cudaMemset(p, 0, 2 * sizeof(unsigned long long)) != cudaSuccess) {
+      cudaFree(p);
+      return nullptr;
+    }
+    ctr[dev] = static_cast<unsigned long long*>(p);
+  }
+  return ctr[dev];
 }
 
 template <int N>
@@ -391,7 +435,12 @@ cudaError_t launch_round_tma(const OrderedWorkers& ow, float* c, int64_t n, int6
   cudaError_t e = smem_optin(reinterpret_cast<const void*>(fn), R::kSmem, dev, optin);
   if (e != cudaSuccess) return e;
   const int grid = (int)std::min<int64_t>(ntiles, sm_count(dev));
-  fn<<<grid, kThreads, R::kSmem, s>>>(ow, c, ntiles, n, alpha);
+  static const bool stat = env_int("TM_ROUND_STATIC", 0) == 1;  // A/B: static tile assignment
+  // no allocation while the stream is being captured: static tiles then
+  cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+  cudaStreamIsCapturing(s, &cap);
+  unsigned long long* ctr = stat ? nullptr : round_tile_ctr(dev, cap == cudaStreamCaptureStatusNone);
+  fn<<<grid, kThreads, R::kSmem, s>>>(ow, c, ntiles, n, alpha, ctr);
   return cudaGetLastError();
 }
 
