@@ -439,7 +439,11 @@ cudaError_t launch_round_tma(const OrderedWorkers& ow, float* c, int64_t n, int6
   // no allocation while the stream is being captured: static tiles then
   cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
   cudaStreamIsCapturing(s, &cap);
-  unsigned long long* ctr = stat ? nullptr : round_tile_ctr(dev, cap == cudaStreamCaptureStatusNone);
+  // Dynamic claims only for N >= 4: one counter serves ~60 K tiles per AlexNet-size
+  // round, and with few workers a tile is so little work that the claims on that
+  // one address become the limit (N = 1: 238 vs 153 us per update, static wins).
+  unsigned long long* ctr =
+      (stat || N < 4) ? nullptr : round_tile_ctr(dev, cap == cudaStreamCaptureStatusNone);
   fn<<<grid, kThreads, R::kSmem, s>>>(ow, c, ntiles, n, alpha, ctr);
   return cudaGetLastError();
 }
