@@ -22,7 +22,7 @@ sys.path.insert(0, ROOT)
 from paper_1605_08325_b200 import tm  # noqa: E402
 from paper_1605_08325_b200.inputs import worker_buffer  # noqa: E402
 
-STRESS_ITERS = 60
+STRESS_ITERS = int(os.environ.get("TM_STRESS_ITERS", "60"))
 ASYNC_ROUNDS, ASYNC_TAU, ASYNC_ETA = 6, 2, 0.25
 
 

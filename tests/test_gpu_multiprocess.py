@@ -287,7 +287,7 @@ def test_multiprocess_async_easgd_loop(tmp_path, k):
 @pytest.mark.parametrize("strategy,kernel", [("asa16", "ws"), ("asa", "reg"), ("asa16", "tma"),
                                              ("asa16", "tmaws")])
 def test_multiprocess_stress_random_delays(tmp_path, strategy, kernel):
-    """60 back-to-back exchanges per rank, each after a per-rank delta and a random
+    """STRESS_ITERS (60; TM_STRESS_ITERS overrides) back-to-back exchanges per rank, each after a per-rank delta and a random
     host delay on half of them: every rank ends bitwise at the oracle's sequence."""
     from mp_worker import STRESS_ITERS
     P, k = 50_003, 2
