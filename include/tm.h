@@ -123,6 +123,7 @@ typedef enum {
 #define TM_BIT_NONFINITE 0x1u
 #define TM_BIT_OVERFLOW16 0x2u
 #define TM_BIT_TIMEOUT 0x4u
+#define TM_BIT_LOG_OVERFLOW 0x8u /* test hook: a chunk saw more locked updates than the order log holds */
 
 typedef struct {
   int32_t rank;    /* first global rank hosted by this process                */
@@ -263,7 +264,10 @@ int tm_easgd_update_ex(float* worker_buf, float* center_buf, int64_t n, float al
  * workers[order[t]] against the centre, in one fused pass over the elements.
  * Bitwise equal to norder serial tm_easgd_update calls.  workers: HOST array of
  * nworkers device pointers; order: HOST array of norder indices in
- * [0, nworkers); nworkers <= 16, norder <= 64.  Does not need init. */
+ * [0, nworkers); nworkers <= 16, norder <= 64.  Does not need init.
+ * Rounds over disjoint buffers may run concurrently on different streams: each
+ * launch claims its tiles from its own counter pair (a per-device ring of 64,
+ * so at most 64 rounds may be in flight on a device at once). */
 int tm_easgd_round(float* const* workers, int nworkers, const int32_t* order, int norder,
                    float* center_buf, int64_t n, float alpha, void* stream);
 
@@ -295,7 +299,8 @@ int tm_easgd_update_locked(float* worker_buf, int worker_id, float alpha, void* 
 /* Test hook: record, for every (shard s, chunk q), the worker_ids of locked
  * updates in arrival order into dev_log[(s*nchunk + q)*max + t] (int32,
  * device memory owned by the caller, nchunk = ceil(seg_len/4096)); resets this
- * process's tickets.  NULL disables. */
+ * process's tickets.  Arrivals past `max` per chunk are not logged and set the
+ * sticky status bit TM_BIT_LOG_OVERFLOW (tm_exchange_status).  NULL disables. */
 int tm_easgd_set_order_log(int32_t* dev_log, int max_updates_per_chunk);
 
 /* ----------------------------------------------------------------------------
@@ -336,7 +341,14 @@ typedef struct tm_loader tm_loader;
 
 /* input_x: trainer-owned device buffer of n*c*crop_h*crop_w floats. */
 int tm_loader_create(const tm_loader_config* cfg, float* input_x, tm_loader** out);
-/* kind: TM_LOADER_*; filename for TM_LOADER_FILE (copied). Non-blocking. */
+/* kind: TM_LOADER_*; filename for TM_LOADER_FILE (copied). Non-blocking.
+ * A FILE message releases the loaded batch into input_x (Alg. 1): the copy
+ * is ordered after all work enqueued on `stream` (a cudaStream_t, the trainer's
+ * stream that reads input_x) before this call -- an event recorded on it here,
+ * waited on by the loader's copy -- so queued kernels still reading the previous
+ * batch are never overwritten.  tm_loader_send uses the legacy default stream
+ * (NULL), which covers work on blocking streams only. */
+int tm_loader_send_after(tm_loader* loader, int kind, const char* filename, void* stream);
 int tm_loader_send(tm_loader* loader, int kind, const char* filename);
 /* Block until the next batch is in input_x (timeout_ms < 0: forever).
  * TM_E_IO / TM_E_CUDA / TM_E_ARG (protocol) if the loader failed;

@@ -153,7 +153,14 @@ easgd_locked_kernel(float* __restrict__ x, const __grid_constant__ ShardArgs sa,
         fence_scope<SYS>();  // acquire: the previous holder's centre writes
         // ticket: the arrival position (an atomic so no stale L1 line is read)
         const uint32_t t = SYS ? atomicAdd_system(sa.tickets[s] + q, 1u) : atomicAdd(sa.tickets[s] + q, 1u);
-        if (sa.order_log) sa.order_log[((int64_t)s * nch + q) * sa.log_stride + t] = sa.worker_id;
+        // the log holds log_stride arrivals per chunk: later ones are not recorded
+        // (TM_BIT_LOG_OVERFLOW) instead of spilling into the next chunk's slots
+        if (sa.order_log) {
+          if (t < (uint32_t)sa.log_stride)
+            sa.order_log[((int64_t)s * nch + q) * sa.log_stride + t] = sa.worker_id;
+          else
+            atomicOr(sa.status, TM_BIT_LOG_OVERFLOW);
+        }
       }
       s_go = go;
     }
@@ -403,25 +410,30 @@ easgd_round_tma_kernel(const __grid_constant__ OrderedWorkers ow, float* c, int6
   }
 }
 
-// Per-device claim / retire words for the round kernel's dynamic tiles (the
-// round needs no exchanger context): allocated and zeroed on first use, reset
-// by each launch's last CTA; null if the allocation failed (static tiles then).
+// Per-device ring of kCtrSlots claim / retire pairs for the round kernel's
+// dynamic tiles (the round needs no exchanger context): allocated and zeroed on
+// first use; each launch takes the next pair, so rounds running concurrently on
+// different streams (e.g. two centres) never claim tiles from one counter; each
+// launch's last CTA resets its pair.  Null if the allocation failed (static
+// tiles then).
 unsigned long long* round_tile_ctr(int dev, bool may_allocate) {
   static std::mutex mu;
-  static unsigned long long* ctr[64] = {};
+  static unsigned long long* ring[64] = {};
+  static uint32_t seq[64] = {};
   std::lock_guard<std::mutex> lk(mu);
   if (dev < 0 || dev >= 64) return nullptr;
-  if (!ctr[dev]) {
+  if (!ring[dev]) {
     if (!may_allocate) return nullptr;
     void* p = nullptr;
-    if (cudaMalloc(&p, 2 * sizeof(unsigned long long)) != cudaSuccess) return nullptr;
-    if (cudaMemset(p, 0, 2 * sizeof(unsigned long long)) != cudaSuccess) {
+    const size_t bytes = (size_t)kCtrSlots * 2 * sizeof(unsigned long long);
+    if (cudaMalloc(&p, bytes) != cudaSuccess) return nullptr;
+    if (cudaMemset(p, 0, bytes) != cudaSuccess) {
       cudaFree(p);
       return nullptr;
     }
-    ctr[dev] = static_cast<unsigned long long*>(p);
+    ring[dev] = static_cast<unsigned long long*>(p);
   }
-  return ctr[dev];
+  return ring[dev] + 2 * (size_t)(seq[dev]++ % kCtrSlots);
 }
 
 template <int N>

@@ -13,6 +13,9 @@ constexpr int kThreads = 256;       // threads per CTA of every kernel
 constexpr int kVec = 8;             // elements per vector unit (16 B of fp16)
 constexpr int64_t kAlign = 256;     // segment / chunk alignment in elements
 constexpr int64_t kMinChunk = 2048; // smallest per-CTA chunk worth a barrier
+// Tile-claim counter pairs per exchanger / per device (EASGD rounds): up to this
+// many dynamic-tile launches may be in flight at once on different streams.
+constexpr int kCtrSlots = 64;
 
 // Flag pad of one rank: u32 flags[kPhases][TM_MAX_RANKS][C] followed by the
 // per-CTA epoch counters u32 ctr[C]; slot [phase][src][c] is written by rank

@@ -59,7 +59,12 @@ struct tm_loader {
   std::thread th;
   std::mutex mu;
   std::condition_variable cv_msg, cv_ready;
-  std::deque<std::pair<int, std::string>> q;
+  struct Msg {
+    int kind;
+    std::string file;
+    cudaEvent_t after;  // FILE: the trainer's work that reads input_x (null = none)
+  };
+  std::deque<Msg> q;
   uint64_t delivered = 0, consumed = 0;
   int error = TM_OK;
   bool exited = false;
@@ -177,12 +182,17 @@ int load_and_preprocess(tm_loader* L, int mode, const std::string& path) {
   return TM_OK;
 }
 
-std::pair<int, std::string> recv(tm_loader* L) {
+tm_loader::Msg recv(tm_loader* L) {
   std::unique_lock<std::mutex> lk(L->mu);
   L->cv_msg.wait(lk, [&] { return !L->q.empty(); });
   auto m = L->q.front();
   L->q.pop_front();
   return m;
+}
+
+void drop_event(tm_loader::Msg& m) {
+  if (m.after) cudaEventDestroy(m.after);
+  m.after = nullptr;
 }
 
 void fail(tm_loader* L, int rc) {
@@ -193,20 +203,22 @@ void fail(tm_loader* L, int rc) {
 
 void loader_main(tm_loader* L) {
   cudaSetDevice(L->cfg.device);
-  std::pair<int, std::string> msg = recv(L);  // L330
+  tm_loader::Msg msg = recv(L);  // L330
   for (;;) {
-    if (msg.first == TM_LOADER_STOP) break;  // L331-332
-    if (msg.first != TM_LOADER_TRAIN && msg.first != TM_LOADER_VAL) {
+    drop_event(msg);  // nothing to order before a mode message or the first file
+    if (msg.kind == TM_LOADER_STOP) break;  // L331-332
+    if (msg.kind != TM_LOADER_TRAIN && msg.kind != TM_LOADER_VAL) {
       fail(L, TM_E_ARG);  // protocol violation: a filename where a mode was due
       break;
     }
-    const int mode = msg.first;  // L334
-    msg = recv(L);               // L336: the first filename
-    if (msg.first != TM_LOADER_FILE) {
+    const int mode = msg.kind;  // L334
+    msg = recv(L);              // L336: the first filename
+    drop_event(msg);
+    if (msg.kind != TM_LOADER_FILE) {
       fail(L, TM_E_ARG);
       break;
     }
-    std::string filename = msg.second;
+    std::string filename = msg.file;
     bool stop_outer = false;
     for (;;) {
       const int rc = load_and_preprocess(L, mode, filename);  // L339-342
@@ -216,13 +228,20 @@ void loader_main(tm_loader* L) {
         break;
       }
       msg = recv(L);  // L343: wait for training on the last input_x
-      if (msg.first != TM_LOADER_FILE) break;  // L344-345 (msg feeds the outer loop)
-      filename = msg.second;                   // L347
+      if (msg.kind != TM_LOADER_FILE) break;  // L344-345 (msg feeds the outer loop)
+      filename = msg.file;                    // L347
       const tm_loader_config& c = L->cfg;
       const size_t out_bytes = (size_t)c.n * c.c * c.crop_h * c.crop_w * sizeof(float);
-      if (cudaMemcpyAsync(L->input_x, L->gpudata, out_bytes, cudaMemcpyDeviceToDevice, L->stream) !=
-              cudaSuccess ||
-          cudaStreamSynchronize(L->stream) != cudaSuccess) {  // L350-351
+      // The trainer's kernels that read input_x may still be queued on its stream
+      // when the FILE message arrives: the copy waits for the event recorded on
+      // that stream at send time, so it cannot overwrite input_x under them.
+      const bool ok_wait = !msg.after || cudaStreamWaitEvent(L->stream, msg.after, 0) == cudaSuccess;
+      const bool ok = ok_wait &&
+                      cudaMemcpyAsync(L->input_x, L->gpudata, out_bytes, cudaMemcpyDeviceToDevice,
+                                      L->stream) == cudaSuccess &&
+                      cudaStreamSynchronize(L->stream) == cudaSuccess;  // L350-351
+      drop_event(msg);
+      if (!ok) {
         fail(L, TM_E_CUDA);
         stop_outer = true;
         break;
@@ -235,8 +254,10 @@ void loader_main(tm_loader* L) {
     }
     if (stop_outer) break;
   }
+  drop_event(msg);
   std::lock_guard<std::mutex> lk(L->mu);
   L->exited = true;
+  for (auto& m : L->q) drop_event(m);
   L->cv_ready.notify_all();
 }
 
@@ -286,16 +307,30 @@ int tm_loader_create(const tm_loader_config* cfg, float* input_x, tm_loader** ou
   return TM_OK;
 }
 
-int tm_loader_send(tm_loader* L, int kind, const char* filename) {
+int tm_loader_send_after(tm_loader* L, int kind, const char* filename, void* stream) {
   if (!L) return TM_E_ARG;
   if (kind < TM_LOADER_TRAIN || kind > TM_LOADER_FILE) return TM_E_ARG;
   if (kind == TM_LOADER_FILE && !filename) return TM_E_ARG;
+  cudaEvent_t ev = nullptr;
+  if (kind == TM_LOADER_FILE) {  // the trainer's work enqueued so far on `stream`
+    if (cudaSetDevice(L->cfg.device) != cudaSuccess ||
+        cudaEventCreateWithFlags(&ev, cudaEventDisableTiming) != cudaSuccess)
+      return TM_E_CUDA;
+    if (cudaEventRecord(ev, static_cast<cudaStream_t>(stream)) != cudaSuccess) {
+      cudaEventDestroy(ev);
+      return TM_E_CUDA;
+    }
+  }
   {
     std::lock_guard<std::mutex> lk(L->mu);
-    L->q.emplace_back(kind, kind == TM_LOADER_FILE ? std::string(filename) : std::string());
+    L->q.push_back({kind, kind == TM_LOADER_FILE ? std::string(filename) : std::string(), ev});
   }
   L->cv_msg.notify_all();
   return TM_OK;
+}
+
+int tm_loader_send(tm_loader* L, int kind, const char* filename) {
+  return tm_loader_send_after(L, kind, filename, nullptr);  // legacy default stream
 }
 
 int tm_loader_wait(tm_loader* L, int64_t timeout_ms) {
@@ -318,7 +353,7 @@ int tm_loader_destroy(tm_loader* L) {
   if (!L) return TM_OK;
   {
     std::lock_guard<std::mutex> lk(L->mu);
-    L->q.emplace_back(TM_LOADER_STOP, std::string());
+    L->q.push_back({TM_LOADER_STOP, std::string(), nullptr});
   }
   L->cv_msg.notify_all();
   if (L->th.joinable()) L->th.join();

@@ -37,7 +37,7 @@ struct NvtxRange {
 };
 
 constexpr uint32_t kMagic = 0x544d4558u;  // "TMEX"
-constexpr uint32_t kVersion = 2;
+constexpr uint32_t kVersion = 3;
 constexpr uint64_t kDefaultTimeoutNs = 10ull * 1000 * 1000 * 1000;
 
 struct Blob {
@@ -47,6 +47,12 @@ struct Blob {
   int64_t off_stage, off_avg, off_flags, off_center;
   int32_t has_nccl, device_ordinal;
   int32_t ag_nccl;  // TM_ALLGATHER=nccl at init: every rank must agree (a collective)
+  // Staged kernel flavour and allgather mode chosen at init (TM_STAGED_KERNEL /
+  // TM_ALLGATHER can differ per process): the flavours use different flag phases
+  // (READY_0..3 + REDUCED = 4 for the warp-specialised ones, READY = 0 and
+  // REDUCED = 1 for the others), so ranks running different flavours would read
+  // each other's READY_1 as REDUCED.  Every rank must agree.
+  int32_t staged_kernel, ag_mode;
   cudaIpcMemHandle_t handle;
   ncclUniqueId nccl_id;
 };
@@ -93,6 +99,12 @@ struct Ctx {
   char* peer_base[TM_MAX_RANKS] = {};  // per process (only the opened ones)
   char* rank_base[TM_MAX_RANKS] = {};  // per global rank, as mapped on this device
   uint32_t epoch = 0;
+  // Tile-claim counters of the dynamic-tile kernels (direct, BSP): a ring of
+  // kCtrSlots (claim, retire) pairs after the status word; each launch takes the
+  // next slot, so launches running concurrently on different streams never share
+  // a counter (a kernel resets its pair when its last CTA retires).
+  unsigned long long* tile_ctrs = nullptr;
+  uint32_t ctr_seq = 0;
   int path = TM_PATH_AUTO;
   int staged_kernel = tmx::kStagedTma;  // staged kernel flavour, fixed at init (it sets C)
   int ag_mode = TM_AG_SM;               // tm_allgather of the staged path
@@ -136,6 +148,11 @@ void release() {
   }
   if (g.slab) cudaFree(g.slab);
   g = Ctx();
+}
+
+// The next launch's tile-claim counter pair (see Ctx::tile_ctrs).
+unsigned long long* next_tile_ctr() {
+  return g.tile_ctrs + 2 * (size_t)(g.ctr_seq++ % tmx::kCtrSlots);
 }
 
 // Launch arguments for an exchange of elements [off, off + n) of the callers'
@@ -245,8 +262,7 @@ int do_exchange(float* const* bufs, int nbufs, int64_t off, int64_t n, cudaStrea
     float* shifted[TM_MAX_RANKS];
     for (int i = 0; i < nbufs; ++i) shifted[i] = bufs[i] + off;
     const char* st_env = getenv("TM_DIRECT_STATIC");  // diagnostics: static tile assignment
-    unsigned long long* ctr =
-        (st_env && st_env[0] == '1') ? nullptr : reinterpret_cast<unsigned long long*>(g.status + 16);
+    unsigned long long* ctr = (st_env && st_env[0] == '1') ? nullptr : next_tile_ctr();
     cudaError_t e = tmx::launch_direct(shifted, g.k, n, g.strategy == TM_ASA16, g.sum, g.status, ctr, s);
     return e == cudaSuccess ? TM_OK : cuda_fail("launch_direct", e);
   }
@@ -285,7 +301,7 @@ int do_bsp(float* const* w, float* const* v, const float* const* gr, int nbufs, 
     bb.lr = lr;
     bb.mu = mu;
     cudaError_t e = tmx::launch_bsp_direct(bb, g.k, g.P, g.strategy == TM_ASA16, mom != 0, g.status,
-                                           reinterpret_cast<unsigned long long*>(g.status + 16), s);
+                                           next_tile_ctr(), s);
     return e == cudaSuccess ? TM_OK : cuda_fail("launch_bsp_direct", e);
   }
   int rc = TM_OK;
@@ -422,7 +438,8 @@ int tm_exchange_init(int64_t nparams, const tm_world* world, int strategy) {
   } else {
     c.rank_stride = 0;
   }
-  c.slab_bytes = c.rank_stride * c.nlocal + 256;  // + status word (+0), tile claim / retire counters (+64, +72)
+  // + status word (+0) and the ring of tile-claim counter pairs (+256)
+  c.slab_bytes = c.rank_stride * c.nlocal + 256 + tmx::kCtrSlots * 16;
   e = cudaMalloc(reinterpret_cast<void**>(&c.slab), c.slab_bytes);
   if (e != cudaSuccess) return cuda_fail("cudaMalloc", e);
   e = cudaMemset(c.slab, 0, c.slab_bytes);
@@ -431,6 +448,7 @@ int tm_exchange_init(int64_t nparams, const tm_world* world, int strategy) {
     return cuda_fail("cudaMemset", e);
   }
   c.status = reinterpret_cast<uint32_t*>(c.slab + c.rank_stride * c.nlocal);
+  c.tile_ctrs = reinterpret_cast<unsigned long long*>(c.slab + c.rank_stride * c.nlocal + 256);
   c.inited = true;
   c.ready = (c.nprocs == 1);
   g = c;
@@ -473,6 +491,8 @@ int tm_bootstrap_export(void* blob, size_t* len) {
   b.off_center = g.off_center;
   b.device_ordinal = g.device;
   b.ag_nccl = g.want_nccl_ag ? 1 : 0;
+  b.staged_kernel = g.staged_kernel;
+  b.ag_mode = g.ag_mode;
   cudaSetDevice(g.device);
   cudaError_t e = cudaIpcGetMemHandle(&b.handle, g.slab);
   if (e != cudaSuccess) return cuda_fail("cudaIpcGetMemHandle", e);
@@ -501,8 +521,8 @@ int tm_bootstrap_import(const void* blobs, size_t len_each) {
     if (b.P != g.P || b.size != g.k || b.strategy != (g.strategy | (g.sum ? TM_OP_SUM : 0)) ||
         b.C != g.C || b.L != g.L ||
         b.Lc != g.Lc || b.nlocal != g.nlocal || b.rank_stride != g.rank_stride ||
-        b.ag_nccl != (g.want_nccl_ag ? 1 : 0) ||
-        b.rank0 != q * g.nlocal)
+        b.ag_nccl != (g.want_nccl_ag ? 1 : 0) || b.staged_kernel != g.staged_kernel ||
+        b.ag_mode != g.ag_mode || b.rank0 != q * g.nlocal)
       return TM_E_MISMATCH;
     if (b.has_nccl) nccl_blob = reinterpret_cast<const Blob*>(p + (size_t)q * len_each);
     if (q == g.proc) continue;

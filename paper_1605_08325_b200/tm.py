@@ -86,6 +86,7 @@ _SIGS = {
     "tm_cast_rn16": (ctypes.c_int, [_P, _P, ctypes.c_int64, _P]),
     "tm_loader_create": (ctypes.c_int, [_P, _P, _P]),
     "tm_loader_send": (ctypes.c_int, [_P, ctypes.c_int, ctypes.c_char_p]),
+    "tm_loader_send_after": (ctypes.c_int, [_P, ctypes.c_int, ctypes.c_char_p, _P]),
     "tm_loader_wait": (ctypes.c_int, [_P, ctypes.c_int64]),
     "tm_loader_destroy": (ctypes.c_int, [_P]),
 }
@@ -136,13 +137,36 @@ def _stream_handle(stream):
     return ctypes.c_void_p(stream.cuda_stream)
 
 
-def _fp32_cuda(t, n=None):
+# What the process's exchanger was initialised with (set by tm_exchange_init,
+# cleared by tm_exchange_finalize): the C ABI takes bare device pointers and
+# cannot check a tensor's length or device, so the wrappers do, before a short
+# tensor or one on another GPU reaches a kernel.
+_ctx = {}
+
+
+def _fp32_cuda(t, n=None, min_n=None):
     if not (isinstance(t, torch.Tensor) and t.is_cuda and t.dtype == torch.float32
             and t.is_contiguous()):
         raise TypeError("expected a contiguous float32 CUDA tensor")
     if n is not None and t.numel() != n:
         raise ValueError(f"expected {n} elements, got {t.numel()}")
+    if min_n is not None and t.numel() < min_n:
+        raise ValueError(f"expected at least {min_n} elements, got {t.numel()}")
     return ctypes.c_void_p(t.data_ptr())
+
+
+def _param_buf(t):
+    """A caller buffer of the exchanger: fp32[nparams] on the exchanger's device."""
+    p = _fp32_cuda(t, n=_ctx.get("nparams"))
+    if "device" in _ctx and t.device.index != _ctx["device"]:
+        raise ValueError(f"tensor on cuda:{t.device.index}, exchanger on cuda:{_ctx['device']}")
+    return p
+
+
+def _check_range(offset, count):
+    P = _ctx.get("nparams")
+    if offset < 0 or count < 0 or (P is not None and offset + count > P):
+        raise ValueError(f"range [{offset}, {offset + count}) outside [0, {P})")
 
 
 # ------------------------------------------------------------------ raw calls
@@ -150,6 +174,8 @@ def _fp32_cuda(t, n=None):
 def tm_exchange_init(nparams, rank, size, device, nlocal, strategy):
     w = tm_world(rank, size, device, nlocal)
     _check(lib().tm_exchange_init(int(nparams), ctypes.byref(w), int(strategy)), "tm_exchange_init")
+    _ctx.clear()
+    _ctx.update(nparams=int(nparams), device=int(device), nlocal=int(nlocal))
 
 
 def tm_bootstrap_export():
@@ -166,47 +192,53 @@ def tm_bootstrap_import(blobs):
 
 
 def tm_exchange(buf, stream=None):
-    _check(lib().tm_exchange(_fp32_cuda(buf), _stream_handle(stream)), "tm_exchange")
+    _check(lib().tm_exchange(_param_buf(buf), _stream_handle(stream)), "tm_exchange")
 
 
 def tm_exchange_group(bufs, stream=None):
-    arr = (ctypes.c_void_p * len(bufs))(*[_fp32_cuda(b).value for b in bufs])
+    arr = (ctypes.c_void_p * len(bufs))(*[_param_buf(b).value for b in bufs])
     _check(lib().tm_exchange_group(arr, len(bufs), _stream_handle(stream)), "tm_exchange_group")
 
 
 def tm_exchange_range(buf, offset, count, stream=None):
-    _check(lib().tm_exchange_range(_fp32_cuda(buf), int(offset), int(count), _stream_handle(stream)),
+    _check_range(int(offset), int(count))
+    _check(lib().tm_exchange_range(_param_buf(buf), int(offset), int(count), _stream_handle(stream)),
            "tm_exchange_range")
 
 
 def tm_exchange_group_range(bufs, offset, count, stream=None):
-    arr = (ctypes.c_void_p * len(bufs))(*[_fp32_cuda(b).value for b in bufs])
+    _check_range(int(offset), int(count))
+    arr = (ctypes.c_void_p * len(bufs))(*[_param_buf(b).value for b in bufs])
     _check(lib().tm_exchange_group_range(arr, len(bufs), int(offset), int(count),
                                          _stream_handle(stream)), "tm_exchange_group_range")
 
 
 def tm_bsp_step(w, v, grad, lr, mu, exchange_momentum=False, stream=None):
-    _check(lib().tm_bsp_step(_fp32_cuda(w), _fp32_cuda(v), _fp32_cuda(grad), ctypes.c_float(lr),
+    _check(lib().tm_bsp_step(_param_buf(w), _param_buf(v), _param_buf(grad), ctypes.c_float(lr),
                              ctypes.c_float(mu), int(bool(exchange_momentum)), _stream_handle(stream)),
            "tm_bsp_step")
 
 
 def tm_bsp_step_group(ws, vs, grads, lr, mu, exchange_momentum=False, stream=None):
     n = len(ws)
-    arr = lambda ts: (ctypes.c_void_p * n)(*[_fp32_cuda(t).value for t in ts])  # noqa: E731
+    arr = lambda ts: (ctypes.c_void_p * n)(*[_param_buf(t).value for t in ts])  # noqa: E731
     _check(lib().tm_bsp_step_group(arr(ws), arr(vs), arr(grads), n, ctypes.c_float(lr),
                                    ctypes.c_float(mu), int(bool(exchange_momentum)),
                                    _stream_handle(stream)), "tm_bsp_step_group")
 
 
 def tm_easgd_update(worker, center, alpha, stream=None):
-    _check(lib().tm_easgd_update(_fp32_cuda(worker), _P(center if isinstance(center, int) else center.data_ptr()),
-                                 ctypes.c_float(alpha), _stream_handle(stream)), "tm_easgd_update")
+    P = _ctx.get("nparams")
+    cptr = center if isinstance(center, int) else _fp32_cuda(center, min_n=P).value
+    _check(lib().tm_easgd_update(_param_buf(worker), _P(cptr), ctypes.c_float(alpha), _stream_handle(stream)),
+           "tm_easgd_update")
 
 
 def tm_easgd_update_ex(worker, center, alpha, concurrent=False, stream=None, n=None):
-    n = worker.numel() if n is None else n
-    cptr = center if isinstance(center, int) else _fp32_cuda(center).value
+    n = worker.numel() if n is None else int(n)
+    if n < 0 or n > worker.numel():
+        raise ValueError(f"n = {n} outside [0, {worker.numel()}]")
+    cptr = center if isinstance(center, int) else _fp32_cuda(center, min_n=n).value
     _check(lib().tm_easgd_update_ex(_fp32_cuda(worker), _P(cptr), int(n), ctypes.c_float(alpha),
                                     int(bool(concurrent)), _stream_handle(stream)), "tm_easgd_update_ex")
 
@@ -220,13 +252,13 @@ def tm_easgd_round(workers, order, center, alpha, stream=None):
 
 
 def tm_easgd_update_sharded(worker, alpha, concurrent=False, stream=None):
-    _check(lib().tm_easgd_update_sharded(_fp32_cuda(worker), ctypes.c_float(alpha),
+    _check(lib().tm_easgd_update_sharded(_param_buf(worker), ctypes.c_float(alpha),
                                          int(bool(concurrent)), _stream_handle(stream)),
            "tm_easgd_update_sharded")
 
 
 def tm_easgd_update_locked(worker, worker_id, alpha, stream=None):
-    _check(lib().tm_easgd_update_locked(_fp32_cuda(worker), int(worker_id), ctypes.c_float(alpha),
+    _check(lib().tm_easgd_update_locked(_param_buf(worker), int(worker_id), ctypes.c_float(alpha),
                                         _stream_handle(stream)), "tm_easgd_update_locked")
 
 
@@ -274,6 +306,7 @@ def tm_set_phase_log(buf):
 
 
 def tm_exchange_finalize():
+    _ctx.clear()
     _check(lib().tm_exchange_finalize(), "tm_exchange_finalize")
 
 
@@ -341,11 +374,14 @@ class Loader:
         _check(lib().tm_loader_create(ctypes.byref(cfg), ctypes.c_void_p(input_x.data_ptr()),
                                       ctypes.byref(self._h)), "tm_loader_create")
 
-    def send(self, kind, filename=None):
+    def send(self, kind, filename=None, stream=None):
+        """A FILE message's copy into input_x waits for the work enqueued so far
+        on `stream` (default: the current stream), i.e. the trainer's kernels
+        still reading the previous batch."""
         k = {"train": TM_LOADER_TRAIN, "val": TM_LOADER_VAL, "stop": TM_LOADER_STOP,
              "file": TM_LOADER_FILE}[kind]
-        _check(lib().tm_loader_send(self._h, k, None if filename is None else filename.encode()),
-               "tm_loader_send")
+        _check(lib().tm_loader_send_after(self._h, k, None if filename is None else filename.encode(),
+                                          _stream_handle(stream)), "tm_loader_send_after")
 
     def wait(self, timeout_ms=-1):
         _check(lib().tm_loader_wait(self._h, int(timeout_ms)), "tm_loader_wait")

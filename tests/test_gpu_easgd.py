@@ -86,6 +86,34 @@ def test_fused_round_equals_arrival_order_sequence(order, n):
         assert_bitwise(gW[r], wW[r], f"worker {r}")
 
 
+def test_concurrent_rounds_on_two_streams_bitwise():
+    """Two servers' rounds (disjoint centres and workers) issued on two streams
+    with no ordering between them, three times each: the dynamic-tile round
+    kernel claims tiles from a per-launch counter pair (a per-device ring), so
+    concurrent launches never split each other's tile claims.  Each centre and
+    worker set ends bitwise at the oracle's arrival-order sequence."""
+    n, nw = 3_000_017, 8
+    orders = [[0, 1, 2, 3, 4, 5, 6, 7], [5, 3, 1, 7, 0, 2, 6, 4]]
+    Ws = [[worker_buffer(n, "D2", 10 * s + r, config=46) for r in range(nw)] for s in range(2)]
+    cs = [worker_buffer(n, "D2", 90 + s, config=46) for s in range(2)]
+    Wds = [to_dev(W) for W in Ws]
+    cds = [to_dev([c])[0] for c in cs]
+    streams = [torch.cuda.Stream(), torch.cuda.Stream()]
+    torch.cuda.synchronize()
+    for _ in range(3):
+        for s in range(2):
+            tm.tm_easgd_round(Wds[s], orders[s], cds[s], 0.5 / 8, stream=streams[s])
+    torch.cuda.synchronize()
+    for s in range(2):
+        wW, wc = Ws[s], cs[s]
+        for _ in range(3):
+            wW, wc = easgd_sequence(wW, wc, 0.5 / 8, orders[s])
+        assert_bitwise(to_host([cds[s]])[0], wc, f"centre {s}")
+        gW = to_host(Wds[s])
+        for r in range(nw):
+            assert_bitwise(gW[r], wW[r], f"server {s} worker {r}")
+
+
 def test_concurrent_workers_invariants():
     """8 workers update one centre concurrently from 8 streams (Q15: no bitwise
     oracle).  Invariants: sum_w x_w + c conserved within the rounding bound, and

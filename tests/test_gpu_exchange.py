@@ -442,3 +442,23 @@ def test_random_bit_patterns(path, strategy):
             assert_bitwise(got[r], want[r], f"{strategy} {path} k={k} rank {r}")
         if strategy == "asa16":
             assert bits_ & tm.TM_BIT_OVERFLOW16
+
+
+def test_binding_rejects_short_buffers_and_bad_ranges():
+    """The C ABI takes bare pointers; the binding checks every caller buffer's
+    length against nparams and a range against [0, nparams) before any launch
+    (a short tensor would otherwise be read / written out of bounds)."""
+    import pytest as _pt
+    P, k = 10_000, 2
+    bufs = [torch.zeros(P, device="cuda") for _ in range(k)]
+    with tm.Exchanger(P, "asa16", size=k, nlocal=k) as ex:
+        with _pt.raises(ValueError):
+            ex.exchange([bufs[0], bufs[1][:-4]])
+        with _pt.raises(ValueError):
+            ex.exchange_range(bufs, P - 8, 16)
+        with _pt.raises(ValueError):
+            ex.exchange_range(bufs, -4, 8)
+        with _pt.raises(ValueError):
+            ex.bsp_step(bufs, bufs, [bufs[0], bufs[1][:100]], 0.1, 0.9)
+        ex.exchange(bufs)  # still usable
+        assert ex.status()[0] == tm.TM_OK

@@ -115,3 +115,31 @@ def test_loading_overlaps_training(tmp_path):
     total = run(load)
     n = len(files) - 1
     assert total <= 0.75 * n * (2 * load) + 0.05, (total, load)
+
+
+def test_file_message_waits_for_trainer_stream(tmp_path):
+    """A FILE message releases the loaded batch into input_x (Alg. 1); the
+    trainer's kernels that still read the previous batch may be queued on its
+    stream when the message is sent, so the loader's copy waits for the work
+    enqueued on that stream before the send (tm_loader_send_after).  Here the
+    trainer's stream sleeps ~0.1 s and then snapshots input_x: the snapshot must
+    be the PREVIOUS batch, not the one the message releases."""
+    paths, raws, mean = _files(tmp_path, 3)
+    f0, f1, f2 = paths
+    x = torch.zeros(N * C * CH * CW, device="cuda")
+    s = torch.cuda.Stream()
+    with tm.Loader(N, C, H, W, CH, CW, mean, x, seed=5) as L:
+        L.send("train"); L.send("file", f0)
+        L.send("file", f1); L.wait(10_000)  # input_x = batch f0 (load 0)
+        want0 = x.clone()
+        torch.cuda.synchronize()
+        with torch.cuda.stream(s):
+            torch.cuda._sleep(200_000_000)  # the trainer is still busy ...
+            snap = x.clone()                # ... and then reads input_x
+            L.send("file", f2, stream=s)    # releases batch f1 into input_x
+        L.wait(10_000)
+        torch.cuda.synchronize()
+        after = x.clone()
+    assert_bitwise(snap.cpu().numpy(), want0.cpu().numpy(), "trainer's read of the previous batch")
+    want1 = ol.preprocess(raws[f1], mean, CH, CW, "train", 5, 1)
+    assert_bitwise(after.cpu().numpy(), want1.reshape(-1), "released batch")
