@@ -50,9 +50,10 @@
  *
  * Environment (read at tm_exchange_init unless noted; every rank of a group must
  * use the same values):
- *   TM_STAGED_KERNEL=reg|tma|ws|tmaws  staged kernel flavour (default: reg for
- *                      segments <= 64 Ki elements, else tma in a single-process
- *                      group and tmaws across processes).
+ *   TM_STAGED_KERNEL=reg|tma|ws|tmaws|oneshot  staged kernel flavour (default:
+ *                      oneshot for segments L <= TM_ONESHOT_MAX_L elements
+ *                      (default 16 Ki), reg for L <= 64 Ki, else tma in a
+ *                      single-process group and tmaws across processes).
  *   TM_ALLGATHER=sm|ce|nccl            allgather mode (tm_set_allgather); nccl
  *                      also creates the NCCL communicator at bootstrap.
  *   TM_PROCS_PER_GPU=n                 n processes share this GPU concurrently
@@ -145,8 +146,11 @@ typedef struct {
   uint32_t epoch;        /* number of staged exchanges issued so far          */
   int32_t path;          /* effective tm_path of the next exchange            */
   int32_t staged_kernel; /* staged flavour: 0 register, 1 TMA engine, 2 warp-specialised,
-                            3 warp-specialised on the TMA engine */
+                            3 warp-specialised on the TMA engine, 4 one-shot */
   int32_t allgather;     /* tm_allgather mode of the staged path                */
+  int32_t selfcheck;     /* bootstrap known-answer check: 0 not run, 1 passed,
+                            2 the chosen flavour failed and every rank fell back
+                            to the register flavour (staged_kernel = 0)        */
 } tm_layout_info;
 
 /* How an ASA / ASA16 exchange moves data (results are bitwise identical):
@@ -195,9 +199,15 @@ int tm_bootstrap_export(void* blob, size_t* len);
 
 /* `blobs` holds size/nlocal blobs of `len_each` bytes, in process order
  * (process p hosts ranks [p*nlocal, (p+1)*nlocal)).  Opens the peers' IPC
- * mappings, checks that every process agrees on nparams, strategy and layout
- * (else TM_E_MISMATCH), and for AR initialises the NCCL communicator
- * (collective: every process must call it). */
+ * mappings, checks that every process agrees on nparams, strategy, layout,
+ * staged flavour and allgather mode (else TM_E_MISMATCH), and for AR
+ * initialises the NCCL communicator (collective: every process must call it).
+ * ASA / ASA16 then run a known-answer self-check of the staged flavour over the
+ * peer mappings: a probe exchange whose average is exact by construction,
+ * checked bit for bit on every rank, with a vote through peer memory; if any
+ * rank fails, all ranks fall back to the register flavour (tm_layout
+ * selfcheck = 2).  TM_E_TIMEOUT if the probe or the vote times out,
+ * TM_E_MISMATCH if the register flavour fails too.  TM_SELFCHECK=0 skips it. */
 int tm_bootstrap_import(const void* blobs, size_t len_each);
 
 /* North-star call: average dev_buf (fp32[nparams], this rank's device, 16-byte

@@ -18,9 +18,13 @@ constexpr int64_t kMinChunk = 2048; // smallest per-CTA chunk worth a barrier
 constexpr int kCtrSlots = 64;
 
 // Flag pad of one rank: u32 flags[kPhases][TM_MAX_RANKS][C] followed by the
-// per-CTA epoch counters u32 ctr[C]; slot [phase][src][c] is written by rank
-// `src` (remote store) and spun on by the owner of the pad; ctr[c] is private
-// to CTA c of the owner.
+// per-CTA epoch counters u32 ctr[C] and a tail of kPadTail words; slot
+// [phase][src][c] is written by rank `src` (remote store) and spun on by the
+// owner of the pad; ctr[c] is private to CTA c of the owner.  Tail: [0] calls,
+// [1] retire -- the one-shot kernel's per-rank call counter (the last CTA of a
+// launch to retire increments `calls`, so every CTA of a launch reads the same
+// value: the staging parity of the call) -- and [8 + src] the bootstrap
+// self-check votes of rank src.
 constexpr int kPhaseReady = 0;    // src finished its pre-cast of chunk c
 constexpr int kPhaseReduced = 1;  // src finished summing its segment's chunk c
 // The warp-specialised staged kernel splits a chunk into kWsSub sub-chunks with
@@ -28,6 +32,12 @@ constexpr int kPhaseReduced = 1;  // src finished summing its segment's chunk c
 // for kPhases phases; the per-CTA epoch counters follow them.
 constexpr int kWsSub = 4;
 constexpr int kPhases = kWsSub + 1;
+constexpr int kPadTail = 16;
+constexpr int kTailCalls = 0, kTailRetire = 1, kTailVotes = 8;
+// Sub-chunk length of the warp-specialised kernels: a chunk is split into at
+// most kWsSub sub-chunks of at least kWsMinSub elements (fewer flag rounds for
+// small chunks, where each round costs more than the overlap gains).
+constexpr int64_t kWsMinSub = 8192;
 
 struct ExchangeArgs {
   void* stage[TM_MAX_RANKS];      // rank j's staging (k*L wire elems), as mapped here
@@ -52,6 +62,14 @@ struct ExchangeArgs {
   // Allgather outside the kernel (TM_AG_CE / TM_AG_NCCL): the kernel returns
   // after the REDUCED barrier and skips a6.
   int32_t ag_external;
+  // Vectors exchanged by this launch: 1, or 2 for the BSP step with momentum
+  // exchange (sgd != 0): vector 0 is w' (into x), vector 1 is v' (into v), both
+  // through the same barriers.  Vector q's wire staging starts q * stage_stride
+  // bytes after stage[j] (the one-shot kernel adds its parity buffers after
+  // those: buffer (parity * nvec_alloc + q)), its averaged segment q *
+  // avg_stride bytes after avg[j].
+  int32_t nvec, nvec_alloc;
+  int64_t stage_stride, avg_stride;
 };
 
 // Persistent fused exchange: pre-cast -> ready barrier -> reduce-scatter pull with
@@ -62,7 +80,15 @@ constexpr int kStampSlots = 8;
 enum { kStampStart = 0, kStampCast = 1, kStampReady = 2, kStampReduce = 3, kStampReduced = 4,
        kStampEnd = 5 };
 // Staged kernel flavours.
-enum StagedKernel { kStagedReg = 0, kStagedTma = 1, kStagedWs = 2, kStagedTmaWs = 3 };
+//   kStagedOneShot: one READY barrier per call; every rank pulls every rank's
+//   whole staging and reduces ALL segments itself in rank order (bitwise the
+//   same average, no reduce-scatter / allgather split, no REDUCED barrier);
+//   staging double-buffered by call parity.  Small segments only: it moves
+//   (k-1) P s bytes per rank over the links instead of 2 (k-1)/k P s.
+enum StagedKernel { kStagedReg = 0, kStagedTma = 1, kStagedWs = 2, kStagedTmaWs = 3, kStagedOneShot = 4 };
+// Per-CTA chunk granularity of the one-shot kernel (each CTA reduces its chunk
+// of all k segments, k times the work of a two-phase CTA per element).
+constexpr int64_t kOneShotChunk = 512;
 cudaError_t launch_exchange(const ExchangeArgs& a, int nlocal, bool wire16, int flavour, cudaStream_t s);
 
 // Single-process group, one pass (the "direct" path): pull the k contributions

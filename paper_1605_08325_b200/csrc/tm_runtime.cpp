@@ -20,7 +20,9 @@
 #include <unistd.h>
 
 #include <algorithm>
+#include <chrono>
 #include <mutex>
+#include <vector>
 
 #include "tm.h"
 #include "tm_internal.h"
@@ -88,6 +90,9 @@ struct Ctx {
   int k = 0, rank0 = 0, nlocal = 0, device = 0, strategy = 0, C = 0;
   int nprocs = 1, proc = 0;
   int64_t rank_stride = 0, off_stage = 0, off_avg = 0, off_flags = 0, off_center = 0;
+  int64_t stage_stride = 0, avg_stride = 0;  // bytes between staging / avg buffers (vectors, parities)
+  int nvec_alloc = 2;                        // staging buffers per parity (w and v of a BSP step)
+  int selfcheck = 0;                         // bootstrap known-answer check: 0 not run, 1 passed, 2 fell back
   int64_t off_locks = 0, off_tickets = 0;  // EASGD locked mode
   int32_t* order_log = nullptr;            // test hook (tm_easgd_set_order_log)
   uint64_t* stamps = nullptr;              // diagnostics (tm_set_phase_log)
@@ -119,6 +124,18 @@ struct Ctx {
 Ctx g;
 Nccl g_nccl;
 std::mutex g_mu;
+
+// Flavour thresholds by segment length L (elements per rank), from the r02
+// latency table (profiles/r02/latency_flavours.txt): one-shot up to
+// kOneShotMaxL, the register two-phase kernel up to kRegMaxL, the TMA-engine
+// kernels above.
+constexpr int64_t kOneShotMaxL = 16384;
+constexpr int64_t kRegMaxL = 65536;
+
+int64_t env_i64(const char* name, int64_t dflt) {
+  const char* v = getenv(name);
+  return (v && *v) ? atoll(v) : dflt;
+}
 
 bool wire16(int strategy) { return strategy == TM_ASA16; }
 int wire_bytes(int strategy) { return wire16(strategy) ? 2 : 4; }
@@ -175,10 +192,15 @@ ExchangeArgs make_args(float* const* bufs, int64_t off, int64_t n) {
     a.C = g.C;
   } else {
     a.L = round_up((n + g.k - 1) / g.k, tmx::kAlign);
-    const int64_t want = std::max<int64_t>(1, (a.L + tmx::kMinChunk - 1) / tmx::kMinChunk);
+    const int64_t chunk = g.staged_kernel == tmx::kStagedOneShot ? tmx::kOneShotChunk : tmx::kMinChunk;
+    const int64_t want = std::max<int64_t>(1, (a.L + chunk - 1) / chunk);
     a.C = (int)std::min<int64_t>(g.C, want);
     a.Lc = round_up((a.L + a.C - 1) / a.C, tmx::kAlign);
   }
+  a.nvec = 1;
+  a.nvec_alloc = g.nvec_alloc;
+  a.stage_stride = g.stage_stride;
+  a.avg_stride = g.avg_stride;
   a.flag_stride = g.C;
   a.k = g.k;
   a.rank0 = g.rank0;
@@ -198,25 +220,28 @@ ExchangeArgs make_args(float* const* bufs, int64_t off, int64_t n) {
 // its send buffer when its kernel completes.
 int external_allgather(const ExchangeArgs& a, cudaStream_t s) {
   const int wb = wire_bytes(g.strategy);
+  for (int vq = 0; vq < a.nvec; ++vq)
   for (int i = 0; i < g.nlocal; ++i) {
     const int r = g.rank0 + i;
-    char* gather = static_cast<char*>(a.stage[r]);
-    float* x = a.x[i];
+    char* gather = static_cast<char*>(a.stage[r]) + vq * a.stage_stride;  // vector vq's own staging
+    float* x = vq ? a.v[i] : a.x[i];
+    const char* avg_r = static_cast<const char*>(a.avg[r]) + vq * a.avg_stride;
     if (g.ag_mode == TM_AG_NCCL) {
       if (!g.comm) return TM_E_NCCL;
-      ncclResult_t nr = g_nccl.AllGather(a.avg[r], gather, (size_t)a.L,
+      ncclResult_t nr = g_nccl.AllGather(avg_r, gather, (size_t)a.L,
                                          wb == 2 ? ncclFloat16 : ncclFloat32, g.comm, s);
       if (nr != ncclSuccess) return TM_E_NCCL;
     }
     for (int j = 0; j < g.k; ++j) {
       const int64_t n = std::min(a.L, a.P - (int64_t)j * a.L);  // elements of segment j < P
+      const char* avg_j = static_cast<const char*>(a.avg[j]) + vq * a.avg_stride;
       if (g.ag_mode == TM_AG_CE) {
         cudaError_t e;
         if (wb == 4) {
           if (n <= 0) break;
-          e = cudaMemcpyAsync(x + (int64_t)j * a.L, a.avg[j], (size_t)n * 4, cudaMemcpyDefault, s);
+          e = cudaMemcpyAsync(x + (int64_t)j * a.L, avg_j, (size_t)n * 4, cudaMemcpyDefault, s);
         } else {
-          e = cudaMemcpyAsync(gather + (int64_t)j * a.L * wb, a.avg[j], (size_t)a.L * wb,
+          e = cudaMemcpyAsync(gather + (int64_t)j * a.L * wb, avg_j, (size_t)a.L * wb,
                               cudaMemcpyDefault, s);
         }
         if (e != cudaSuccess) return cuda_fail("allgather copy", e);
@@ -235,7 +260,8 @@ int external_allgather(const ExchangeArgs& a, cudaStream_t s) {
 }
 
 int launch_staged(ExchangeArgs& a, cudaStream_t s) {
-  a.ag_external = g.ag_mode != TM_AG_SM;
+  // the one-shot kernel has no allgather phase to hand to the copy engines / NCCL
+  a.ag_external = g.ag_mode != TM_AG_SM && g.staged_kernel != tmx::kStagedOneShot;
   cudaError_t e = tmx::launch_exchange(a, g.nlocal, wire16(g.strategy), g.staged_kernel, s);
   if (e != cudaSuccess) return cuda_fail("launch_exchange", e);
   ++g.epoch;  // host-side count for tm_layout; the kernels keep their own
@@ -309,6 +335,9 @@ int do_bsp(float* const* w, float* const* v, const float* const* gr, int nbufs, 
     // Staged path: the step is fused into the exchange's pre-cast (a2), which
     // reads w, v, g, writes v' and the wire staging of w' = w + v'; w' itself is
     // never written (the allgather overwrites every element of w).
+    // With the momentum exchange (mom) the same launch also exchanges v': the
+    // pre-cast writes v' to the wire as a second vector (not back to v), and
+    // both vectors share the staging layout, the barriers and the launch.
     ExchangeArgs a = make_args(w, 0, g.P);
     for (int i = 0; i < nbufs; ++i) {
       a.v[i] = v[i];
@@ -317,7 +346,8 @@ int do_bsp(float* const* w, float* const* v, const float* const* gr, int nbufs, 
     a.lr = lr;
     a.mu = mu;
     a.sgd = 1;
-    rc = launch_staged(a, s);
+    a.nvec = mom ? 2 : 1;
+    return launch_staged(a, s);
   } else {
     for (int i = 0; i < nbufs; ++i) {
       cudaError_t e = tmx::launch_sgd(w[i], v[i], gr[i], g.P, lr, mu, s);
@@ -328,6 +358,135 @@ int do_bsp(float* const* w, float* const* v, const float* const* gr, int nbufs, 
   }
   if (rc != TM_OK || !mom) return rc;
   return do_exchange(v, nbufs, 0, g.P, s);
+}
+
+// ---------------------------------------------------------------------------
+// Bootstrap known-answer self-check (one process per GPU).  The first staged
+// exchange over the peer mappings is the first time this flavour's loads (for
+// the TMA flavours: bulk copies of IPC-mapped peer memory over NVLink) run on
+// this box, so before any caller data moves, every rank exchanges a probe whose
+// average is exact by construction: x_r[i] = (m + r + 1) * 2^-8 with
+// m = i mod 251, so the mean is (2m + k + 1) * 2^-9 (the sum k m + k(k+1)/2
+// times 2^-8 in SUBGD sum mode) -- every value, every partial sum and the
+// result have at most 11 significant bits, exact in binary16 and fp32 whatever
+// the order.  Element-varying values catch misaddressed loads, rank-dependent
+// ones a mixed-up peer.  Each rank compares its own result bit for bit, then
+// the ranks vote through peer memory (each writes its verdict into every
+// peer's pad tail with a copy through the IPC mapping and polls its own); if
+// any rank failed, every rank falls back to the register flavour (plain 16-byte
+// loads of peer memory), records it (tm_layout selfcheck = 2) and re-runs the
+// probe on it.  A probe that times out is reported as TM_E_TIMEOUT.
+// TM_SELFCHECK=0 skips it; TM_SELFCHECK_FAULT=r makes rank r report a mismatch
+// (fault injection for the tests).
+// ---------------------------------------------------------------------------
+uint32_t* pad_tail(int rank) {
+  return reinterpret_cast<uint32_t*>(g.rank_base[rank] + g.off_flags +
+                                     ((int64_t)tmx::kPhases * TM_MAX_RANKS + 1) * g.C * 4) ;
+}
+
+int probe_once(float* probe, int64_t n, cudaStream_t st, bool* ok) {
+  const float s8 = 1.0f / 256.0f;
+  std::vector<float> h((size_t)n), back((size_t)n);
+  for (int64_t i = 0; i < n; ++i) h[(size_t)i] = (float)((i % 251) + g.rank0 + 1) * s8;
+  cudaError_t e = cudaMemcpy(probe, h.data(), (size_t)n * 4, cudaMemcpyHostToDevice);
+  if (e != cudaSuccess) return cuda_fail("probe upload", e);
+  float* bufs[1] = {probe};
+  ExchangeArgs a = make_args(bufs, 0, n);
+  const uint64_t saved = g.timeout_ns;
+  g.timeout_ns = std::min<uint64_t>(g.timeout_ns, 5ull * 1000 * 1000 * 1000);
+  a.timeout_ns = g.timeout_ns;
+  const int saved_ag = g.ag_mode;
+  g.ag_mode = TM_AG_SM;  // the probe checks the kernel's own data path
+  int rc = launch_staged(a, st);
+  g.ag_mode = saved_ag;
+  g.timeout_ns = saved;
+  if (rc != TM_OK) return rc;
+  e = cudaStreamSynchronize(st);
+  if (e != cudaSuccess) return cuda_fail("probe sync", e);
+  uint32_t bits = 0;
+  e = cudaMemcpy(&bits, g.status, 4, cudaMemcpyDeviceToHost);
+  if (e != cudaSuccess) return cuda_fail("probe status", e);
+  cudaMemset(g.status, 0, 4);
+  if (bits & TM_BIT_TIMEOUT) return TM_E_TIMEOUT;
+  e = cudaMemcpy(back.data(), probe, (size_t)n * 4, cudaMemcpyDeviceToHost);
+  if (e != cudaSuccess) return cuda_fail("probe download", e);
+  const int k = g.k;
+  bool good = bits == 0;
+  for (int64_t i = 0; good && i < n; ++i) {
+    const int64_t m = i % 251;
+    const float want = g.sum ? (float)(k * m + k * (k + 1) / 2) * s8 : (float)(2 * m + k + 1) * (s8 * 0.5f);
+    uint32_t wb, gb;
+    memcpy(&wb, &want, 4);
+    memcpy(&gb, &back[(size_t)i], 4);
+    good = wb == gb;
+  }
+  *ok = good;
+  return TM_OK;
+}
+
+// Every rank's verdict for `round`, through the peers' pad tails.
+int vote(uint32_t round, bool mine, bool* all) {
+  const uint32_t v = (round << 8) | (mine ? 1u : 0u);
+  for (int j = 0; j < g.k; ++j) {
+    cudaError_t e = cudaMemcpy(pad_tail(j) + tmx::kTailVotes + g.rank0, &v, 4, cudaMemcpyDefault);
+    if (e != cudaSuccess) return cuda_fail("vote", e);
+  }
+  uint32_t got[TM_MAX_RANKS];
+  const auto t0 = std::chrono::steady_clock::now();
+  for (;;) {
+    cudaError_t e = cudaMemcpy(got, pad_tail(g.rank0) + tmx::kTailVotes, 4 * g.k, cudaMemcpyDeviceToHost);
+    if (e != cudaSuccess) return cuda_fail("vote poll", e);
+    bool in = true, ok = true;
+    for (int j = 0; j < g.k; ++j) {
+      in = in && (got[j] >> 8) == round;
+      ok = ok && (got[j] & 1u);
+    }
+    if (in) {
+      *all = ok;
+      return TM_OK;
+    }
+    if (std::chrono::steady_clock::now() - t0 > std::chrono::nanoseconds(g.timeout_ns)) return TM_E_TIMEOUT;
+    usleep(200);
+  }
+}
+
+int self_check() {
+  const char* off = getenv("TM_SELFCHECK");
+  if ((off && off[0] == '0') || g.nprocs == 1 || (g.strategy != TM_ASA && g.strategy != TM_ASA16))
+    return TM_OK;
+  const int64_t n = std::min<int64_t>(g.P, (int64_t)g.k * 8192);
+  float* probe = nullptr;
+  cudaError_t e = cudaMalloc(&probe, (size_t)n * 4);
+  if (e != cudaSuccess) return cuda_fail("probe alloc", e);
+  cudaStream_t st = nullptr;
+  e = cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking);
+  if (e != cudaSuccess) {
+    cudaFree(probe);
+    return cuda_fail("probe stream", e);
+  }
+  const int fault = getenv("TM_SELFCHECK_FAULT") ? atoi(getenv("TM_SELFCHECK_FAULT")) : -1;
+  int rc = TM_OK;
+  for (uint32_t round = 1; round <= 2 && rc == TM_OK; ++round) {
+    bool ok = false, all = false;
+    rc = probe_once(probe, n, st, &ok);
+    if (rc != TM_OK) break;
+    if (round == 1 && fault == g.rank0) ok = false;  // fault injection
+    rc = vote(round, ok, &all);
+    if (rc != TM_OK) break;
+    if (all) {
+      g.selfcheck = round == 1 ? 1 : 2;
+      break;
+    }
+    if (round == 2 || g.staged_kernel == tmx::kStagedReg) {
+      rc = TM_E_MISMATCH;  // the plain flavour fails too: nothing left to fall back to
+      break;
+    }
+    if (getenv("TM_DEBUG")) fprintf(stderr, "[tm] rank %d: self-check failed, register flavour\n", g.rank0);
+    g.staged_kernel = tmx::kStagedReg;  // every rank takes the same decision (same votes)
+  }
+  cudaStreamDestroy(st);
+  cudaFree(probe);
+  return rc;
 }
 
 }  // namespace
@@ -399,7 +558,11 @@ int tm_exchange_init(int64_t nparams, const tm_world* world, int strategy) {
     // Small segments (L <= 64 Ki elements): the register kernel, whose phases
     // have no bulk-copy round trips to drain (measured 6-16 us vs 15-22 us for the
     // TMA / warp-specialised kernels at k = 8, P <= 256 Ki; profiles/r01/latency_flavours.txt).
-    c.staged_kernel = c.L <= (int64_t)1 << 16 ? tmx::kStagedReg
+    // Segments of at most TM_ONESHOT_MAX_L elements (default kOneShotMaxL,
+    // profiles/r02/latency_flavours.txt): the one-shot kernel (one barrier).
+    const int64_t oneshot_max = env_i64("TM_ONESHOT_MAX_L", kOneShotMaxL);
+    c.staged_kernel = c.L <= oneshot_max     ? tmx::kStagedOneShot
+                      : c.L <= kRegMaxL      ? tmx::kStagedReg
                       : (c.nprocs == 1 ? tmx::kStagedTma : tmx::kStagedTmaWs);
     const char* sk = getenv("TM_STAGED_KERNEL");
     const char* ldg = getenv("TM_STAGED_LDG");
@@ -410,6 +573,7 @@ int tm_exchange_init(int64_t nparams, const tm_world* world, int strategy) {
     if (sk && !strcmp(sk, "tma")) c.staged_kernel = tmx::kStagedTma;
     if (sk && !strcmp(sk, "ws")) c.staged_kernel = tmx::kStagedWs;
     if (sk && !strcmp(sk, "tmaws")) c.staged_kernel = tmx::kStagedTmaWs;
+    if (sk && !strcmp(sk, "oneshot")) c.staged_kernel = tmx::kStagedOneShot;
     const char* ag = getenv("TM_ALLGATHER");  // sm | ce | nccl
     if (ag && !strcmp(ag, "ce")) c.ag_mode = TM_AG_CE;
     c.want_nccl_ag = ag && !strcmp(ag, "nccl") && c.nprocs > 1;
@@ -421,13 +585,22 @@ int tm_exchange_init(int64_t nparams, const tm_world* world, int strategy) {
     int cmax = k >= 2 ? tmx::exchange_max_ctas(c.device, wire16(strategy), k, c.staged_kernel) / c.nlocal / share
                       : 1;
     if (k >= 2 && cmax < 1) return TM_E_CUDA;
-    const int64_t want = std::max<int64_t>(1, (c.L + tmx::kMinChunk - 1) / tmx::kMinChunk);
+    const int64_t chunk = c.staged_kernel == tmx::kStagedOneShot ? tmx::kOneShotChunk : tmx::kMinChunk;
+    const int64_t want = std::max<int64_t>(1, (c.L + chunk - 1) / chunk);
     c.C = (int)std::min<int64_t>(std::max(cmax, 1), want);
     c.Lc = round_up((c.L + c.C - 1) / c.C, tmx::kAlign);
+    // Staging: nvec_alloc buffers of k*L wire elements (w, and v for the BSP step
+    // with momentum exchange), twice over (call parity) for the one-shot kernel;
+    // then nvec_alloc averaged segments of L; then the flag pad.
+    c.nvec_alloc = 2;
+    const int nstage = c.staged_kernel == tmx::kStagedOneShot ? 2 * c.nvec_alloc : c.nvec_alloc;
+    c.stage_stride = round_up((int64_t)k * c.L * wb, 256);
+    c.avg_stride = round_up(c.L * wb, 256);
     c.off_stage = 0;
-    c.off_avg = round_up(c.off_stage + (int64_t)k * c.L * wb, 256);
-    c.off_flags = round_up(c.off_avg + c.L * wb, 256);
-    c.rank_stride = round_up(c.off_flags + ((int64_t)tmx::kPhases * TM_MAX_RANKS + 1) * c.C * 4, 4096);
+    c.off_avg = c.off_stage + nstage * c.stage_stride;
+    c.off_flags = c.off_avg + c.nvec_alloc * c.avg_stride;
+    c.rank_stride = round_up(c.off_flags + ((int64_t)tmx::kPhases * TM_MAX_RANKS + 1) * c.C * 4 +
+                                 tmx::kPadTail * 4, 4096);
   } else if (strategy == TM_EASGD) {
     // Centre sharded by segment: rank s hosts c[s*L, min((s+1)*L, P)).
     c.off_center = 0;
@@ -540,7 +713,9 @@ int tm_bootstrap_import(const void* blobs, size_t len_each) {
     if (g_nccl.CommInitRank(&g.comm, g.nprocs, nb.nccl_id, g.proc) != ncclSuccess) return TM_E_NCCL;
   }
   g.ready = true;
-  return TM_OK;
+  const int rc = self_check();
+  if (rc != TM_OK) g.ready = false;
+  return rc;
 }
 
 int tm_exchange(float* dev_buf, void* stream) {
@@ -728,6 +903,7 @@ int tm_layout(tm_layout_info* out) {
   out->path = effective_path();
   out->staged_kernel = g.staged_kernel;
   out->allgather = g.ag_mode;
+  out->selfcheck = g.selfcheck;
   return TM_OK;
 }
 

@@ -157,10 +157,13 @@ __device__ __forceinline__ void precast_unit(const ExchangeArgs& a, int lr, int6
         if constexpr (SGD) {
 #pragma unroll
           for (int q = 0; q < E; ++q) {
-            fv[u][q] = sgd_v1(fv[u][q], fg[u][q], a.lr, a.mu);
+            fv[u][q] = g + q < P ? sgd_v1(fv[u][q], fg[u][q], a.lr, a.mu) : 0.0f;
             f[u][q] = g + q < P ? __fadd_rn(f[u][q], fv[u][q]) : 0.0f;
           }
-          if (g + E <= P) {
+          if (a.nvec == 2) {  // momentum exchanged: v' goes to the wire (vector 1), not back to v
+            st |= unit_status<W16, E>(fv[u]);
+            st16_cg(stage_r + a.stage_stride + g * WB, U::encode(fv[u]));
+          } else if (g + E <= P) {
 #pragma unroll
             for (int q = 0; q < E; q += 4)
               st16_f(a.v[lr] + g + q, make_float4(fv[u][q], fv[u][q + 1], fv[u][q + 2], fv[u][q + 3]));
@@ -226,11 +229,11 @@ tm_exchange_kernel(const __grid_constant__ ExchangeArgs a) {
   stamp(a, kStampReady);
 
   // ---------------- a4: reduce-scatter pull, fused sum / (1/k) / cast -------
-  {
+  for (int vq = 0; vq < a.nvec; ++vq) {
     const char* src[K];
 #pragma unroll
-    for (int j = 0; j < K; ++j) src[j] = reinterpret_cast<const char*>(a.stage[j]);
-    char* const avg_r = reinterpret_cast<char*>(a.avg[r]);
+    for (int j = 0; j < K; ++j) src[j] = reinterpret_cast<const char*>(a.stage[j]) + vq * a.stage_stride;
+    char* const avg_r = reinterpret_cast<char*>(a.avg[r]) + vq * a.avg_stride;
     const int64_t seg0 = (int64_t)r * L + e0;
     for (int64_t v = threadIdx.x; v < nu; v += kThreads) {
       const int64_t off = (seg0 + v * E) * WB;
@@ -263,14 +266,15 @@ tm_exchange_kernel(const __grid_constant__ ExchangeArgs a) {
   if (a.ag_external) return;  // a6 by the copy engines / NCCL (tm_allgather)
 
   // ---------------- a6: allgather pull, fused widen, store to caller ---------
-  {
+  for (int vq = 0; vq < a.nvec; ++vq) {
     constexpr int G = K;  // all k owners' units in flight at once
+    float* __restrict__ x = vq ? a.v[lr] : a.x[lr];
     for (int v = threadIdx.x; v < nu32; v += kThreads) {
       const int64_t ev = e0 + (int64_t)v * E;
       uint4 raw[G];
 #pragma unroll
       for (int j = 0; j < G; ++j)
-        raw[j] = ld16_cg(reinterpret_cast<const char*>(a.avg[j]) + ev * WB);
+        raw[j] = ld16_cg(reinterpret_cast<const char*>(a.avg[j]) + vq * a.avg_stride + ev * WB);
 #pragma unroll
       for (int j = 0; j < G; ++j) {
         const int64_t g = (int64_t)j * L + ev;
@@ -330,12 +334,12 @@ tm_exchange_ws_kernel(const __grid_constant__ ExchangeArgs a) {
   __syncthreads();
   const uint32_t epoch = s_epoch;
   stamp(a, kStampStart);
-  float* __restrict__ x = a.x[lr];
   const int64_t P = a.P, L = a.L;
   const int64_t e0 = (int64_t)c * a.Lc;
   const int64_t e1 = min(e0 + a.Lc, L);
   const int64_t nel = e1 > e0 ? e1 - e0 : 0;
-  const int64_t Ls = ((nel + kWsSub - 1) / kWsSub + 255) / 256 * 256;  // sub-chunk length
+  const int nsub = (int)max((int64_t)1, min((int64_t)kWsSub, nel / kWsMinSub));  // same on every rank
+  const int64_t Ls = ((nel + nsub - 1) / nsub + 255) / 256 * 256;  // sub-chunk length
   char* const stage_r = reinterpret_cast<char*>(a.stage[r]);
   const int grp = threadIdx.x / kWsGroup;
   const int tg = threadIdx.x - grp * kWsGroup;
@@ -343,7 +347,7 @@ tm_exchange_ws_kernel(const __grid_constant__ ExchangeArgs a) {
 
   if (grp == 0) {
     // ------------------------------------------------ casters: a2 per sub-chunk
-    for (int t = 0; t < kWsSub; ++t) {
+    for (int t = 0; t < nsub; ++t) {
       const int64_t s0e = e0 + (int64_t)t * Ls;
       const int64_t s1e = min(s0e + Ls, e1);
       const int nu = s1e > s0e ? (int)((s1e - s0e) / E) : 0;
@@ -357,11 +361,7 @@ tm_exchange_ws_kernel(const __grid_constant__ ExchangeArgs a) {
     }
   } else {
     // ------------------------------------------------ reducers: a4 per sub-chunk
-    const char* src[K];
-#pragma unroll
-    for (int j = 0; j < K; ++j) src[j] = reinterpret_cast<const char*>(a.stage[j]);
-    char* const avg_r = reinterpret_cast<char*>(a.avg[r]);
-    for (int t = 0; t < kWsSub; ++t) {
+    for (int t = 0; t < nsub; ++t) {
       if (tg < K) {  // READY_t from rank tg
         const uint32_t* mine = a.flags[r] + (size_t)(t * TM_MAX_RANKS + tg) * a.flag_stride + c;
         if ((int32_t)(ld_acquire<SYS>(mine) - epoch) < 0) {
@@ -381,7 +381,13 @@ tm_exchange_ws_kernel(const __grid_constant__ ExchangeArgs a) {
       const int64_t s0e = e0 + (int64_t)t * Ls;
       const int64_t s1e = min(s0e + Ls, e1);
       const int nu = s1e > s0e ? (int)((s1e - s0e) / E) : 0;
-      for (int v = tg; v < nu; v += kWsGroup) {
+      for (int vw = tg; vw < nu * a.nvec; vw += kWsGroup) {
+        const int vq = vw >= nu;  // vector of this unit (0: w / x, 1: v)
+        const int v = vw - vq * nu;
+        const char* src[K];
+#pragma unroll
+        for (int j = 0; j < K; ++j) src[j] = reinterpret_cast<const char*>(a.stage[j]) + vq * a.stage_stride;
+        char* const avg_r = reinterpret_cast<char*>(a.avg[r]) + vq * a.avg_stride;
         const int64_t e = s0e + (int64_t)v * E;
         const int64_t off = ((int64_t)r * L + e) * WB;
         uint4 raw[K];
@@ -416,11 +422,15 @@ tm_exchange_ws_kernel(const __grid_constant__ ExchangeArgs a) {
 
   // ---------------- a6: allgather pull with all 16 warps ----------------------
   const int nu32 = (int)(nel / E);
-  for (int v = threadIdx.x; v < nu32; v += kWsThreads) {
+  for (int vw = threadIdx.x; vw < nu32 * a.nvec; vw += kWsThreads) {
+    const int vq = vw >= nu32;
+    const int v = vw - vq * nu32;
+    float* __restrict__ x = vq ? a.v[lr] : a.x[lr];
     const int64_t ev = e0 + (int64_t)v * E;
     uint4 raw[K];
 #pragma unroll
-    for (int j = 0; j < K; ++j) raw[j] = ld16_cg(reinterpret_cast<const char*>(a.avg[j]) + ev * WB);
+    for (int j = 0; j < K; ++j)
+      raw[j] = ld16_cg(reinterpret_cast<const char*>(a.avg[j]) + vq * a.avg_stride + ev * WB);
 #pragma unroll
     for (int j = 0; j < K; ++j) {
       const int64_t g = (int64_t)j * L + ev;
@@ -539,7 +549,7 @@ __device__ __forceinline__ void precast_phase(const PhaseCtx& pc, int gtid, int6
   constexpr int WB = W16 ? 2 : 4;
   constexpr int TP = G::kInB / 4;                 // plain tile: fp32 in one input slot
   constexpr int TPS = G::kInB / 16;               // SGD tile: w, v, g in one input slot (2048 for 32 KB: 1.82 ms vs 1.87 for 2560)
-  static_assert(TP * WB <= G::kOutB && TPS >= 256, "pre-cast tiles");
+  static_assert(TP * WB <= G::kOutB && TPS >= 256 && 2 * TPS * WB <= G::kOutB, "pre-cast tiles");
   const ExchangeArgs& a = *pc.a;
   const int tp = SGD ? TPS : TP;
   float* const x = pc.x;
@@ -575,8 +585,10 @@ __device__ __forceinline__ void precast_phase(const PhaseCtx& pc, int gtid, int6
         const float* fin = reinterpret_cast<const float*>(in);
         const float* fvin = fin + TPS;
         const float* fgin = fin + 2 * TPS;
+        const bool mom = SGD && a.nvec == 2;  // v' to the wire (second output tile), not back to v
+        uint4* out2 = reinterpret_cast<uint4*>(out + TPS * WB);
         for (int v = gtid; v < (int)(n / E); v += G::kNT) {
-          float f[E];
+          float f[E], f2[SGD ? E : 1];
           if ((v + 1) * E <= nbi) {
 #pragma unroll
             for (int q = 0; q < E; q += 4) {
@@ -584,7 +596,11 @@ __device__ __forceinline__ void precast_phase(const PhaseCtx& pc, int gtid, int6
               if (SGD) {
                 const float4 vn = sgd_v(reinterpret_cast<const float4*>(fvin + v * E)[q / 4],
                                         reinterpret_cast<const float4*>(fgin + v * E)[q / 4], a.lr, a.mu);
-                st16_f(vr + g0 + v * E + q, vn);
+                if (mom) {
+                  f2[q] = vn.x; f2[q + 1] = vn.y; f2[q + 2] = vn.z; f2[q + 3] = vn.w;
+                } else {
+                  st16_f(vr + g0 + v * E + q, vn);
+                }
                 t4 = add4(t4, vn);
               }
               f[q] = t4.x; f[q + 1] = t4.y; f[q + 2] = t4.z; f[q + 3] = t4.w;
@@ -593,18 +609,21 @@ __device__ __forceinline__ void precast_phase(const PhaseCtx& pc, int gtid, int6
 #pragma unroll
             for (int q = 0; q < E; ++q) {
               const int e = v * E + q;
+              if (SGD) f2[q] = 0.0f;
               if (e < nbi) {
                 f[q] = fin[e];
                 if (SGD) {
                   const float vn = sgd_v1(fvin[e], fgin[e], a.lr, a.mu);
-                  vr[g0 + e] = vn;
+                  if (mom) f2[q] = vn;
+                  else vr[g0 + e] = vn;
                   f[q] = __fadd_rn(f[q], vn);
                 }
               } else if (g0 + e < P) {  // the <= 3 elements in [P & ~3, P): plain accesses
                 f[q] = x[g0 + e];
                 if (SGD) {
                   const float vn = sgd_v1(vr[g0 + e], gr[g0 + e], a.lr, a.mu);
-                  vr[g0 + e] = vn;
+                  if (mom) f2[q] = vn;
+                  else vr[g0 + e] = vn;
                   f[q] = __fadd_rn(f[q], vn);
                 }
               } else {
@@ -614,12 +633,20 @@ __device__ __forceinline__ void precast_phase(const PhaseCtx& pc, int gtid, int6
           }
           st |= unit_status<W16, E>(f);
           reinterpret_cast<uint4*>(out)[v] = U::encode(f);
+          if constexpr (SGD) {
+            if (mom) {
+              st |= unit_status<W16, E>(f2);
+              out2[v] = U::encode(f2);
+            }
+          }
         }
       },
       [&](int i, const char* out) {
         int64_t g0, n;
         geom(i, g0, n);
         bulk_store(pc.stage_r + g0 * WB, out, (uint32_t)(n * WB));
+        if (SGD && a.nvec == 2)
+          bulk_store(pc.stage_r + a.stage_stride + g0 * WB, out + TPS * WB, (uint32_t)(n * WB));
       });
 }
 
@@ -628,7 +655,7 @@ __device__ __forceinline__ void precast_phase(const PhaseCtx& pc, int gtid, int6
 template <class G, int K, bool W16>
 __device__ __forceinline__ void reduce_phase(const PhaseCtx& pc, int gtid, int64_t s0, int64_t s1,
                                              uint32_t& use, uint32_t& outn, char* in_ring,
-                                             char* out_ring, uint64_t* full, uint32_t& st) {
+                                             char* out_ring, uint64_t* full, uint32_t& st, int vq = 0) {
   using U = Unit<W16>;
   constexpr int E = U::kElems;
   constexpr int WB = W16 ? 2 : 4;
@@ -640,7 +667,8 @@ __device__ __forceinline__ void reduce_phase(const PhaseCtx& pc, int gtid, int64
   const ExchangeArgs& a = *pc.a;
   const int r = pc.r;
   const int64_t L = pc.L;
-  char* const avg_r = reinterpret_cast<char*>(a.avg[r]);
+  char* const avg_r = reinterpret_cast<char*>(a.avg[r]) + vq * a.avg_stride;
+  const int64_t soff = vq * a.stage_stride;  // vector vq's staging
   const int nt = (int)((max((int64_t)0, s1 - s0) + TR - 1) / TR);
   tile_pipeline<G>(
       gtid, nt, use, outn, in_ring, out_ring, full,
@@ -650,7 +678,8 @@ __device__ __forceinline__ void reduce_phase(const PhaseCtx& pc, int gtid, int64
         mbar_expect_tx(bar, (uint32_t)(K * n * WB));
 #pragma unroll
         for (int j = 0; j < K; ++j)
-          bulk_load(slot + j * TR * WB, reinterpret_cast<const char*>(a.stage[j]) + ((int64_t)r * L + e) * WB,
+          bulk_load(slot + j * TR * WB,
+                    reinterpret_cast<const char*>(a.stage[j]) + soff + ((int64_t)r * L + e) * WB,
                     (uint32_t)(n * WB), bar);
       },
       [&](int i, const char* in, char* out) {
@@ -690,14 +719,15 @@ __device__ __forceinline__ void reduce_phase(const PhaseCtx& pc, int gtid, int64
 template <class G, int K, bool W16>
 __device__ __forceinline__ void gather_phase(const PhaseCtx& pc, int gtid, int64_t e0, int64_t e1,
                                              uint32_t& use, uint32_t& outn, char* in_ring,
-                                             char* out_ring, uint64_t* full) {
+                                             char* out_ring, uint64_t* full, int vq = 0) {
   using U = Unit<W16>;
   constexpr int E = U::kElems;
   constexpr int WB = W16 ? 2 : 4;
   constexpr int TA = G::kOutB / 4;  // fp32 out tile fills one output slot
   static_assert(TA * WB <= G::kInB, "a6 tile");
   const ExchangeArgs& a = *pc.a;
-  float* const x = pc.x;
+  float* const x = vq ? a.v[pc.lr] : pc.x;  // vector vq's caller buffer
+  const int64_t aoff = vq * a.avg_stride;
   const int64_t P = pc.P, L = pc.L, P4 = pc.P4;
   const int64_t nel = e1 > e0 ? e1 - e0 : 0;
   const int nt = (int)((nel + TA - 1) / TA);
@@ -714,7 +744,7 @@ __device__ __forceinline__ void gather_phase(const PhaseCtx& pc, int gtid, int64
         int64_t e, n;
         geom(i, j, e, n);
         mbar_expect_tx(bar, (uint32_t)(n * WB));
-        bulk_load(slot, reinterpret_cast<const char*>(a.avg[j]) + e * WB, (uint32_t)(n * WB), bar);
+        bulk_load(slot, reinterpret_cast<const char*>(a.avg[j]) + aoff + e * WB, (uint32_t)(n * WB), bar);
       },
       [&](int i, const char* in, char* out) {
         int j;
@@ -789,7 +819,8 @@ tm_exchange_tma_kernel(const __grid_constant__ ExchangeArgs a) {
   stamp(a, kStampReady);
   if (tid == 0) fence_proxy_async_global();  // peers' staging, acquired above -> bulk loads
 
-  reduce_phase<FullGrp, K, W16>(pc, tid, e0, e1, use, outn, in_ring, out_ring, full, st);
+  for (int vq = 0; vq < a.nvec; ++vq)
+    reduce_phase<FullGrp, K, W16>(pc, tid, e0, e1, use, outn, in_ring, out_ring, full, st, vq);
   if (st) atomicOr(a.status, st);
   if (tid == 0) drain_bulk_stores_thread();
   stamp(a, kStampReduce);
@@ -798,7 +829,8 @@ tm_exchange_tma_kernel(const __grid_constant__ ExchangeArgs a) {
   if (a.ag_external) return;  // a6 by the copy engines / NCCL (tm_allgather)
   if (tid == 0) fence_proxy_async_global();
 
-  gather_phase<FullGrp, K, W16>(pc, tid, e0, e1, use, outn, in_ring, out_ring, full);
+  for (int vq = 0; vq < a.nvec; ++vq)
+    gather_phase<FullGrp, K, W16>(pc, tid, e0, e1, use, outn, in_ring, out_ring, full, vq);
   if (tid == 0) bulk_wait_all<0>();  // kernel exit also waits; explicit for clarity
   stamp(a, kStampEnd);
 }
@@ -837,7 +869,8 @@ tm_exchange_tmaws_kernel(const __grid_constant__ ExchangeArgs a) {
   const int64_t e0 = (int64_t)c * a.Lc;
   const int64_t e1 = min(e0 + a.Lc, a.L);
   const int64_t nel = e1 > e0 ? e1 - e0 : 0;
-  const int64_t Ls = ((nel + kWsSub - 1) / kWsSub + 255) / 256 * 256;  // sub-chunk length
+  const int nsub = (int)max((int64_t)1, min((int64_t)kWsSub, nel / kWsMinSub));  // same on every rank
+  const int64_t Ls = ((nel + nsub - 1) / nsub + 255) / 256 * 256;  // sub-chunk length
   const int tid = threadIdx.x;
   constexpr int NT = CastGrp::kNT;
   const int grp = tid / NT;
@@ -863,7 +896,7 @@ tm_exchange_tmaws_kernel(const __grid_constant__ ExchangeArgs a) {
     uint32_t use = 0, outn = 0;
     char* const in_ring = base;
     char* const out_ring = base + CastGrp::kNin * CastGrp::kInB;
-    for (int t = 0; t < kWsSub; ++t) {
+    for (int t = 0; t < nsub; ++t) {
       const int64_t s0 = e0 + (int64_t)t * Ls;
       const int64_t s1 = min(s0 + Ls, e1);
       if (s1 > s0)
@@ -878,7 +911,7 @@ tm_exchange_tmaws_kernel(const __grid_constant__ ExchangeArgs a) {
     uint32_t use = 0, outn = 0;
     char* const in_ring = base + 2 * CastGrp::kNin * CastGrp::kInB;
     char* const out_ring = in_ring + RedGrp::kNin * RedGrp::kInB;
-    for (int t = 0; t < kWsSub; ++t) {
+    for (int t = 0; t < nsub; ++t) {
       if (gtid < K) {  // READY_t from rank gtid
         const uint32_t* mine = a.flags[r] + (size_t)(t * TM_MAX_RANKS + gtid) * a.flag_stride + c;
         if ((int32_t)(ld_acquire<SYS>(mine) - epoch) < 0) {
@@ -898,7 +931,9 @@ tm_exchange_tmaws_kernel(const __grid_constant__ ExchangeArgs a) {
       if (gtid == 0) fence_proxy_async_global();  // acquired peers' staging -> bulk loads
       const int64_t s0 = e0 + (int64_t)t * Ls;
       const int64_t s1 = min(s0 + Ls, e1);
-      if (s1 > s0) reduce_phase<RedGrp, K, W16>(pc, gtid, s0, s1, use, outn, in_ring, out_ring, full_r, st);
+      if (s1 > s0)
+        for (int vq = 0; vq < a.nvec; ++vq)
+          reduce_phase<RedGrp, K, W16>(pc, gtid, s0, s1, use, outn, in_ring, out_ring, full_r, st, vq);
     }
     if (gtid == 0) drain_bulk_stores_thread();  // avg in memory before REDUCED
   }
@@ -913,8 +948,112 @@ tm_exchange_tmaws_kernel(const __grid_constant__ ExchangeArgs a) {
 
   // ---------------- a6: allgather pull with the whole CTA ---------------------
   uint32_t use = 0, outn = 0;
-  gather_phase<FullGrp, K, W16>(pc, tid, e0, e1, use, outn, base, base + kInSlots * kSlotBytes, full);
+  for (int vq = 0; vq < a.nvec; ++vq)
+    gather_phase<FullGrp, K, W16>(pc, tid, e0, e1, use, outn, base, base + kInSlots * kSlotBytes, full, vq);
   if (tid == 0) bulk_wait_all<0>();
+  stamp(a, kStampEnd);
+}
+
+// ---------------------------------------------------------------------------
+// One-shot staged kernel (small segments; latency-bound regime): ONE barrier per
+// call.  a2 pre-casts chunk c of all k segments into the own staging buffer of
+// this call's parity; after READY from every rank, every rank pulls chunk c of
+// ALL k segments from ALL k ranks' staging (register loads of peer memory) and
+// reduces them itself in ascending rank order, /k, round -- the same arithmetic
+// as the owner's a4, so every rank computes bitwise the same average without the
+// reduce-scatter / allgather split and without the REDUCED barrier.
+// Reuse: staging is double-buffered by the rank's call parity (a per-rank call
+// counter in the pad tail: every CTA reads it at start, the last CTA to retire
+// increments it, so all CTAs of a launch agree).  Call n writes buffer n & 1;
+// the last readers of that buffer are call n-2's, and every rank finished call
+// n-2 before it signalled READY(n-1), which this rank acquired in call n-1.
+// ---------------------------------------------------------------------------
+template <int K, bool W16, bool SYS, bool SGD>
+__global__ void __launch_bounds__(kThreads, K == 6 ? 3 : 4)
+tm_exchange_oneshot_kernel(const __grid_constant__ ExchangeArgs a) {
+  using U = Unit<W16>;
+  constexpr int E = U::kElems;
+  constexpr int WB = W16 ? 2 : 4;
+  __shared__ int s_abort;
+  __shared__ uint32_t s_epoch, s_par;
+
+  const int lr = blockIdx.x / a.C;
+  const int c = blockIdx.x - lr * a.C;
+  const int r = a.rank0 + lr;
+  uint32_t* const tail = a.flags[r] + (size_t)(kPhases * TM_MAX_RANKS + 1) * a.flag_stride;
+  if (threadIdx.x == 0) {
+    s_abort = 0;
+    uint32_t* ctr = a.flags[r] + (size_t)kPhases * TM_MAX_RANKS * a.flag_stride + c;
+    s_epoch = *ctr + 1;
+    *ctr = s_epoch;
+    s_par = __ldcg(tail + kTailCalls) & 1u;  // this call's staging parity
+    __threadfence();
+    // retire: the last of this rank's C CTAs advances the call counter (every CTA
+    // has read it by then); the kernel boundary orders it before the next call
+    if (atomicAdd(tail + kTailRetire, 1u) == (uint32_t)a.C - 1) {
+      tail[kTailRetire] = 0;
+      tail[kTailCalls] = __ldcg(tail + kTailCalls) + 1;
+    }
+  }
+  __syncthreads();
+  const uint32_t epoch = s_epoch;
+  const int64_t boff = (int64_t)s_par * a.nvec_alloc * a.stage_stride;
+  stamp(a, kStampStart);
+  const int64_t P = a.P, L = a.L;
+  const int64_t e0 = (int64_t)c * a.Lc;
+  const int64_t e1 = min(e0 + a.Lc, L);
+  const int nu = e1 > e0 ? (int)((e1 - e0) / E) : 0;  // wire units per segment chunk
+  char* const stage_r = reinterpret_cast<char*>(a.stage[r]) + boff;
+
+  // ---------------- a2: pre-cast chunk c of all k segments (this parity) -------
+  uint32_t st = 0;
+  for (int v = threadIdx.x; v < nu; v += kThreads)
+    precast_unit<W16, K, SGD>(a, lr, e0 + (int64_t)v * E, stage_r, st);
+  if (st) atomicOr(a.status, st);
+  st = 0;
+  stamp(a, kStampCast);
+  if (!rank_barrier<K, SYS>(a, kPhaseReady, r, c, epoch, &s_abort)) return;
+  stamp(a, kStampReady);
+
+  // ---------------- reduce chunk c of EVERY segment from every rank ------------
+  for (int vq = 0; vq < a.nvec; ++vq) {
+    const char* src[K];
+#pragma unroll
+    for (int j = 0; j < K; ++j) src[j] = reinterpret_cast<const char*>(a.stage[j]) + boff + vq * a.stage_stride;
+    float* __restrict__ x = vq ? a.v[lr] : a.x[lr];
+    for (int vw = threadIdx.x; vw < nu * K; vw += kThreads) {  // unit u of segment sg, u fastest
+      const int sg = vw / nu;
+      const int64_t g = (int64_t)sg * L + e0 + (int64_t)(vw - sg * nu) * E;
+      uint4 raw[K];
+#pragma unroll
+      for (int j = 0; j < K; ++j) raw[j] = ld16_cg(src[j] + g * WB);
+      float sm[E], t[E];
+      U::decode(raw[0], sm);
+#pragma unroll
+      for (int j = 1; j < K; ++j) {
+        U::decode(raw[j], t);
+#pragma unroll
+        for (int q = 0; q < E; ++q) sm[q] = __fadd_rn(sm[q], t[q]);
+      }
+      if (!a.sum) {
+#pragma unroll
+        for (int q = 0; q < E; ++q) sm[q] = div_k<K>(sm[q]);
+      } else if (W16) {  // a sum can leave the binary16 range
+#pragma unroll
+        for (int q = 0; q < E; ++q) st |= status_of(sm[q], true) & TM_BIT_OVERFLOW16;
+      }
+      float f[E];
+      U::decode(U::encode(sm), f);  // the wire rounding of the average (ASA16: widen(rn16(a)))
+      if (g + E <= P) {
+        U::store_dst(x + g, f);
+      } else {
+#pragma unroll
+        for (int q = 0; q < E; ++q)
+          if (g + q < P) x[g + q] = f[q];
+      }
+    }
+  }
+  if (st) atomicOr(a.status, st);
   stamp(a, kStampEnd);
 }
 
@@ -929,6 +1068,9 @@ const void* exchange_fn(bool sys, int fl) {
   if (fl == kStagedTmaWs)
     return sys ? reinterpret_cast<const void*>(&tm_exchange_tmaws_kernel<K, W16, true, SGD>)
                : reinterpret_cast<const void*>(&tm_exchange_tmaws_kernel<K, W16, false, SGD>);
+  if (fl == kStagedOneShot)
+    return sys ? reinterpret_cast<const void*>(&tm_exchange_oneshot_kernel<K, W16, true, SGD>)
+               : reinterpret_cast<const void*>(&tm_exchange_oneshot_kernel<K, W16, false, SGD>);
   return sys ? reinterpret_cast<const void*>(&tm_exchange_kernel<K, W16, true, SGD>)
              : reinterpret_cast<const void*>(&tm_exchange_kernel<K, W16, false, SGD>);
 }

@@ -49,7 +49,7 @@ class tm_layout_info(ctypes.Structure):
                 ("sm_count", ctypes.c_int32), ("wire_bytes", ctypes.c_int32),
                 ("lib_bytes", ctypes.c_int64), ("epoch", ctypes.c_uint32),
                 ("path", ctypes.c_int32), ("staged_kernel", ctypes.c_int32),
-                ("allgather", ctypes.c_int32)]
+                ("allgather", ctypes.c_int32), ("selfcheck", ctypes.c_int32)]
 
 
 _lib = None

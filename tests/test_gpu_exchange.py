@@ -350,9 +350,13 @@ def test_range_argument_errors():
         with pytest.raises(tm.TmError) as e:
             tm.tm_exchange_group_range(b, 2, 100)  # offset not a multiple of 4
         assert e.value.code == tm.TM_E_ALIGN
-        with pytest.raises(tm.TmError) as e:
-            tm.tm_exchange_group_range(b, 4000, 100)  # past nparams
-        assert e.value.code == tm.TM_E_ARG
+        with pytest.raises(ValueError):  # past nparams: the binding refuses it ...
+            tm.tm_exchange_group_range(b, 4000, 100)
+        import ctypes  # ... and so does the C ABI itself
+        arr = (ctypes.c_void_p * 2)(*[t.data_ptr() for t in b])
+        code = tm.lib().tm_exchange_group_range(arr, 2, 4000, 100,
+                                                ctypes.c_void_p(torch.cuda.current_stream().cuda_stream))
+        assert code == tm.TM_E_ARG
         tm.tm_exchange_group_range(b, 0, 0)  # empty range: no-op
 
 
@@ -406,11 +410,13 @@ def test_phase_log_does_not_change_results(path):
 
 
 def test_default_staged_flavour_by_segment_length(monkeypatch):
-    """Without TM_STAGED_KERNEL: the register kernel for segments of <= 64 Ki
-    elements (latency-bound), the TMA-engine kernel above that in a
-    single-process group."""
+    """Without TM_STAGED_KERNEL: the one-shot kernel for segments of <= 16 Ki
+    elements, the register two-phase kernel up to 64 Ki (latency-bound), the
+    TMA-engine kernel above that in a single-process group."""
     monkeypatch.delenv("TM_STAGED_KERNEL", raising=False)
-    for P, k, want in ((100_003, 2, 0), (131_072 * 8, 8, 1), (65_536 * 4, 4, 0), (1_000_003, 2, 1)):
+    monkeypatch.delenv("TM_ONESHOT_MAX_L", raising=False)
+    for P, k, want in ((100_003, 2, 0), (131_072 * 8, 8, 1), (65_536 * 4, 4, 0), (1_000_003, 2, 1),
+                       (16_384 * 8, 8, 4), (10_000, 2, 4), (16_385 * 8, 8, 0)):
         with tm.Exchanger(P, "asa16", size=k, nlocal=k, path="staged") as ex:
             assert ex.layout()["staged_kernel"] == want, (P, k)
 
@@ -462,3 +468,38 @@ def test_binding_rejects_short_buffers_and_bad_ranges():
             ex.bsp_step(bufs, bufs, [bufs[0], bufs[1][:100]], 0.1, 0.9)
         ex.exchange(bufs)  # still usable
         assert ex.status()[0] == tm.TM_OK
+
+
+@pytest.mark.parametrize("strategy", ["asa16", "asa"])
+@pytest.mark.parametrize("k", [2, 3, 8])
+def test_oneshot_interleaved_ranges_bitwise(monkeypatch, strategy, k):
+    """The one-shot kernel double-buffers its staging by call parity (a per-rank
+    device call counter): full exchanges and ranges of different layouts
+    (different L' and C') interleaved, each on fresh perturbations, must all
+    match the oracle bitwise -- an odd number of calls between two full
+    exchanges flips the parity under a different layout."""
+    monkeypatch.setenv("TM_STAGED_KERNEL", "oneshot")
+    P = 12_289 * k
+    X = worker_buffers(P, k, "D2", config=150)
+    bufs = to_dev(X)
+    plan = [(0, P), (4, 3000), (0, P), (P // 2 // 4 * 4, P - P // 2 // 4 * 4), (8, 5), (0, P)]
+    with tm.Exchanger(P, strategy, size=k, nlocal=k, path="staged") as ex:
+        assert ex.layout()["staged_kernel"] == 4
+        want = [x.copy() for x in X]
+        for i, (off, cnt) in enumerate(plan):
+            d = worker_buffers(P, k, "D1", config=151 + i)
+            for r in range(k):
+                bufs[r].add_(torch.from_numpy(d[r]).cuda() * 1e-3)
+                want[r] = np.add(want[r], np.multiply(d[r], np.float32(1e-3), dtype=np.float32), dtype=np.float32)
+            if cnt == P:
+                ex.exchange(bufs)
+            else:
+                ex.exchange_range(bufs, off, cnt)
+            seg = ox.exchange([w[off:off + cnt] for w in want], strategy)
+            for r in range(k):
+                want[r][off:off + cnt] = seg[r]
+        code, _ = ex.status()
+    assert code == tm.TM_OK
+    got = to_host(bufs)
+    for r in range(k):
+        assert_bitwise(got[r], want[r], f"rank {r}")

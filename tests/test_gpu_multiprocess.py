@@ -68,7 +68,7 @@ def launch(tmp_path, k, strategy, P, dist, mode="normal", timeout=240, extra_env
     return res
 
 
-KERNEL_ID = {"reg": 0, "tma": 1, "ws": 2, "tmaws": 3}
+KERNEL_ID = {"reg": 0, "tma": 1, "ws": 2, "tmaws": 3, "oneshot": 4}
 
 
 @pytest.mark.parametrize("strategy,k,op,kernel", [("asa16", 2, "avg", "ws"), ("asa", 2, "avg", "ws"),
@@ -76,7 +76,9 @@ KERNEL_ID = {"reg": 0, "tma": 1, "ws": 2, "tmaws": 3}
                                                   ("asa16", 2, "range", "ws"), ("asa16", 2, "avg", "tma"),
                                                   ("asa", 3, "range", "tma"), ("asa16", 2, "avg", "reg"),
                                                   ("asa", 3, "range", "reg"), ("asa16", 2, "avg", "tmaws"),
-                                                  ("asa", 3, "range", "tmaws"), ("asa16", 3, "sum", "tmaws")])
+                                                  ("asa", 3, "range", "tmaws"), ("asa16", 3, "sum", "tmaws"),
+                                                  ("asa16", 2, "avg", "oneshot"), ("asa", 3, "range", "oneshot"),
+                                                  ("asa16", 4, "sum", "oneshot")])
 def test_multiprocess_bitwise(tmp_path, strategy, k, op, kernel):
     P = 100_003
     env = {"TM_STAGED_KERNEL": kernel}
@@ -97,7 +99,8 @@ def test_multiprocess_bitwise(tmp_path, strategy, k, op, kernel):
 @pytest.mark.parametrize("strategy,k,mode,kernel", [("asa16", 2, "bsp", "ws"), ("asa16", 3, "bspmom", "ws"),
                                                     ("asa", 2, "bsp", "tma"), ("asa16", 3, "bspmom", "tma"),
                                                     ("asa16", 2, "bsp", "reg"), ("asa", 3, "bspmom", "reg"),
-                                                    ("asa16", 3, "bspmom", "tmaws")])
+                                                    ("asa16", 3, "bspmom", "tmaws"), ("asa16", 3, "bspmom", "oneshot"),
+                                                    ("asa", 2, "bsp", "oneshot")])
 def test_multiprocess_bsp_fused_bitwise(tmp_path, strategy, k, mode, kernel):
     """tm_bsp_step across processes: the momentum-SGD step is fused into the
     staged kernel's pre-cast; two iterations vs oracle/bsp.py."""
@@ -220,12 +223,12 @@ def test_multiprocess_k4_k8_cross_rank_identity(tmp_path, k, kernel):
         assert_bitwise(got[r], got[0], f"rank {r} vs rank 0")
 
 
-@pytest.mark.parametrize("kernel", ["reg", "tma", "ws", "tmaws"])
+@pytest.mark.parametrize("kernel", ["reg", "tma", "ws", "tmaws", "oneshot"])
 def test_multiprocess_timeout_instead_of_hang(tmp_path, kernel):
     """Fault injection: rank 1 never calls tm_exchange; rank 0's
     kernel times out in its first barrier, sets TM_E_TIMEOUT and exits -- every
     staged flavour (the warp-specialised ones time out in the reducer group)."""
-    P = 4096 if kernel == "reg" else 300_007
+    P = 4096 if kernel in ("reg", "oneshot") else 300_007
     res = launch(tmp_path, 2, "asa16", P, "D1", mode="skip1", extra_env={"TM_STAGED_KERNEL": kernel})
     assert res[0]["code"] == 7 and res[0]["bits"] & 4  # TM_E_TIMEOUT
 
@@ -318,7 +321,7 @@ def test_multiprocess_async_easgd_loop(tmp_path, k):
 
 
 @pytest.mark.parametrize("strategy,kernel", [("asa16", "ws"), ("asa", "reg"), ("asa16", "tma"),
-                                             ("asa16", "tmaws")])
+                                             ("asa16", "tmaws"), ("asa16", "oneshot")])
 def test_multiprocess_stress_random_delays(tmp_path, strategy, kernel):
     """STRESS_ITERS (60; TM_STRESS_ITERS overrides) back-to-back exchanges per rank, each after a per-rank delta and a random
     host delay on half of them: every rank ends bitwise at the oracle's sequence."""
@@ -334,3 +337,37 @@ def test_multiprocess_stress_random_delays(tmp_path, strategy, kernel):
     for r in range(k):
         assert res[r]["code"] == 0, res[r]
         assert_bitwise(np.load(os.path.join(tmp_path, f"rank{r}.npy")), X[r], f"rank {r}")
+
+
+@pytest.mark.parametrize("strategy,k,kernel", [("asa16", 2, "tmaws"), ("asa", 3, "tma"), ("asa16", 4, "oneshot")])
+def test_multiprocess_bootstrap_selfcheck(tmp_path, strategy, k, kernel):
+    """The bootstrap's known-answer probe passes on every rank (tm_layout
+    selfcheck = 1) and the chosen flavour stays."""
+    P = 100_003
+    res = launch(tmp_path, k, strategy, P, "D2", extra_env={"TM_STAGED_KERNEL": kernel})
+    want = [worker_buffer(P, "D2", r, config=50) for r in range(k)]
+    for _ in range(3):
+        want = ox.exchange(want, strategy)
+    for r in range(k):
+        assert res[r]["code"] == 0, res[r]
+        assert res[r]["layout"]["selfcheck"] == 1 and res[r]["layout"]["staged_kernel"] == KERNEL_ID[kernel]
+        assert_bitwise(np.load(os.path.join(tmp_path, f"rank{r}.npy")), want[r], f"rank {r}")
+
+
+@pytest.mark.parametrize("strategy,k,kernel,bad", [("asa16", 2, "tmaws", 1), ("asa", 3, "tma", 0),
+                                                   ("asa16", 4, "oneshot", 3)])
+def test_multiprocess_selfcheck_fault_falls_back(tmp_path, strategy, k, kernel, bad):
+    """Fault injection (TM_SELFCHECK_FAULT=r: rank r reports a probe mismatch):
+    the vote through peer memory reaches every rank, ALL ranks fall back to the
+    register flavour together (selfcheck = 2, staged_kernel = 0), the re-run
+    probe passes, and the exchanges that follow are bitwise the oracle's."""
+    P = 100_003
+    res = launch(tmp_path, k, strategy, P, "D2",
+                 extra_env={"TM_STAGED_KERNEL": kernel, "TM_SELFCHECK_FAULT": str(bad)})
+    want = [worker_buffer(P, "D2", r, config=50) for r in range(k)]
+    for _ in range(3):
+        want = ox.exchange(want, strategy)
+    for r in range(k):
+        assert res[r]["code"] == 0, res[r]
+        assert res[r]["layout"]["selfcheck"] == 2 and res[r]["layout"]["staged_kernel"] == 0, res[r]
+        assert_bitwise(np.load(os.path.join(tmp_path, f"rank{r}.npy")), want[r], f"rank {r}")
