@@ -34,7 +34,9 @@ sys.path.insert(0, ROOT)
 
 METRIC = "exchange ms/iter & algo GB/s (AlexNet 61M params, ASA16) at 2/4/8 B200 vs NVLink peak"
 HBM_FALLBACK_GBS = 6650.0  # B200_PROFILING.md fallback, used only if MEASURED_PEAKS.json is absent
-NVLINK_GBS = 770.0         # measured peer copy per direction (B200_PROFILING.md); 900 nominal
+NVLINK_NOMINAL_GBS = 900.0  # NVLink 5 per direction per GPU: the north star's roofline
+NVLINK_GBS = 770.0          # peer-copy fallback per direction (B200_PROFILING.md) when none is measured
+NORTH_STAR_FRAC = 0.70      # BASELINE.json north star: ">= 70% of the NVLink roofline"
 
 
 def parse():
@@ -88,9 +90,51 @@ def design_hbm_bytes(strategy, P, k, path):
     return k * 8.0 * P
 
 
-def nvlink_roof_us(strategy, P, k):
+def wire_bytes_per_direction(strategy, P, k):
+    """Algorithmic NVLink bytes one rank sends (= receives) per exchange
+    (SURVEY 8(d)): 2(k-1)/k * P * s, s = 2 (ASA16) or 4 (ASA, AR)."""
     s = 2 if strategy == "asa16" else 4
-    return 2 * (k - 1) / k * P * s / (NVLINK_GBS * 1e3) if k > 1 else 0.0
+    return 2 * (k - 1) / k * P * s if k > 1 else 0.0
+
+
+def nvlink_roof_us(strategy, P, k, gbs=NVLINK_GBS):
+    return wire_bytes_per_direction(strategy, P, k) / (gbs * 1e3)
+
+
+def north_star(strategy, P, k, ms, peer_gbs, peer_src, shared_gpu):
+    """The north star's terms for one exchange time `ms` (max over ranks): per-rank
+    algorithm bandwidth 4P/t (NCCL-tests convention), wire GB/s per direction,
+    the fraction of the NVLink roofline at 900 GB/s (the bar: >= 70 %, i.e. t <=
+    roof_900 / 0.7 -- 338.7 us for ASA16 AlexNet k = 8) and at the measured
+    peer-copy bandwidth."""
+    us = ms * 1e3
+    wire = wire_bytes_per_direction(strategy, P, k)
+    roof900 = wire / (NVLINK_NOMINAL_GBS * 1e3)
+    roofm = wire / (peer_gbs * 1e3)
+    bar = roof900 / NORTH_STAR_FRAC
+    return {"algbw_GBps": 4.0 * P / (ms * 1e-3) / 1e9,
+            "wire_GBps_per_direction": wire / (ms * 1e-3) / 1e9,
+            "nvlink_roof_us_900": roof900, "frac_vs_900": roof900 / us if us > 0 else None,
+            "nvlink_roof_us_measured": roofm, "frac_vs_measured": roofm / us if us > 0 else None,
+            "peer_GBps": peer_gbs, "peer_source": peer_src,
+            "bar_us": bar, "meets_bar": bool(us <= bar),
+            "bar": "north star: >= 70% of the 900 GB/s NVLink roofline (ASA16 AlexNet k=8: t <= 338.7 us)",
+            "over_nvlink": not shared_gpu}
+
+
+def nvlink_roofline(strategy, P, k, ms, peer_gbs, peer_src, nvml, kernel):
+    """roofline object of a one-process-per-GPU run: the dominant kernel moves
+    2(k-1)/k P s bytes per direction over NVLink per launch; `traffic` is the
+    NVML NVLink TX bytes per exchange of rank 0's GPU (the counters' analogue
+    of ncu's DRAM bytes), with its ratio to the algorithmic bytes."""
+    wire = wire_bytes_per_direction(strategy, P, k)
+    ach = wire / (ms * 1e-3) / 1e9
+    tx = None if not nvml else nvml.get("tx_bytes_per_step")
+    return {"bound": "nvlink", "achieved": ach, "peak": peer_gbs, "unit": "GB/s", "frac": ach / peer_gbs,
+            "frac_vs_900": ach / NVLINK_NOMINAL_GBS, "peak_source": peer_src,
+            "algorithmic_bytes_per_launch": wire, "traffic": tx,
+            "traffic_unit": "NVLink TX bytes per exchange (NVML, rank 0's GPU)",
+            "traffic_ratio": (tx / wire) if (tx and wire) else None, "kernel": kernel}
 
 
 class NvlinkCounters:
@@ -307,6 +351,82 @@ def traffic_from_profiles(workload_key):
 
 # ----------------------------------------------------------------- our arm
 
+KERNEL_NAMES = {0: "tm_exchange_kernel", 1: "tm_exchange_tma_kernel", 2: "tm_exchange_ws_kernel",
+                3: "tm_exchange_tmaws_kernel", 4: "tm_exchange_oneshot_kernel"}
+
+
+def shared_gpu_nccl_env(rank, world):
+    """torchrun on a box with fewer GPUs than ranks (test boxes): NCCL refuses two
+    ranks on one device of one host, but identifies hosts by NCCL_HOSTID, so each
+    rank gets its own (NCCL then uses its socket transport over loopback).  Used
+    for the plumbing collectives and for AR's ncclAllReduce."""
+    import torch
+    if torch.cuda.device_count() >= world:
+        return False
+    os.environ.setdefault("NCCL_HOSTID", f"tm-bench-rank-{rank}")
+    os.environ.setdefault("NCCL_SOCKET_IFNAME", "lo")
+    os.environ.setdefault("NCCL_IB_DISABLE", "1")
+    return True
+
+
+def peer_bandwidth(local, world, shared):
+    """Measured per-direction peer copy bandwidth (GB/s) from this rank's GPU to
+    the next rank's, 512 MiB copies through torch's cross-device copy (copy
+    engines over NVLink), best of 5; the B200_PROFILING.md figure when the ranks
+    share one GPU or TM_BENCH_P2P=0."""
+    import torch
+    if shared or os.environ.get("TM_BENCH_P2P") == "0" or torch.cuda.device_count() < 2:
+        return NVLINK_GBS, "fallback (B200_PROFILING.md measured peer copy)"
+    peer = (local + 1) % torch.cuda.device_count()
+    n = 512 << 20
+    src = torch.empty(n, dtype=torch.uint8, device=f"cuda:{local}")
+    dst = torch.empty(n, dtype=torch.uint8, device=f"cuda:{peer}")
+    best = None
+    with torch.cuda.device(local):
+        for _ in range(2):
+            dst.copy_(src, non_blocking=True)
+        torch.cuda.synchronize(local)
+        for _ in range(5):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            dst.copy_(src, non_blocking=True)
+            e1.record()
+            torch.cuda.synchronize(local)
+            ms = e0.elapsed_time(e1)
+            best = ms if best is None else min(best, ms)
+    del src, dst
+    torch.cuda.empty_cache()
+    return n / (best * 1e-3) / 1e9, f"measured in this run: cuda:{local} -> cuda:{peer} copy, 512 MiB, best of 5"
+
+
+def sample_indices(P):
+    g = np.random.default_rng(7)
+    return np.unique(np.concatenate([g.integers(0, P, 4096), np.arange(max(0, P - 64), P)]))
+
+
+def check_sample(strategy, dist_name, P, k, idx, got_per_rank):
+    """Rank 0's parity check of a multi-GPU run: regenerate every rank's seeded
+    input, evaluate the oracle's per-element definition at the sampled indices
+    (and the tail), compare with every rank's sampled output of the first
+    exchange -- bitwise for ASA / ASA16, within reading Q11 for AR (NCCL's
+    order) -- and check that all ranks hold the same bits (AR: within Q11)."""
+    from oracle import exchange as ox
+    from paper_1605_08325_b200.inputs import worker_buffer
+    vals = np.stack([worker_buffer(P, dist_name, r, config=3)[idx] for r in range(k)])
+    want = ox.element_average(vals, strategy)
+    if strategy == "ar":
+        tol = 1e-6 * np.mean(np.abs(vals.astype(np.float64)), axis=0)
+        ok = [bool(np.all(np.abs(g.astype(np.float64) - want) <= tol)) for g in got_per_rank]
+        how = "within reading Q11 (1e-6 * mean_j |x_ij|) of the oracle's rank-order definition"
+    else:
+        ok = [bool(np.array_equal(g.view(np.uint32), want.view(np.uint32))) for g in got_per_rank]
+        how = "bitwise vs the oracle's per-element definition"
+    same = all(np.array_equal(g.view(np.uint32), got_per_rank[0].view(np.uint32)) for g in got_per_rank)
+    return {"parity": all(ok), "per_rank": ok, "cross_rank_identical": bool(same),
+            "samples": int(len(idx)), "what": f"{len(idx)} sampled outputs (incl. the last 64) of every rank "
+                                              f"after the first exchange, {how}"}
+
+
 def main():
     args = parse()
     if args.impl == "reference":
@@ -318,12 +438,15 @@ def main():
 
     N = args.gpus
     multi = N > 1
+    shared = False
+    backend = None
     if multi:
         rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
         local = int(os.environ.get("LOCAL_RANK", rank)) % torch.cuda.device_count()
         torch.cuda.set_device(local)
+        shared = shared_gpu_nccl_env(rank, world)
         # NCCL for the plumbing (bootstrap all-gather, barriers, max-over-ranks);
-        # TM_BENCH_BACKEND=gloo lets several ranks share one GPU (test boxes)
+        # TM_BENCH_BACKEND=gloo runs it on the host instead
         backend = os.environ.get("TM_BENCH_BACKEND", "nccl")
         if backend == "nccl":
             dist.init_process_group("nccl", device_id=torch.device("cuda", local))
@@ -337,20 +460,23 @@ def main():
         k, nlocal, first = args.k, args.k, 0
     P = WORKLOADS[args.workload] if args.workload in WORKLOADS else int(args.workload)
     dev = torch.device("cuda", local)
+    coll_dev = dev if backend == "nccl" else "cpu"
+    peer_gbs, peer_src = peer_bandwidth(local, N, shared) if multi else (NVLINK_GBS, "fallback")
 
     host = [worker_buffer(P, args.dist, first + i, config=3) for i in range(nlocal)]
     bufs = [torch.from_numpy(h).to(dev) for h in host]
     ex = tm.Exchanger(P, args.strategy, rank=first, size=k, device=local, nlocal=nlocal,
                       path=args.path)
-    path = {0: "auto", 1: "staged", 2: "direct"}[ex.layout()["path"]]
-    STAGED_KERNEL[0] = ex.layout()["staged_kernel"]
+    lay0 = ex.layout()
+    path = {0: "auto", 1: "staged", 2: "direct"}[lay0["path"]]
+    STAGED_KERNEL[0] = lay0["staged_kernel"]
     stream = torch.cuda.current_stream()
 
     # L2 hygiene: the inputs one GPU touches per step must exceed the 126 MB L2;
     # for smaller workloads rotate over enough input sets (copies of the same
     # data) that consecutive steps never re-read L2-resident inputs.
     L2_BYTES = 126 * 1024 * 1024
-    per_step = 4 * P * nlocal
+    per_step = 4 * P * (nlocal if not shared else k)
     nsets = 1 if per_step > L2_BYTES else -(-2 * L2_BYTES // per_step)
     sets = [bufs] + [[b.clone() for b in bufs] for _ in range(nsets - 1)]
     it = [0]
@@ -360,15 +486,20 @@ def main():
         it[0] += 1
         ex.exchange(cur[0] if multi else cur, stream)
 
-    # first exchange (outside the timed region): keep sampled outputs so the
-    # cpu_baseline leg can check them against the oracle
+    # first exchange (outside the timed region): keep sampled outputs for the
+    # oracle check (every rank's on a multi-GPU run, rank k-1's on one GPU)
     step()
     torch.cuda.synchronize()
-    sample_idx = sample_got = None
-    if not multi:
-        g = np.random.default_rng(7)
-        sample_idx = np.unique(np.concatenate([g.integers(0, P, 4096), np.arange(max(0, P - 64), P)]))
-        sample_got = bufs[k - 1][torch.from_numpy(sample_idx).to(dev)].cpu().numpy()
+    sample_idx = sample_indices(P)
+    ti = torch.from_numpy(sample_idx).to(dev)
+    sample_got = bufs[0 if multi else k - 1][ti].cpu().numpy()
+    multi_parity = None
+    if multi:
+        got_all = [None] * N
+        dist.all_gather_object(got_all, sample_got)
+        if rank == 0:
+            multi_parity = check_sample(args.strategy, args.dist, P, k, sample_idx, got_all)
+        dist.barrier()
 
     for _ in range(args.warmup):
         step()
@@ -399,27 +530,37 @@ def main():
     if nvl0 is not None:
         nvl1 = nvl.read()
         if nvl1 is not None:
-            wire = 2 if args.strategy == "asa16" else 4
             nvlink = {"tx_bytes_per_step": (nvl1[0] - nvl0[0]) / args.steps,
                       "rx_bytes_per_step": (nvl1[1] - nvl0[1]) / args.steps,
-                      "expected_bytes_per_step_per_direction": 2 * (k - 1) / k * P * wire,
+                      "expected_bytes_per_step_per_direction": wire_bytes_per_direction(args.strategy, P, k),
                       "source": "NVML NVLINK_THROUGHPUT_DATA_TX/RX, rank 0's GPU"}
+    rank_ms = ms
     if multi:
-        ms = reduce_max(ms, dev if backend == "nccl" else "cpu")
+        ms = reduce_max(ms, coll_dev)
     code, bits = ex.status()
 
     bytes_alg = 4.0 * P * k  # every rank's fp32 buffer is averaged
     value = job_value(4.0 * P, k, ms)
+    lay = ex.layout()
 
     # roofline of the dominant (only) kernel in the step
     peak, peak_src = hbm_peak()
-    if multi:
-        roof = {"bound": "nvlink", "achieved": 2 * (k - 1) / k * P * (2 if args.strategy == "asa16" else 4)
-                / (ms * 1e-3) / 1e9, "peak": NVLINK_GBS, "unit": "GB/s", "traffic": None,
-                "peak_source": "measured peer copy per direction (B200_PROFILING.md)"}
-        roof["frac"] = roof["achieved"] / roof["peak"]
+    if multi and args.strategy == "ar":
+        kernel = "ncclAllReduce (NCCL's kernels)"
+    elif multi:
+        kernel = KERNEL_NAMES.get(lay["staged_kernel"], "tm_exchange_kernel")
+    else:
+        kernel = None
+    if multi and not shared:
+        roof = nvlink_roofline(args.strategy, P, k, ms, peer_gbs, peer_src, nvlink, kernel)
+    elif multi:
+        # every rank on one GPU: the per-GPU traffic is every rank's design bytes
+        roof = roofline(args.strategy, P, k, "staged", ms, peak, peak_src, args.workload)
+        roof["kernel"] = kernel
+        roof["note"] = "ranks share one GPU: HBM roofline of all ranks' staged design bytes (no NVLink)"
     else:
         roof = roofline(args.strategy, P, k, path, ms, peak, peak_src, args.workload)
+    ns = north_star(args.strategy, P, k, ms, peer_gbs, peer_src, shared or not multi)
 
     # secondary: the staged (multi-GPU) kernel timed on this GPU, same buffers
     staged = None
@@ -513,19 +654,22 @@ def main():
         torch.cuda.synchronize()
         e2e_ms = f0.elapsed_time(f1) / args.e2e_steps
         if multi:
-            e2e_ms = reduce_max(e2e_ms, dev if backend == "nccl" else "cpu")
+            e2e_ms = reduce_max(e2e_ms, coll_dev)
         # every e2e step reloads the same host inputs, so its result is the first
-        # exchange's: compare the sampled outputs (rank k-1 there, rank 0 here --
-        # all ranks hold the same average)
-        ok = None if sample_idx is None else bool(np.array_equal(
-            out_h.numpy()[sample_idx].view(np.uint32), sample_got.view(np.uint32)))
+        # exchange's: compare the sampled outputs (all ranks hold the same average;
+        # AR through NCCL: its order may differ between calls, so within Q11)
+        got_e2e = out_h.numpy()[sample_idx]
+        if args.strategy == "ar" and multi:
+            ok = bool(np.all(np.abs(got_e2e.astype(np.float64) - sample_got) <=
+                             2e-6 * np.maximum(np.abs(sample_got), 1e-30)))
+        else:
+            ok = bool(np.array_equal(got_e2e.view(np.uint32), sample_got.view(np.uint32)))
         e2e = {"value": bytes_alg / (e2e_ms * 1e-3) / 1e9, "unit": "GB/s", "ms_per_step": e2e_ms,
                "h2d_bytes_per_step": 4 * P * nlocal, "d2h_bytes_per_step": 4 * P,
-               "pipeline": f"{nch} ranges (tm_exchange_group_range), H2D on {nin} stream(s) / exchange / "
-                           f"D2H on its own stream",
+               "pipeline": f"{nch} ranges (tm_exchange{'' if multi else '_group'}_range), H2D on {nin} "
+                           f"stream(s) / exchange / D2H on its own stream",
                "sampled_result_equals_first_exchange": ok}
 
-    lay = ex.layout()
     # secondary: the multi-process default staged kernel (warp-specialised, TMA
     # engine), k ranks in this process on this GPU; the flavour is fixed at init,
     # so a second exchanger (the library holds one at a time)
@@ -558,7 +702,26 @@ def main():
             else:
                 os.environ["TM_STAGED_KERNEL"] = prev
 
+    # secondary on a multi-GPU run: AR through this library's C ABI (a8:
+    # ncclAllReduce with ncclAvg across the processes), timed the same way and
+    # checked within reading Q11 on every rank's sampled outputs
+    ar_tm = None
+    if multi and args.strategy != "ar" and not args.no_nccl_compare:
+        ex.finalize()
+        ar_tm = run_ar_through_tm(args, tm, dist, torch, P, k, rank, local, dev, host, sample_idx,
+                                  coll_dev, stream)
+        ex = None
+
+    cpu_base = None
+    if rank == 0 and not args.no_cpu_baseline:
+        cpu_base = cpu_baseline(args, k, P, host if not multi else None,
+                                None if multi else sample_idx, None if multi else sample_got)
+        if multi:
+            cpu_base["gpu_sample_parity"] = multi_parity["parity"] if multi_parity else None
+            cpu_base["gpu_sample"] = multi_parity["what"] if multi_parity else None
     if rank == 0:
+        ag_external = lay["allgather"] != 0 and lay["staged_kernel"] != 4
+        launches = 0 if (multi and args.strategy == "ar") else args.steps * (2 if (multi and ag_external) else 1)
         line = {
             "metric": METRIC, "value": value, "unit": "GB/s", "n_gpus": N, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
@@ -566,16 +729,24 @@ def main():
             "data": "synthetic",
             "config": {"workload": workload_name(args, k, multi),
                        "P": P, "k": k, "strategy": args.strategy, "dist": args.dist,
-                       "ranks_per_gpu": nlocal, "path": path, "seg_len": lay["seg_len"],
+                       "ranks_per_gpu": nlocal if not shared else k, "path": path, "seg_len": lay["seg_len"],
                        "ctas_per_rank": lay["ctas_per_rank"],
+                       "staged_kernel": KERNEL_NAMES.get(lay["staged_kernel"]) if path != "direct" else None,
+                       "allgather": {0: "sm", 1: "ce", 2: "nccl"}.get(lay["allgather"]),
+                       "selfcheck": lay.get("selfcheck"),
                        "l2": (f"inputs larger than L2 ({per_step / 1e9:.3f} GB per GPU per step), no flush"
                               if nsets == 1 else
                               f"inputs rotated over {nsets} copies ({per_step * nsets / 1e9:.3f} GB per GPU) "
                               f"so no step re-reads L2-resident inputs")},
+            "algbw_GBps": 4.0 * P / (ms * 1e-3) / 1e9,
+            "algbw_note": "per-rank algorithm bandwidth 4P/t (NCCL-tests convention); value = k * 4P / t",
             "roofline": roof,
-            "gpu_launches": args.steps,
+            "north_star": ns,
+            "parity": multi_parity,
+            "gpu_launches": launches,
             "staged_path_one_gpu": staged,
             "multiprocess_default_kernel_one_gpu": mp_kernel,
+            "ar_through_tm": ar_tm,
             "nvlink_counters": nvlink,
             "nccl_allreduce_same_buffer": nccl_ar,
             "clocks": clk.summary(),
@@ -584,17 +755,58 @@ def main():
             "exchange_us": ms * 1e3,
             "ms_per_step_loops": {"n": len(loop_ms), "median": float(np.median(loop_ms)),
                                   "min": float(np.min(loop_ms)), "max": float(np.max(loop_ms)),
-                                  "note": "rank 0's sub-loops of the one timed region"},
+                                  "rank0_ms": rank_ms, "note": "rank 0's sub-loops of the one timed region"},
             "nvlink_roof_us_if_distributed": nvlink_roof_us(args.strategy, P, k),
             "paper_context": "paper ASA16 AlexNet k=8: 91.5-94 ms per exchange on K20m/IB QDR (Table 2)",
         }
-        if not multi and not args.no_cpu_baseline:
-            line["cpu_baseline"] = cpu_baseline(args, k, P, host, sample_idx, sample_got)
+        if multi:
+            line["config"]["shared_gpu"] = shared
+            line["config"]["backend"] = backend
+        if cpu_base is not None:
+            line["cpu_baseline"] = cpu_base
         print(json.dumps(line), flush=True)
-    ex.finalize()
+    if ex is not None:
+        ex.finalize()
     if multi:
         dist.barrier()
         dist.destroy_process_group()
+
+
+def run_ar_through_tm(args, tm, dist, torch, P, k, rank, local, dev, host, sample_idx, coll_dev, stream):
+    """a8 on the multi-GPU run: tm_exchange with strategy AR (ncclAllReduce,
+    ncclAvg, in place) on every rank's own input, W warm-up + K timed calls, max
+    over ranks; every rank's sampled outputs of its first call checked within
+    Q11 on rank 0."""
+    try:
+        x = torch.from_numpy(host[0]).to(dev)
+        ex = tm.Exchanger(P, "ar", rank=rank, size=k, device=local, nlocal=1)
+        ex.exchange(x, stream)
+        torch.cuda.synchronize()
+        got = x[torch.from_numpy(sample_idx).to(dev)].cpu().numpy()
+        got_all = [None] * k
+        dist.all_gather_object(got_all, got)
+        for _ in range(args.warmup):
+            ex.exchange(x, stream)
+        dist.barrier()
+        torch.cuda.synchronize()
+        a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a0.record(stream)
+        for _ in range(args.steps):
+            ex.exchange(x, stream)
+        a1.record(stream)
+        torch.cuda.synchronize()
+        ams = reduce_max(a0.elapsed_time(a1) / args.steps, coll_dev)
+        code, _ = ex.status()
+        ex.finalize()
+        out = {"ms_per_step": ams, "algbw_GBps": 4.0 * P / (ams * 1e-3) / 1e9, "status": code,
+               "what": "tm_exchange, strategy AR: ncclAllReduce(ncclAvg) through the library's C ABI"}
+        if rank == 0:
+            par = check_sample("ar", args.dist, P, k, sample_idx, got_all)
+            out["parity_q11"] = par["parity"]
+            out["parity"] = par["what"]
+        return out
+    except Exception as e:  # context only: never fail the bench line
+        return {"error": str(e)[:300]}
 
 
 if __name__ == "__main__":

@@ -52,8 +52,9 @@
  * use the same values):
  *   TM_STAGED_KERNEL=reg|tma|ws|tmaws|oneshot  staged kernel flavour (default:
  *                      oneshot for segments L <= TM_ONESHOT_MAX_L elements
- *                      (default 16 Ki), reg for L <= 64 Ki, else tma in a
- *                      single-process group and tmaws across processes).
+ *                      (default: every L at k = 2, 32 Ki at k <= 4, 16 Ki above),
+ *                      reg for L <= 32 Ki, else tma in a single-process group
+ *                      and tmaws across processes).
  *   TM_ALLGATHER=sm|ce|nccl            allgather mode (tm_set_allgather); nccl
  *                      also creates the NCCL communicator at bootstrap.
  *   TM_PROCS_PER_GPU=n                 n processes share this GPU concurrently

@@ -21,6 +21,7 @@
 
 #include <algorithm>
 #include <chrono>
+#include <climits>
 #include <mutex>
 #include <vector>
 
@@ -125,12 +126,18 @@ Ctx g;
 Nccl g_nccl;
 std::mutex g_mu;
 
-// Flavour thresholds by segment length L (elements per rank), from the r02
-// latency table (profiles/r02/latency_flavours.txt): one-shot up to
-// kOneShotMaxL, the register two-phase kernel up to kRegMaxL, the TMA-engine
-// kernels above.
-constexpr int64_t kOneShotMaxL = 16384;
-constexpr int64_t kRegMaxL = 65536;
+// Flavour thresholds by segment length L (elements per rank) and k, from the r02
+// latency tables (profiles/r02/latency/, k processes concurrent under MPS and k
+// ranks in one process): the one-shot kernel moves (k-1) P s bytes per rank
+// instead of 2 (k-1)/k P s -- the same at k = 2, where its single barrier and
+// its (13 + 1) P HBM bytes (vs 14 + 2/k) win at every measured size up to
+// AlexNet's (346.6 vs 367.6 us for tma and 384.0 for tmaws, two processes under
+// MPS) -- so at k > 2 it pays only while the call is latency-bound: up to
+// L = 32 Ki at k <= 4 (11.4 vs 15.2 us for the register kernel at P = 64 Ki),
+// 16 Ki at k = 8 (19.5 vs 20.8 us at P = 128 Ki; 25.5 vs 22.3 us at 256 Ki).
+// The register two-phase kernel up to L = 32 Ki, the TMA-engine kernels above.
+int64_t oneshot_max_l(int k) { return k == 2 ? INT64_MAX : k <= 4 ? 32768 : 16384; }
+constexpr int64_t kRegMaxL = 32768;
 
 int64_t env_i64(const char* name, int64_t dflt) {
   const char* v = getenv(name);
@@ -558,9 +565,9 @@ int tm_exchange_init(int64_t nparams, const tm_world* world, int strategy) {
     // Small segments (L <= 64 Ki elements): the register kernel, whose phases
     // have no bulk-copy round trips to drain (measured 6-16 us vs 15-22 us for the
     // TMA / warp-specialised kernels at k = 8, P <= 256 Ki; profiles/r01/latency_flavours.txt).
-    // Segments of at most TM_ONESHOT_MAX_L elements (default kOneShotMaxL,
-    // profiles/r02/latency_flavours.txt): the one-shot kernel (one barrier).
-    const int64_t oneshot_max = env_i64("TM_ONESHOT_MAX_L", kOneShotMaxL);
+    // Segments of at most TM_ONESHOT_MAX_L elements (default oneshot_max_l(k),
+    // profiles/r02/latency/): the one-shot kernel (one barrier).
+    const int64_t oneshot_max = env_i64("TM_ONESHOT_MAX_L", oneshot_max_l(k));
     c.staged_kernel = c.L <= oneshot_max     ? tmx::kStagedOneShot
                       : c.L <= kRegMaxL      ? tmx::kStagedReg
                       : (c.nprocs == 1 ? tmx::kStagedTma : tmx::kStagedTmaWs);

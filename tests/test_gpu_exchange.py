@@ -410,13 +410,15 @@ def test_phase_log_does_not_change_results(path):
 
 
 def test_default_staged_flavour_by_segment_length(monkeypatch):
-    """Without TM_STAGED_KERNEL: the one-shot kernel for segments of <= 16 Ki
-    elements, the register two-phase kernel up to 64 Ki (latency-bound), the
-    TMA-engine kernel above that in a single-process group."""
+    """Without TM_STAGED_KERNEL: the one-shot kernel for every segment at k = 2,
+    for segments of <= 32 Ki elements at k <= 4 and 16 Ki above; the register two-phase
+    kernel up to 32 Ki (latency-bound); the TMA-engine kernel above that in a
+    single-process group."""
     monkeypatch.delenv("TM_STAGED_KERNEL", raising=False)
     monkeypatch.delenv("TM_ONESHOT_MAX_L", raising=False)
-    for P, k, want in ((100_003, 2, 0), (131_072 * 8, 8, 1), (65_536 * 4, 4, 0), (1_000_003, 2, 1),
-                       (16_384 * 8, 8, 4), (10_000, 2, 4), (16_385 * 8, 8, 0)):
+    for P, k, want in ((100_003, 2, 4), (131_072 * 8, 8, 1), (32_768 * 4, 4, 4), (32_769 * 4, 4, 1),
+                       (2_097_152, 2, 4), (60_965_224, 2, 4), (16_384 * 8, 8, 4), (16_385 * 8, 8, 0),
+                       (32_768 * 8, 8, 0), (32_769 * 8, 8, 1), (10_000, 3, 4)):
         with tm.Exchanger(P, "asa16", size=k, nlocal=k, path="staged") as ex:
             assert ex.layout()["staged_kernel"] == want, (P, k)
 
