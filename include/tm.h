@@ -52,7 +52,7 @@
  * use the same values):
  *   TM_STAGED_KERNEL=reg|tma|ws|tmaws|oneshot  staged kernel flavour (default:
  *                      oneshot for segments L <= TM_ONESHOT_MAX_L elements
- *                      (default: every L at k = 2, 32 Ki at k <= 4, 16 Ki above),
+ *                      (default 1 Mi at k = 2, 32 Ki at k <= 4, 16 Ki above),
  *                      reg for L <= 32 Ki, else tma in a single-process group
  *                      and tmaws across processes).
  *   TM_ALLGATHER=sm|ce|nccl            allgather mode (tm_set_allgather); nccl
@@ -393,6 +393,14 @@ int tm_set_allgather(int mode);
  * 0, 3, 4, 5).  capacity in uint64 slots (>= nlocal*C*8, else ignored); NULL
  * disables. */
 int tm_set_phase_log(uint64_t* dev_buf, int64_t capacity);
+
+/* CTA budget of range (bucket) exchanges, per rank (0 = none, the default;
+ * TM_RANGE_CTAS at init sets it too): a bucket exchanged while backward still
+ * runs should occupy few SMs.  Staged path: at most `ctas` CTAs per rank (every
+ * rank must set the same budget).  Direct path: the register kernel (no shared
+ * memory, so its CTAs can share SMs with a GEMM's) on at most `ctas` CTAs.
+ * Full exchanges (tm_exchange / tm_exchange_group) are not affected. */
+int tm_set_range_ctas(int ctas);
 
 /* Barrier spin timeout in nanoseconds (default 10 s; 0 restores default). */
 int tm_set_timeout_ns(uint64_t ns);

@@ -287,34 +287,35 @@ cudaError_t direct_tma(const LocalBufs& lb, int64_t P, uint32_t* status, unsigne
 
 template <int K>
 cudaError_t direct_k(const LocalBufs& lb, int64_t P, uint32_t* status, unsigned long long* ctr,
-                     bool q16, int dev, cudaStream_t s) {
+                     bool q16, int dev, cudaStream_t s, int max_ctas) {
   static const bool force_ldg = env_int("TM_DIRECT_LDG", 0) == 1;
-  if (P >= 2048 && !force_ldg)
+  if (P >= 2048 && !force_ldg && max_ctas <= 0)
     return q16 ? direct_tma<K, true>(lb, P, status, ctr, dev, s)
                : direct_tma<K, false>(lb, P, status, ctr, dev, s);
   const int64_t want = (P / 4 + kThreads - 1) / kThreads;
   const int per_sm = K >= 7 ? 3 : 4;  // = the kernel's __launch_bounds__ residency
-  const int grid = (int)std::min<int64_t>(std::max<int64_t>(want, 1), per_sm * sm_count(dev));
+  const int64_t cap = max_ctas > 0 ? max_ctas : (int64_t)per_sm * sm_count(dev);
+  const int grid = (int)std::min<int64_t>(std::max<int64_t>(want, 1), cap);
   if (q16) tm_direct_kernel<K, true><<<grid, kThreads, 0, s>>>(lb, 0, P, status);
   else tm_direct_kernel<K, false><<<grid, kThreads, 0, s>>>(lb, 0, P, status);
   return cudaGetLastError();
 }
 
 cudaError_t launch_direct(float* const* bufs, int k, int64_t P, bool q16, bool sum,
-                          uint32_t* status, unsigned long long* tile_ctr, cudaStream_t s) {
+                          uint32_t* status, unsigned long long* tile_ctr, cudaStream_t s, int max_ctas) {
   LocalBufs lb{};
   lb.sum = sum ? 1 : 0;
   for (int j = 0; j < k; ++j) lb.b[j] = bufs[j];
   int dev = 0;
   cudaGetDevice(&dev);
   switch (k) {
-    case 2: return direct_k<2>(lb, P, status, tile_ctr, q16, dev, s);
-    case 3: return direct_k<3>(lb, P, status, tile_ctr, q16, dev, s);
-    case 4: return direct_k<4>(lb, P, status, tile_ctr, q16, dev, s);
-    case 5: return direct_k<5>(lb, P, status, tile_ctr, q16, dev, s);
-    case 6: return direct_k<6>(lb, P, status, tile_ctr, q16, dev, s);
-    case 7: return direct_k<7>(lb, P, status, tile_ctr, q16, dev, s);
-    case 8: return direct_k<8>(lb, P, status, tile_ctr, q16, dev, s);
+    case 2: return direct_k<2>(lb, P, status, tile_ctr, q16, dev, s, max_ctas);
+    case 3: return direct_k<3>(lb, P, status, tile_ctr, q16, dev, s, max_ctas);
+    case 4: return direct_k<4>(lb, P, status, tile_ctr, q16, dev, s, max_ctas);
+    case 5: return direct_k<5>(lb, P, status, tile_ctr, q16, dev, s, max_ctas);
+    case 6: return direct_k<6>(lb, P, status, tile_ctr, q16, dev, s, max_ctas);
+    case 7: return direct_k<7>(lb, P, status, tile_ctr, q16, dev, s, max_ctas);
+    case 8: return direct_k<8>(lb, P, status, tile_ctr, q16, dev, s, max_ctas);
     default: return cudaErrorInvalidValue;
   }
 }

@@ -98,8 +98,12 @@ cudaError_t launch_exchange(const ExchangeArgs& a, int nlocal, bool wire16, int 
 // tile_ctr: two zero-initialised device words for dynamic tile claiming (the
 // kernel's last CTA resets them: no memset node per launch), or null for the
 // static tile assignment.
+// max_ctas > 0: a CTA budget (bucketed exchanges beside compute kernels): the
+// register kernel (no shared memory, so its CTAs can co-reside with a GEMM's)
+// on at most max_ctas CTAs.
 cudaError_t launch_direct(float* const* bufs, int k, int64_t P, bool q16, bool sum,
-                          uint32_t* status, unsigned long long* tile_ctr, cudaStream_t s);
+                          uint32_t* status, unsigned long long* tile_ctr, cudaStream_t s,
+                          int max_ctas = 0);
 
 cudaError_t launch_easgd(float* x, float* c, int64_t n, float alpha, bool concurrent,
                          cudaStream_t s);

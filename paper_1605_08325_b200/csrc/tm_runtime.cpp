@@ -21,7 +21,6 @@
 
 #include <algorithm>
 #include <chrono>
-#include <climits>
 #include <mutex>
 #include <vector>
 
@@ -111,6 +110,7 @@ struct Ctx {
   // a counter (a kernel resets its pair when its last CTA retires).
   unsigned long long* tile_ctrs = nullptr;
   uint32_t ctr_seq = 0;
+  int range_ctas = 0;  // CTA budget of range (bucket) exchanges per rank; 0 = none
   int path = TM_PATH_AUTO;
   int staged_kernel = tmx::kStagedTma;  // staged kernel flavour, fixed at init (it sets C)
   int ag_mode = TM_AG_SM;               // tm_allgather of the staged path
@@ -129,14 +129,19 @@ std::mutex g_mu;
 // Flavour thresholds by segment length L (elements per rank) and k, from the r02
 // latency tables (profiles/r02/latency/, k processes concurrent under MPS and k
 // ranks in one process): the one-shot kernel moves (k-1) P s bytes per rank
-// instead of 2 (k-1)/k P s -- the same at k = 2, where its single barrier and
-// its (13 + 1) P HBM bytes (vs 14 + 2/k) win at every measured size up to
-// AlexNet's (346.6 vs 367.6 us for tma and 384.0 for tmaws, two processes under
-// MPS) -- so at k > 2 it pays only while the call is latency-bound: up to
-// L = 32 Ki at k <= 4 (11.4 vs 15.2 us for the register kernel at P = 64 Ki),
-// 16 Ki at k = 8 (19.5 vs 20.8 us at P = 128 Ki; 25.5 vs 22.3 us at 256 Ki).
+// instead of 2 (k-1)/k P s -- the same at k = 2, where its single barrier wins
+// at every measured size (two processes under MPS: P = 2 Ki .. 2 Mi, and up to
+// AlexNet's 346.6 vs 367.6 us for tma) -- so at k > 2 it pays only while the
+// call is latency-bound: up to L = 32 Ki at k <= 4 (11.4 vs 15.2 us for the
+// register kernel at P = 64 Ki), 16 Ki at k = 8 (19.5 vs 20.8 us at P = 128 Ki;
+// 25.5 vs 22.3 us at 256 Ki).  At k = 2 the cap is L = 1 Mi all the same: over
+// NVLink the one-shot's pull cannot start on a chunk before that chunk's whole
+// pre-cast, while the warp-specialised two-phase kernel overlaps the pre-cast
+// (HBM) with the pull (NVLink) sub-chunk by sub-chunk -- an overlap one GPU,
+// where both are HBM traffic, cannot show; above ~2 M parameters the pre-cast
+// (6P bytes of HBM) is long enough for that to matter.
 // The register two-phase kernel up to L = 32 Ki, the TMA-engine kernels above.
-int64_t oneshot_max_l(int k) { return k == 2 ? INT64_MAX : k <= 4 ? 32768 : 16384; }
+int64_t oneshot_max_l(int k) { return k == 2 ? (int64_t)1 << 20 : k <= 4 ? 32768 : 16384; }
 constexpr int64_t kRegMaxL = 32768;
 
 int64_t env_i64(const char* name, int64_t dflt) {
@@ -202,6 +207,7 @@ ExchangeArgs make_args(float* const* bufs, int64_t off, int64_t n) {
     const int64_t chunk = g.staged_kernel == tmx::kStagedOneShot ? tmx::kOneShotChunk : tmx::kMinChunk;
     const int64_t want = std::max<int64_t>(1, (a.L + chunk - 1) / chunk);
     a.C = (int)std::min<int64_t>(g.C, want);
+    if (g.range_ctas > 0) a.C = std::min(a.C, g.range_ctas);  // bucket beside compute kernels
     a.Lc = round_up((a.L + a.C - 1) / a.C, tmx::kAlign);
   }
   a.nvec = 1;
@@ -296,7 +302,9 @@ int do_exchange(float* const* bufs, int nbufs, int64_t off, int64_t n, cudaStrea
     for (int i = 0; i < nbufs; ++i) shifted[i] = bufs[i] + off;
     const char* st_env = getenv("TM_DIRECT_STATIC");  // diagnostics: static tile assignment
     unsigned long long* ctr = (st_env && st_env[0] == '1') ? nullptr : next_tile_ctr();
-    cudaError_t e = tmx::launch_direct(shifted, g.k, n, g.strategy == TM_ASA16, g.sum, g.status, ctr, s);
+    const bool range = !(off == 0 && n == g.P);
+    cudaError_t e = tmx::launch_direct(shifted, g.k, n, g.strategy == TM_ASA16, g.sum, g.status, ctr, s,
+                                       range ? g.range_ctas : 0);
     return e == cudaSuccess ? TM_OK : cuda_fail("launch_direct", e);
   }
   if (g.strategy == TM_AR) {
@@ -629,6 +637,7 @@ int tm_exchange_init(int64_t nparams, const tm_world* world, int strategy) {
   }
   c.status = reinterpret_cast<uint32_t*>(c.slab + c.rank_stride * c.nlocal);
   c.tile_ctrs = reinterpret_cast<unsigned long long*>(c.slab + c.rank_stride * c.nlocal + 256);
+  c.range_ctas = std::max(0, getenv("TM_RANGE_CTAS") ? atoi(getenv("TM_RANGE_CTAS")) : 0);
   c.inited = true;
   c.ready = (c.nprocs == 1);
   g = c;
@@ -938,6 +947,14 @@ int tm_set_phase_log(uint64_t* dev_buf, int64_t capacity) {
   if (dev_buf && capacity < 1) return TM_E_ARG;
   g.stamps = dev_buf;
   g.stamps_cap = dev_buf ? capacity : 0;
+  return TM_OK;
+}
+
+int tm_set_range_ctas(int ctas) {
+  std::lock_guard<std::mutex> lk(g_mu);
+  if (!g.inited) return TM_E_STATE;
+  if (ctas < 0) return TM_E_ARG;
+  g.range_ctas = ctas;
   return TM_OK;
 }
 

@@ -78,6 +78,7 @@ _SIGS = {
     "tm_exchange_status": (ctypes.c_int, [_P, ctypes.POINTER(ctypes.c_uint32)]),
     "tm_layout": (ctypes.c_int, [ctypes.POINTER(tm_layout_info)]),
     "tm_set_timeout_ns": (ctypes.c_int, [ctypes.c_uint64]),
+    "tm_set_range_ctas": (ctypes.c_int, [ctypes.c_int]),
     "tm_set_path": (ctypes.c_int, [ctypes.c_int]),
     "tm_set_allgather": (ctypes.c_int, [ctypes.c_int]),
     "tm_set_phase_log": (ctypes.c_int, [_P, ctypes.c_int64]),
@@ -288,6 +289,10 @@ def tm_layout():
 
 def tm_set_timeout_ns(ns):
     _check(lib().tm_set_timeout_ns(int(ns)), "tm_set_timeout_ns")
+
+
+def tm_set_range_ctas(ctas):
+    _check(lib().tm_set_range_ctas(int(ctas)), "tm_set_range_ctas")
 
 
 def tm_set_path(path):

@@ -410,14 +410,14 @@ def test_phase_log_does_not_change_results(path):
 
 
 def test_default_staged_flavour_by_segment_length(monkeypatch):
-    """Without TM_STAGED_KERNEL: the one-shot kernel for every segment at k = 2,
-    for segments of <= 32 Ki elements at k <= 4 and 16 Ki above; the register two-phase
+    """Without TM_STAGED_KERNEL: the one-shot kernel for segments of <= 1 Mi
+    elements at k = 2, 32 Ki at k <= 4 and 16 Ki above; the register two-phase
     kernel up to 32 Ki (latency-bound); the TMA-engine kernel above that in a
     single-process group."""
     monkeypatch.delenv("TM_STAGED_KERNEL", raising=False)
     monkeypatch.delenv("TM_ONESHOT_MAX_L", raising=False)
     for P, k, want in ((100_003, 2, 4), (131_072 * 8, 8, 1), (32_768 * 4, 4, 4), (32_769 * 4, 4, 1),
-                       (2_097_152, 2, 4), (60_965_224, 2, 4), (16_384 * 8, 8, 4), (16_385 * 8, 8, 0),
+                       (2_097_152, 2, 4), (2_097_153 + 511, 2, 1), (16_384 * 8, 8, 4), (16_385 * 8, 8, 0),
                        (32_768 * 8, 8, 0), (32_769 * 8, 8, 1), (10_000, 3, 4)):
         with tm.Exchanger(P, "asa16", size=k, nlocal=k, path="staged") as ex:
             assert ex.layout()["staged_kernel"] == want, (P, k)
@@ -502,6 +502,27 @@ def test_oneshot_interleaved_ranges_bitwise(monkeypatch, strategy, k):
                 want[r][off:off + cnt] = seg[r]
         code, _ = ex.status()
     assert code == tm.TM_OK
+    got = to_host(bufs)
+    for r in range(k):
+        assert_bitwise(got[r], want[r], f"rank {r}")
+
+
+@pytest.mark.parametrize("path", PATHS)
+@pytest.mark.parametrize("budget", [1, 8])
+def test_range_cta_budget_bitwise(path, budget):
+    """tm_set_range_ctas: bucket exchanges on at most `budget` CTAs per rank
+    (the register direct kernel / fewer staged CTAs) give the oracle's bits."""
+    k, P = 4, 300_007
+    X = worker_buffers(P, k, "D2", config=160)
+    bufs = to_dev(X)
+    with tm.Exchanger(P, "asa16", size=k, nlocal=k, path=path) as ex:
+        tm.tm_set_range_ctas(budget)
+        b1, b2 = P // 3 // 4 * 4, 2 * P // 3 // 4 * 4
+        for off, cnt in ((b2, P - b2), (b1, b2 - b1), (0, b1)):
+            ex.exchange_range(bufs, off, cnt)
+        code, _ = ex.status()
+    assert code == tm.TM_OK
+    want = ox.asa16_average(X)
     got = to_host(bufs)
     for r in range(k):
         assert_bitwise(got[r], want[r], f"rank {r}")

@@ -13,8 +13,16 @@ FLOPs follow AlexNet's per-layer backward cost for a 128-image batch per worker
 Prints ms per iteration of each schedule (CUDA events, median of 10 after 3
 warm-ups) and the exchange alone.  Run with TM_DIRECT_LDG=1 to use the register
 kernel, which leaves shared memory free for the GEMMs' CTAs.
+
+    python tools/overlap.py [--budgets 0,8,16,32,64] [--priority]
+
+--budgets: CTA budgets of the bucket exchanges (tm_set_range_ctas; 0 = none,
+the full persistent grid); --priority: the exchange stream at high priority,
+so its CTAs are dispatched as soon as a GEMM CTA retires.
 """
 
+import argparse
+import json
 import os
 import statistics
 import sys
@@ -33,6 +41,10 @@ LAYERS = [("conv1", 34_944, 105e6), ("conv2", 307_456, 224e6), ("conv3", 885_120
 
 
 def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--budgets", default="0,8,16,32,64")
+    ap.add_argument("--priority", action="store_true")
+    args = ap.parse_args()
     torch.cuda.set_device(0)
     k, batch = 8, 128
     P = sum(n for _, n, _ in LAYERS)
@@ -47,7 +59,8 @@ def main():
         n = max(256, int(round((flops / 2) ** (1 / 3) / 128)) * 128)
         a = torch.randn(n, n, device="cuda", dtype=torch.bfloat16)
         gemms.append((a, torch.randn(n, n, device="cuda", dtype=torch.bfloat16)))
-    sa, sb = torch.cuda.Stream(), torch.cuda.Stream()
+    sa = torch.cuda.Stream()
+    sb = torch.cuda.Stream(priority=-1) if args.priority else torch.cuda.Stream()
     ex = tm.Exchanger(P, "asa16", size=k, nlocal=k)
 
     def backward(stream, events=None):
@@ -92,13 +105,24 @@ def main():
                 out.append(e0.elapsed_time(e1))
         return statistics.median(out)
 
+    def buckets_only():
+        for li in reversed(range(len(LAYERS))):
+            ex.exchange_range(bufs, offs[li], LAYERS[li][1], sb)
+
     res = {name: timed(fn) for name, fn in (("backward_only", backward_only), ("exchange_only", exchange_only),
-                                            ("serial", serial), ("overlapped", overlapped))}
+                                            ("serial", serial))}
+    for b in [int(v) for v in args.budgets.split(",")]:
+        tm.tm_set_range_ctas(b)
+        res[f"buckets_only_budget{b}"] = timed(buckets_only)
+        res[f"overlapped_budget{b}"] = timed(overlapped)
+    tm.tm_set_range_ctas(0)
     code, _ = ex.status()
     ex.finalize()
     kern = "register" if os.environ.get("TM_DIRECT_LDG") == "1" else "tma"
-    print({"direct_kernel": kern, **{k_: round(v, 3) for k_, v in res.items()}, "status": code,
-           "hidden_ms": round(res["serial"] - res["overlapped"], 3)})
+    best = min((v, n) for n, v in res.items() if n.startswith("overlapped"))
+    print(json.dumps({"direct_kernel": kern, "priority_stream": args.priority,
+                      **{k_: round(v, 3) for k_, v in res.items()}, "status": code,
+                      "best_overlapped": best[1], "hidden_ms": round(res["serial"] - best[0], 3)}))
 
 
 if __name__ == "__main__":
