@@ -57,6 +57,9 @@
  *                      and tmaws across processes).
  *   TM_ALLGATHER=sm|ce|nccl            allgather mode (tm_set_allgather); nccl
  *                      also creates the NCCL communicator at bootstrap.
+ *   TM_AG_TABLE=path                   without TM_ALLGATHER: the mode by (k, L)
+ *                      from a table measured on the multi-GPU box, one rule
+ *                      "k L_max mode" per line, first match wins (default sm).
  *   TM_PROCS_PER_GPU=n                 n processes share this GPU concurrently
  *                      (CUDA MPS): each keeps 1/n of the co-resident CTAs.
  *   TM_NCCL_LIB=path                   libnccl.so.2 to dlopen (the binding sets

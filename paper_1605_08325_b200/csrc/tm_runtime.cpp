@@ -149,6 +149,31 @@ int64_t env_i64(const char* name, int64_t dflt) {
   return (v && *v) ? atoll(v) : dflt;
 }
 
+// The allgather decision step (north star: "falling back to NCCL allgather ...
+// only where it measures faster"): TM_AG_TABLE names a table measured on the
+// multi-GPU box (tools/ag_decide.py writes it from tools/multigpu_eval.sh's
+// bench lines), one rule per line "k L_max mode" (mode sm | ce | nccl, '#'
+// comments); the first rule with this k and L <= L_max picks the mode.  No
+// table or no matching rule: the fused SM pull (measured fastest on one GPU:
+// 0.97 vs 1.85 ms for the copy engines, profiles/r01/allgather_modes.jsonl).
+// Every rank reads the same table, and the bootstrap checks the modes agree.
+const char* ag_table_mode(const char* path, int k, int64_t L) {
+  FILE* f = fopen(path, "r");
+  if (!f) return nullptr;
+  char line[256];
+  const char* mode = nullptr;
+  while (!mode && fgets(line, sizeof line, f)) {
+    int kk = 0;
+    long long lmax = 0;
+    char m[16] = {0};
+    if (line[0] == '#' || sscanf(line, "%d %lld %15s", &kk, &lmax, m) != 3) continue;
+    if (kk != k || L > lmax) continue;
+    mode = !strcmp(m, "nccl") ? "nccl" : !strcmp(m, "ce") ? "ce" : "sm";
+  }
+  fclose(f);
+  return mode;
+}
+
 bool wire16(int strategy) { return strategy == TM_ASA16; }
 int wire_bytes(int strategy) { return wire16(strategy) ? 2 : 4; }
 int64_t round_up(int64_t a, int64_t b) { return (a + b - 1) / b * b; }
@@ -590,6 +615,8 @@ int tm_exchange_init(int64_t nparams, const tm_world* world, int strategy) {
     if (sk && !strcmp(sk, "tmaws")) c.staged_kernel = tmx::kStagedTmaWs;
     if (sk && !strcmp(sk, "oneshot")) c.staged_kernel = tmx::kStagedOneShot;
     const char* ag = getenv("TM_ALLGATHER");  // sm | ce | nccl
+    const char* ag_table = getenv("TM_AG_TABLE");
+    if (!ag && ag_table && c.nprocs > 1) ag = ag_table_mode(ag_table, k, c.L);
     if (ag && !strcmp(ag, "ce")) c.ag_mode = TM_AG_CE;
     c.want_nccl_ag = ag && !strcmp(ag, "nccl") && c.nprocs > 1;
     if (c.want_nccl_ag) c.ag_mode = TM_AG_NCCL;

@@ -102,3 +102,26 @@ def test_roofline_fraction_and_traffic():
 def test_job_value_is_whole_job():
     # every rank's fp32 buffer over the max-over-ranks time
     assert bench.job_value(4.0 * ALEXNET, 8, 0.57) == pytest.approx(4.0 * ALEXNET * 8 / 0.57e-3 / 1e9)
+
+
+def test_allgather_decision_table(tmp_path):
+    """tools/ag_decide.py keeps, per (k, L), the fastest allgather mode among the
+    bench lines whose parity passed, and writes the TM_AG_TABLE rules."""
+    import subprocess
+    import sys as _sys
+
+    def line(k, L, ms, ag, parity=True, kern="tm_exchange_tmaws_kernel"):
+        return {"ms_per_step": ms, "parity": {"parity": parity},
+                "config": {"k": k, "seg_len": L, "staged_kernel": kern, "allgather": ag}}
+    rows = {"bench_n8_alexnet_tmaws_agsm.json": line(8, 7620864, 0.30, "sm"),
+            "bench_n8_alexnet_tmaws_agnccl.json": line(8, 7620864, 0.28, "nccl"),
+            "bench_n8_alexnet_tmaws_agce.json": line(8, 7620864, 0.25, "ce", parity=False),
+            "bench_n8_googlenet_tmaws_agsm.json": line(8, 875008, 0.040, "sm"),
+            "bench_n8_googlenet_tmaws_agnccl.json": line(8, 875008, 0.050, "nccl"),
+            "bench_n8_googlenet_oneshot_agce.json": line(8, 875008, 0.001, "ce", kern="tm_exchange_oneshot_kernel")}
+    for name, d in rows.items():
+        (tmp_path / name).write_text(json.dumps(d) + "\n")
+    out = subprocess.run([_sys.executable, os.path.join(ROOT, "tools", "ag_decide.py"), str(tmp_path)],
+                         capture_output=True, text=True, check=True).stdout
+    rules = [l.split("#")[0].split() for l in out.splitlines() if l and not l.startswith("#")]
+    assert rules == [["8", str((875008 + 7620864) // 2), "sm"], ["8", str(1 << 62), "nccl"]]

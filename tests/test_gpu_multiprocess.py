@@ -371,3 +371,19 @@ def test_multiprocess_selfcheck_fault_falls_back(tmp_path, strategy, k, kernel, 
         assert res[r]["code"] == 0, res[r]
         assert res[r]["layout"]["selfcheck"] == 2 and res[r]["layout"]["staged_kernel"] == 0, res[r]
         assert_bitwise(np.load(os.path.join(tmp_path, f"rank{r}.npy")), want[r], f"rank {r}")
+
+
+def test_multiprocess_allgather_decision_table(tmp_path):
+    """TM_AG_TABLE (the allgather decision step): without TM_ALLGATHER every rank
+    takes the mode of the first matching "k L_max mode" rule -- here the copy
+    engines for k = 2 -- and the exchange stays bitwise."""
+    table = tmp_path / "ag_table.txt"
+    table.write_text("# k L_max mode\n4 1000000000 nccl\n2 100 sm\n2 1000000000 ce\n")
+    P, k = 100_003, 2
+    res = launch(tmp_path, k, "asa16", P, "D2", extra_env={"TM_AG_TABLE": str(table), "TM_STAGED_KERNEL": "tma"})
+    want = [worker_buffer(P, "D2", r, config=50) for r in range(k)]
+    for _ in range(3):
+        want = ox.exchange(want, "asa16")
+    for r in range(k):
+        assert res[r]["code"] == 0 and res[r]["layout"]["allgather"] == 1, res[r]
+        assert_bitwise(np.load(os.path.join(tmp_path, f"rank{r}.npy")), want[r], f"rank {r}")

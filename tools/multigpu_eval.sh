@@ -1,6 +1,14 @@
 #!/usr/bin/env bash
-# Multi-GPU evaluation for an 8 x B200 box (not runnable on the one-GPU boxes of
-# round 1).  Writes everything under gpurun_out/multigpu/.
+# Multi-GPU evaluation for an 8 x B200 box (the one-GPU boxes of rounds 1-2
+# cannot run it).  Writes everything under gpurun_out/multigpu/:
+#   p2p.jsonl                 peer copy bandwidth of every pair (tools/p2p_probe.py)
+#   bench_n{N}_{wl}_{fl}_ag{ag}.json   bench.py at N = 2, 4, 8 per staged flavour and
+#                             allgather mode (each line: north-star block, NVML
+#                             NVLink bytes vs algorithmic, oracle parity of every rank)
+#   bench_n{N}_{strategy}.json         ASA fp32 and AR (NCCL) at AlexNet size
+#   ag_table.txt              the allgather decision table (tools/ag_decide.py)
+#   nsys_n8.*                 an nsys capture with NVLink GPU metrics, if nsys exists
+#   pytest_multiprocess.txt   the multi-process GPU tests with one GPU per rank
 #   bash tools/multigpu_eval.sh [steps]
 set -u
 STEPS=${1:-200}
@@ -10,23 +18,36 @@ NG=$(python -c 'import torch; print(torch.cuda.device_count())')
 echo "GPUs: $NG"
 python tools/p2p_probe.py > "$OUT/p2p.jsonl" 2>&1
 PORT=29511
+run() {  # N out-name extra-args...
+  local N=$1 NAME=$2; shift 2
+  PORT=$((PORT + 1))
+  timeout 900 python -m torch.distributed.run --nnodes=1 --nproc-per-node "$N" --master-addr 127.0.0.1 \
+    --master-port "$PORT" bench.py --gpus "$N" --steps "$STEPS" --warmup 10 "$@" > "$OUT/$NAME.json" 2> "$OUT/$NAME.err"
+  echo "$NAME rc=$?"
+}
 for N in 2 4 8; do
   [ "$N" -le "$NG" ] || continue
-  for FL in tmaws tma ws reg; do
-    for AG in sm ce nccl; do
-      PORT=$((PORT + 1))
-      TM_STAGED_KERNEL=$FL TM_ALLGATHER=$AG timeout 600 python -m torch.distributed.run --nnodes=1 \
-        --nproc-per-node "$N" --master-addr 127.0.0.1 --master-port "$PORT" bench.py --gpus "$N" \
-        --steps "$STEPS" --warmup 10 --no-e2e > "$OUT/bench_n${N}_${FL}_${AG}.json" 2> "$OUT/bench_n${N}_${FL}_${AG}.err"
-      echo "N=$N $FL $AG rc=$?"
+  run "$N" "bench_n${N}_default" --no-e2e
+  for WL in alexnet googlenet 1m; do
+    for FL in tmaws tma oneshot reg; do
+      for AG in sm ce nccl; do
+        TM_STAGED_KERNEL=$FL TM_ALLGATHER=$AG run "$N" "bench_n${N}_${WL}_${FL}_ag${AG}" --workload "$WL" --no-e2e \
+          --no-cpu-baseline --no-nccl-compare
+      done
     done
   done
   for S in asa ar; do
-    PORT=$((PORT + 1))
-    timeout 600 python -m torch.distributed.run --nnodes=1 --nproc-per-node "$N" --master-addr 127.0.0.1 \
-      --master-port "$PORT" bench.py --gpus "$N" --strategy "$S" --steps "$STEPS" --warmup 10 --no-e2e \
-      > "$OUT/bench_n${N}_${S}.json" 2> "$OUT/bench_n${N}_${S}.err"
+    run "$N" "bench_n${N}_${S}" --strategy "$S" --no-e2e
   done
 done
+python tools/ag_decide.py "$OUT" > "$OUT/ag_table.txt"
+if command -v nsys > /dev/null && [ "$NG" -ge 8 ]; then
+  nsys profile --gpu-metrics-devices=all -o "$OUT/nsys_n8" --force-overwrite true \
+    python -m torch.distributed.run --nnodes=1 --nproc-per-node 8 --master-addr 127.0.0.1 --master-port 29599 \
+    bench.py --gpus 8 --steps 20 --warmup 5 --no-e2e --no-cpu-baseline > "$OUT/nsys_n8.log" 2>&1
+  echo "nsys rc=$?"
+else
+  echo "nsys not installed: NVLink bytes come from the NVML counters in each bench line" > "$OUT/nsys_n8.log"
+fi
 timeout 3600 python -m pytest tests/test_gpu_multiprocess.py -x -q > "$OUT/pytest_multiprocess.txt" 2>&1
 echo "done: $OUT"
