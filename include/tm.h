@@ -264,12 +264,17 @@ int tm_bsp_step_group(float* const* w, float* const* v, const float* const* grad
  * reading Q15).  Works in any initialised context; n = init nparams. */
 int tm_easgd_update(float* worker_buf, float* center_buf, float alpha, void* stream);
 
-/* Extended form: explicit length n, and concurrent != 0 applies the centre
- * update with an atomic add (red.global.add.f32, system scope) so several
- * workers may update one centre at once (no lost updates; order not fixed).
- * The float atomic flushes fp32-subnormal operands and results of the centre's
- * add to signed zero (hardware semantics), unlike the exclusive update.
- * Does not need tm_exchange_init. */
+/* Extended form: explicit length n, and a concurrent mode so several workers
+ * may update one centre at once (no lost updates; order not fixed):
+ *   concurrent = 0  exclusive (the caller serialises the workers);
+ *   concurrent = 1  centre += e by the hardware float atomic
+ *                   (red.global.add(.v4).f32, system scope): it flushes
+ *                   fp32-subnormal operands and results of the centre's add to
+ *                   signed zero, unlike the exclusive update;
+ *   concurrent = 2  centre += e by a compare-and-swap loop around one IEEE
+ *                   fp32 add (gradual underflow, reading Q6): every update is
+ *                   exactly fl(c + e) of the value it replaced; slower.
+ * TM_E_ARG for another value.  Does not need tm_exchange_init. */
 int tm_easgd_update_ex(float* worker_buf, float* center_buf, int64_t n, float alpha,
                        int concurrent, void* stream);
 
@@ -296,8 +301,9 @@ int tm_easgd_center(int owner_rank, float** center);
 /* One elastic update (as tm_easgd_update) of this worker's full fp32[nparams]
  * buffer against the sharded centre: element i meets the shard of rank i / L.
  * concurrent == 0: the caller serialises the workers (bitwise equal to the
- * oracle's arrival order); concurrent != 0: centre += e by atomic add (system
- * scope across processes), no lost updates, order not fixed. */
+ * oracle's arrival order); 1 / 2: centre += e by the float atomic / the
+ * CAS-loop IEEE add of tm_easgd_update_ex (system scope across processes), no
+ * lost updates, order not fixed. */
 int tm_easgd_update_sharded(float* worker_buf, float alpha, int concurrent, void* stream);
 
 /* Per-worker ATOMIC exchange with the sharded centre (the server

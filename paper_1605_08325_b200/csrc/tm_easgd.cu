@@ -17,13 +17,51 @@ using namespace dev;
 // ---------------------------------------------------------------------------
 // EASGD elastic update, one fp32 op per step:
 //   d = fl(x - c); e = fl(alpha d); x' = fl(x - e); c' = fl(c + e).
-// Concurrent mode applies c += e with red.relaxed.sys.global.add.f32 so several
-// workers (possibly on other GPUs, through an IPC mapping) may update one
-// centre at once without lost updates; each worker then read a possibly stale c.
+// Concurrent modes let several workers (possibly on other GPUs, through an IPC
+// mapping) update one centre at once without lost updates; each worker then
+// read a possibly stale c:
+//   Mode 1: c += e with red.relaxed.sys.global.add(.v4).f32 -- the hardware
+//           float atomic, which flushes fp32-subnormal operands and results to
+//           signed zero;
+//   Mode 2: c += e with a compare-and-swap loop around __fadd_rn -- one exact
+//           IEEE add per update with gradual underflow (reading Q6), at the cost
+//           of a CAS round trip per element.
 // ---------------------------------------------------------------------------
-template <bool Concurrent>
+template <bool SYS>
+__device__ __forceinline__ void cas_add(float* p, float v) {
+  unsigned int* a = reinterpret_cast<unsigned int*>(p);
+  unsigned int old = __ldcg(a);
+  for (;;) {
+    const unsigned int want = __float_as_uint(__fadd_rn(__uint_as_float(old), v));
+    const unsigned int got = SYS ? atomicCAS_system(a, old, want) : atomicCAS(a, old, want);
+    if (got == old) break;
+    old = got;
+  }
+}
+
+template <int Mode, bool SYS>
+__device__ __forceinline__ void centre_add4(float* c, float4 e) {
+  if constexpr (Mode == 1) {
+    if (SYS) red_add4_sys(c, e);
+    else red_add4_gpu(c, e);
+  } else {
+    cas_add<SYS>(c, e.x); cas_add<SYS>(c + 1, e.y); cas_add<SYS>(c + 2, e.z); cas_add<SYS>(c + 3, e.w);
+  }
+}
+template <int Mode, bool SYS>
+__device__ __forceinline__ void centre_add1(float* c, float e) {
+  if constexpr (Mode == 1) {
+    if (SYS) red_add_sys(c, e);
+    else red_add_gpu(c, e);
+  } else {
+    cas_add<SYS>(c, e);
+  }
+}
+
+template <int Mode>
 __global__ void __launch_bounds__(kThreads)
 easgd_kernel(float* __restrict__ x, float* c, int64_t n, float alpha, int vec) {
+  constexpr bool Concurrent = Mode != 0;
   const int64_t stride = (int64_t)gridDim.x * kThreads;
   const int64_t tid = (int64_t)blockIdx.x * kThreads + threadIdx.x;
   int64_t done = 0;
@@ -39,7 +77,7 @@ easgd_kernel(float* __restrict__ x, float* c, int64_t n, float alpha, int vec) {
       xv.z = __fsub_rn(xv.z, ez); xv.w = __fsub_rn(xv.w, ew);
       st16_f(x + v * 4, xv);
       if (Concurrent) {
-        red_add4_sys(c + v * 4, make_float4(ex, ey, ez, ew));
+        centre_add4<Mode, true>(c + v * 4, make_float4(ex, ey, ez, ew));
       } else {
         cv.x = __fadd_rn(cv.x, ex); cv.y = __fadd_rn(cv.y, ey);
         cv.z = __fadd_rn(cv.z, ez); cv.w = __fadd_rn(cv.w, ew);
@@ -53,7 +91,7 @@ easgd_kernel(float* __restrict__ x, float* c, int64_t n, float alpha, int vec) {
     const float ci = Concurrent ? __ldcg(c + i) : c[i];
     const float e = elastic_diff(xi, ci, alpha);
     x[i] = __fsub_rn(xi, e);
-    if (Concurrent) red_add_sys(c + i, e);
+    if (Concurrent) centre_add1<Mode, true>(c + i, e);
     else c[i] = __fadd_rn(ci, e);
   }
 }
@@ -63,9 +101,10 @@ easgd_kernel(float* __restrict__ x, float* c, int64_t n, float alpha, int vec) {
 // Segments are multiples of 256 elements, so a 16-byte vector never straddles
 // two shards.  Concurrent mode: c += e by red.add at system scope when the
 // shard may be on another GPU.
-template <bool Concurrent, bool SYS>
+template <int Mode, bool SYS>
 __global__ void __launch_bounds__(kThreads)
 easgd_sharded_kernel(float* __restrict__ x, const __grid_constant__ ShardArgs sa, float alpha) {
+  constexpr bool Concurrent = Mode != 0;
   const int64_t stride = (int64_t)gridDim.x * kThreads;
   const int64_t tid = (int64_t)blockIdx.x * kThreads + threadIdx.x;
   for (int s = 0; s < sa.k; ++s) {
@@ -84,8 +123,7 @@ easgd_sharded_kernel(float* __restrict__ x, const __grid_constant__ ShardArgs sa
       xv.z = __fsub_rn(xv.z, ez); xv.w = __fsub_rn(xv.w, ew);
       st16_f(xs + v * 4, xv);
       if (Concurrent) {
-        if (SYS) red_add4_sys(c + v * 4, make_float4(ex, ey, ez, ew));
-        else red_add4_gpu(c + v * 4, make_float4(ex, ey, ez, ew));
+        centre_add4<Mode, SYS>(c + v * 4, make_float4(ex, ey, ez, ew));
       } else {
         cv.x = __fadd_rn(cv.x, ex); cv.y = __fadd_rn(cv.y, ey);
         cv.z = __fadd_rn(cv.z, ez); cv.w = __fadd_rn(cv.w, ew);
@@ -97,7 +135,7 @@ easgd_sharded_kernel(float* __restrict__ x, const __grid_constant__ ShardArgs sa
       const float ci = __ldcg(c + i);
       const float e = elastic_diff(xi, ci, alpha);
       xs[i] = __fsub_rn(xi, e);
-      if (Concurrent) { if (SYS) red_add_sys(c + i, e); else red_add_gpu(c + i, e); }
+      if (Concurrent) centre_add1<Mode, SYS>(c + i, e);
       else c[i] = __fadd_rn(ci, e);
     }
   }
@@ -483,12 +521,13 @@ cast_rn16_kernel(const float* __restrict__ in, uint16_t* __restrict__ out, int64
 
 }  // namespace
 
-cudaError_t launch_easgd(float* x, float* c, int64_t n, float alpha, bool concurrent,
+cudaError_t launch_easgd(float* x, float* c, int64_t n, float alpha, int concurrent,
                          cudaStream_t s) {
   const int vec = ((reinterpret_cast<uintptr_t>(x) | reinterpret_cast<uintptr_t>(c)) & 15) == 0;
   const int grid = streaming_grid(vec ? n / 4 + 4 : n);
-  if (concurrent) easgd_kernel<true><<<grid, kThreads, 0, s>>>(x, c, n, alpha, vec);
-  else easgd_kernel<false><<<grid, kThreads, 0, s>>>(x, c, n, alpha, vec);
+  if (concurrent == 2) easgd_kernel<2><<<grid, kThreads, 0, s>>>(x, c, n, alpha, vec);
+  else if (concurrent) easgd_kernel<1><<<grid, kThreads, 0, s>>>(x, c, n, alpha, vec);
+  else easgd_kernel<0><<<grid, kThreads, 0, s>>>(x, c, n, alpha, vec);
   return cudaGetLastError();
 }
 
@@ -531,14 +570,17 @@ cudaError_t launch_easgd_round(float* const* w, int nw, const int32_t* order, in
   return cudaGetLastError();
 }
 
-cudaError_t launch_easgd_sharded(float* x, const ShardArgs& sa, float alpha, bool concurrent,
+cudaError_t launch_easgd_sharded(float* x, const ShardArgs& sa, float alpha, int concurrent,
                                  cudaStream_t s) {
   const int grid = streaming_grid(sa.L / 4 + 4);
-  if (concurrent) {
-    if (sa.sys) easgd_sharded_kernel<true, true><<<grid, kThreads, 0, s>>>(x, sa, alpha);
-    else easgd_sharded_kernel<true, false><<<grid, kThreads, 0, s>>>(x, sa, alpha);
+  if (concurrent == 2) {
+    if (sa.sys) easgd_sharded_kernel<2, true><<<grid, kThreads, 0, s>>>(x, sa, alpha);
+    else easgd_sharded_kernel<2, false><<<grid, kThreads, 0, s>>>(x, sa, alpha);
+  } else if (concurrent) {
+    if (sa.sys) easgd_sharded_kernel<1, true><<<grid, kThreads, 0, s>>>(x, sa, alpha);
+    else easgd_sharded_kernel<1, false><<<grid, kThreads, 0, s>>>(x, sa, alpha);
   } else {
-    easgd_sharded_kernel<false, false><<<grid, kThreads, 0, s>>>(x, sa, alpha);
+    easgd_sharded_kernel<0, false><<<grid, kThreads, 0, s>>>(x, sa, alpha);
   }
   return cudaGetLastError();
 }

@@ -105,7 +105,8 @@ cudaError_t launch_direct(float* const* bufs, int k, int64_t P, bool q16, bool s
                           uint32_t* status, unsigned long long* tile_ctr, cudaStream_t s,
                           int max_ctas = 0);
 
-cudaError_t launch_easgd(float* x, float* c, int64_t n, float alpha, bool concurrent,
+// concurrent: 0 exclusive, 1 hardware float atomic (red.add), 2 CAS-loop IEEE add
+cudaError_t launch_easgd(float* x, float* c, int64_t n, float alpha, int concurrent,
                          cudaStream_t s);
 cudaError_t launch_easgd_round(float* const* w, int nw, const int32_t* order, int norder,
                                float* c, int64_t n, float alpha, cudaStream_t s);
@@ -124,7 +125,7 @@ struct ShardArgs {
   uint64_t timeout_ns;
 };
 constexpr int64_t kLockChunk = 4096;  // elements per lock in locked EASGD
-cudaError_t launch_easgd_sharded(float* x, const ShardArgs& sa, float alpha, bool concurrent,
+cudaError_t launch_easgd_sharded(float* x, const ShardArgs& sa, float alpha, int concurrent,
                                  cudaStream_t s);
 // Locked mode: each (shard, chunk) is updated under a spin lock, so every
 // worker's update of an element is one atomic read-modify-write of the centre

@@ -807,7 +807,8 @@ int tm_easgd_update_ex(float* worker_buf, float* center_buf, int64_t n, float al
   if (n == 0) return TM_OK;
   if ((reinterpret_cast<uintptr_t>(worker_buf) | reinterpret_cast<uintptr_t>(center_buf)) & 3)
     return TM_E_ALIGN;
-  cudaError_t e = tmx::launch_easgd(worker_buf, center_buf, n, alpha, concurrent != 0,
+  if (concurrent < 0 || concurrent > 2) return TM_E_ARG;
+  cudaError_t e = tmx::launch_easgd(worker_buf, center_buf, n, alpha, concurrent,
                                    static_cast<cudaStream_t>(stream));
   return e == cudaSuccess ? TM_OK : cuda_fail("easgd", e);
 }
@@ -855,7 +856,8 @@ int tm_easgd_update_sharded(float* worker_buf, float alpha, int concurrent, void
     sa.sys = g.nprocs > 1;
     cudaSetDevice(g.device);
   }
-  cudaError_t e = tmx::launch_easgd_sharded(worker_buf, sa, alpha, concurrent != 0,
+  if (concurrent < 0 || concurrent > 2) return TM_E_ARG;
+  cudaError_t e = tmx::launch_easgd_sharded(worker_buf, sa, alpha, concurrent,
                                             static_cast<cudaStream_t>(stream));
   return e == cudaSuccess ? TM_OK : cuda_fail("easgd_sharded", e);
 }

@@ -240,8 +240,9 @@ def tm_easgd_update_ex(worker, center, alpha, concurrent=False, stream=None, n=N
     if n < 0 or n > worker.numel():
         raise ValueError(f"n = {n} outside [0, {worker.numel()}]")
     cptr = center if isinstance(center, int) else _fp32_cuda(center, min_n=n).value
+    mode = 2 if concurrent == "exact" else int(concurrent)  # 0, 1 (red.add), 2 / "exact" (CAS loop)
     _check(lib().tm_easgd_update_ex(_fp32_cuda(worker), _P(cptr), int(n), ctypes.c_float(alpha),
-                                    int(bool(concurrent)), _stream_handle(stream)), "tm_easgd_update_ex")
+                                    mode, _stream_handle(stream)), "tm_easgd_update_ex")
 
 
 def tm_easgd_round(workers, order, center, alpha, stream=None):
@@ -253,8 +254,9 @@ def tm_easgd_round(workers, order, center, alpha, stream=None):
 
 
 def tm_easgd_update_sharded(worker, alpha, concurrent=False, stream=None):
+    mode = 2 if concurrent == "exact" else int(concurrent)
     _check(lib().tm_easgd_update_sharded(_param_buf(worker), ctypes.c_float(alpha),
-                                         int(bool(concurrent)), _stream_handle(stream)),
+                                         mode, _stream_handle(stream)),
            "tm_easgd_update_sharded")
 
 

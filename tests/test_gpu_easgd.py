@@ -304,3 +304,56 @@ def test_concurrent_mode_flushes_subnormals():
     assert_bitwise(gx, wx)  # the worker side is plain IEEE arithmetic
     assert np.all(gc[:8] == 0) and np.all(wc[:8] != 0)
     assert_bitwise(gc[8:], wc[8:])
+
+
+@pytest.mark.parametrize("dist", ["D1", "D6"])
+def test_exact_concurrent_mode_keeps_subnormals_bitwise(dist):
+    """Concurrent mode 2 ("exact") adds e to the centre with a compare-and-swap
+    loop around one IEEE fp32 add (gradual underflow, reading Q6): a single
+    worker's update is bitwise the exclusive update and the oracle's, subnormal
+    e and c' included (where mode 1's float atomic flushes them)."""
+    n = 100_003
+    x = worker_buffer(n, dist, 0, config=47)
+    c = worker_buffer(n, dist, 1, config=47)
+    x[:8] = np.float32(1e-39)
+    c[:8] = np.float32(0.0)
+    xd, cd = to_dev([x, c])
+    tm.tm_easgd_update_ex(xd, cd, 0.5, concurrent="exact")
+    gx, gc = to_host([xd, cd])
+    wx, wc = easgd_update(x, c, 0.5)
+    assert_bitwise(gx, wx, "worker")
+    assert_bitwise(gc, wc, "centre")
+    assert np.all(gc[:8] != 0)
+
+
+def test_exact_concurrent_workers_conserve_and_keep_subnormals():
+    """8 workers on 8 streams in exact concurrent mode (Q15: no bitwise oracle,
+    the order is the hardware's).  No update is lost: sum_w x_w + c is conserved
+    within the rounding bound; and on a block of fp32-subnormal values -- where
+    every subtraction, product by 2^-4 and sum is exact whatever the order (the
+    values are multiples of 2^-149 below 2^-126) -- the centre is EXACTLY c plus
+    the sum of the workers' moves, i.e. nothing was flushed to zero."""
+    n = 1 << 20
+    nw, alpha = 8, 0.0625
+    W = [worker_buffer(n, "D1", r, config=48) for r in range(nw)]
+    c = worker_buffer(n, "D1", 99, config=48)
+    tiny = np.float32(2.0 ** -149)
+    for w in range(nw):
+        W[w][:256] = tiny * np.float32(16 * (w + 1)) * np.arange(1, 257, dtype=np.float32)
+    c[:256] = np.float32(0.0)
+    Wd = to_dev(W)
+    cd = to_dev([c])[0]
+    streams = [torch.cuda.Stream() for _ in range(nw)]
+    torch.cuda.synchronize()
+    for w, s in zip(Wd, streams):
+        tm.tm_easgd_update_ex(w, cd, alpha, concurrent="exact", stream=s)
+    torch.cuda.synchronize()
+    gW = to_host(Wd)
+    gc = to_host([cd])[0]
+    moves = sum(W[w][:256].astype(np.float64) - gW[w][:256] for w in range(nw))
+    assert np.all(gc[:256] != 0)
+    assert np.array_equal(gc[:256].astype(np.float64), moves)
+    tot0 = sum(w.astype(np.float64) for w in W) + c
+    tot1 = sum(w.astype(np.float64) for w in gW) + gc
+    scale = sum(np.abs(w.astype(np.float64)) for w in gW) + np.abs(gc)
+    assert np.all(np.abs(tot1 - tot0) <= 2 * (nw + 1) * 2.0 ** -24 * scale + 1e-44)

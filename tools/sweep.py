@@ -113,17 +113,20 @@ def easgd_rows(P, nw, alpha, pk):
                  "hbm_GBps": (8.0 * P * nw + 8.0 * P) / (ms * 1e-3) / 1e9})
     streams = [torch.cuda.Stream() for _ in range(nw)]
 
-    def concurrent():
+    def concurrent(mode):
         cur = torch.cuda.current_stream()
         ev = torch.cuda.Event()
         ev.record(cur)
         for w, s in zip(W, streams):
             s.wait_event(ev)
-            tm.tm_easgd_update_ex(w, c, alpha, concurrent=True, stream=s)
+            tm.tm_easgd_update_ex(w, c, alpha, concurrent=mode, stream=s)
         for s in streams:
             cur.wait_stream(s)
-    ms = timeit(concurrent)
+    ms = timeit(lambda: concurrent(1))
     rows.append({"mode": f"{nw} concurrent updates (red.add, {nw} streams)", "us": ms * 1e3,
+                 "hbm_GBps": 16.0 * P * nw / (ms * 1e-3) / 1e9})
+    ms = timeit(lambda: concurrent("exact"))
+    rows.append({"mode": f"{nw} concurrent updates (exact: CAS-loop IEEE add, {nw} streams)", "us": ms * 1e3,
                  "hbm_GBps": 16.0 * P * nw / (ms * 1e-3) / 1e9})
     del c
     with tm.Exchanger(P, "easgd", size=nw, nlocal=nw) as ex:
