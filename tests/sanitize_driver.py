@@ -72,6 +72,27 @@ def main():
             check(Wt[r].cpu().numpy(), ww[r], f"bsp w {path}")
             check(Vt[r].cpu().numpy(), vv[r], f"bsp v {path}")
         n_ok += 1
+    # round 2: exact concurrent EASGD (CAS loop), and bucket exchanges under a CTA budget
+    W2 = worker_buffers(20011, 2, "D1", config=76)
+    c2 = worker_buffers(20011, 1, "D1", config=77)[0]
+    W2d = [torch.from_numpy(w).cuda() for w in W2]
+    c2d = torch.from_numpy(c2).cuda()
+    tm.tm_easgd_update_ex(W2d[0], c2d, 0.25, concurrent="exact")
+    w0, cc2 = easgd_update(W2[0], c2, 0.25)
+    check(c2d.cpu().numpy(), cc2, "easgd exact centre")
+    check(W2d[0].cpu().numpy(), w0, "easgd exact worker")
+    for path in ("direct", "staged"):
+        k, P = 3, 30011
+        X = worker_buffers(P, k, "D2", config=78)
+        bufs = [torch.from_numpy(x).cuda() for x in X]
+        with tm.Exchanger(P, "asa16", size=k, nlocal=k, path=path) as ex:
+            tm.tm_set_range_ctas(2)
+            ex.exchange_range(bufs, 12000, P - 12000)
+            ex.exchange_range(bufs, 0, 12000)
+        want = ox.exchange(X, "asa16")
+        for r in range(k):
+            check(bufs[r].cpu().numpy(), want[r], f"budget range {path}")
+        n_ok += 1
     x = torch.randn(100003, device="cuda")
     h = tm.tm_cast_rn16(x)
     torch.cuda.synchronize()
