@@ -41,6 +41,16 @@ for N in 2 4 8; do
   done
 done
 python tools/ag_decide.py "$OUT" > "$OUT/ag_table.txt"
+# config 5: message-size sweep 64 KB .. 1 GB (fp32 bytes per rank), ASA16 vs NCCL's allreduce
+for N in 2 4 8; do
+  [ "$N" -le "$NG" ] || continue
+  PORT=$((PORT + 1))
+  timeout 1800 python -m torch.distributed.run --nnodes=1 --nproc-per-node "$N" --master-addr 127.0.0.1 \
+    --master-port "$PORT" tools/latency_mp.py --nccl --flavours default \
+    --P 16384,65536,262144,1048576,4194304,16777216,67108864,268435456 --inner 8 --reps 10 \
+    > "$OUT/sweep_n$N.jsonl" 2> "$OUT/sweep_n$N.err"
+  echo "sweep N=$N rc=$?"
+done
 if command -v nsys > /dev/null && [ "$NG" -ge 8 ]; then
   nsys profile --gpu-metrics-devices=all -o "$OUT/nsys_n8" --force-overwrite true \
     python -m torch.distributed.run --nnodes=1 --nproc-per-node 8 --master-addr 127.0.0.1 --master-port 29599 \

@@ -2,7 +2,10 @@
 """A few calls of one library entry point at AlexNet size, k = 8 ranks on one GPU
 (a short target for ncu captures; no timing).
 
-    python tools/one_call.py exchange-direct|exchange-staged|bsp-direct|bsp-staged|easgd-round [n]
+    python tools/one_call.py exchange-direct|exchange-staged|bsp-direct|bsp-staged|bsp-staged-mom|easgd-round [n]
+
+TM_ONE_CALL_P / TM_ONE_CALL_K override the size and rank count (e.g. a small P
+for the one-shot kernel).
 """
 
 import os
@@ -15,7 +18,8 @@ sys.path.insert(0, ROOT)
 
 from paper_1605_08325_b200 import tm  # noqa: E402
 
-P, K = 60_965_224, 8
+P = int(os.environ.get("TM_ONE_CALL_P", "60965224"))
+K = int(os.environ.get("TM_ONE_CALL_K", "8"))
 
 
 def main():
@@ -33,7 +37,7 @@ def main():
         G = [torch.randn(P, device="cuda", generator=g) * 0.01 for _ in range(K)]
         with tm.Exchanger(P, "asa16", size=K, nlocal=K, path=what.split("-")[1]) as ex:
             for _ in range(n):
-                ex.bsp_step(W, V, G, 0.01, 0.9)
+                ex.bsp_step(W, V, G, 0.01, 0.9, exchange_momentum=what.endswith("-mom"))
     elif what == "easgd-round":
         c = torch.randn(P, device="cuda", generator=g) * 0.01
         for _ in range(n):
