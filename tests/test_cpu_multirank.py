@@ -89,3 +89,49 @@ def test_reference_arm_rank0_only(tmp_path):
     assert d["impl"] == "reference" and d["n_gpus"] == 2 and d["config"]["k"] == 2
     assert d["unit"] == "GB/s" and d["value"] > 0 and d["cpu_baseline"]["kind"] == "oracle"
     assert d["e2e"]["h2d_bytes_per_step"] == 0
+
+
+PARITY_WORKER = r'''
+import json, os, sys
+sys.path.insert(0, sys.argv[1])
+import numpy as np
+import torch.distributed as dist
+dist.init_process_group("gloo")
+r, n = dist.get_rank(), dist.get_world_size()
+import bench
+from oracle import exchange as ox
+from paper_1605_08325_b200.inputs import worker_buffer
+P = 20_011
+idx = bench.sample_indices(P)
+# what every rank's GPU result would hold at the sampled indices (the oracle's
+# average of all ranks' seeded inputs); rank 1 flips one bit when asked to
+vals = np.stack([worker_buffer(P, "D2", q, config=3)[idx] for q in range(n)])
+mine = ox.element_average(vals, "asa16")
+if r == 1 and sys.argv[3] == "corrupt":
+    mine.view(np.uint32)[5] ^= 1
+got = [None] * n
+dist.all_gather_object(got, mine)
+if r == 0:
+    res = bench.check_sample("asa16", "D2", P, n, idx, got)
+    json.dump(res, open(os.path.join(sys.argv[2], "parity.json"), "w"))
+dist.barrier()
+dist.destroy_process_group()
+'''
+
+
+@pytest.mark.parametrize("mode", ["clean", "corrupt"])
+def test_multi_rank_parity_check_flow(tmp_path, mode):
+    """bench.py's N>1 parity path over gloo, world size 2: every rank's sampled
+    outputs are all-gathered to rank 0, which regenerates every rank's seeded
+    input and checks them against the oracle's per-element definition; a single
+    flipped bit on rank 1 fails that rank and the cross-rank identity."""
+    script = tmp_path / "p.py"
+    script.write_text(PARITY_WORKER)
+    outs = _launch(2, [sys.executable, str(script), ROOT, str(tmp_path), mode], tmp_path)
+    for rc, o, e in outs:
+        assert rc == 0, e[-2000:]
+    res = json.load(open(tmp_path / "parity.json"))
+    if mode == "clean":
+        assert res["parity"] and res["per_rank"] == [True, True] and res["cross_rank_identical"]
+    else:
+        assert not res["parity"] and res["per_rank"] == [True, False] and not res["cross_rank_identical"]
