@@ -162,7 +162,7 @@ def test_multiprocess_nccl_allgather(tmp_path, strategy, k, kernel):
         assert_bitwise(np.load(os.path.join(tmp_path, f"rank{r}.npy")), want[r], f"rank {r}")
 
 
-@pytest.mark.parametrize("k", [2, 4, 8])
+@pytest.mark.parametrize("k", [2, 3, 4, 8])
 def test_multiprocess_ar_nccl_within_q11(tmp_path, k):
     """AR across processes is NCCL's allreduce (ncclAvg, a8): its summation order
     is NCCL's, so it is checked against the oracle within reading Q11.  On a
