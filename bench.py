@@ -387,22 +387,28 @@ def peer_bandwidth(local, world, shared):
     n = 512 << 20
     src = torch.empty(n, dtype=torch.uint8, device=f"cuda:{local}")
     dst = torch.empty(n, dtype=torch.uint8, device=f"cuda:{peer}")
-    best = None
-    with torch.cuda.device(local):
-        for _ in range(2):
-            dst.copy_(src, non_blocking=True)
+
+    def sync():
         torch.cuda.synchronize(local)
-        for _ in range(5):
-            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            e0.record()
+        torch.cuda.synchronize(peer)
+    # host clock around back-to-back copies, both devices synchronised: a
+    # cross-device copy may be enqueued on either device's stream, so events on
+    # one of them need not bracket it
+    for _ in range(2):
+        dst.copy_(src, non_blocking=True)
+    sync()
+    best = None
+    for _ in range(3):
+        t0 = time.perf_counter()
+        for _ in range(4):
             dst.copy_(src, non_blocking=True)
-            e1.record()
-            torch.cuda.synchronize(local)
-            ms = e0.elapsed_time(e1)
-            best = ms if best is None else min(best, ms)
+        sync()
+        ms = (time.perf_counter() - t0) * 1e3 / 4
+        best = ms if best is None else min(best, ms)
     del src, dst
     torch.cuda.empty_cache()
-    return n / (best * 1e-3) / 1e9, f"measured in this run: cuda:{local} -> cuda:{peer} copy, 512 MiB, best of 5"
+    return n / (best * 1e-3) / 1e9, (f"measured in this run: cuda:{local} -> cuda:{peer} copy engines, 512 MiB, "
+                                     f"best of 3 x 4 back-to-back copies")
 
 
 def sample_indices(P):
