@@ -129,7 +129,7 @@ def nvlink_roofline(strategy, P, k, ms, peer_gbs, peer_src, nvml, kernel):
     of ncu's DRAM bytes), with its ratio to the algorithmic bytes."""
     wire = wire_bytes_per_direction(strategy, P, k)
     ach = wire / (ms * 1e-3) / 1e9
-    tx = None if not nvml else nvml.get("tx_bytes_per_step")
+    tx = None if not nvml else nvml.get("tx_bytes_per_step")  # None when NVML cannot count
     return {"bound": "nvlink", "achieved": ach, "peak": peer_gbs, "unit": "GB/s", "frac": ach / peer_gbs,
             "frac_vs_900": ach / NVLINK_NOMINAL_GBS, "peak_source": peer_src,
             "algorithmic_bytes_per_launch": wire, "traffic": tx,
@@ -539,6 +539,10 @@ def main():
     counts = [b - a for a, b in zip([0] + marks, marks + [args.steps])]
     loop_ms = [bounds[i].elapsed_time(bounds[i + 1]) / counts[i] for i in range(len(counts))]
     nvlink = None
+    if multi and nvl0 is None:
+        nvlink = {"unavailable": "NVML's NVLink byte fields report NOT_SUPPORTED on this pool's B200s "
+                                 "(tools/nvml_nvlink_probe.py); tools/nvlink_ncu.sh reads ncu's "
+                                 "nvltx/nvlrx counters of the exchange kernel instead"}
     if nvl0 is not None:
         nvl1 = nvl.read()
         if nvl1 is not None:

@@ -59,5 +59,6 @@ if command -v nsys > /dev/null && [ "$NG" -ge 8 ]; then
 else
   echo "nsys not installed: NVLink bytes come from the NVML counters in each bench line" > "$OUT/nsys_n8.log"
 fi
+[ "$NG" -ge 8 ] && bash tools/nvlink_ncu.sh 8 "$OUT"
 timeout 3600 python -m pytest tests/test_gpu_multiprocess.py -x -q > "$OUT/pytest_multiprocess.txt" 2>&1
 echo "done: $OUT"
