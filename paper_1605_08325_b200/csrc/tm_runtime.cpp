@@ -631,6 +631,13 @@ int tm_exchange_init(int64_t nparams, const tm_world* world, int strategy) {
     const int64_t want = std::max<int64_t>(1, (c.L + chunk - 1) / chunk);
     c.C = (int)std::min<int64_t>(std::max(cmax, 1), want);
     c.Lc = round_up((c.L + c.C - 1) / c.C, tmx::kAlign);
+    // The warp-specialised kernel overlaps the pre-cast with the pull only across
+    // sub-chunks (>= kWsMinSub elements each); a chunk too short for two of them
+    // would run both phases on half a CTA each with nothing to overlap, so the
+    // TMA kernel (same shared memory, same C) takes it (k = 8 under MPS: 34.4 vs
+    // 36.3 us at P = 1 Mi, 54.7 vs 58.0 us at 2 Mi; profiles/r02/latency/).
+    if (c.staged_kernel == tmx::kStagedTmaWs && !(sk && *sk) && c.Lc < 2 * tmx::kWsMinSub)
+      c.staged_kernel = tmx::kStagedTma;
     // Staging: nvec_alloc buffers of k*L wire elements (w, and v for the BSP step
     // with momentum exchange), twice over (call parity) for the one-shot kernel;
     // then nvec_alloc averaged segments of L; then the flag pad.

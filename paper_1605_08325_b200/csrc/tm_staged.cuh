@@ -491,10 +491,37 @@ using FullGrp = Grp<kTmaThreads, 0, kInSlots, kOutSlots, kSlotBytes, kSlotBytes>
 // compute(i, in, out) [all group threads] transforms; store(i, out) [group
 // thread 0] issues the bulk stores.  `use` / `outn` continue across calls so
 // slot parities stay consistent.
+// Wait for a ring slot whose bulk copies may read PEER memory (NVLink): a copy
+// that never completes must not hang the box, so after the barrier timeout the
+// wait sets TM_BIT_TIMEOUT and traps (the launch fails with an error the host
+// sees, instead of spinning forever).
+__device__ __forceinline__ void mbar_wait_bounded(uint64_t* bar, uint32_t parity, uint64_t timeout_ns,
+                                                  uint32_t* status) {
+  const uint32_t a = smem_u32(bar);
+  uint32_t done = 0;
+  asm volatile(
+      "{\n.reg .pred p;\nmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\nselp.u32 %0, 1, 0, p;\n}\n"
+      : "=r"(done) : "r"(a), "r"(parity) : "memory");
+  if (done) return;
+  const uint64_t t0 = globaltimer();
+  for (;;) {
+    asm volatile(
+        "{\n.reg .pred p;\nmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\nselp.u32 %0, 1, 0, p;\n}\n"
+        : "=r"(done) : "r"(a), "r"(parity) : "memory");
+    if (done) return;
+    if (globaltimer() - t0 > timeout_ns) {
+      atomicOr(status, TM_BIT_TIMEOUT);
+      __threadfence_system();
+      __trap();
+    }
+  }
+}
+
 template <class G, class IssueF, class ComputeF, class StoreF>
 __device__ __forceinline__ void tile_pipeline(int gtid, int n_items, uint32_t& use, uint32_t& outn,
                                               char* in_ring, char* out_ring, uint64_t* full,
-                                              IssueF issue, ComputeF compute, StoreF store) {
+                                              IssueF issue, ComputeF compute, StoreF store,
+                                              uint64_t timeout_ns, uint32_t* status) {
   if (gtid == 0) {
     for (int i = 0; i < G::kNin && i < n_items; ++i) {
       const uint32_t slot = (use + i) % G::kNin;
@@ -504,7 +531,7 @@ __device__ __forceinline__ void tile_pipeline(int gtid, int n_items, uint32_t& u
   for (int i = 0; i < n_items; ++i) {
     const uint32_t u = use + i;
     const uint32_t slot = u % G::kNin;
-    mbar_wait(&full[slot], (u / G::kNin) & 1);
+    mbar_wait_bounded(&full[slot], (u / G::kNin) & 1, timeout_ns, status);
     char* out = out_ring + (outn % G::kNout) * G::kOutB;
     compute(i, in_ring + slot * G::kInB, out);
     fence_proxy_async_smem();                             // generic smem writes -> bulk store
@@ -647,7 +674,8 @@ __device__ __forceinline__ void precast_phase(const PhaseCtx& pc, int gtid, int6
         bulk_store(pc.stage_r + g0 * WB, out, (uint32_t)(n * WB));
         if (SGD && a.nvec == 2)
           bulk_store(pc.stage_r + a.stage_stride + g0 * WB, out + TPS * WB, (uint32_t)(n * WB));
-      });
+      },
+      a.timeout_ns, a.status);
 }
 
 // a4 on the TMA engine: pull [s0, s1) of the own segment from every rank's
@@ -711,7 +739,8 @@ __device__ __forceinline__ void reduce_phase(const PhaseCtx& pc, int gtid, int64
         const int64_t e = s0 + (int64_t)i * TR;
         const int64_t n = min((int64_t)TR, s1 - e);
         bulk_store(avg_r + e * WB, out, (uint32_t)(n * WB));
-      });
+      },
+      a.timeout_ns, a.status);
 }
 
 // a6 on the TMA engine: pull chunk [e0, e1) of every rank's avg, widen, store
@@ -776,7 +805,8 @@ __device__ __forceinline__ void gather_phase(const PhaseCtx& pc, int gtid, int64
         const int64_t g0 = (int64_t)j * L + e;
         const int64_t nb = max((int64_t)0, min(g0 + n, P4) - g0);
         if (nb > 0) bulk_store(x + g0, out, (uint32_t)(nb * 4));
-      });
+      },
+      a.timeout_ns, a.status);
 }
 
 template <int K, bool W16, bool SYS, bool SGD>
