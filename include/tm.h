@@ -65,7 +65,9 @@
  *   TM_NCCL_LIB=path                   libnccl.so.2 to dlopen (the binding sets
  *                      torch's); TM_DEBUG=1 prints CUDA errors to stderr.
  *   Diagnostics (read at first use): TM_DIRECT_LDG=1 register kernels instead of
- *   the TMA ones on the direct / BSP / EASGD-round paths; TM_DIRECT_STATIC=1
+ *   the TMA ones on the direct / BSP / EASGD-round paths; TM_DIRECT_TMA=1 the
+ *   TMA direct kernel also for small exchanges (k * P <= 8 Mi elements, which
+ *   use the register kernel by default: latency-bound); TM_DIRECT_STATIC=1
  *   static tile assignment; TM_TMA_CFG=n direct-kernel tile/ring variant;
  *   TM_BSP_UNFUSED=1 SGD pass + exchange instead of the fused kernels.
  *

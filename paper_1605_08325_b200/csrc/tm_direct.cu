@@ -285,11 +285,21 @@ cudaError_t direct_tma(const LocalBufs& lb, int64_t P, uint32_t* status, unsigne
   return launch_tma<K, Q16, 2048, 96, 1>(lb, P, status, ctr, dev, s);
 }
 
+// Small exchanges are latency-bound: the register kernel spreads one float4 of
+// every buffer per thread over many CTAs, while the TMA kernel walks 2048-element
+// tiles one per CTA through a load -> compute -> store chain.  Measured with 64
+// exchanges per CUDA graph (profiles/r02/latency/direct_{tma,ldg}.jsonl): k = 8
+// 2.2 vs 4.7 us at P = 128 Ki, 4.3 vs 6.3 us at 512 Ki, 15.4 vs 14.4 us at 2 Mi;
+// k = 4 at 2 Mi 7.2 vs 10.4 us.  So the register kernel up to k * P = 8 Mi
+// elements (32 MB of fp32 inputs), the TMA kernel above.
+constexpr int64_t kDirectLdgMaxElems = (int64_t)8 << 20;
+
 template <int K>
 cudaError_t direct_k(const LocalBufs& lb, int64_t P, uint32_t* status, unsigned long long* ctr,
                      bool q16, int dev, cudaStream_t s, int max_ctas) {
   static const bool force_ldg = env_int("TM_DIRECT_LDG", 0) == 1;
-  if (P >= 2048 && !force_ldg && max_ctas <= 0)
+  static const bool force_tma = env_int("TM_DIRECT_TMA", 0) == 1;  // diagnostics: TMA at every size
+  if (P >= 2048 && !force_ldg && max_ctas <= 0 && (force_tma || (int64_t)K * P > kDirectLdgMaxElems))
     return q16 ? direct_tma<K, true>(lb, P, status, ctr, dev, s)
                : direct_tma<K, false>(lb, P, status, ctr, dev, s);
   const int64_t want = (P / 4 + kThreads - 1) / kThreads;

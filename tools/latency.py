@@ -35,7 +35,7 @@ def main():
     for P in [int(v) for v in a.P.split(",")]:
         for k in [int(v) for v in a.k.split(",")]:
             bufs = [torch.randn(P, device="cuda") for _ in range(k)]
-            variants = [("direct", None)] + [("staged", f) for f in a.flavours.split(",")]
+            variants = [("direct", None)] + [("staged", f) for f in a.flavours.split(",") if f]
             for path, fl in variants:
                 os.environ.pop("TM_STAGED_KERNEL", None)
                 if fl and fl != "default":
