@@ -149,6 +149,13 @@ int64_t env_i64(const char* name, int64_t dflt) {
   return (v && *v) ? atoll(v) : dflt;
 }
 
+// Per-CTA chunk of the one-shot kernel (TM_ONESHOT_CHUNK, a multiple of 256,
+// overrides for A/B runs; every rank must use the same value).
+int64_t oneshot_chunk() {
+  const int64_t c = env_i64("TM_ONESHOT_CHUNK", tmx::kOneShotChunk);
+  return c >= 256 ? c / 256 * 256 : tmx::kOneShotChunk;
+}
+
 // The allgather decision step (north star: "falling back to NCCL allgather ...
 // only where it measures faster"): TM_AG_TABLE names a table measured on the
 // multi-GPU box (tools/ag_decide.py writes it from tools/multigpu_eval.sh's
@@ -229,7 +236,7 @@ ExchangeArgs make_args(float* const* bufs, int64_t off, int64_t n) {
     a.C = g.C;
   } else {
     a.L = round_up((n + g.k - 1) / g.k, tmx::kAlign);
-    const int64_t chunk = g.staged_kernel == tmx::kStagedOneShot ? tmx::kOneShotChunk : tmx::kMinChunk;
+    const int64_t chunk = g.staged_kernel == tmx::kStagedOneShot ? oneshot_chunk() : tmx::kMinChunk;
     const int64_t want = std::max<int64_t>(1, (a.L + chunk - 1) / chunk);
     a.C = (int)std::min<int64_t>(g.C, want);
     if (g.range_ctas > 0) a.C = std::min(a.C, g.range_ctas);  // bucket beside compute kernels
@@ -627,7 +634,7 @@ int tm_exchange_init(int64_t nparams, const tm_world* world, int strategy) {
     int cmax = k >= 2 ? tmx::exchange_max_ctas(c.device, wire16(strategy), k, c.staged_kernel) / c.nlocal / share
                       : 1;
     if (k >= 2 && cmax < 1) return TM_E_CUDA;
-    const int64_t chunk = c.staged_kernel == tmx::kStagedOneShot ? tmx::kOneShotChunk : tmx::kMinChunk;
+    const int64_t chunk = c.staged_kernel == tmx::kStagedOneShot ? oneshot_chunk() : tmx::kMinChunk;
     const int64_t want = std::max<int64_t>(1, (c.L + chunk - 1) / chunk);
     c.C = (int)std::min<int64_t>(std::max(cmax, 1), want);
     c.Lc = round_up((c.L + c.C - 1) / c.C, tmx::kAlign);

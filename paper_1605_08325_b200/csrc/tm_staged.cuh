@@ -180,6 +180,63 @@ __device__ __forceinline__ void precast_unit(const ExchangeArgs& a, int lr, int6
   }
 }
 
+// a2 for one wire unit of ONE segment: E elements at global offset g (a unit
+// never straddles two segments: L is a multiple of 256).  Same arithmetic as
+// precast_unit; the one-shot kernel spreads (segment, unit) pairs over its
+// threads, so a small chunk keeps every thread busy with independent loads.
+template <bool W16, bool SGD>
+__device__ __forceinline__ void precast_seg_unit(const ExchangeArgs& a, int lr, int64_t g, char* stage_r,
+                                                 uint32_t& st) {
+  using U = Unit<W16>;
+  constexpr int E = U::kElems;
+  constexpr int WB = W16 ? 2 : 4;
+  const float* __restrict__ x = a.x[lr];
+  const int64_t P = a.P;
+  float f[E], fv[SGD ? E : 1], fg[SGD ? E : 1];
+  if (g + E <= P) {
+#pragma unroll
+    for (int q = 0; q < E; q += 4) {
+      const float4 t = ld16_f(x + g + q);
+      f[q] = t.x; f[q + 1] = t.y; f[q + 2] = t.z; f[q + 3] = t.w;
+      if constexpr (SGD) {
+        const float4 tv = ld16_f(a.v[lr] + g + q), tg = ld16_f(a.g[lr] + g + q);
+        fv[q] = tv.x; fv[q + 1] = tv.y; fv[q + 2] = tv.z; fv[q + 3] = tv.w;
+        fg[q] = tg.x; fg[q + 1] = tg.y; fg[q + 2] = tg.z; fg[q + 3] = tg.w;
+      }
+    }
+  } else {
+#pragma unroll
+    for (int q = 0; q < E; ++q) {
+      const bool in = g + q < P;
+      f[q] = in ? x[g + q] : 0.0f;
+      if constexpr (SGD) {
+        fv[q] = in ? a.v[lr][g + q] : 0.0f;
+        fg[q] = in ? a.g[lr][g + q] : 0.0f;
+      }
+    }
+  }
+  if constexpr (SGD) {
+#pragma unroll
+    for (int q = 0; q < E; ++q) {
+      fv[q] = g + q < P ? sgd_v1(fv[q], fg[q], a.lr, a.mu) : 0.0f;
+      f[q] = g + q < P ? __fadd_rn(f[q], fv[q]) : 0.0f;
+    }
+    if (a.nvec == 2) {  // momentum exchanged: v' goes to the wire (vector 1)
+      st |= unit_status<W16, E>(fv);
+      st16_cg(stage_r + a.stage_stride + g * WB, U::encode(fv));
+    } else if (g + E <= P) {
+#pragma unroll
+      for (int q = 0; q < E; q += 4) st16_f(a.v[lr] + g + q, make_float4(fv[q], fv[q + 1], fv[q + 2], fv[q + 3]));
+    } else {
+#pragma unroll
+      for (int q = 0; q < E; ++q)
+        if (g + q < P) a.v[lr][g + q] = fv[q];
+    }
+  }
+  st |= unit_status<W16, E>(f);
+  st16_cg(stage_r + g * WB, U::encode(f));
+}
+
 template <int K, bool W16, bool SYS, bool SGD>
 __global__ void __launch_bounds__(kThreads, K == 6 ? 3 : 4)
 tm_exchange_kernel(const __grid_constant__ ExchangeArgs a) {
@@ -1036,9 +1093,12 @@ tm_exchange_oneshot_kernel(const __grid_constant__ ExchangeArgs a) {
   char* const stage_r = reinterpret_cast<char*>(a.stage[r]) + boff;
 
   // ---------------- a2: pre-cast chunk c of all k segments (this parity) -------
+  // (segment, unit) pairs spread over the threads, unit fastest (coalesced)
   uint32_t st = 0;
-  for (int v = threadIdx.x; v < nu; v += kThreads)
-    precast_unit<W16, K, SGD>(a, lr, e0 + (int64_t)v * E, stage_r, st);
+  for (int vw = threadIdx.x; vw < nu * K; vw += kThreads) {
+    const int sg = vw / nu;
+    precast_seg_unit<W16, SGD>(a, lr, (int64_t)sg * L + e0 + (int64_t)(vw - sg * nu) * E, stage_r, st);
+  }
   if (st) atomicOr(a.status, st);
   st = 0;
   stamp(a, kStampCast);
