@@ -271,10 +271,17 @@ cudaError_t bsp_tma_launch(const BspBufs& bb, int64_t P, uint32_t* status, unsig
   return cudaGetLastError();
 }
 
+// Small steps are latency-bound: the register kernel (one float4 of every
+// buffer per thread, many CTAs) beats the tile pipeline up to k * P = 4 Mi
+// elements (k = 8, momentum exchanged: 3.5 vs 5.6 us at P = 4 Ki, 9.5 vs 11.9 us
+// at 512 Ki, 21.9 vs 21.0 us at 1 Mi; profiles/r02/latency/small_bsp_easgd_*.jsonl).
+constexpr int64_t kBspLdgMaxElems = (int64_t)4 << 20;
+
 template <int K, bool Q16, bool MOM>
 cudaError_t bsp_launch(const BspBufs& bb, int64_t P, uint32_t* status, unsigned long long* ctr,
                        int dev, cudaStream_t s) {
-  if (ctr) {
+  static const bool force_tma = env_int("TM_DIRECT_TMA", 0) == 1;  // diagnostics: TMA at every size
+  if (ctr && (force_tma || (int64_t)K * P > kBspLdgMaxElems)) {
     // Tile per buffer: 2048 elements for k <= 4, 1024 above (AlexNet size: k = 2 / 4 /
     // 8 at 355 / 707 / 1421 us = 1.05 of the copy peak, vs 578 / 876 / 1478 us with
     // 512-element tiles, whose per-tile overhead dominated at small k;

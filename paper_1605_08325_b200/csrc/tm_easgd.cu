@@ -498,12 +498,18 @@ cudaError_t launch_round_tma(const OrderedWorkers& ow, float* c, int64_t n, int6
   return cudaGetLastError();
 }
 
+// Small rounds are latency-bound: the register kernel beats the tile pipeline
+// up to n (N + 1) = 18 Mi elements (N = 8: 1.8 vs 4.9 us at n = 4 Ki, 15.0 vs
+// 19.3 us at 2 Mi, 51.3 vs 47.7 us at 4 Mi; profiles/r02/latency/small_bsp_easgd_*.jsonl).
+constexpr int64_t kRoundLdgMaxElems = (int64_t)18 << 20;
+
 template <int N>
 cudaError_t launch_round_distinct(const OrderedWorkers& ow, float* c, int64_t n, float alpha,
                                   cudaStream_t s) {
   static const bool force_ldg = env_int("TM_DIRECT_LDG", 0) == 1;  // diagnostics: register kernel
+  static const bool force_tma = env_int("TM_DIRECT_TMA", 0) == 1;  // diagnostics: TMA at every size
   const int64_t ntiles = n / kRoundTile;
-  if (ntiles > 0 && !force_ldg) {
+  if (ntiles > 0 && !force_ldg && (force_tma || n * (N + 1) > kRoundLdgMaxElems)) {
     return launch_round_tma<N>(ow, c, n, ntiles, alpha, s);
   }
   easgd_round_distinct_kernel<N><<<streaming_grid(n / 4 + 4), kThreads, 0, s>>>(ow, c, n, alpha);
