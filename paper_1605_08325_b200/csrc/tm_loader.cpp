@@ -313,13 +313,15 @@ int tm_loader_send_after(tm_loader* L, int kind, const char* filename, void* str
   if (kind == TM_LOADER_FILE && !filename) return TM_E_ARG;
   cudaEvent_t ev = nullptr;
   if (kind == TM_LOADER_FILE) {  // the trainer's work enqueued so far on `stream`
-    if (cudaSetDevice(L->cfg.device) != cudaSuccess ||
-        cudaEventCreateWithFlags(&ev, cudaEventDisableTiming) != cudaSuccess)
-      return TM_E_CUDA;
-    if (cudaEventRecord(ev, static_cast<cudaStream_t>(stream)) != cudaSuccess) {
+    int prev = 0;  // the caller's current device is restored below
+    if (cudaGetDevice(&prev) != cudaSuccess || cudaSetDevice(L->cfg.device) != cudaSuccess) return TM_E_CUDA;
+    bool ok = cudaEventCreateWithFlags(&ev, cudaEventDisableTiming) == cudaSuccess;
+    if (ok && cudaEventRecord(ev, static_cast<cudaStream_t>(stream)) != cudaSuccess) {
       cudaEventDestroy(ev);
-      return TM_E_CUDA;
+      ok = false;
     }
+    cudaSetDevice(prev);
+    if (!ok) return TM_E_CUDA;
   }
   {
     std::lock_guard<std::mutex> lk(L->mu);
