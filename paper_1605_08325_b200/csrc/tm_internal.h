@@ -1,5 +1,6 @@
 // Internal interface between the C++ runtime (tm_runtime.cpp) and the sm_100a
-// kernels (tm_kernels.cu).  Not part of the public ABI.
+// kernels (tm_staged*.cu, tm_direct.cu, tm_bsp.cu, tm_easgd.cu,
+// tm_loader_kernels.cu).  Not part of the public ABI.
 #pragma once
 
 #include <cuda_runtime.h>

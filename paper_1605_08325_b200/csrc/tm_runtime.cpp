@@ -600,13 +600,12 @@ int tm_exchange_init(int64_t nparams, const tm_world* world, int strategy) {
     // (NVLink) sub-chunk by sub-chunk, both fed by bulk copies; on one GPU it
     // measures as the TMA kernel (0.982 vs 0.984 ms at AlexNet k = 8) and ahead
     // of the register warp-specialised kernel (1.248 ms).
-    // TM_STAGED_KERNEL=reg|tma|ws|tmaws overrides (TM_STAGED_LDG=1 /
+    // TM_STAGED_KERNEL=reg|tma|ws|tmaws|oneshot overrides (TM_STAGED_LDG=1 /
     // TM_STAGED_TMA=1 are accepted too).
-    // Small segments (L <= 64 Ki elements): the register kernel, whose phases
-    // have no bulk-copy round trips to drain (measured 6-16 us vs 15-22 us for the
-    // TMA / warp-specialised kernels at k = 8, P <= 256 Ki; profiles/r01/latency_flavours.txt).
     // Segments of at most TM_ONESHOT_MAX_L elements (default oneshot_max_l(k),
-    // profiles/r02/latency/): the one-shot kernel (one barrier).
+    // profiles/r02/latency/): the one-shot kernel (one barrier).  Up to
+    // kRegMaxL: the register two-phase kernel, whose phases have no bulk-copy
+    // round trips to drain (profiles/r01/latency_flavours.txt, r02/latency/).
     const int64_t oneshot_max = env_i64("TM_ONESHOT_MAX_L", oneshot_max_l(k));
     c.staged_kernel = c.L <= oneshot_max     ? tmx::kStagedOneShot
                       : c.L <= kRegMaxL      ? tmx::kStagedReg

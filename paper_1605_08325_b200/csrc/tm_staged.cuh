@@ -6,15 +6,19 @@
 // sets compile in parallel.  Every definition is internal to the including
 // translation unit.
 //
-// Four flavours of the same protocol (results bitwise identical):
-//   tm_exchange_kernel        phases in sequence, 16-byte register loads/stores
-//                             (default for segments <= 64 Ki elements);
+// Five flavours (results bitwise identical; the runtime picks one at init by
+// segment length and k):
+//   tm_exchange_oneshot_kernel one barrier per call: every rank reduces every
+//                             segment from every rank's staging (small segments);
+//   tm_exchange_kernel        phases in sequence, 16-byte register loads/stores;
 //   tm_exchange_ws_kernel     caster warps / reducer warps overlap a2 and a4 per
 //                             sub-chunk, register loads;
 //   tm_exchange_tma_kernel    phases in sequence as bulk-copy (TMA engine) tile
-//                             pipelines (single-process default);
+//                             pipelines (single-process default above the small sizes);
 //   tm_exchange_tmaws_kernel  the ws overlap with TMA pipelines in both warp
-//                             groups (multi-process default).
+//                             groups (multi-process default above the small sizes).
+// Every flavour also exchanges a second vector between the same barriers
+// (ExchangeArgs::nvec = 2: the BSP step with momentum exchange).
 // The TMA phases (precast_phase / reduce_phase / gather_phase) are written once
 // and parameterised by the thread group that runs them (Grp: whole CTA or half).
 //
