@@ -287,33 +287,47 @@ def run_reference(args):
     print(json.dumps(line), flush=True)
 
 
-def cpu_baseline(args, k, P, host, sample_idx, sample_got):
-    """The cpu_baseline leg: the oracle timed on a bounded sample (~10 s of CPU,
-    one core), and the oracle's per-element definition checked against the GPU's
-    sampled outputs of the first exchange (bitwise; AR within Q11)."""
+def cpu_baseline(args, k, P, host, sample_idx, sample_got, rank_samples=None, ar_samples=None,
+                 time_oracle=True):
+    """The cpu_baseline leg -- the only place our arm runs oracle/ code: (i)
+    the oracle timed on a bounded sample (~10 s of CPU, one core; skipped with
+    --no-cpu-baseline), and (ii) the GPU's sampled outputs of the first exchange
+    checked against the oracle's per-element definition: rank k-1's on one GPU
+    (bitwise; AR within Q11), every rank's on a multi-GPU run (`rank_samples`,
+    check_sample), and the samples of the AR run through the library
+    (`ar_samples`, within Q11).  Returns (cpu_baseline or None, parity, ar_parity)."""
     from oracle import exchange as ox
     from paper_1605_08325_b200.inputs import worker_buffers
-    sample = min(P, (1 << 22) if args.strategy == "asa16" else (1 << 24))
-    X = worker_buffers(sample, k, args.dist, config=3)
-    t = time.perf_counter()
-    ox.exchange(X, args.strategy)
-    dt = time.perf_counter() - t
+    base = None
+    if time_oracle:
+        sample = min(P, (1 << 22) if args.strategy == "asa16" else (1 << 24))
+        X = worker_buffers(sample, k, args.dist, config=3)
+        t = time.perf_counter()
+        ox.exchange(X, args.strategy)
+        dt = time.perf_counter() - t
+        base = {"value": k * 4 * sample / dt / 1e9, "unit": "GB/s", "cores": 1, "kind": "oracle",
+                "sample": f"one {args.strategy} exchange of {sample} of {P} elements x {k} ranks "
+                          f"({dt:.1f} s, numpy single-threaded)",
+                "cpu": _cpu_model(), "host_cpus": os.cpu_count()}
     parity = None
-    if sample_idx is not None:
+    if rank_samples is not None:
+        parity = check_sample(args.strategy, args.dist, P, k, sample_idx, rank_samples)
+    elif sample_idx is not None and host is not None:
         vals = np.stack([h[sample_idx] for h in host])
         want = ox.element_average(vals, args.strategy)
         if args.strategy == "ar":
-            parity = bool(np.all(np.abs(sample_got.astype(np.float64) - want) <=
-                                 1e-6 * np.mean(np.abs(vals.astype(np.float64)), axis=0)))
+            ok = bool(np.all(np.abs(sample_got.astype(np.float64) - want) <=
+                             1e-6 * np.mean(np.abs(vals.astype(np.float64)), axis=0)))
         else:
-            parity = bool(np.array_equal(sample_got.view(np.uint32), want.view(np.uint32)))
-    return {"value": k * 4 * sample / dt / 1e9, "unit": "GB/s", "cores": 1, "kind": "oracle",
-            "sample": f"one {args.strategy} exchange of {sample} of {P} elements x {k} ranks "
-                      f"({dt:.1f} s, numpy single-threaded)",
-            "cpu": _cpu_model(), "host_cpus": os.cpu_count(),
-            "gpu_sample_parity": parity,
-            "gpu_sample": f"{0 if sample_idx is None else len(sample_idx)} sampled outputs of rank k-1 "
-                          "after the first exchange vs the oracle's per-element definition"}
+            ok = bool(np.array_equal(sample_got.view(np.uint32), want.view(np.uint32)))
+        parity = {"parity": ok, "samples": int(len(sample_idx)),
+                  "what": f"{len(sample_idx)} sampled outputs of rank k-1 after the first exchange vs the "
+                          f"oracle's per-element definition"}
+    ar_parity = None if ar_samples is None else check_sample("ar", args.dist, P, k, sample_idx, ar_samples)
+    if base is not None and parity is not None:
+        base["gpu_sample_parity"] = parity["parity"]
+        base["gpu_sample"] = parity["what"]
+    return base, parity, ar_parity
 
 
 def _cpu_model():
@@ -417,7 +431,8 @@ def sample_indices(P):
 
 
 def check_sample(strategy, dist_name, P, k, idx, got_per_rank):
-    """Rank 0's parity check of a multi-GPU run: regenerate every rank's seeded
+    """(Called from the cpu_baseline leg only.)  Rank 0's parity check of a
+    multi-GPU run: regenerate every rank's seeded
     input, evaluate the oracle's per-element definition at the sampled indices
     (and the tail), compare with every rank's sampled output of the first
     exchange -- bitwise for ASA / ASA16, within reading Q11 for AR (NCCL's
@@ -505,12 +520,10 @@ def main():
     sample_idx = sample_indices(P)
     ti = torch.from_numpy(sample_idx).to(dev)
     sample_got = bufs[0 if multi else k - 1][ti].cpu().numpy()
-    multi_parity = None
+    rank_samples = None  # every rank's sampled outputs (multi-GPU), checked in the cpu_baseline leg
     if multi:
-        got_all = [None] * N
-        dist.all_gather_object(got_all, sample_got)
-        if rank == 0:
-            multi_parity = check_sample(args.strategy, args.dist, P, k, sample_idx, got_all)
+        rank_samples = [None] * N
+        dist.all_gather_object(rank_samples, sample_got)
         dist.barrier()
 
     for _ in range(args.warmup):
@@ -728,13 +741,16 @@ def main():
                                   coll_dev, stream)
         ex = None
 
-    cpu_base = None
-    if rank == 0 and not args.no_cpu_baseline:
-        cpu_base = cpu_baseline(args, k, P, host if not multi else None,
-                                None if multi else sample_idx, None if multi else sample_got)
-        if multi:
-            cpu_base["gpu_sample_parity"] = multi_parity["parity"] if multi_parity else None
-            cpu_base["gpu_sample"] = multi_parity["what"] if multi_parity else None
+    cpu_base = multi_parity = None
+    if rank == 0:
+        ar_samples = ar_tm.pop("samples", None) if isinstance(ar_tm, dict) else None
+        cpu_base, parity, ar_parity = cpu_baseline(
+            args, k, P, host if not multi else None, sample_idx, sample_got,
+            rank_samples=rank_samples, ar_samples=ar_samples, time_oracle=not args.no_cpu_baseline)
+        multi_parity = parity  # every rank's samples (N > 1) / rank k-1's (N = 1)
+        if ar_parity is not None:
+            ar_tm["parity_q11"] = ar_parity["parity"]
+            ar_tm["parity"] = ar_parity["what"]
     if rank == 0:
         ag_external = lay["allgather"] != 0 and lay["staged_kernel"] != 4
         launches = 0 if (multi and args.strategy == "ar") else args.steps * (2 if (multi and ag_external) else 1)
@@ -791,8 +807,8 @@ def main():
 def run_ar_through_tm(args, tm, dist, torch, P, k, rank, local, dev, host, sample_idx, coll_dev, stream):
     """a8 on the multi-GPU run: tm_exchange with strategy AR (ncclAllReduce,
     ncclAvg, in place) on every rank's own input, W warm-up + K timed calls, max
-    over ranks; every rank's sampled outputs of its first call checked within
-    Q11 on rank 0."""
+    over ranks; every rank's sampled outputs of its first call are returned to
+    rank 0 for the cpu_baseline leg's check within Q11."""
     try:
         x = torch.from_numpy(host[0]).to(dev)
         ex = tm.Exchanger(P, "ar", rank=rank, size=k, device=local, nlocal=1)
@@ -817,9 +833,7 @@ def run_ar_through_tm(args, tm, dist, torch, P, k, rank, local, dev, host, sampl
         out = {"ms_per_step": ams, "algbw_GBps": 4.0 * P / (ams * 1e-3) / 1e9, "status": code,
                "what": "tm_exchange, strategy AR: ncclAllReduce(ncclAvg) through the library's C ABI"}
         if rank == 0:
-            par = check_sample("ar", args.dist, P, k, sample_idx, got_all)
-            out["parity_q11"] = par["parity"]
-            out["parity"] = par["what"]
+            out["samples"] = got_all  # checked within Q11 in the cpu_baseline leg
         return out
     except Exception as e:  # context only: never fail the bench line
         return {"error": str(e)[:300]}
