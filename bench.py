@@ -248,10 +248,14 @@ def run_reference(args):
     multi = args.gpus > 1
     k = args.gpus if multi else args.k
     budget = float(os.environ.get("REF_BUDGET_S", "120"))
-    cal = worker_buffers(1 << 16, k, args.dist, config=3)
+    # calibrate on 1 Mi elements: a cache-resident calibration overstates the
+    # rate at the sample sizes the steps use (round 1 used 64 Ki and overshot
+    # the time budget ~1.8x)
+    ncal = min(P, 1 << 20)
+    cal = worker_buffers(ncal, k, args.dist, config=3)
     t = time.perf_counter()
     ox.exchange(cal, args.strategy)
-    rate = (1 << 16) / max(time.perf_counter() - t, 1e-6)  # elements (x k ranks) per second
+    rate = ncal / max(time.perf_counter() - t, 1e-6)  # elements (x k ranks) per second
     per_step = budget / max(1, args.steps + args.warmup)
     sample = int(min(P, max(4096, rate * per_step)) // 4096 * 4096) or min(P, 4096)
     X = worker_buffers(sample, k, args.dist, config=3)
