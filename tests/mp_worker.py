@@ -4,7 +4,7 @@ all_gather_object.  Used by tests/test_gpu_multiprocess.py; on a one-GPU box
 every rank uses cuda:0 (IPC between processes on one device), on a multi-GPU
 box rank r uses cuda:r.
 
-argv: outdir strategy P dist mode      (mode: normal | sum | range | locked | async | skip1 | mismatch | stress | bsp | bspmom)
+argv: outdir strategy P dist mode      (mode: normal | sum | range | locked | async | skip1 | mismatch | stress | bsp | bspmom | graph)
 """
 
 import json
@@ -24,6 +24,7 @@ from paper_1605_08325_b200.inputs import worker_buffer  # noqa: E402
 
 STRESS_ITERS = int(os.environ.get("TM_STRESS_ITERS", "60"))
 ASYNC_ROUNDS, ASYNC_TAU, ASYNC_ETA = 6, 2, 0.25
+GRAPH_PER, GRAPH_REPLAYS = 4, 3
 
 
 def main():
@@ -117,6 +118,35 @@ def main():
         np.save(os.path.join(outdir, f"vel{rank}.npy"), v.cpu().numpy())
         json.dump(result, open(os.path.join(outdir, f"rank{rank}.json"), "w"))
         dist.barrier()
+        ex.finalize()
+        dist.destroy_process_group()
+        return
+    if mode == "graph":
+        # GRAPH_PER x (per-rank delta of alternating sign; exchange) captured once in a
+        # CUDA graph and replayed GRAPH_REPLAYS times: the epochs and the one-shot
+        # kernel's call parity live on the device, so replays stay collective
+        d = torch.from_numpy(np.random.default_rng([1606, rank]).standard_normal(P).astype(np.float32)
+                             * np.float32(1e-3)).cuda()
+        s = torch.cuda.Stream()
+        s.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(s):
+            ex.exchange(x, s)  # one eager exchange first (warm-up, and bootstrapped state)
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g, stream=s):
+                for j in range(GRAPH_PER):
+                    x.sub_(d) if j % 2 else x.add_(d)
+                    ex.exchange(x, s)
+        torch.cuda.current_stream().wait_stream(s)
+        for _ in range(GRAPH_REPLAYS):
+            dist.barrier()
+            g.replay()
+        torch.cuda.synchronize()
+        code, bits = ex.status()
+        result.update({"code": code, "bits": bits, "layout": ex.layout()})
+        np.save(os.path.join(outdir, f"rank{rank}.npy"), x.cpu().numpy())
+        json.dump(result, open(os.path.join(outdir, f"rank{rank}.json"), "w"))
+        dist.barrier()
+        del g
         ex.finalize()
         dist.destroy_process_group()
         return

@@ -387,3 +387,27 @@ def test_multiprocess_allgather_decision_table(tmp_path):
     for r in range(k):
         assert res[r]["code"] == 0 and res[r]["layout"]["allgather"] == 1, res[r]
         assert_bitwise(np.load(os.path.join(tmp_path, f"rank{r}.npy")), want[r], f"rank {r}")
+
+
+@pytest.mark.parametrize("strategy,k,kernel", [("asa16", 2, "oneshot"), ("asa16", 3, "tmaws"), ("asa", 4, "oneshot"),
+                                               ("asa16", 2, "reg")])
+def test_multiprocess_cuda_graph_replays(tmp_path, strategy, k, kernel):
+    """Each process captures 4 x (its delta, exchange) in a CUDA graph and
+    replays it 3 times: device-side epochs (and the one-shot kernel's device call
+    parity) keep the replayed exchanges collective; every rank ends bitwise at
+    the oracle's sequence of 13 exchanges."""
+    import mp_worker as mw
+    P = 40_003
+    res = launch(tmp_path, k, strategy, P, "D2", mode="graph", extra_env={"TM_STAGED_KERNEL": kernel})
+    X = [worker_buffer(P, "D2", r, config=50) for r in range(k)]
+    D = [np.random.default_rng([1606, r]).standard_normal(P).astype(np.float32) * np.float32(1e-3)
+         for r in range(k)]
+    X = ox.exchange(X, strategy)
+    for _ in range(mw.GRAPH_REPLAYS):
+        for j in range(mw.GRAPH_PER):
+            X = [(np.subtract if j % 2 else np.add)(X[r], D[r], dtype=np.float32) for r in range(k)]
+            X = ox.exchange(X, strategy)
+    for r in range(k):
+        assert res[r]["code"] == 0, res[r]
+        assert res[r]["layout"]["staged_kernel"] == KERNEL_ID[kernel]
+        assert_bitwise(np.load(os.path.join(tmp_path, f"rank{r}.npy")), X[r], f"rank {r}")
