@@ -28,7 +28,8 @@ using namespace dev;
 // ---------------------------------------------------------------------------
 struct LocalBufs {
   float* b[TM_MAX_RANKS];
-  int sum;  // SUBGD sum mode: no 1/k
+  int sum;     // SUBGD sum mode: no 1/k
+  int l2hint;  // A/B knob TM_L2_HINT: bit 0 evict_first on the bulk loads, bit 1 on the bulk stores
 };
 
 // The method's arithmetic on 4 elements of k contributions (registers in, one
@@ -143,6 +144,7 @@ tm_direct_tma_kernel(const __grid_constant__ LocalBufs lb, int64_t ntiles, int64
   static_assert(S <= kMaxStages, "ring depth");
 
   const int tid = threadIdx.x;
+  const uint64_t pol = lb.l2hint ? l2_policy_evict_first() : 0;
   // Tiles are claimed dynamically from a per-launch counter (work stealing), so
   // a slow SM does not hold back the end of the kernel; without a counter the
   // static assignment blockIdx.x + i * gridDim.x is used.
@@ -166,9 +168,15 @@ tm_direct_tma_kernel(const __grid_constant__ LocalBufs lb, int64_t ntiles, int64
       return;
     }
     mbar_expect_tx(&full[s], K * TB);
+    if (lb.l2hint & 1) {
 #pragma unroll
-    for (int j = 0; j < K; ++j)
-      bulk_load(ring + ((size_t)s * K + j) * TILE, lb.b[j] + t * TILE, TB, &full[s]);
+      for (int j = 0; j < K; ++j)
+        bulk_load_hint(ring + ((size_t)s * K + j) * TILE, lb.b[j] + t * TILE, TB, &full[s], pol);
+    } else {
+#pragma unroll
+      for (int j = 0; j < K; ++j)
+        bulk_load(ring + ((size_t)s * K + j) * TILE, lb.b[j] + t * TILE, TB, &full[s]);
+    }
   };
 
   if (tid == 0) {
@@ -197,8 +205,13 @@ tm_direct_tma_kernel(const __grid_constant__ LocalBufs lb, int64_t ntiles, int64
     if (tid == 0) bulk_wait_read<kOutRing - 2>();  // out slot of tile i+1 is free
     __syncthreads();
     if (tid == 0) {
+      if (lb.l2hint & 2) {
 #pragma unroll
-      for (int j = 0; j < K; ++j) bulk_store(lb.b[j] + t * TILE, out, TB);
+        for (int j = 0; j < K; ++j) bulk_store_hint(lb.b[j] + t * TILE, out, TB, pol);
+      } else {
+#pragma unroll
+        for (int j = 0; j < K; ++j) bulk_store(lb.b[j] + t * TILE, out, TB);
+      }
       bulk_commit();
       issue(i + S);  // every thread has finished reading ring slot s
     }
@@ -315,6 +328,8 @@ cudaError_t launch_direct(float* const* bufs, int k, int64_t P, bool q16, bool s
                           uint32_t* status, unsigned long long* tile_ctr, cudaStream_t s, int max_ctas) {
   LocalBufs lb{};
   lb.sum = sum ? 1 : 0;
+  static const int l2hint = env_int("TM_L2_HINT", 0) & 3;
+  lb.l2hint = l2hint;
   for (int j = 0; j < k; ++j) lb.b[j] = bufs[j];
   int dev = 0;
   cudaGetDevice(&dev);
