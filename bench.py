@@ -57,7 +57,7 @@ def parse():
     ap.add_argument("--e2e-steps", type=int, default=5)
     ap.add_argument("--e2e-h2d-streams", type=int, default=2,
                     help="streams the e2e leg spreads the per-rank H2D copies over")
-    ap.add_argument("--e2e-chunks", type=int, default=16,
+    ap.add_argument("--e2e-chunks", type=int, default=8,
                     help="element ranges the e2e leg pipelines H2D / exchange / D2H over (1 = none)")
     ap.add_argument("--path", choices=["auto", "staged", "direct"], default="auto",
                     help="data path of the exchange (auto: direct for a one-GPU group)")
