@@ -1,4 +1,5 @@
 # A/B of the e2e leg: per-rank copies vs one 2-D copy per range, pipeline depth, H2D streams.
+# (The --e2e-copy 2d option was removed after this A/B: no gain; see profiles/r02/ab/README.md.)
 set -u
 mkdir -p gpurun_out/r02d/e2e2
 for cp in 2d per-rank; do
