@@ -247,6 +247,8 @@ def tm_easgd_update_ex(worker, center, alpha, concurrent=False, stream=None, n=N
 
 def tm_easgd_round(workers, order, center, alpha, stream=None):
     n = center.numel()
+    if any(w.device != center.device for w in workers):
+        raise ValueError("workers and centre must be on one device")
     arr = (ctypes.c_void_p * len(workers))(*[_fp32_cuda(w, n).value for w in workers])
     o = (ctypes.c_int32 * len(order))(*[int(i) for i in order])
     _check(lib().tm_easgd_round(arr, len(workers), o, len(order), _fp32_cuda(center), int(n),
@@ -265,9 +267,24 @@ def tm_easgd_update_locked(worker, worker_id, alpha, stream=None):
                                         _stream_handle(stream)), "tm_easgd_update_locked")
 
 
+TM_LOCK_CHUNK = 4096  # elements per lock of the locked EASGD mode (include/tm.h, tm_easgd_update_locked)
+
+
 def tm_easgd_set_order_log(log, max_updates_per_chunk):
-    """log: int32 CUDA tensor of >= k * nchunk * max entries, or None."""
-    ptr = None if log is None else ctypes.c_void_p(log.data_ptr())
+    """log: int32 CUDA tensor of >= k * nchunk * max entries (nchunk =
+    ceil(seg_len / 4096)) on the exchanger's device, or None."""
+    ptr = None
+    if log is not None:
+        lay = tm_layout()
+        need = lay["k"] * -(-lay["seg_len"] // TM_LOCK_CHUNK) * int(max_updates_per_chunk)
+        if not (isinstance(log, torch.Tensor) and log.is_cuda and log.dtype == torch.int32
+                and log.is_contiguous()):
+            raise TypeError("expected a contiguous int32 CUDA tensor")
+        if log.numel() < need:
+            raise ValueError(f"order log holds {log.numel()} entries, needs {need}")
+        if "device" in _ctx and log.device.index != _ctx["device"]:
+            raise ValueError(f"order log on cuda:{log.device.index}, exchanger on cuda:{_ctx['device']}")
+        ptr = ctypes.c_void_p(log.data_ptr())
     _check(lib().tm_easgd_set_order_log(ptr, int(max_updates_per_chunk)), "tm_easgd_set_order_log")
 
 
@@ -321,6 +338,9 @@ def tm_cast_rn16(x, out16=None, stream=None):
     """Device binary16 RNE rounding (the exchange's own); returns int16 bit patterns."""
     if out16 is None:
         out16 = torch.empty(x.numel(), dtype=torch.int16, device=x.device)
+    if not (out16.dtype in (torch.int16, torch.float16) and out16.device == x.device
+            and out16.is_contiguous() and out16.numel() >= x.numel()):
+        raise ValueError("out16: a contiguous 16-bit tensor of >= x.numel() elements on x's device")
     _check(lib().tm_cast_rn16(_fp32_cuda(x), _P(out16.data_ptr()), x.numel(), _stream_handle(stream)),
            "tm_cast_rn16")
     return out16
@@ -446,10 +466,14 @@ class Exchanger:
             tm_set_timeout_ns(int(timeout_s * 1e9))
         if path != "auto":
             tm_set_path(path)
-        if nlocal != size:
-            tm_bootstrap_import(gather_blobs(tm_bootstrap_export(), size // nlocal, group))
-        if allgather is not None:
-            tm_set_allgather(allgather)
+        try:
+            if nlocal != size:
+                tm_bootstrap_import(gather_blobs(tm_bootstrap_export(), size // nlocal, group))
+            if allgather is not None:
+                tm_set_allgather(allgather)
+        except Exception:
+            tm_exchange_finalize()  # no half-initialised process-global exchanger left behind
+            raise
 
     def exchange(self, bufs, stream=None):
         if isinstance(bufs, torch.Tensor):

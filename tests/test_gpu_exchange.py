@@ -472,6 +472,42 @@ def test_binding_rejects_short_buffers_and_bad_ranges():
         assert ex.status()[0] == tm.TM_OK
 
 
+def test_binding_rejects_short_order_log_and_rn16_output():
+    """The order log and the rn16 output are caller device buffers the kernels
+    write through bare pointers: the binding checks their size, type and device."""
+    import pytest as _pt
+    P, k = 3 * 4096 * 2 + 5, 2
+    with tm.Exchanger(P, "easgd", size=k, nlocal=k) as ex:
+        L = ex.layout()["seg_len"]
+        need = k * -(-L // 4096) * 3
+        with _pt.raises(ValueError):
+            tm.tm_easgd_set_order_log(torch.zeros(need - 1, dtype=torch.int32, device="cuda"), 3)
+        with _pt.raises(TypeError):
+            tm.tm_easgd_set_order_log(torch.zeros(need, dtype=torch.float32, device="cuda"), 3)
+        tm.tm_easgd_set_order_log(torch.zeros(need, dtype=torch.int32, device="cuda"), 3)
+        tm.tm_easgd_set_order_log(None, 0)
+    x = torch.zeros(1000, device="cuda")
+    with _pt.raises(ValueError):
+        tm.tm_cast_rn16(x, torch.zeros(999, dtype=torch.int16, device="cuda"))
+    with _pt.raises(ValueError):
+        tm.tm_cast_rn16(x, torch.zeros(1000, dtype=torch.int32, device="cuda"))
+
+
+def test_failed_bootstrap_leaves_no_exchanger(monkeypatch):
+    """An Exchanger whose bootstrap fails finalizes the process-global exchanger,
+    so the next init succeeds (no half-initialised state left behind)."""
+    import pytest as _pt
+
+    def boom(*a, **kw):
+        raise RuntimeError("bootstrap failed")
+    monkeypatch.setattr(tm, "gather_blobs", boom)
+    with _pt.raises(RuntimeError):
+        tm.Exchanger(4096, "asa16", rank=0, size=2, nlocal=1)
+    monkeypatch.undo()
+    with tm.Exchanger(4096, "asa16", size=2, nlocal=2) as ex:
+        assert ex.layout()["k"] == 2
+
+
 @pytest.mark.parametrize("strategy", ["asa16", "asa"])
 @pytest.mark.parametrize("k", [2, 3, 8])
 def test_oneshot_interleaved_ranges_bitwise(monkeypatch, strategy, k):
