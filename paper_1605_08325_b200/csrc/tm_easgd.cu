@@ -465,7 +465,8 @@ unsigned long long* round_tile_ctr(int dev, bool may_allocate) {
     void* p = nullptr;
     const size_t bytes = (size_t)kCtrSlots * 2 * sizeof(unsigned long long);
     if (cudaMalloc(&p, bytes) != cudaSuccess) return nullptr;
-    if (cudaMemset(p, 0, bytes) != cudaSuccess) {
+    // zeroed before any round on any (non-blocking) stream claims from it
+    if (cudaMemset(p, 0, bytes) != cudaSuccess || cudaDeviceSynchronize() != cudaSuccess) {
       cudaFree(p);
       return nullptr;
     }

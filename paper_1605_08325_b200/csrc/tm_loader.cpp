@@ -298,7 +298,10 @@ int tm_loader_create(const tm_loader_config* cfg, float* input_x, tm_loader** ou
       cudaMalloc(reinterpret_cast<void**>(&L->gpudata), outn * 4) != cudaSuccess ||
       cudaMalloc(reinterpret_cast<void**>(&L->dev_crop), (size_t)c.n * 3 * 4) != cudaSuccess ||
       cudaStreamCreateWithFlags(&L->stream, cudaStreamNonBlocking) != cudaSuccess ||
-      cudaMemcpy(L->dev_mean, cfg->mean, img * 4, cudaMemcpyHostToDevice) != cudaSuccess) {
+      cudaMemcpy(L->dev_mean, cfg->mean, img * 4, cudaMemcpyHostToDevice) != cudaSuccess ||
+      // a pageable-memory cudaMemcpy may return before its DMA lands; the loader's
+      // stream is non-blocking, so wait before its first preprocess kernel
+      cudaDeviceSynchronize() != cudaSuccess) {
     free_loader(L);
     return TM_E_CUDA;
   }

@@ -435,7 +435,10 @@ int probe_once(float* probe, int64_t n, cudaStream_t st, bool* ok) {
   const float s8 = 1.0f / 256.0f;
   std::vector<float> h((size_t)n), back((size_t)n);
   for (int64_t i = 0; i < n; ++i) h[(size_t)i] = (float)((i % 251) + g.rank0 + 1) * s8;
-  cudaError_t e = cudaMemcpy(probe, h.data(), (size_t)n * 4, cudaMemcpyHostToDevice);
+  // Stream-ordered upload: a cudaMemcpy from pageable memory may return before
+  // its DMA lands, and the probe runs on a non-blocking stream.
+  cudaError_t e = cudaMemcpyAsync(probe, h.data(), (size_t)n * 4, cudaMemcpyHostToDevice, st);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(st);
   if (e != cudaSuccess) return cuda_fail("probe upload", e);
   float* bufs[1] = {probe};
   ExchangeArgs a = make_args(bufs, 0, n);
@@ -453,20 +456,32 @@ int probe_once(float* probe, int64_t n, cudaStream_t st, bool* ok) {
   uint32_t bits = 0;
   e = cudaMemcpy(&bits, g.status, 4, cudaMemcpyDeviceToHost);
   if (e != cudaSuccess) return cuda_fail("probe status", e);
-  cudaMemset(g.status, 0, 4);
+  e = cudaMemsetAsync(g.status, 0, 4, st);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+  if (e != cudaSuccess) return cuda_fail("probe status clear", e);
   if (bits & TM_BIT_TIMEOUT) return TM_E_TIMEOUT;
   e = cudaMemcpy(back.data(), probe, (size_t)n * 4, cudaMemcpyDeviceToHost);
   if (e != cudaSuccess) return cuda_fail("probe download", e);
   const int k = g.k;
   bool good = bits == 0;
-  for (int64_t i = 0; good && i < n; ++i) {
+  int64_t nbad = 0, first_bad = -1;
+  for (int64_t i = 0; i < n; ++i) {
     const int64_t m = i % 251;
     const float want = g.sum ? (float)(k * m + k * (k + 1) / 2) * s8 : (float)(2 * m + k + 1) * (s8 * 0.5f);
     uint32_t wb, gb;
     memcpy(&wb, &want, 4);
     memcpy(&gb, &back[(size_t)i], 4);
-    good = wb == gb;
+    if (wb != gb) {
+      if (first_bad < 0) first_bad = i;
+      ++nbad;
+    }
   }
+  good = good && nbad == 0;
+  if (!good && getenv("TM_DEBUG"))
+    fprintf(stderr, "[tm] rank %d: self-check probe (flavour %d, n %lld, C %d): status bits %u, %lld of %lld "
+                    "elements wrong, first at %lld (got %a)\n",
+            g.rank0, g.staged_kernel, (long long)n, a.C, bits, (long long)nbad, (long long)n,
+            (long long)first_bad, first_bad >= 0 ? (double)back[(size_t)first_bad] : 0.0);
   *ok = good;
   return TM_OK;
 }
@@ -670,7 +685,11 @@ int tm_exchange_init(int64_t nparams, const tm_world* world, int strategy) {
   c.slab_bytes = c.rank_stride * c.nlocal + 256 + tmx::kCtrSlots * 16;
   e = cudaMalloc(reinterpret_cast<void**>(&c.slab), c.slab_bytes);
   if (e != cudaSuccess) return cuda_fail("cudaMalloc", e);
+  // cudaMemset is asynchronous to the host (legacy stream): wait for it, so the
+  // slab is zero before any kernel on a non-blocking stream, or any peer (after
+  // the bootstrap), touches it.
   e = cudaMemset(c.slab, 0, c.slab_bytes);
+  if (e == cudaSuccess) e = cudaDeviceSynchronize();
   if (e != cudaSuccess) {
     cudaFree(c.slab);
     return cuda_fail("cudaMemset", e);
@@ -917,7 +936,8 @@ int tm_easgd_set_order_log(int32_t* dev_log, int max_updates_per_chunk) {
     cudaError_t e = cudaMemset(g.rank_base[g.rank0 + i] + g.off_tickets, 0, nch * 4);
     if (e != cudaSuccess) return cuda_fail("ticket reset", e);
   }
-  return TM_OK;
+  const cudaError_t e = cudaDeviceSynchronize();  // the reset lands before any later launch
+  return e == cudaSuccess ? TM_OK : cuda_fail("ticket reset sync", e);
 }
 
 int tm_exchange_status(void* stream, uint32_t* bits) {
@@ -929,7 +949,10 @@ int tm_exchange_status(void* stream, uint32_t* bits) {
   uint32_t h = 0;
   e = cudaMemcpy(&h, g.status, 4, cudaMemcpyDeviceToHost);
   if (e != cudaSuccess) return cuda_fail("status copy", e);
-  e = cudaMemset(g.status, 0, 4);
+  // cleared on the caller's stream and waited for: a cudaMemset (legacy stream)
+  // could land after the next exchange on a non-blocking stream set a bit
+  e = cudaMemsetAsync(g.status, 0, 4, static_cast<cudaStream_t>(stream));
+  if (e == cudaSuccess) e = cudaStreamSynchronize(static_cast<cudaStream_t>(stream));
   if (e != cudaSuccess) return cuda_fail("status clear", e);
   if (bits) *bits = h;
   if (h & TM_BIT_TIMEOUT) return TM_E_TIMEOUT;

@@ -4,7 +4,7 @@ all_gather_object.  Used by tests/test_gpu_multiprocess.py; on a one-GPU box
 every rank uses cuda:0 (IPC between processes on one device), on a multi-GPU
 box rank r uses cuda:r.
 
-argv: outdir strategy P dist mode      (mode: normal | sum | range | locked | async | skip1 | mismatch | stress | bsp | bspmom | graph)
+argv: outdir strategy P dist mode      (mode: normal | sum | range | locked | async | skip1 | mismatch | stress | bsp | bspmom | graph | fuzz)
 """
 
 import json
@@ -105,6 +105,39 @@ def main():
         dist.destroy_process_group()
         return
     x = torch.from_numpy(worker_buffer(P, dist_name, rank, config=50)).cuda()
+    if mode == "fuzz":
+        # seeded random cases (tests/gpu_helpers.py::fuzz_cases), each on
+        # an exchanger of its own: init + bootstrap (with the self-check), 1-3
+        # calls (full or a bucket with a CTA budget) on fresh inputs, finalize
+        ex.finalize()
+        from gpu_helpers import fuzz_cases
+        for i, c in enumerate(fuzz_cases(size, P)):
+            if c["flavour"]:
+                os.environ["TM_STAGED_KERNEL"] = c["flavour"]
+            else:
+                os.environ.pop("TM_STAGED_KERNEL", None)
+            ex = tm.Exchanger(c["P"], c["strategy"], rank=rank, size=size, device=device, nlocal=1,
+                              timeout_s=20.0, op=c["op"])
+            for n, (off, cnt, budget) in enumerate(c["calls"]):
+                xi = torch.from_numpy(worker_buffer(c["P"], c["dist"], rank, config=800 + 4 * i + n)).cuda()
+                tm.tm_set_range_ctas(budget)
+                if off == 0 and cnt == c["P"]:
+                    ex.exchange(xi)
+                else:
+                    ex.exchange_range(xi, off, cnt)
+                code, bits = ex.status()
+                result[f"code{i}_{n}"] = code
+                np.save(os.path.join(outdir, f"fuzz{i}_{n}_rank{rank}.npy"), xi.cpu().numpy())
+            lay = ex.layout()
+            result[f"kernel{i}"] = lay["staged_kernel"]
+            result[f"selfcheck{i}"] = lay["selfcheck"]
+            dist.barrier()  # every rank done with the peers' slabs
+            ex.finalize()
+        result["code"] = 0
+        json.dump(result, open(os.path.join(outdir, f"rank{rank}.json"), "w"))
+        dist.barrier()
+        dist.destroy_process_group()
+        return
     if mode in ("bsp", "bspmom"):
         # two BSP iterations (momentum SGD fused into the staged pre-cast, then
         # the exchange of w, and of v for bspmom)

@@ -14,7 +14,7 @@ import sys
 import numpy as np
 import pytest
 
-from gpu_helpers import assert_bitwise
+from gpu_helpers import assert_bitwise, fuzz_cases
 from oracle import exchange as ox
 from paper_1605_08325_b200.inputs import worker_buffer
 
@@ -411,3 +411,28 @@ def test_multiprocess_cuda_graph_replays(tmp_path, strategy, k, kernel):
         assert res[r]["code"] == 0, res[r]
         assert res[r]["layout"]["staged_kernel"] == KERNEL_ID[kernel]
         assert_bitwise(np.load(os.path.join(tmp_path, f"rank{r}.npy")), X[r], f"rank {r}")
+
+
+@pytest.mark.parametrize("k", [2, 3, 5, 8])
+def test_multiprocess_fuzz_bitwise(tmp_path, k):
+    """k processes (one rank each), seeded random combinations of size, strategy,
+    op, flavour, distribution, buckets and CTA budgets, each case on a fresh
+    exchanger (bootstrap and self-check included), bitwise vs the oracle on every
+    rank."""
+    pmax = 1 << 18
+    res = launch(tmp_path, k, "asa16", pmax, "D1", mode="fuzz", timeout=600)
+    for i, c in enumerate(fuzz_cases(k, pmax)):
+        for n, (off, cnt, _) in enumerate(c["calls"]):
+            X = [worker_buffer(c["P"], c["dist"], r, config=800 + 4 * i + n) for r in range(k)]
+            want = [x.copy() for x in X]
+            if cnt:
+                seg = ox.exchange([x[off:off + cnt] for x in X], c["strategy"], op=c["op"])
+                for r in range(k):
+                    want[r][off:off + cnt] = seg[r]
+            for r in range(k):
+                assert res[r][f"code{i}_{n}"] == 0, (i, n, c, res[r])
+                assert res[r][f"selfcheck{i}"] == 1, (i, c, res[r])  # the flavour's probe passed
+                if c["flavour"]:
+                    assert res[r][f"kernel{i}"] == KERNEL_ID[c["flavour"]], (i, c, res[r])
+                got = np.load(os.path.join(tmp_path, f"fuzz{i}_{n}_rank{r}.npy"))
+                assert_bitwise(got, want[r], f"mp fuzz k={k} case {i} {c} call {n} rank {r}")
