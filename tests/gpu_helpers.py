@@ -40,8 +40,9 @@ def fuzz_cases(k, pmax, n=None):
     fuzz mode, checked by test_gpu_multiprocess.py::test_multiprocess_fuzz_bitwise):
     P log-uniform in [1, pmax] (ragged), ASA or ASA16, avg or sum, any staged
     flavour or the runtime's choice, D1-D5, 1-3 calls each a full exchange or a
-    bucket with a CTA budget."""
-    n = int(os.environ.get("TM_MP_FUZZ_CASES", "10")) if n is None else n
+    bucket with a CTA budget -- or (bsp) two BSP iterations, momentum-SGD step
+    fused into the exchange, with or without the momentum exchange."""
+    n = int(os.environ.get("TM_MP_FUZZ_CASES", "24")) if n is None else n
     flavours = [None, "reg", "tma", "ws", "tmaws", "oneshot"]
     out = []
     for i in range(n):
@@ -58,5 +59,9 @@ def fuzz_cases(k, pmax, n=None):
                 calls.append((off, int(g.integers(0, P - off + 1)), [0, 1, 3, 16][int(g.integers(0, 4))]))
             else:
                 calls.append((0, P, 0))
-        out.append(dict(P=P, strategy=strategy, op=op, flavour=flavour, dist=dist, calls=calls))
+        bsp = None
+        if op == "avg" and g.random() < 0.3:  # a BSP iteration pair instead of the calls
+            bsp = dict(mom=bool(g.random() < 0.5), lr=float(np.float32(g.choice([0.01, 0.3]))),
+                       mu=float(np.float32(g.choice([0.0, 0.9]))))
+        out.append(dict(P=P, strategy=strategy, op=op, flavour=flavour, dist=dist, calls=calls, bsp=bsp))
     return out

@@ -118,7 +118,18 @@ def main():
                 os.environ.pop("TM_STAGED_KERNEL", None)
             ex = tm.Exchanger(c["P"], c["strategy"], rank=rank, size=size, device=device, nlocal=1,
                               timeout_s=20.0, op=c["op"])
-            for n, (off, cnt, budget) in enumerate(c["calls"]):
+            if c["bsp"]:
+                b = c["bsp"]
+                w = torch.from_numpy(worker_buffer(c["P"], c["dist"], rank, config=800 + 4 * i)).cuda()
+                v = torch.from_numpy(worker_buffer(c["P"], "D4", rank, config=801 + 4 * i)).cuda()
+                gr = torch.from_numpy(worker_buffer(c["P"], "D2", rank, config=802 + 4 * i)).cuda()
+                for _ in range(2):
+                    ex.bsp_step(w, v, gr, b["lr"], b["mu"], exchange_momentum=b["mom"])
+                code, bits = ex.status()
+                result[f"code{i}_0"] = code
+                np.save(os.path.join(outdir, f"fuzz{i}_w_rank{rank}.npy"), w.cpu().numpy())
+                np.save(os.path.join(outdir, f"fuzz{i}_v_rank{rank}.npy"), v.cpu().numpy())
+            for n, (off, cnt, budget) in enumerate([] if c["bsp"] else c["calls"]):
                 xi = torch.from_numpy(worker_buffer(c["P"], c["dist"], rank, config=800 + 4 * i + n)).cuda()
                 tm.tm_set_range_ctas(budget)
                 if off == 0 and cnt == c["P"]:

@@ -413,15 +413,31 @@ def test_multiprocess_cuda_graph_replays(tmp_path, strategy, k, kernel):
         assert_bitwise(np.load(os.path.join(tmp_path, f"rank{r}.npy")), X[r], f"rank {r}")
 
 
-@pytest.mark.parametrize("k", [2, 3, 5, 8])
+@pytest.mark.parametrize("k", [2, 3, 4, 5, 8])
 def test_multiprocess_fuzz_bitwise(tmp_path, k):
     """k processes (one rank each), seeded random combinations of size, strategy,
-    op, flavour, distribution, buckets and CTA budgets, each case on a fresh
-    exchanger (bootstrap and self-check included), bitwise vs the oracle on every
-    rank."""
+    op, flavour, distribution, buckets and CTA budgets (or two BSP iterations),
+    each case on a fresh exchanger (bootstrap and self-check included), bitwise vs
+    the oracle on every rank."""
     pmax = 1 << 18
     res = launch(tmp_path, k, "asa16", pmax, "D1", mode="fuzz", timeout=600)
+    from oracle.bsp import bsp_iteration
     for i, c in enumerate(fuzz_cases(k, pmax)):
+        if c["bsp"]:
+            b = c["bsp"]
+            W = [worker_buffer(c["P"], c["dist"], r, config=800 + 4 * i) for r in range(k)]
+            V = [worker_buffer(c["P"], "D4", r, config=801 + 4 * i) for r in range(k)]
+            G = [worker_buffer(c["P"], "D2", r, config=802 + 4 * i) for r in range(k)]
+            for _ in range(2):
+                W, V = bsp_iteration(W, V, G, np.float32(b["lr"]), np.float32(b["mu"]), c["strategy"],
+                                     exchange_momentum=b["mom"])
+            for r in range(k):
+                assert res[r][f"code{i}_0"] == 0, (i, c, res[r])
+                assert res[r][f"selfcheck{i}"] == 1, (i, c, res[r])
+                for name, want in (("w", W[r]), ("v", V[r])):
+                    got = np.load(os.path.join(tmp_path, f"fuzz{i}_{name}_rank{r}.npy"))
+                    assert_bitwise(got, want, f"mp fuzz bsp k={k} case {i} {c} {name} rank {r}")
+            continue
         for n, (off, cnt, _) in enumerate(c["calls"]):
             X = [worker_buffer(c["P"], c["dist"], r, config=800 + 4 * i + n) for r in range(k)]
             want = [x.copy() for x in X]
