@@ -12,8 +12,9 @@ mod 256); strategy AR / ASA / ASA16; op avg (AWAGD) or sum (SUBGD, ASA and
 ASA16); path direct or staged with any of the five staged flavours (or the
 runtime's own choice); distribution D1-D6; then 1-3 calls, each a full
 exchange or a bucket [offset, offset + count) with an optional CTA budget,
-on fresh inputs, each compared bitwise with oracle/exchange.py on exactly the
-elements it covers (the rest must be untouched).  PAPER L237-269 (ASA,
+on fresh inputs, on the default stream or a fresh non-blocking one, each
+compared bitwise with oracle/exchange.py on exactly the elements it covers (the
+rest must be untouched).  PAPER L237-269 (ASA,
 ASA16), L233-237 (AR; a single-process group sums in ascending rank order, so
 bitwise too), L384-389 (SUBGD sum).
 """
@@ -56,7 +57,9 @@ def draw_case(i):
             calls.append((off, cnt, budget))
         else:
             calls.append((0, P, 0))
-    return dict(k=k, P=P, strategy=strategy, op=op, path=path, flavour=flavour, dist=dist, calls=calls)
+    side = bool(g.random() < 0.5)  # calls on a fresh non-blocking stream
+    return dict(k=k, P=P, strategy=strategy, op=op, path=path, flavour=flavour, dist=dist, calls=calls,
+                side=side)
 
 
 @pytest.mark.parametrize("i", range(NCASES))
@@ -77,11 +80,13 @@ def test_fuzz_case_bitwise(monkeypatch, i):
                 X = [np.clip(x, -60000.0 / k, 60000.0 / k).astype(np.float32) for x in X]
             bufs = to_dev(X)
             tm.tm_set_range_ctas(budget)
+            st = torch.cuda.Stream() if c["side"] else torch.cuda.current_stream()
+            st.wait_stream(torch.cuda.current_stream())
             if off == 0 and cnt == P:
-                ex.exchange(bufs)
+                ex.exchange(bufs, st)
             else:
-                ex.exchange_range(bufs, off, cnt)
-            code, bits = ex.status()
+                ex.exchange_range(bufs, off, cnt, st)
+            code, bits = ex.status(st)
             assert code in (tm.TM_OK, tm.TM_E_NONFINITE, tm.TM_E_OVERFLOW16), (what, code, bits)
             got = to_host(bufs)
             want = [x.copy() for x in X]
@@ -129,3 +134,44 @@ def test_fuzz_bsp_bitwise(monkeypatch, i):
     for r in range(k):
         assert_bitwise(gW[r], ww[r], f"{what} w rank {r}")
         assert_bitwise(gV[r], vv[r], f"{what} v rank {r}")
+
+
+NEASGD = int(os.environ.get("TM_FUZZ_EASGD_CASES", "64"))
+
+
+@pytest.mark.parametrize("i", range(NEASGD))
+def test_fuzz_easgd_bitwise(i):
+    """EASGD: random combinations of the centre size
+    n (ragged), the number of workers, an arrival order (distinct workers, or
+    with repeats), alpha (dyadic 0.5 / 0.5/k or not, 0.3) and the call -- the
+    fused round (tm_easgd_round) or one exclusive update per arrival
+    (tm_easgd_update_ex) -- on the default stream or a fresh non-blocking
+    stream, bitwise against oracle.easgd.easgd_sequence."""
+    from oracle.easgd import easgd_sequence
+    g = np.random.default_rng([1605, 8325, 781, i])
+    n = max(1, int(np.exp(g.uniform(0.0, np.log(1 << 20)))) + int(g.integers(0, 4)))
+    nw = int(g.integers(1, 17))
+    if g.random() < 0.5:
+        order = [int(w) for w in g.permutation(nw)[: int(g.integers(1, nw + 1))]]
+    else:
+        order = [int(w) for w in g.integers(0, nw, int(g.integers(1, 33)))]
+    alpha = float(np.float32(g.choice([0.5, 0.5 / nw, 0.3])))
+    call = "round" if g.random() < 0.7 else "updates"
+    side = g.random() < 0.5
+    what = f"easgd case {i}: n={n} nw={nw} order={order} alpha={alpha} {call} side_stream={side}"
+    W = worker_buffers(n, nw, str(g.choice(["D1", "D2", "D3"])), config=790)
+    c0 = worker_buffers(n, 1, "D1", config=791)[0]
+    Wd, cd = to_dev(W), to_dev([c0])[0]
+    st = torch.cuda.Stream() if side else torch.cuda.current_stream()
+    st.wait_stream(torch.cuda.current_stream())
+    if call == "round":
+        tm.tm_easgd_round(Wd, order, cd, alpha, stream=st)
+    else:
+        for w in order:
+            tm.tm_easgd_update_ex(Wd[w], cd, alpha, stream=st)
+    st.synchronize()
+    ww, cc = easgd_sequence(W, c0, np.float32(alpha), order)
+    gW, gc = to_host(Wd), to_host([cd])[0]
+    assert_bitwise(gc, cc, f"{what} centre")
+    for w in range(nw):
+        assert_bitwise(gW[w], ww[w], f"{what} worker {w}")
