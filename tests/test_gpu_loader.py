@@ -143,3 +143,42 @@ def test_file_message_waits_for_trainer_stream(tmp_path):
     assert_bitwise(snap.cpu().numpy(), want0.cpu().numpy(), "trainer's read of the previous batch")
     want1 = ol.preprocess(raws[f1], mean, CH, CW, "train", 5, 1)
     assert_bitwise(after.cpu().numpy(), want1.reshape(-1), "released batch")
+
+
+@pytest.mark.parametrize("i", range(16))
+def test_fuzz_loader_sequences_bitwise(tmp_path, i):
+    """Seeded random Alg. 1 sessions: random batch geometry (odd
+    sizes, crop up to the full image), 2-4 mode segments (train / val) of 1-4
+    files each, the trainer waiting for every delivery the state machine makes
+    (oracle deliveries()) and reading input_x after it; every delivered batch
+    bitwise equal to oracle.loader.preprocess with the loader's load index."""
+    g = np.random.default_rng([1605, 8325, 61, i])
+    n, c = int(g.integers(1, 6)), int(g.integers(1, 4))
+    h, w = int(g.integers(1, 40)), int(g.integers(1, 40))
+    ch, cw = int(g.integers(1, h + 1)), int(g.integers(1, w + 1))
+    seed = int(g.integers(0, 1 << 62))
+    mean = g.uniform(0, 255, (c, h, w)).astype(np.float32)
+    msgs, raws = [], {}
+    for s in range(int(g.integers(2, 5))):
+        msgs.append((str(g.choice(["train", "val"])), None))
+        for f in range(int(g.integers(1, 5))):
+            p = str(tmp_path / f"b{s}_{f}.pxb")
+            raws[p] = g.integers(0, 256, (n, c, h, w)).astype(np.uint8)
+            tm.write_batch_file(p, raws[p])
+            msgs.append(("file", p))
+    msgs.append(("stop", None))
+    expected = ol.deliveries(msgs)
+    x = torch.zeros(n * c * ch * cw, device="cuda")
+    got = []
+    with tm.Loader(n, c, h, w, ch, cw, mean, x, seed=seed) as L:
+        prev_file = False
+        for kind, name in msgs:
+            L.send(kind, name)
+            if kind == "file" and prev_file:  # a FILE after a loaded file delivers it
+                L.wait(10_000)
+                got.append(x.clone())
+            prev_file = kind == "file"
+    assert len(got) == len(expected), (len(got), expected)
+    for (name, mode, idx), t in zip(expected, got):
+        want = ol.preprocess(raws[name], mean, ch, cw, mode, seed, idx)
+        assert_bitwise(t.cpu().numpy(), want.reshape(-1), f"case {i} {name} {mode} load {idx}")
