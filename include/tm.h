@@ -194,8 +194,10 @@ typedef enum { TM_AG_SM = 0, TM_AG_CE = 1, TM_AG_NCCL = 2 } tm_allgather;
 /* Create the process-global exchanger.  nparams >= 1; world as above; strategy
  * a tm_strategy.  Allocates the library-owned buffers on world->device.  For
  * nlocal == size the exchanger is ready on return; otherwise the bootstrap
- * below must follow.  Returns TM_OK, TM_E_ARG, TM_E_STATE (already
- * initialised) or TM_E_CUDA. */
+ * below must follow.  The buffers are zeroed before the call returns (the
+ * first exchange may run on any stream, and peers write into them after the
+ * bootstrap).  Returns TM_OK, TM_E_ARG, TM_E_STATE (already initialised) or
+ * TM_E_CUDA. */
 int tm_exchange_init(int64_t nparams, const tm_world* world, int strategy);
 
 /* Write this process's bootstrap blob (CUDA IPC handle of its slab, layout, and
@@ -381,7 +383,9 @@ int tm_loader_destroy(tm_loader* loader);
 
 /* Synchronise `stream`, then return the most severe sticky status
  * (TM_E_TIMEOUT > TM_E_OVERFLOW16 > TM_E_NONFINITE > TM_OK) and clear it.
- * `bits` (optional) receives the TM_BIT_* mask. */
+ * `bits` (optional) receives the TM_BIT_* mask.  The clear is enqueued on
+ * `stream` and waited for before the call returns, so a bit set by any later
+ * launch (on any stream) survives it. */
 int tm_exchange_status(void* stream, uint32_t* bits);
 
 /* Layout of the current exchanger (for tests and the bench). */
