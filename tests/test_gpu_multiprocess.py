@@ -54,8 +54,13 @@ def launch(tmp_path, k, strategy, P, dist, mode="normal", timeout=240, extra_env
     for r in range(k):
         env = dict(os.environ, RANK=str(r), WORLD_SIZE=str(k), MASTER_ADDR="127.0.0.1",
                    MASTER_PORT=str(port), LOCAL_RANK=str(r), **nccl_shared_gpu_env(r, k), **extra)
-        procs.append(subprocess.Popen([sys.executable, os.path.join(HERE, "mp_worker.py"), str(tmp_path),
-                                       strategy, str(P), dist, mode], env=env))
+        # TM_TEST_SANITIZER=memcheck|synccheck|racecheck: every worker under
+        # compute-sanitizer (its log next to the rank's results)
+        san = os.environ.get("TM_TEST_SANITIZER")
+        pre = (["compute-sanitizer", "--tool", san, "--error-exitcode", "9",
+                "--log-file", os.path.join(str(tmp_path), f"san_{san}_rank{r}.txt")] if san else [])
+        procs.append(subprocess.Popen(pre + [sys.executable, os.path.join(HERE, "mp_worker.py"), str(tmp_path),
+                                             strategy, str(P), dist, mode], env=env))
     try:
         for p in procs:
             p.wait(timeout=timeout)
