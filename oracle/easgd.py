@@ -27,10 +27,23 @@ per operation: d = fl(x - t); x = fl(x - fl(eta * d)).
 Parity status: easgd_update and easgd_sequence are pinned
 (tests/test_oracle_easgd.py: SPEC L478 example, alpha = 1 swap-converge, exact
 rational brute force of each rounding step, conservation of x + c in exact
-arithmetic and within one rounding in fp32).  Concurrent (unordered) updates have
-no bitwise oracle: "parity unpinned" for bitwise comparison; they are checked by
-invariants only.
+arithmetic and within one rounding in fp32).
+
+Concurrent updates (reading Q15: several workers update one centre at once,
+each reading a possibly stale c, the adds atomic -- "without the Round-Robin
+scheme", L573-581) have no single result.  easgd_interleavings enumerates
+every result they can produce -- every order of the atomic adds and every
+state of c each worker can have read -- and easgd_concurrent_admissible tests
+a result for membership, element by element.  Pinned (tests/test_oracle_easgd.py)
+by the hand-derived two-worker example of tests/golden/easgd_interleavings.txt,
+by N = 1 reducing to easgd_update, by every arrival order of easgd_sequence
+being a member, by the path count N!^2, and by lost updates, a second add of one
+worker and an FMA-contracted update failing membership.  The `ftz` add models
+the hardware float atomic of the fast concurrent mode (PTX red.add.f32 flushes
+subnormal operands and results to sign-preserving zero; reading Q15).
 """
+
+import itertools
 
 import numpy as np
 
@@ -81,3 +94,67 @@ def easgd_async_replay(workers, center, targets, eta, tau, alpha, order):
         ws[w] = quadratic_sgd_steps(ws[w], targets[w], eta, tau)
         ws[w], c = easgd_update(ws[w], c, alpha)
     return ws, c
+
+
+def _ftz(v):
+    """Sign-preserving flush of fp32 subnormals to zero."""
+    v = np.asarray(v, dtype=np.float32)
+    return np.where(np.abs(v) < np.float32(2.0 ** -126), np.copysign(np.float32(0.0), v), v).astype(np.float32)
+
+
+def _centre_add(c, e, add):
+    """One atomic centre add: "ieee" = fl(c + e); "ftz" = the hardware float
+    atomic (subnormal operands and result flushed, reading Q15)."""
+    if add == "ieee":
+        return np.add(c, e, dtype=np.float32)
+    if add == "ftz":
+        return _ftz(np.add(_ftz(c), _ftz(e), dtype=np.float32))
+    raise ValueError(add)
+
+
+def easgd_interleavings(workers, center, alpha, add="ieee"):
+    """Every result N CONCURRENT elastic updates of one centre can produce
+    (reading Q15), as a list of (new_workers, new_center), one per path.
+
+    A path is an order sigma of the N atomic centre adds plus, for the worker
+    whose add comes t-th, the state of c it read: c_r with 0 <= r <= t (c_0 the
+    initial centre, c_{t+1} = add(c_t, e_sigma(t))) -- a worker reads before its
+    own add, and an atomic centre only ever holds one of the c_t.  Worker w then
+    computes, as in easgd_update, d = fl(x_w - c_r), e_w = fl(alpha d),
+    x_w' = fl(x_w - e_w).  N! orders times t+1 read choices per position: N!^2
+    paths (1, 4, 36, 576 for N = 1..4)."""
+    ws0 = [np.asarray(w, dtype=np.float32) for w in workers]
+    c0 = np.asarray(center, dtype=np.float32)
+    a = np.float32(alpha)
+    n = len(ws0)
+    if not 1 <= n <= 4:
+        raise ValueError("interleavings are enumerated for 1..4 workers")
+    out = []
+    for sigma in itertools.permutations(range(n)):
+        for reads in itertools.product(*[range(t + 1) for t in range(n)]):
+            states = [c0]
+            ws = list(ws0)
+            for t, w in enumerate(sigma):
+                d = np.subtract(ws0[w], states[reads[t]], dtype=np.float32)
+                e = np.multiply(a, d, dtype=np.float32)
+                ws[w] = np.subtract(ws0[w], e, dtype=np.float32)
+                states.append(_centre_add(states[-1], e, add))
+            out.append((ws, states[-1]))
+    return out
+
+
+def easgd_concurrent_admissible(workers, center, alpha, got_workers, got_center, add="ieee"):
+    """Per element: True where (got_workers, got_center) equals, bit for bit (NaNs
+    matching NaNs), the result of at least one path of easgd_interleavings --
+    the same path for the workers and the centre of that element."""
+    def same(u, v):
+        u = np.asarray(u, dtype=np.float32)
+        v = np.asarray(v, dtype=np.float32)
+        return (u.view(np.uint32) == v.view(np.uint32)) | (np.isnan(u) & np.isnan(v))
+    ok = np.zeros(np.asarray(center).shape, dtype=bool)
+    for ws, c in easgd_interleavings(workers, center, alpha, add):
+        m = same(c, got_center)
+        for w, g in zip(ws, got_workers):
+            m &= same(w, g)
+        ok |= m
+    return ok

@@ -158,3 +158,100 @@ def test_property_update_vs_brute_force(x, c, alpha):
         e = exact.mul(a, d)
         assert exact.same_bits32(x2[i], exact.sub(float(xs[i]), e))
         assert exact.same_bits32(c2[i], exact.add(float(cs[i]), e))
+
+
+# ---------------------------------------------------------------------------
+# Concurrent updates: easgd_interleavings / easgd_concurrent_admissible (Q15)
+# ---------------------------------------------------------------------------
+import itertools as _it  # noqa: E402
+import math as _math  # noqa: E402
+import os as _os  # noqa: E402
+
+from oracle.easgd import easgd_concurrent_admissible, easgd_interleavings  # noqa: E402
+
+
+def _golden_interleavings():
+    path = _os.path.join(_os.path.dirname(__file__), "golden", "easgd_interleavings.txt")
+    cases, cur = [], None
+    for line in open(path):
+        line = line.split("#")[0].strip()
+        if not line:
+            continue
+        if line.startswith("case"):
+            cur = ([float(v) for v in line.split()[1:]], set())
+            cases.append(cur)
+        else:
+            cur[1].add(tuple(float(v) for v in line.split()))
+    return cases
+
+
+def test_interleavings_golden_two_workers():
+    """The distinct results equal the hand-derived sets (tests/golden/
+    easgd_interleavings.txt, SPEC L475 + PAPER L573-581)."""
+    cases = _golden_interleavings()
+    assert len(cases) == 2
+    for (xa, xb, c, alpha), want in cases:
+        got = {(float(ws[0][0]), float(ws[1][0]), float(cc[0]))
+               for ws, cc in easgd_interleavings([np.float32([xa]), np.float32([xb])], np.float32([c]), alpha)}
+        assert got == want
+
+
+@pytest.mark.parametrize("n", [1, 2, 3, 4])
+def test_interleavings_path_count(n):
+    X = [worker_buffer(5, "D1", r, config=70) for r in range(n)]
+    c = worker_buffer(5, "D1", 9, config=70)
+    assert len(easgd_interleavings(X, c, 0.3)) == _math.factorial(n) ** 2
+
+
+def test_interleavings_one_worker_is_the_update():
+    x, c = worker_buffer(1000, "D2", 0, config=71), worker_buffer(1000, "D2", 1, config=71)
+    (ws, cc), = easgd_interleavings([x], c, 0.3)
+    wx, wc = easgd_update(x, c, 0.3)
+    assert np.array_equal(ws[0].view(np.uint32), wx.view(np.uint32))
+    assert np.array_equal(cc.view(np.uint32), wc.view(np.uint32))
+
+
+@pytest.mark.parametrize("n", [2, 3, 4])
+def test_every_arrival_order_is_admissible(n):
+    """A serial arrival order (each worker reads the centre after all earlier adds)
+    is one of the interleavings: easgd_sequence's result is a member everywhere."""
+    P = 4000
+    X = [worker_buffer(P, "D1", r, config=72) for r in range(n)]
+    c = worker_buffer(P, "D1", 9, config=72)
+    for order in _it.permutations(range(n)):
+        ws, cc = easgd_sequence(X, c, 0.3, list(order))
+        assert easgd_concurrent_admissible(X, c, 0.3, ws, cc).all()
+
+
+def test_stale_reads_are_admissible_but_lost_or_doubled_updates_are_not():
+    """All workers reading the initial centre (every update stale) is admissible;
+    dropping one worker's add, adding one twice, or an FMA-contracted update is
+    not (on generic inputs: fails on most elements)."""
+    P, n, a = 4000, 3, np.float32(0.3)
+    X = [worker_buffer(P, "D1", r, config=73) for r in range(n)]
+    c = worker_buffer(P, "D1", 9, config=73)
+    es = [np.multiply(a, np.subtract(x, c, dtype=np.float32), dtype=np.float32) for x in X]
+    stale_w = [np.subtract(x, e, dtype=np.float32) for x, e in zip(X, es)]
+    cc = c
+    for e in es:
+        cc = np.add(cc, e, dtype=np.float32)
+    assert easgd_concurrent_admissible(X, c, a, stale_w, cc).all()
+    lost = np.add(np.add(c, es[0], dtype=np.float32), es[1], dtype=np.float32)
+    assert easgd_concurrent_admissible(X, c, a, stale_w, lost).mean() < 0.05
+    doubled = np.add(cc, es[2], dtype=np.float32)
+    assert easgd_concurrent_admissible(X, c, a, stale_w, doubled).mean() < 0.05
+    # FMA contraction of x' = x - alpha (x - c): one rounding instead of two
+    fma_w = [np.float32(np.float64(x) - np.float64(a) * np.float64(np.subtract(x, c, dtype=np.float32)))
+             for x in X]
+    fma_w = [np.asarray(w, dtype=np.float32) for w in fma_w]
+    assert easgd_concurrent_admissible(X, c, a, fma_w, cc).mean() < 0.9
+
+
+def test_ftz_add_flushes_subnormals():
+    """The `ftz` centre add (model of the hardware float atomic, Q15) flushes a
+    subnormal sum to signed zero; the IEEE add keeps it."""
+    tiny = np.float32(2.0 ** -130)
+    x, c = np.float32([2 * tiny]), np.float32([0.0])  # e = alpha * 2 tiny = tiny (alpha = 1/2)
+    ieee = {float(cc[0]) for _, cc in easgd_interleavings([x], c, 0.5, add="ieee")}
+    ftz = {float(cc[0]) for _, cc in easgd_interleavings([x], c, 0.5, add="ftz")}
+    assert ieee == {float(tiny)} and ftz == {0.0}
