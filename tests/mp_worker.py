@@ -4,7 +4,7 @@ all_gather_object.  Used by tests/test_gpu_multiprocess.py; on a one-GPU box
 every rank uses cuda:0 (IPC between processes on one device), on a multi-GPU
 box rank r uses cuda:r.
 
-argv: outdir strategy P dist mode      (mode: normal | sum | range | locked | async | skip1 | mismatch | stress | bsp | bspmom | graph | fuzz)
+argv: outdir strategy P dist mode      (mode: normal | sum | range | locked | concurrent | concurrent_exact | async | skip1 | mismatch | stress | bsp | bspmom | graph | fuzz)
 """
 
 import json
@@ -78,6 +78,10 @@ def main():
                     torch.cuda.synchronize()
                     time.sleep(rnd.random() * 0.002)
                 tm.tm_easgd_update_locked(x, rank, 0.5 / size)
+            torch.cuda.synchronize()
+        elif mode in ("concurrent", "concurrent_exact"):  # all workers at once, atomic centre adds
+            dist.barrier()
+            tm.tm_easgd_update_sharded(x, 0.3, concurrent=(True if mode == "concurrent" else "exact"))
             torch.cuda.synchronize()
         elif mode == "locked":  # all workers at once; per-chunk locks order them
             nch = -(-L // 4096)

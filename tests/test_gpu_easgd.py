@@ -141,6 +141,92 @@ def test_concurrent_workers_invariants():
     assert np.max(np.abs(gc.astype(np.float64) - wc)) < 0.25
 
 
+@pytest.mark.parametrize("mode", [True, "exact"])
+@pytest.mark.parametrize("scale", ["D1", "subnormal"])
+@pytest.mark.parametrize("sharded", [False, True])
+def test_concurrent_updates_are_admissible_interleavings(mode, scale, sharded):
+    """4 workers update one centre concurrently from 4 streams (PAPER L573-581,
+    reading Q15).  Every sampled element of every worker and of the centre must
+    equal, bit for bit, one result of the oracle's enumeration of all
+    interleavings (oracle.easgd.easgd_concurrent_admissible: every order of the
+    atomic adds, every centre state a worker can have read); the fast mode
+    (red.add) against the flushing add, the exact mode (CAS) against the IEEE
+    add.  Inputs of the 'subnormal' scale put the centre and the elastic
+    differences in fp32's subnormal range, where the two modes differ."""
+    from oracle.easgd import easgd_concurrent_admissible
+    nw, P = 4, 1 << 20
+    alpha = np.float32(0.3)
+    W = [worker_buffer(P, "D1", r, config=49) for r in range(nw)]
+    c = worker_buffer(P, "D1", 98, config=49)
+    if scale == "subnormal":
+        f = np.float32(2.0 ** -130)
+        W = [np.multiply(w, f, dtype=np.float32) for w in W]
+        c = np.multiply(c, f, dtype=np.float32)
+    Wd = to_dev(W)
+    streams = [torch.cuda.Stream() for _ in range(nw)]
+    if sharded:
+        with tm.Exchanger(P, "easgd", size=nw, nlocal=nw) as ex:
+            L = ex.layout()["seg_len"]
+            for s in range(nw):
+                sh = ex.center_shard(s)
+                sh.copy_(torch.from_numpy(c[s * L: s * L + sh.numel()]))
+            torch.cuda.synchronize()
+            go = _hold_streams(streams)
+            for w, st in zip(Wd, streams):
+                tm.tm_easgd_update_sharded(w, float(alpha), concurrent=mode, stream=st)
+            torch.cuda.synchronize()
+            gW, gc = to_host(Wd), _read_centre(ex, P, nw)
+    else:
+        cd = to_dev([c])[0]
+        torch.cuda.synchronize()
+        go = _hold_streams(streams)
+        for w, st in zip(Wd, streams):
+            tm.tm_easgd_update_ex(w, cd, float(alpha), concurrent=mode, stream=st)
+        torch.cuda.synchronize()
+        gW, gc = to_host(Wd), to_host([cd])[0]
+    del go
+    idx = np.unique(np.concatenate([np.random.default_rng(5).integers(0, P, 1 << 16), np.arange(P - 64, P)]))
+    ok = easgd_concurrent_admissible([w[idx] for w in W], c[idx], alpha, [g[idx] for g in gW], gc[idx],
+                                     add="ftz" if mode is True else "ieee")
+    bad = np.flatnonzero(~ok)
+    assert bad.size == 0, (f"{bad.size} of {idx.size} sampled elements are no interleaving's result; first "
+                           f"at {idx[bad[0]]}: workers {[float(g[idx[bad[0]]]) for g in gW]} centre {gc[idx[bad[0]]]}")
+    # how often the updates really interleaved: elements no serial arrival order explains
+    import itertools
+    serial = np.zeros(idx.size, dtype=bool)
+    for order in itertools.permutations(range(nw)):
+        sw, sc = easgd_sequence([w[idx] for w in W], c[idx], alpha, list(order))
+        if mode is True:  # the flushing add: compare through the admissibility of that one order
+            continue
+        m = bits_equal(sc, gc[idx])
+        for a_, b_ in zip(sw, [g[idx] for g in gW]):
+            m &= bits_equal(a_, b_)
+        serial |= m
+    if mode is not True:
+        print(f"[interleaving] mode={mode} scale={scale} sharded={sharded}: "
+              f"{int((~serial).sum())} of {idx.size} sampled elements match no serial arrival order")
+    if scale == "subnormal" and mode is True:  # the flush is visible: the IEEE model rejects it
+        ieee_ok = easgd_concurrent_admissible([w[idx] for w in W], c[idx], alpha, [g[idx] for g in gW], gc[idx],
+                                              add="ieee")
+        assert not ieee_ok.all()
+
+
+def bits_equal(a, b):
+    return np.asarray(a, np.float32).view(np.uint32) == np.asarray(b, np.float32).view(np.uint32)
+
+
+def _hold_streams(streams):
+    """Make the streams' next launches start together: each waits on an event
+    recorded after a ~1 ms spin on the current stream, so the host enqueues every
+    worker's update before any of them can run."""
+    torch.cuda._sleep(2_000_000)
+    go = torch.cuda.Event()
+    go.record()
+    for st in streams:
+        st.wait_event(go)
+    return go
+
+
 def _sharded_setup(P, k, config):
     W = [worker_buffer(P, "D1", r, config=config) for r in range(k)]
     c0 = worker_buffer(P, "D1", 99, config=config)

@@ -244,6 +244,28 @@ def test_multiprocess_mismatch_detected(tmp_path):
     assert any(r.get("init_error") == 6 for r in res), res
 
 
+@pytest.mark.parametrize("mode", ["concurrent", "concurrent_exact"])
+@pytest.mark.parametrize("k", [2, 4])
+def test_multiprocess_concurrent_easgd_admissible(tmp_path, mode, k):
+    """k processes update the sharded centre at once (system-scope atomic adds
+    into the peers' shards over the IPC mappings, reading Q15):
+    every element of every worker and of the centre is bitwise one of the
+    oracle's interleavings (oracle.easgd.easgd_concurrent_admissible; the fast
+    mode against the flushing add, the exact mode against the IEEE add)."""
+    from oracle.easgd import easgd_concurrent_admissible
+    P = 100_003
+    res = launch(tmp_path, k, "easgd", P, "D1", mode=mode)
+    W = [worker_buffer(P, "D1", r, config=51) for r in range(k)]
+    c0 = worker_buffer(P, "D1", 99, config=51)
+    L = res[0]["seg_len"]
+    gW = [np.load(os.path.join(tmp_path, f"rank{r}.npy")) for r in range(k)]
+    gc = np.concatenate([np.load(os.path.join(tmp_path, f"shard{r}.npy")) for r in range(k)])[:P]
+    assert L * (k - 1) < P
+    ok = easgd_concurrent_admissible(W, c0, np.float32(0.3), gW, gc,
+                                     add="ftz" if mode == "concurrent" else "ieee")
+    assert ok.all(), f"{int((~ok).sum())} of {P} elements are no interleaving's result"
+
+
 def test_multiprocess_sharded_easgd(tmp_path):
     """EASGD centre sharded across two processes; worker updates reach the peer's
     shard through the IPC mapping; bitwise the oracle's serial order."""
