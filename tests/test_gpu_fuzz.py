@@ -175,3 +175,68 @@ def test_fuzz_easgd_bitwise(i):
     assert_bitwise(gc, cc, f"{what} centre")
     for w in range(nw):
         assert_bitwise(gW[w], ww[w], f"{what} worker {w}")
+
+
+NGRAPH = int(os.environ.get("TM_FUZZ_GRAPH_CASES", "32"))
+
+
+@pytest.mark.parametrize("i", range(NGRAPH))
+def test_fuzz_graph_replays_bitwise(monkeypatch, i):
+    """CUDA-graph capture of a random plan -- 1-4 steps, each a per-rank
+    perturbation x_r <- fl(x_r + d_r) followed by a full exchange or a bucket --
+    replayed 1-3 times; the epochs and the one-shot kernel's staging parity live
+    on the device, so every replay must equal the oracle applied step by step."""
+    g = np.random.default_rng([1605, 8325, 782, i])
+    k = int(g.integers(2, 9))
+    P = max(8, int(np.exp(g.uniform(np.log(8), np.log(1 << 19)))) + int(g.integers(0, 4)))
+    strategy = str(g.choice(["asa", "asa16"]))
+    path = "direct" if g.random() < 0.3 else "staged"
+    flavour = FLAVOURS[int(g.integers(0, len(FLAVOURS)))] if path == "staged" else None
+    plan = []
+    for _ in range(int(g.integers(1, 5))):
+        if g.random() < 0.5:
+            off = int(g.integers(0, P // 4)) * 4
+            plan.append((off, int(g.integers(0, P - off + 1))))
+        else:
+            plan.append((0, P))
+    replays = int(g.integers(1, 4))
+    if flavour:
+        monkeypatch.setenv("TM_STAGED_KERNEL", flavour)
+    else:
+        monkeypatch.delenv("TM_STAGED_KERNEL", raising=False)
+    what = f"graph case {i}: k={k} P={P} {strategy} {path} {flavour} plan={plan} replays={replays}"
+    X = worker_buffers(P, k, "D2", config=783)
+    D = [np.multiply(d, np.float32(1e-3), dtype=np.float32) for d in worker_buffers(P, k, "D1", config=784)]
+    bufs, dd = to_dev(X), to_dev(D)
+    with tm.Exchanger(P, strategy, size=k, nlocal=k, path=path) as ex:
+        s = torch.cuda.Stream()
+        s.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(s):
+            ex.exchange(bufs, s)  # eager warm-up call (also part of the expected sequence)
+            graph = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(graph, stream=s):
+                for off, cnt in plan:
+                    for b, d in zip(bufs, dd):
+                        b.add_(d)
+                    if off == 0 and cnt == P:
+                        ex.exchange(bufs, s)
+                    else:
+                        ex.exchange_range(bufs, off, cnt, s)
+        torch.cuda.current_stream().wait_stream(s)
+        for _ in range(replays):
+            graph.replay()
+        torch.cuda.synchronize()
+        code, _ = ex.status()
+        got = to_host(bufs)
+        del graph
+    assert code == tm.TM_OK, what
+    want = ox.exchange(X, strategy)
+    for _ in range(replays):
+        for off, cnt in plan:
+            want = [np.add(w, d, dtype=np.float32) for w, d in zip(want, D)]
+            if cnt:
+                seg = ox.exchange([w[off:off + cnt] for w in want], strategy)
+                for r in range(k):
+                    want[r][off:off + cnt] = seg[r]
+    for r in range(k):
+        assert_bitwise(got[r], want[r], f"{what} rank {r}")
