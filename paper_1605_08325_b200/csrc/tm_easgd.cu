@@ -454,7 +454,7 @@ easgd_round_tma_kernel(const __grid_constant__ OrderedWorkers ow, float* c, int6
 // different streams (e.g. two centres) never claim tiles from one counter; each
 // launch's last CTA resets its pair.  Null if the allocation failed (static
 // tiles then).
-unsigned long long* round_tile_ctr(int dev, bool may_allocate) {
+unsigned long long* round_tile_ctr(int dev, bool may_allocate, cudaStream_t stream) {
   static std::mutex mu;
   static unsigned long long* ring[64] = {};
   static uint32_t seq[64] = {};
@@ -465,8 +465,9 @@ unsigned long long* round_tile_ctr(int dev, bool may_allocate) {
     void* p = nullptr;
     const size_t bytes = (size_t)kCtrSlots * 2 * sizeof(unsigned long long);
     if (cudaMalloc(&p, bytes) != cudaSuccess) return nullptr;
-    // zeroed before any round on any (non-blocking) stream claims from it
-    if (cudaMemset(p, 0, bytes) != cudaSuccess || cudaDeviceSynchronize() != cudaSuccess) {
+    // zeroed, and waited for, before any round on any stream claims from it (a
+    // legacy-stream cudaMemset would not order a non-blocking stream's round)
+    if (cudaMemsetAsync(p, 0, bytes, stream) != cudaSuccess || cudaStreamSynchronize(stream) != cudaSuccess) {
       cudaFree(p);
       return nullptr;
     }
@@ -494,7 +495,7 @@ cudaError_t launch_round_tma(const OrderedWorkers& ow, float* c, int64_t n, int6
   // round, and with few workers a tile is so little work that the claims on that
   // one address become the limit (N = 1: 238 vs 153 us per update, static wins).
   unsigned long long* ctr =
-      (stat || N < 4) ? nullptr : round_tile_ctr(dev, cap == cudaStreamCaptureStatusNone);
+      (stat || N < 4) ? nullptr : round_tile_ctr(dev, cap == cudaStreamCaptureStatusNone, s);
   fn<<<grid, kThreads, R::kSmem, s>>>(ow, c, ntiles, n, alpha, ctr);
   return cudaGetLastError();
 }
