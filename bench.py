@@ -351,9 +351,7 @@ def roofline(strategy, P, k, path, ms, peak, peak_src, workload):
     alg = design_hbm_bytes(strategy, P, k, path)
     ach = alg / (ms * 1e-3) / 1e9
     if path == "staged" and strategy != "ar":
-        kernel = {0: "tm_exchange_kernel", 1: "tm_exchange_tma_kernel", 2: "tm_exchange_ws_kernel",
-                  3: "tm_exchange_tmaws_kernel"}.get(
-            STAGED_KERNEL[0], "tm_exchange_kernel")
+        kernel = KERNEL_NAMES.get(STAGED_KERNEL[0], "tm_exchange_kernel")
     else:
         kernel = ("tm_direct_kernel" if os.environ.get("TM_DIRECT_LDG") == "1" or P < 2048
                   else "tm_direct_tma_kernel")
@@ -376,7 +374,8 @@ def traffic_from_profiles(workload_key):
 # ----------------------------------------------------------------- our arm
 
 KERNEL_NAMES = {0: "tm_exchange_kernel", 1: "tm_exchange_tma_kernel", 2: "tm_exchange_ws_kernel",
-                3: "tm_exchange_tmaws_kernel", 4: "tm_exchange_oneshot_kernel"}
+                3: "tm_exchange_tmaws_kernel", 4: "tm_exchange_oneshot_kernel",
+                5: "tm_exchange_ll_kernel"}
 
 
 def shared_gpu_nccl_env(rank, world):

@@ -50,7 +50,7 @@
  *
  * Environment (read at tm_exchange_init unless noted; every rank of a group must
  * use the same values):
- *   TM_STAGED_KERNEL=reg|tma|ws|tmaws|oneshot  staged kernel flavour (default:
+ *   TM_STAGED_KERNEL=reg|tma|ws|tmaws|oneshot|ll  staged kernel flavour (default:
  *                      oneshot for segments L <= TM_ONESHOT_MAX_L elements
  *                      (default 1 Mi at k = 2, 32 Ki at k <= 4, 16 Ki above),
  *                      reg for L <= 32 Ki, else tma in a single-process group
@@ -152,7 +152,8 @@ typedef struct {
   uint32_t epoch;        /* number of staged exchanges issued so far          */
   int32_t path;          /* effective tm_path of the next exchange            */
   int32_t staged_kernel; /* staged flavour: 0 register, 1 TMA engine, 2 warp-specialised,
-                            3 warp-specialised on the TMA engine, 4 one-shot */
+                            3 warp-specialised on the TMA engine, 4 one-shot,
+                            5 low-latency (LL: epoch inside every line, no barrier) */
   int32_t allgather;     /* tm_allgather mode of the staged path                */
   int32_t selfcheck;     /* bootstrap known-answer check: 0 not run, 1 passed,
                             2 the chosen flavour failed and every rank fell back

@@ -86,7 +86,14 @@ enum { kStampStart = 0, kStampCast = 1, kStampReady = 2, kStampReduce = 3, kStam
 //   same average, no reduce-scatter / allgather split, no REDUCED barrier);
 //   staging double-buffered by call parity.  Small segments only: it moves
 //   (k-1) P s bytes per rank over the links instead of 2 (k-1)/k P s.
-enum StagedKernel { kStagedReg = 0, kStagedTma = 1, kStagedWs = 2, kStagedTmaWs = 3, kStagedOneShot = 4 };
+//   kStagedLL: no barrier at all -- each thread pushes its unit's wire lines,
+//   the call's epoch inside every 16-byte line, into every rank's receive
+//   buffer and polls its own for the k ranks' lines (tm_exchange_ll_kernel).
+//   Smallest exchanges only: (k-1) P s bytes per rank, at half payload density.
+enum StagedKernel { kStagedReg = 0, kStagedTma = 1, kStagedWs = 2, kStagedTmaWs = 3, kStagedOneShot = 4,
+                    kStagedLL = 5 };
+// Elements per CTA of the LL kernel (one 4-element unit per thread).
+constexpr int64_t kLLChunk = 4 * 256;
 // Per-CTA chunk granularity of the one-shot kernel (each CTA reduces its chunk
 // of all k segments, k times the work of a two-phase CTA per element).
 constexpr int64_t kOneShotChunk = 512;

@@ -22,6 +22,7 @@
 #include <algorithm>
 #include <chrono>
 #include <mutex>
+#include <numeric>
 #include <vector>
 
 #include "tm.h"
@@ -237,7 +238,10 @@ ExchangeArgs make_args(float* const* bufs, int64_t off, int64_t n) {
   } else {
     a.L = round_up((n + g.k - 1) / g.k, tmx::kAlign);
     const int64_t chunk = g.staged_kernel == tmx::kStagedOneShot ? oneshot_chunk() : tmx::kMinChunk;
-    const int64_t want = std::max<int64_t>(1, (a.L + chunk - 1) / chunk);
+    // the LL kernel spreads the call's n elements (not a segment) over its CTAs
+    const int64_t want = g.staged_kernel == tmx::kStagedLL
+                             ? std::max<int64_t>(1, (n + tmx::kLLChunk - 1) / tmx::kLLChunk)
+                             : std::max<int64_t>(1, (a.L + chunk - 1) / chunk);
     a.C = (int)std::min<int64_t>(g.C, want);
     if (g.range_ctas > 0) a.C = std::min(a.C, g.range_ctas);  // bucket beside compute kernels
     a.Lc = round_up((a.L + a.C - 1) / a.C, tmx::kAlign);
@@ -306,7 +310,8 @@ int external_allgather(const ExchangeArgs& a, cudaStream_t s) {
 
 int launch_staged(ExchangeArgs& a, cudaStream_t s) {
   // the one-shot kernel has no allgather phase to hand to the copy engines / NCCL
-  a.ag_external = g.ag_mode != TM_AG_SM && g.staged_kernel != tmx::kStagedOneShot;
+  a.ag_external = g.ag_mode != TM_AG_SM && g.staged_kernel != tmx::kStagedOneShot &&
+                  g.staged_kernel != tmx::kStagedLL;
   cudaError_t e = tmx::launch_exchange(a, g.nlocal, wire16(g.strategy), g.staged_kernel, s);
   if (e != cudaSuccess) return cuda_fail("launch_exchange", e);
   ++g.epoch;  // host-side count for tm_layout; the kernels keep their own
@@ -635,6 +640,7 @@ int tm_exchange_init(int64_t nparams, const tm_world* world, int strategy) {
     if (sk && !strcmp(sk, "ws")) c.staged_kernel = tmx::kStagedWs;
     if (sk && !strcmp(sk, "tmaws")) c.staged_kernel = tmx::kStagedTmaWs;
     if (sk && !strcmp(sk, "oneshot")) c.staged_kernel = tmx::kStagedOneShot;
+    if (sk && !strcmp(sk, "ll")) c.staged_kernel = tmx::kStagedLL;
     const char* ag = getenv("TM_ALLGATHER");  // sm | ce | nccl
     const char* ag_table = getenv("TM_AG_TABLE");
     if (!ag && ag_table && c.nprocs > 1) ag = ag_table_mode(ag_table, k, c.L);
@@ -649,7 +655,9 @@ int tm_exchange_init(int64_t nparams, const tm_world* world, int strategy) {
                       : 1;
     if (k >= 2 && cmax < 1) return TM_E_CUDA;
     const int64_t chunk = c.staged_kernel == tmx::kStagedOneShot ? oneshot_chunk() : tmx::kMinChunk;
-    const int64_t want = std::max<int64_t>(1, (c.L + chunk - 1) / chunk);
+    const int64_t want = c.staged_kernel == tmx::kStagedLL
+                             ? std::max<int64_t>(1, (nparams + tmx::kLLChunk - 1) / tmx::kLLChunk)
+                             : std::max<int64_t>(1, (c.L + chunk - 1) / chunk);
     c.C = (int)std::min<int64_t>(std::max(cmax, 1), want);
     c.Lc = round_up((c.L + c.C - 1) / c.C, tmx::kAlign);
     // The warp-specialised kernel overlaps the pre-cast with the pull only across
@@ -663,8 +671,18 @@ int tm_exchange_init(int64_t nparams, const tm_world* world, int strategy) {
     // with momentum exchange), twice over (call parity) for the one-shot kernel;
     // then nvec_alloc averaged segments of L; then the flag pad.
     c.nvec_alloc = 2;
-    const int nstage = c.staged_kernel == tmx::kStagedOneShot ? 2 * c.nvec_alloc : c.nvec_alloc;
+    const bool twice = c.staged_kernel == tmx::kStagedOneShot || c.staged_kernel == tmx::kStagedLL;
+    const int nstage = twice ? 2 * c.nvec_alloc : c.nvec_alloc;
     c.stage_stride = round_up((int64_t)k * c.L * wb, 256);
+    if (c.staged_kernel == tmx::kStagedLL) {
+      // receive buffer per (parity, vector): k sources x LPS 16-byte lines, one
+      // line per 4 elements (fp16 wire) or two (fp32 wire); the kernel derives
+      // LPS = stage_stride / (16 k), which the staged flavours' own layout
+      // (the register fallback of the self-check) also fits in
+      const int64_t lps = round_up((nparams + 3) / 4, 16) * (wb == 2 ? 1 : 2);
+      const int64_t unit = std::lcm<int64_t>(16 * (int64_t)k, 256);  // exact LPS, 256-byte aligned
+      c.stage_stride = round_up(std::max<int64_t>(c.stage_stride, 16 * (int64_t)k * lps), unit);
+    }
     c.avg_stride = round_up(c.L * wb, 256);
     c.off_stage = 0;
     c.off_avg = c.off_stage + nstage * c.stage_stride;

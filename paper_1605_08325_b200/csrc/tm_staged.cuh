@@ -1151,6 +1151,188 @@ tm_exchange_oneshot_kernel(const __grid_constant__ ExchangeArgs a) {
   stamp(a, kStampEnd);
 }
 
+// ---------------------------------------------------------------------------
+// Low-latency ("LL") staged kernel (small exchanges; latency-bound regime): NO
+// barrier and no flag round trip.  Each wire line is 16 bytes {payload word,
+// epoch, payload word, epoch}: the epoch travels in the same single-copy-atomic
+// 8-byte halves as the data, so a reader that sees the call's epoch in a half
+// has that half's data.  Each thread owns a unit of 4 elements end to end:
+//   push  load its 4 fp32 elements (or compute w' = w + v' of the fused BSP
+//         step), encode them on the wire (ASA16: rn16, one line; ASA: fp32, two
+//         lines) and store the line(s) into EVERY rank's receive buffer, slot of
+//         the own rank (remote stores over NVLink; the own rank's locally);
+//   pull  poll the own receive buffer until the k ranks' lines of this unit
+//         carry the call's epoch, then reduce them in ascending rank order, /k,
+//         wire rounding (ASA16: widen(rn16(a)), reading R1) and store the unit.
+// Bitwise the owner's a4 arithmetic for every element (as the one-shot kernel).
+// The epoch is the rank's device call counter + 1 (the one-shot kernel's tail
+// counter: every CTA reads it at start, the last to retire increments it) and
+// the receive buffers are double-buffered by its parity: call n writes buffer
+// n & 1 of every peer, whose previous use was call n-2, finished on that peer
+// before it pushed call n-1's lines, which this rank received before starting
+// call n.  Stale lines of call n-2 carry epoch n-1 != n+1 and are never taken.
+// Receive buffer of rank j (in its staging region): line
+//   ((parity * nvec_alloc + vq) * k + src) * LPS + unit * LPU + h
+// with LPS = stage_stride / (16 k) lines per source and LPU = 1 (fp16 wire) or
+// 2 (fp32 wire) lines per unit.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ void st_ll(void* p, uint32_t d0, uint32_t d1, uint32_t ep) {
+  asm volatile("st.volatile.global.v4.u32 [%0], {%1, %2, %3, %4};" ::"l"(p), "r"(d0), "r"(ep), "r"(d1), "r"(ep)
+               : "memory");
+}
+__device__ __forceinline__ uint4 ld_ll(const void* p) {
+  uint4 v;
+  asm volatile("ld.volatile.global.v4.u32 {%0, %1, %2, %3}, [%4];"
+               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+               : "l"(p)
+               : "memory");
+  return v;
+}
+
+template <int K, bool W16, bool SYS, bool SGD>
+__global__ void __launch_bounds__(kThreads)
+tm_exchange_ll_kernel(const __grid_constant__ ExchangeArgs a) {
+  constexpr int LPU = W16 ? 1 : 2;
+  __shared__ uint32_t s_calls;
+  const int lr = blockIdx.x / a.C;
+  const int c = blockIdx.x - lr * a.C;
+  const int r = a.rank0 + lr;
+  uint32_t* const tail = a.flags[r] + (size_t)(kPhases * TM_MAX_RANKS + 1) * a.flag_stride;
+  if (threadIdx.x == 0) {
+    s_calls = __ldcg(tail + kTailCalls);
+    __threadfence();
+    if (atomicAdd(tail + kTailRetire, 1u) == (uint32_t)a.C - 1) {  // as the one-shot kernel
+      tail[kTailRetire] = 0;
+      tail[kTailCalls] = __ldcg(tail + kTailCalls) + 1;
+    }
+  }
+  __syncthreads();
+  const uint32_t epoch = s_calls + 1;
+  const int par = (int)(s_calls & 1u);
+  stamp(a, kStampStart);
+  const int64_t n = a.P;
+  const int64_t nu = (n + 3) / 4;
+  const int64_t lps = a.stage_stride / (16 * (int64_t)a.k);
+  const int64_t stride = (int64_t)a.C * kThreads;
+  float* const x = a.x[lr];
+  uint32_t st = 0;
+  bool late = false;
+  for (int64_t u = (int64_t)c * kThreads + threadIdx.x; u < nu; u += stride) {
+    const int64_t g = u * 4;
+    // ---------------- push: encode the unit, store it into every rank's buffer
+    float f[4], fv[4];
+    if (g + 4 <= n) {
+      const float4 t = ld16_f(x + g);
+      f[0] = t.x; f[1] = t.y; f[2] = t.z; f[3] = t.w;
+    } else {
+#pragma unroll
+      for (int q = 0; q < 4; ++q) f[q] = g + q < n ? x[g + q] : 0.0f;
+    }
+    if constexpr (SGD) {
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        fv[q] = g + q < n ? sgd_v1(a.v[lr][g + q], a.g[lr][g + q], a.lr, a.mu) : 0.0f;
+        f[q] = g + q < n ? __fadd_rn(f[q], fv[q]) : 0.0f;
+      }
+      if (a.nvec == 1) {  // v' back to v (the momentum is not exchanged)
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+          if (g + q < n) a.v[lr][g + q] = fv[q];
+      } else {
+        st |= unit_status<W16, 4>(fv);
+      }
+    }
+    st |= unit_status<W16, 4>(f);
+    for (int vq = 0; vq < a.nvec; ++vq) {
+      const float* src = (SGD && vq == 1) ? fv : f;
+      uint32_t w[2 * LPU];
+      if constexpr (W16) {
+        w[0] = pack_rn16x2(src[0], src[1]);
+        w[1] = pack_rn16x2(src[2], src[3]);
+      } else {
+#pragma unroll
+        for (int q = 0; q < 4; ++q) w[q] = __float_as_uint(src[q]);
+      }
+      const int64_t line = ((int64_t)(par * a.nvec_alloc + vq) * a.k + r) * lps + u * LPU;
+#pragma unroll
+      for (int j = 0; j < K; ++j) {
+        char* dst = reinterpret_cast<char*>(a.stage[j]) + line * 16;
+#pragma unroll
+        for (int h = 0; h < LPU; ++h) st_ll(dst + h * 16, w[2 * h], w[2 * h + 1], epoch);
+      }
+    }
+    // ---------------- pull: the k ranks' lines of this unit, rank order
+    for (int vq = 0; vq < a.nvec; ++vq) {
+      const char* base = reinterpret_cast<const char*>(a.stage[r]) +
+                         (((int64_t)(par * a.nvec_alloc + vq) * a.k) * lps + u * LPU) * 16;
+      uint4 ln[K][LPU];
+      uint32_t ready = 0;  // bit j: rank j's line(s) in
+      uint64_t t0 = 0;
+      for (int spin = 0; ready != (1u << K) - 1u && !late; ++spin) {
+#pragma unroll
+        for (int j = 0; j < K; ++j) {
+          if (!(ready >> j & 1u)) {
+            bool ok = true;
+#pragma unroll
+            for (int h = 0; h < LPU; ++h) {
+              ln[j][h] = ld_ll(base + ((int64_t)j * lps + h) * 16);
+              ok = ok && ln[j][h].y == epoch && ln[j][h].w == epoch;
+            }
+            if (ok) ready |= 1u << j;
+          }
+        }
+        if (ready != (1u << K) - 1u && (spin & 63) == 63) {
+          const uint64_t now = globaltimer();
+          if (t0 == 0) t0 = now;
+          else if (now - t0 > a.timeout_ns) late = true;
+        }
+      }
+      if (late) break;
+      float sm[4], t[4];
+#pragma unroll
+      for (int j = 0; j < K; ++j) {
+        if constexpr (W16) {
+          const float2 lo = unpack16x2(ln[j][0].x), hi = unpack16x2(ln[j][0].z);
+          t[0] = lo.x; t[1] = lo.y; t[2] = hi.x; t[3] = hi.y;
+        } else {
+          t[0] = __uint_as_float(ln[j][0].x); t[1] = __uint_as_float(ln[j][0].z);
+          t[2] = __uint_as_float(ln[j][LPU - 1].x); t[3] = __uint_as_float(ln[j][LPU - 1].z);
+        }
+        if (j == 0) {
+#pragma unroll
+          for (int q = 0; q < 4; ++q) sm[q] = t[q];
+        } else {
+#pragma unroll
+          for (int q = 0; q < 4; ++q) sm[q] = __fadd_rn(sm[q], t[q]);
+        }
+      }
+      if (!a.sum) {
+#pragma unroll
+        for (int q = 0; q < 4; ++q) sm[q] = div_k<K>(sm[q]);
+      } else if (W16) {  // a sum can leave the binary16 range
+#pragma unroll
+        for (int q = 0; q < 4; ++q) st |= status_of(sm[q], true) & TM_BIT_OVERFLOW16;
+      }
+      if constexpr (W16) {  // the wire rounding of the average: widen(rn16(a))
+        const float2 lo = unpack16x2(pack_rn16x2(sm[0], sm[1])), hi = unpack16x2(pack_rn16x2(sm[2], sm[3]));
+        sm[0] = lo.x; sm[1] = lo.y; sm[2] = hi.x; sm[3] = hi.y;
+      }
+      float* dstx = vq ? a.v[lr] : x;
+      if (g + 4 <= n) {
+        st16_f(dstx + g, make_float4(sm[0], sm[1], sm[2], sm[3]));
+      } else {
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+          if (g + q < n) dstx[g + q] = sm[q];
+      }
+    }
+    if (late) break;
+  }
+  if (late) st |= TM_BIT_TIMEOUT;
+  if (st) atomicOr(a.status, st);
+  stamp(a, kStampEnd);
+}
+
 template <int K, bool W16, bool SGD>
 const void* exchange_fn(bool sys, int fl) {
   if (fl == kStagedTma)
@@ -1165,6 +1347,9 @@ const void* exchange_fn(bool sys, int fl) {
   if (fl == kStagedOneShot)
     return sys ? reinterpret_cast<const void*>(&tm_exchange_oneshot_kernel<K, W16, true, SGD>)
                : reinterpret_cast<const void*>(&tm_exchange_oneshot_kernel<K, W16, false, SGD>);
+  if (fl == kStagedLL)
+    return sys ? reinterpret_cast<const void*>(&tm_exchange_ll_kernel<K, W16, true, SGD>)
+               : reinterpret_cast<const void*>(&tm_exchange_ll_kernel<K, W16, false, SGD>);
   return sys ? reinterpret_cast<const void*>(&tm_exchange_kernel<K, W16, true, SGD>)
              : reinterpret_cast<const void*>(&tm_exchange_kernel<K, W16, false, SGD>);
 }
