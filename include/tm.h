@@ -51,7 +51,9 @@
  * Environment (read at tm_exchange_init unless noted; every rank of a group must
  * use the same values):
  *   TM_STAGED_KERNEL=reg|tma|ws|tmaws|oneshot|ll  staged kernel flavour (default:
- *                      oneshot for segments L <= TM_ONESHOT_MAX_L elements
+ *                      ll for segments L <= TM_LL_MAX_L elements (default
+ *                      512 Ki at k = 2, 128 Ki at k <= 4, 8 Ki above), then
+ *                      oneshot for L <= TM_ONESHOT_MAX_L elements
  *                      (default 1 Mi at k = 2, 32 Ki at k <= 4, 16 Ki above),
  *                      reg for L <= 32 Ki, else tma in a single-process group
  *                      and tmaws across processes).

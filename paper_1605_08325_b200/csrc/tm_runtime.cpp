@@ -143,6 +143,16 @@ std::mutex g_mu;
 // (6P bytes of HBM) is long enough for that to matter.
 // The register two-phase kernel up to L = 32 Ki, the TMA-engine kernels above.
 int64_t oneshot_max_l(int k) { return k == 2 ? (int64_t)1 << 20 : k <= 4 ? 32768 : 16384; }
+// The LL kernel (no barrier; the epoch travels inside every wire line) below
+// these segment lengths, from the r02 LL latency tables (profiles/r02/ll/: k
+// processes concurrent under MPS, and k ranks in one process; 64 exchanges per
+// graph).  Under MPS, LL vs the previous default: k = 2 4.6-5.5 us vs 7.5-17 us
+// up to P = 256 Ki and 10.4 vs 18.9 us at 1 Mi; k = 4 5.3-9.8 vs 8.5-19.5 us up
+// to 256 Ki, 17.6 vs 23.3 at 512 Ki, 45.1 vs 26.0 at 1 Mi; k = 8 7.3-9.5 vs
+// 9.8-13.7 us up to 64 Ki, level at 128 Ki, behind above (every rank pushes
+// every element to every rank, and polls k lines per unit).  So up to P =
+// 1 Mi at k = 2, 512 Ki at k <= 4, 64 Ki above.
+int64_t ll_max_l(int k) { return k == 2 ? (int64_t)1 << 19 : k <= 4 ? (int64_t)1 << 17 : 8192; }
 constexpr int64_t kRegMaxL = 32768;
 
 int64_t env_i64(const char* name, int64_t dflt) {
@@ -620,14 +630,18 @@ int tm_exchange_init(int64_t nparams, const tm_world* world, int strategy) {
     // (NVLink) sub-chunk by sub-chunk, both fed by bulk copies; on one GPU it
     // measures as the TMA kernel (0.982 vs 0.984 ms at AlexNet k = 8) and ahead
     // of the register warp-specialised kernel (1.248 ms).
-    // TM_STAGED_KERNEL=reg|tma|ws|tmaws|oneshot overrides (TM_STAGED_LDG=1 /
+    // TM_STAGED_KERNEL=reg|tma|ws|tmaws|oneshot|ll overrides (TM_STAGED_LDG=1 /
     // TM_STAGED_TMA=1 are accepted too).
     // Segments of at most TM_ONESHOT_MAX_L elements (default oneshot_max_l(k),
     // profiles/r02/latency/): the one-shot kernel (one barrier).  Up to
     // kRegMaxL: the register two-phase kernel, whose phases have no bulk-copy
     // round trips to drain (profiles/r01/latency_flavours.txt, r02/latency/).
+    // Segments of at most TM_LL_MAX_L elements (default ll_max_l(k)): the LL
+    // kernel, no barrier at all.
     const int64_t oneshot_max = env_i64("TM_ONESHOT_MAX_L", oneshot_max_l(k));
-    c.staged_kernel = c.L <= oneshot_max     ? tmx::kStagedOneShot
+    const int64_t ll_max = env_i64("TM_LL_MAX_L", ll_max_l(k));
+    c.staged_kernel = c.L <= ll_max          ? tmx::kStagedLL
+                      : c.L <= oneshot_max   ? tmx::kStagedOneShot
                       : c.L <= kRegMaxL      ? tmx::kStagedReg
                       : (c.nprocs == 1 ? tmx::kStagedTma : tmx::kStagedTmaWs);
     const char* sk = getenv("TM_STAGED_KERNEL");
