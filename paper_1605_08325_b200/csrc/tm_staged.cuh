@@ -1330,6 +1330,12 @@ tm_exchange_ll_kernel(const __grid_constant__ ExchangeArgs a) {
   }
   if (late) st |= TM_BIT_TIMEOUT;
   if (st) atomicOr(a.status, st);
+  // push and pull are fused per unit (no phase boundary): the intermediate
+  // phase stamps all mark the end of the fused loop
+  stamp(a, kStampCast);
+  stamp(a, kStampReady);
+  stamp(a, kStampReduce);
+  stamp(a, kStampReduced);
   stamp(a, kStampEnd);
 }
 
