@@ -375,7 +375,7 @@ def traffic_from_profiles(workload_key):
 
 KERNEL_NAMES = {0: "tm_exchange_kernel", 1: "tm_exchange_tma_kernel", 2: "tm_exchange_ws_kernel",
                 3: "tm_exchange_tmaws_kernel", 4: "tm_exchange_oneshot_kernel",
-                5: "tm_exchange_ll_kernel"}
+                5: "tm_exchange_ll_kernel", 6: "tm_exchange_ll2_kernel"}
 
 
 def shared_gpu_nccl_env(rank, world):

@@ -50,9 +50,10 @@
  *
  * Environment (read at tm_exchange_init unless noted; every rank of a group must
  * use the same values):
- *   TM_STAGED_KERNEL=reg|tma|ws|tmaws|oneshot|ll  staged kernel flavour (default:
+ *   TM_STAGED_KERNEL=reg|tma|ws|tmaws|oneshot|ll|ll2  staged kernel flavour (default:
  *                      ll for segments L <= TM_LL_MAX_L elements (default
- *                      512 Ki at k = 2, 128 Ki at k <= 4, 8 Ki above), then
+ *                      512 Ki at k = 2, 64 Ki at k <= 4, 8 Ki above), ll2 for
+ *                      L <= TM_LL2_MAX_L (1 Mi, 256 Ki, 64 Ki), then
  *                      oneshot for L <= TM_ONESHOT_MAX_L elements
  *                      (default 1 Mi at k = 2, 32 Ki at k <= 4, 16 Ki above),
  *                      reg for L <= 32 Ki, else tma in a single-process group
@@ -155,7 +156,8 @@ typedef struct {
   int32_t path;          /* effective tm_path of the next exchange            */
   int32_t staged_kernel; /* staged flavour: 0 register, 1 TMA engine, 2 warp-specialised,
                             3 warp-specialised on the TMA engine, 4 one-shot,
-                            5 low-latency (LL: epoch inside every line, no barrier) */
+                            5 low-latency (LL: epoch inside every line, no barrier),
+                            6 two-shot LL (push to the owner, owner pushes the average) */
   int32_t allgather;     /* tm_allgather mode of the staged path                */
   int32_t selfcheck;     /* bootstrap known-answer check: 0 not run, 1 passed,
                             2 the chosen flavour failed and every rank fell back

@@ -90,8 +90,11 @@ enum { kStampStart = 0, kStampCast = 1, kStampReady = 2, kStampReduce = 3, kStam
 //   the call's epoch inside every 16-byte line, into every rank's receive
 //   buffer and polls its own for the k ranks' lines (tm_exchange_ll_kernel).
 //   Smallest exchanges only: (k-1) P s bytes per rank, at half payload density.
+//   kStagedLL2: the two-shot version (tm_exchange_ll2_kernel): units pushed to
+//   their owner, the owner's averages pushed to every rank -- the ASA split with
+//   epoch-tagged lines instead of barriers; 2 (k-1)/k P 2s bytes per rank.
 enum StagedKernel { kStagedReg = 0, kStagedTma = 1, kStagedWs = 2, kStagedTmaWs = 3, kStagedOneShot = 4,
-                    kStagedLL = 5 };
+                    kStagedLL = 5, kStagedLL2 = 6 };
 // Elements per CTA of the LL kernel (one 4-element unit per thread).
 constexpr int64_t kLLChunk = 4 * 256;
 // Per-CTA chunk granularity of the one-shot kernel (each CTA reduces its chunk

@@ -150,9 +150,15 @@ int64_t oneshot_max_l(int k) { return k == 2 ? (int64_t)1 << 20 : k <= 4 ? 32768
 // up to P = 256 Ki and 10.4 vs 18.9 us at 1 Mi; k = 4 5.3-9.8 vs 8.5-19.5 us up
 // to 256 Ki, 17.6 vs 23.3 at 512 Ki, 45.1 vs 26.0 at 1 Mi; k = 8 7.3-9.5 vs
 // 9.8-13.7 us up to 64 Ki, level at 128 Ki, behind above (every rank pushes
-// every element to every rank, and polls k lines per unit).  So up to P =
-// 1 Mi at k = 2, 512 Ki at k <= 4, 64 Ki above.
-int64_t ll_max_l(int k) { return k == 2 ? (int64_t)1 << 19 : k <= 4 ? (int64_t)1 << 17 : 8192; }
+// every element to every rank, and polls k lines per unit).  Above LL, the
+// two-shot LL2 kernel (profiles/r02/ll2/): under MPS k = 4 12.4 vs 18.3 us (LL)
+// at P = 512 Ki, 21.0 vs 25.6 (tma) at 1 Mi; k = 8 15.5 vs 16.2 (one-shot) at
+// 128 Ki, 19.0 vs 21.9 (reg) at 256 Ki, 27.5 vs 27.7 (one-shot) at 512 Ki (one
+// process: 9.9 / 13.5 / 20.4 vs 12.8 / 14.1 / 22.7); k = 2 19.0 vs 21.3
+// (one-shot) at 2 Mi.  So LL up to P = 1 Mi at k = 2, 256 Ki at k <= 4, 64 Ki
+// above; LL2 up to 2 Mi, 1 Mi and 512 Ki; the two-phase kernels above.
+int64_t ll_max_l(int k) { return k == 2 ? (int64_t)1 << 19 : k <= 4 ? (int64_t)1 << 16 : 8192; }
+int64_t ll2_max_l(int k) { return k == 2 ? (int64_t)1 << 20 : k <= 4 ? (int64_t)1 << 18 : (int64_t)1 << 16; }
 constexpr int64_t kRegMaxL = 32768;
 
 int64_t env_i64(const char* name, int64_t dflt) {
@@ -249,9 +255,9 @@ ExchangeArgs make_args(float* const* bufs, int64_t off, int64_t n) {
     a.L = round_up((n + g.k - 1) / g.k, tmx::kAlign);
     const int64_t chunk = g.staged_kernel == tmx::kStagedOneShot ? oneshot_chunk() : tmx::kMinChunk;
     // the LL kernel spreads the call's n elements (not a segment) over its CTAs
-    const int64_t want = g.staged_kernel == tmx::kStagedLL
-                             ? std::max<int64_t>(1, (n + tmx::kLLChunk - 1) / tmx::kLLChunk)
-                             : std::max<int64_t>(1, (a.L + chunk - 1) / chunk);
+    const bool ll = g.staged_kernel == tmx::kStagedLL || g.staged_kernel == tmx::kStagedLL2;
+    const int64_t want = ll ? std::max<int64_t>(1, (n + tmx::kLLChunk - 1) / tmx::kLLChunk)
+                            : std::max<int64_t>(1, (a.L + chunk - 1) / chunk);
     a.C = (int)std::min<int64_t>(g.C, want);
     if (g.range_ctas > 0) a.C = std::min(a.C, g.range_ctas);  // bucket beside compute kernels
     a.Lc = round_up((a.L + a.C - 1) / a.C, tmx::kAlign);
@@ -321,7 +327,7 @@ int external_allgather(const ExchangeArgs& a, cudaStream_t s) {
 int launch_staged(ExchangeArgs& a, cudaStream_t s) {
   // the one-shot kernel has no allgather phase to hand to the copy engines / NCCL
   a.ag_external = g.ag_mode != TM_AG_SM && g.staged_kernel != tmx::kStagedOneShot &&
-                  g.staged_kernel != tmx::kStagedLL;
+                  g.staged_kernel != tmx::kStagedLL && g.staged_kernel != tmx::kStagedLL2;
   cudaError_t e = tmx::launch_exchange(a, g.nlocal, wire16(g.strategy), g.staged_kernel, s);
   if (e != cudaSuccess) return cuda_fail("launch_exchange", e);
   ++g.epoch;  // host-side count for tm_layout; the kernels keep their own
@@ -637,10 +643,13 @@ int tm_exchange_init(int64_t nparams, const tm_world* world, int strategy) {
     // kRegMaxL: the register two-phase kernel, whose phases have no bulk-copy
     // round trips to drain (profiles/r01/latency_flavours.txt, r02/latency/).
     // Segments of at most TM_LL_MAX_L elements (default ll_max_l(k)): the LL
-    // kernel, no barrier at all.
+    // kernel, no barrier at all; up to TM_LL2_MAX_L (ll2_max_l(k)) the two-shot
+    // LL2 kernel.
     const int64_t oneshot_max = env_i64("TM_ONESHOT_MAX_L", oneshot_max_l(k));
     const int64_t ll_max = env_i64("TM_LL_MAX_L", ll_max_l(k));
+    const int64_t ll2_max = env_i64("TM_LL2_MAX_L", ll2_max_l(k));
     c.staged_kernel = c.L <= ll_max          ? tmx::kStagedLL
+                      : c.L <= ll2_max       ? tmx::kStagedLL2
                       : c.L <= oneshot_max   ? tmx::kStagedOneShot
                       : c.L <= kRegMaxL      ? tmx::kStagedReg
                       : (c.nprocs == 1 ? tmx::kStagedTma : tmx::kStagedTmaWs);
@@ -655,6 +664,7 @@ int tm_exchange_init(int64_t nparams, const tm_world* world, int strategy) {
     if (sk && !strcmp(sk, "tmaws")) c.staged_kernel = tmx::kStagedTmaWs;
     if (sk && !strcmp(sk, "oneshot")) c.staged_kernel = tmx::kStagedOneShot;
     if (sk && !strcmp(sk, "ll")) c.staged_kernel = tmx::kStagedLL;
+    if (sk && !strcmp(sk, "ll2")) c.staged_kernel = tmx::kStagedLL2;
     const char* ag = getenv("TM_ALLGATHER");  // sm | ce | nccl
     const char* ag_table = getenv("TM_AG_TABLE");
     if (!ag && ag_table && c.nprocs > 1) ag = ag_table_mode(ag_table, k, c.L);
@@ -669,9 +679,9 @@ int tm_exchange_init(int64_t nparams, const tm_world* world, int strategy) {
                       : 1;
     if (k >= 2 && cmax < 1) return TM_E_CUDA;
     const int64_t chunk = c.staged_kernel == tmx::kStagedOneShot ? oneshot_chunk() : tmx::kMinChunk;
-    const int64_t want = c.staged_kernel == tmx::kStagedLL
-                             ? std::max<int64_t>(1, (nparams + tmx::kLLChunk - 1) / tmx::kLLChunk)
-                             : std::max<int64_t>(1, (c.L + chunk - 1) / chunk);
+    const bool ll = c.staged_kernel == tmx::kStagedLL || c.staged_kernel == tmx::kStagedLL2;
+    const int64_t want = ll ? std::max<int64_t>(1, (nparams + tmx::kLLChunk - 1) / tmx::kLLChunk)
+                            : std::max<int64_t>(1, (c.L + chunk - 1) / chunk);
     c.C = (int)std::min<int64_t>(std::max(cmax, 1), want);
     c.Lc = round_up((c.L + c.C - 1) / c.C, tmx::kAlign);
     // The warp-specialised kernel overlaps the pre-cast with the pull only across
@@ -685,7 +695,8 @@ int tm_exchange_init(int64_t nparams, const tm_world* world, int strategy) {
     // with momentum exchange), twice over (call parity) for the one-shot kernel;
     // then nvec_alloc averaged segments of L; then the flag pad.
     c.nvec_alloc = 2;
-    const bool twice = c.staged_kernel == tmx::kStagedOneShot || c.staged_kernel == tmx::kStagedLL;
+    const bool twice = c.staged_kernel == tmx::kStagedOneShot || c.staged_kernel == tmx::kStagedLL ||
+                       c.staged_kernel == tmx::kStagedLL2;
     const int nstage = twice ? 2 * c.nvec_alloc : c.nvec_alloc;
     c.stage_stride = round_up((int64_t)k * c.L * wb, 256);
     if (c.staged_kernel == tmx::kStagedLL) {
@@ -696,6 +707,14 @@ int tm_exchange_init(int64_t nparams, const tm_world* world, int strategy) {
       const int64_t lps = round_up((nparams + 3) / 4, 16) * (wb == 2 ? 1 : 2);
       const int64_t unit = std::lcm<int64_t>(16 * (int64_t)k, 256);  // exact LPS, 256-byte aligned
       c.stage_stride = round_up(std::max<int64_t>(c.stage_stride, 16 * (int64_t)k * lps), unit);
+    }
+    if (c.staged_kernel == tmx::kStagedLL2) {
+      // per (parity, vector): [reduce-scatter: k source slots][allgather: k owner
+      // slots] of LPG lines (one segment's units); the kernel derives LPG =
+      // stage_stride / (32 k)
+      const int64_t lpg = round_up((c.L + 3) / 4, 16) * (wb == 2 ? 1 : 2);
+      const int64_t unit = std::lcm<int64_t>(32 * (int64_t)k, 256);
+      c.stage_stride = round_up(std::max<int64_t>(c.stage_stride, 32 * (int64_t)k * lpg), unit);
     }
     c.avg_stride = round_up(c.L * wb, 256);
     c.off_stage = 0;

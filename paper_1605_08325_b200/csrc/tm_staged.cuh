@@ -1339,6 +1339,210 @@ tm_exchange_ll_kernel(const __grid_constant__ ExchangeArgs a) {
   stamp(a, kStampEnd);
 }
 
+// ---------------------------------------------------------------------------
+// Two-shot LL kernel ("LL2", mid-size exchanges): the ASA split of Fig. 2 with
+// epoch-tagged lines instead of barriers.  Per call, each thread runs
+//   A  push: for every unit (4 elements) of the own buffer it is assigned,
+//      encode it (wire rounding) and store its line(s) into the OWNER's
+//      reduce-scatter buffer, slot of the own rank (one remote store per unit);
+//   B  reduce: for every unit of the own segment it is assigned, poll the k
+//      ranks' lines, sum in ascending rank order, /k, round to the wire, and
+//      store the averaged line(s) into EVERY rank's allgather buffer, slot of
+//      the own segment (the fused a4 + a6 push);
+//   C  pull: for every unit of the own buffer it is assigned, poll the owner's
+//      averaged line and widen it into the caller's buffer.
+// Every thread finishes all its A before any B, and all its B before any C, so
+// no thread waits on a line another thread only writes after waiting itself.
+// Bitwise the owner's a4 arithmetic (same result as every flavour).  Reuse by
+// the device call parity (as LL): rank r writes owner s's reduce-scatter slot
+// in call n only after its call n-1 received s's averaged lines of call n-1,
+// which s pushed after finishing call n-2; owner s writes rank j's allgather
+// slot in call n only after receiving j's call-n lines, i.e. after j finished
+// call n-2.  Layout of rank j's receive region per (parity, vector): [RS: k
+// source slots][AG: k owner slots] of LPG lines each, LPG = stage_stride /
+// (32 k), LPU lines per unit (1 fp16 wire, 2 fp32).
+// ---------------------------------------------------------------------------
+template <int LPU>
+__device__ __forceinline__ bool poll_lines(const char* p, uint32_t epoch, uint4 (&ln)[LPU], uint64_t timeout_ns) {
+  uint64_t t0 = 0;
+  for (int spin = 0;; ++spin) {
+    bool ok = true;
+#pragma unroll
+    for (int h = 0; h < LPU; ++h) {
+      ln[h] = ld_ll(p + h * 16);
+      ok = ok && ln[h].y == epoch && ln[h].w == epoch;
+    }
+    if (ok) return true;
+    if ((spin & 63) == 63) {
+      const uint64_t now = globaltimer();
+      if (t0 == 0) t0 = now;
+      else if (now - t0 > timeout_ns) return false;
+    }
+  }
+}
+
+template <int K, bool W16, bool SYS, bool SGD>
+__global__ void __launch_bounds__(kThreads)
+tm_exchange_ll2_kernel(const __grid_constant__ ExchangeArgs a) {
+  constexpr int LPU = W16 ? 1 : 2;
+  __shared__ uint32_t s_calls;
+  const int lr = blockIdx.x / a.C;
+  const int c = blockIdx.x - lr * a.C;
+  const int r = a.rank0 + lr;
+  uint32_t* const tail = a.flags[r] + (size_t)(kPhases * TM_MAX_RANKS + 1) * a.flag_stride;
+  if (threadIdx.x == 0) {
+    s_calls = __ldcg(tail + kTailCalls);
+    __threadfence();
+    if (atomicAdd(tail + kTailRetire, 1u) == (uint32_t)a.C - 1) {
+      tail[kTailRetire] = 0;
+      tail[kTailCalls] = __ldcg(tail + kTailCalls) + 1;
+    }
+  }
+  __syncthreads();
+  const uint32_t epoch = s_calls + 1;
+  const int par = (int)(s_calls & 1u);
+  stamp(a, kStampStart);
+  const int64_t n = a.P, L = a.L;
+  const int64_t lpg = a.stage_stride / (32 * (int64_t)a.k);  // lines per slot
+  const int64_t stride = (int64_t)a.C * kThreads;
+  const int64_t t = (int64_t)c * kThreads + threadIdx.x;
+  float* const x = a.x[lr];
+  uint32_t st = 0;
+  bool late = false;
+  // line address: region 0 = reduce-scatter, 1 = allgather
+  auto line = [&](int j, int vq, int region, int slot, int64_t unit) -> char* {
+    return reinterpret_cast<char*>(a.stage[j]) + (int64_t)(par * a.nvec_alloc + vq) * a.stage_stride +
+           (((int64_t)region * a.k + slot) * lpg + unit * LPU) * 16;
+  };
+  // ---------------- A: push every assigned unit to its owner -----------------
+  const int64_t nu = (n + 3) / 4;
+  for (int64_t u = t; u < nu; u += stride) {
+    const int64_t g = u * 4;
+    const int s = (int)(g / L);
+    const int64_t us = (g - (int64_t)s * L) / 4;  // unit within segment s
+    float f[4], fv[4];
+    if (g + 4 <= n) {
+      const float4 t4 = ld16_f(x + g);
+      f[0] = t4.x; f[1] = t4.y; f[2] = t4.z; f[3] = t4.w;
+    } else {
+#pragma unroll
+      for (int q = 0; q < 4; ++q) f[q] = g + q < n ? x[g + q] : 0.0f;
+    }
+    if constexpr (SGD) {
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        fv[q] = g + q < n ? sgd_v1(a.v[lr][g + q], a.g[lr][g + q], a.lr, a.mu) : 0.0f;
+        f[q] = g + q < n ? __fadd_rn(f[q], fv[q]) : 0.0f;
+      }
+      if (a.nvec == 1) {
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+          if (g + q < n) a.v[lr][g + q] = fv[q];
+      } else {
+        st |= unit_status<W16, 4>(fv);
+      }
+    }
+    st |= unit_status<W16, 4>(f);
+    for (int vq = 0; vq < a.nvec; ++vq) {
+      const float* src = (SGD && vq == 1) ? fv : f;
+      uint32_t w[2 * LPU];
+      if constexpr (W16) {
+        w[0] = pack_rn16x2(src[0], src[1]);
+        w[1] = pack_rn16x2(src[2], src[3]);
+      } else {
+#pragma unroll
+        for (int q = 0; q < 4; ++q) w[q] = __float_as_uint(src[q]);
+      }
+      char* dst = line(s, vq, 0, r, us);
+#pragma unroll
+      for (int h = 0; h < LPU; ++h) st_ll(dst + h * 16, w[2 * h], w[2 * h + 1], epoch);
+    }
+  }
+  // ---------------- B: reduce the own segment's units, push the averages ------
+  const int64_t seg_n = max((int64_t)0, min(L, n - (int64_t)r * L));
+  const int64_t nus = (seg_n + 3) / 4;
+  for (int64_t v = t; v < nus && !late; v += stride) {
+    for (int vq = 0; vq < a.nvec && !late; ++vq) {
+      float sm[4], tt[4];
+#pragma unroll
+      for (int j = 0; j < K; ++j) {
+        uint4 ln[LPU];
+        if (!poll_lines<LPU>(line(r, vq, 0, j, v), epoch, ln, a.timeout_ns)) {
+          late = true;
+          break;
+        }
+        if constexpr (W16) {
+          const float2 lo = unpack16x2(ln[0].x), hi = unpack16x2(ln[0].z);
+          tt[0] = lo.x; tt[1] = lo.y; tt[2] = hi.x; tt[3] = hi.y;
+        } else {
+          tt[0] = __uint_as_float(ln[0].x); tt[1] = __uint_as_float(ln[0].z);
+          tt[2] = __uint_as_float(ln[LPU - 1].x); tt[3] = __uint_as_float(ln[LPU - 1].z);
+        }
+#pragma unroll
+        for (int q = 0; q < 4; ++q) sm[q] = j == 0 ? tt[q] : __fadd_rn(sm[q], tt[q]);
+      }
+      if (late) break;
+      if (!a.sum) {
+#pragma unroll
+        for (int q = 0; q < 4; ++q) sm[q] = div_k<K>(sm[q]);
+      } else if (W16) {
+#pragma unroll
+        for (int q = 0; q < 4; ++q) st |= status_of(sm[q], true) & TM_BIT_OVERFLOW16;
+      }
+      uint32_t w[2 * LPU];
+      if constexpr (W16) {
+        w[0] = pack_rn16x2(sm[0], sm[1]);
+        w[1] = pack_rn16x2(sm[2], sm[3]);
+      } else {
+#pragma unroll
+        for (int q = 0; q < 4; ++q) w[q] = __float_as_uint(sm[q]);
+      }
+#pragma unroll
+      for (int j = 0; j < K; ++j) {
+        char* dst = line(j, vq, 1, r, v);
+#pragma unroll
+        for (int h = 0; h < LPU; ++h) st_ll(dst + h * 16, w[2 * h], w[2 * h + 1], epoch);
+      }
+    }
+  }
+  // ---------------- C: pull every assigned unit's average from its owner ------
+  for (int64_t u = t; u < nu && !late; u += stride) {
+    const int64_t g = u * 4;
+    const int s = (int)(g / L);
+    const int64_t us = (g - (int64_t)s * L) / 4;
+    for (int vq = 0; vq < a.nvec; ++vq) {
+      uint4 ln[LPU];
+      if (!poll_lines<LPU>(line(r, vq, 1, s, us), epoch, ln, a.timeout_ns)) {
+        late = true;
+        break;
+      }
+      float f[4];
+      if constexpr (W16) {
+        const float2 lo = unpack16x2(ln[0].x), hi = unpack16x2(ln[0].z);
+        f[0] = lo.x; f[1] = lo.y; f[2] = hi.x; f[3] = hi.y;
+      } else {
+        f[0] = __uint_as_float(ln[0].x); f[1] = __uint_as_float(ln[0].z);
+        f[2] = __uint_as_float(ln[LPU - 1].x); f[3] = __uint_as_float(ln[LPU - 1].z);
+      }
+      float* dstx = vq ? a.v[lr] : x;
+      if (g + 4 <= n) {
+        st16_f(dstx + g, make_float4(f[0], f[1], f[2], f[3]));
+      } else {
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+          if (g + q < n) dstx[g + q] = f[q];
+      }
+    }
+  }
+  if (late) st |= TM_BIT_TIMEOUT;
+  if (st) atomicOr(a.status, st);
+  stamp(a, kStampCast);
+  stamp(a, kStampReady);
+  stamp(a, kStampReduce);
+  stamp(a, kStampReduced);
+  stamp(a, kStampEnd);
+}
+
 template <int K, bool W16, bool SGD>
 const void* exchange_fn(bool sys, int fl) {
   if (fl == kStagedTma)
@@ -1356,6 +1560,9 @@ const void* exchange_fn(bool sys, int fl) {
   if (fl == kStagedLL)
     return sys ? reinterpret_cast<const void*>(&tm_exchange_ll_kernel<K, W16, true, SGD>)
                : reinterpret_cast<const void*>(&tm_exchange_ll_kernel<K, W16, false, SGD>);
+  if (fl == kStagedLL2)
+    return sys ? reinterpret_cast<const void*>(&tm_exchange_ll2_kernel<K, W16, true, SGD>)
+               : reinterpret_cast<const void*>(&tm_exchange_ll2_kernel<K, W16, false, SGD>);
   return sys ? reinterpret_cast<const void*>(&tm_exchange_kernel<K, W16, true, SGD>)
              : reinterpret_cast<const void*>(&tm_exchange_kernel<K, W16, false, SGD>);
 }

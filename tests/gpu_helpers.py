@@ -43,7 +43,7 @@ def fuzz_cases(k, pmax, n=None):
     bucket with a CTA budget -- or (bsp) two BSP iterations, momentum-SGD step
     fused into the exchange, with or without the momentum exchange."""
     n = int(os.environ.get("TM_MP_FUZZ_CASES", "24")) if n is None else n
-    flavours = [None, "reg", "tma", "ws", "tmaws", "oneshot", "ll"]
+    flavours = [None, "reg", "tma", "ws", "tmaws", "oneshot", "ll", "ll2"]
     out = []
     for i in range(n):
         g = np.random.default_rng([1605, 8325, 779, k, i])

@@ -46,7 +46,7 @@ def test_bsp_step_rejects_sum_mode():
         assert e.value.code == tm.TM_E_ARG
 
 
-@pytest.mark.parametrize("kernel", ["reg", "tma", "ws", "tmaws", "oneshot", "ll"])
+@pytest.mark.parametrize("kernel", ["reg", "tma", "ws", "tmaws", "oneshot", "ll", "ll2"])
 @pytest.mark.parametrize("unfused", ["0", "1"])
 def test_bsp_staged_flavours_bitwise(monkeypatch, kernel, unfused):
     """Single-process group on the staged path, every staged kernel flavour, with
@@ -62,7 +62,7 @@ def test_bsp_staged_flavours_bitwise(monkeypatch, kernel, unfused):
         G = worker_buffers(P, k, "D2", config=112)
         Wd, Vd, Gd = to_dev(W), to_dev(V), to_dev(G)
         with tm.Exchanger(P, strategy, size=k, nlocal=k, path="staged") as ex:
-            assert ex.layout()["staged_kernel"] == {"reg": 0, "tma": 1, "ws": 2, "tmaws": 3, "oneshot": 4, "ll": 5}[kernel]
+            assert ex.layout()["staged_kernel"] == {"reg": 0, "tma": 1, "ws": 2, "tmaws": 3, "oneshot": 4, "ll": 5, "ll2": 6}[kernel]
             for _ in range(3):
                 ex.bsp_step(Wd, Vd, Gd, lr, mu, exchange_momentum=mom)
             code, _ = ex.status()

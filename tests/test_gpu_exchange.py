@@ -411,17 +411,18 @@ def test_phase_log_does_not_change_results(path):
 
 def test_default_staged_flavour_by_segment_length(monkeypatch):
     """Without TM_STAGED_KERNEL: the LL kernel for segments of <= 512 Ki
-    elements at k = 2, 128 Ki at k <= 4 and 8 Ki above; then the one-shot
-    kernel up to 1 Mi at k = 2, 32 Ki at k <= 4 (none left there) and 16 Ki
-    above; the register two-phase kernel up to 32 Ki (latency-bound); the
-    TMA-engine kernel above that in a single-process group."""
+    elements at k = 2, 64 Ki at k <= 4 and 8 Ki above; the two-shot LL2 kernel
+    up to 1 Mi, 256 Ki and 64 Ki (which covers the one-shot's and the register
+    two-phase kernel's former ranges); the TMA-engine kernel above that in a
+    single-process group."""
     monkeypatch.delenv("TM_STAGED_KERNEL", raising=False)
     monkeypatch.delenv("TM_ONESHOT_MAX_L", raising=False)
     monkeypatch.delenv("TM_LL_MAX_L", raising=False)
-    for P, k, want in ((100_003, 2, 5), (1_048_576, 2, 5), (1_048_577 + 511, 2, 4), (2_097_152, 2, 4),
-                       (2_097_153 + 511, 2, 1), (32_768 * 4, 4, 5), (131_072 * 4, 4, 5), (131_073 * 4, 4, 1),
-                       (131_072 * 8, 8, 1), (8_192 * 8, 8, 5), (8_193 * 8, 8, 4), (16_384 * 8, 8, 4),
-                       (16_385 * 8, 8, 0), (32_768 * 8, 8, 0), (32_769 * 8, 8, 1), (10_000, 3, 5)):
+    monkeypatch.delenv("TM_LL2_MAX_L", raising=False)
+    for P, k, want in ((100_003, 2, 5), (1_048_576, 2, 5), (1_048_577 + 511, 2, 6), (2_097_152, 2, 6),
+                       (2_097_153 + 511, 2, 1), (65_536 * 4, 4, 5), (65_537 * 4, 4, 6), (262_144 * 4, 4, 6),
+                       (262_145 * 4, 4, 1), (8_192 * 8, 8, 5), (8_193 * 8, 8, 6), (65_536 * 8, 8, 6),
+                       (65_537 * 8, 8, 1), (131_072 * 8, 8, 1), (10_000, 3, 5)):
         with tm.Exchanger(P, "asa16", size=k, nlocal=k, path="staged") as ex:
             assert ex.layout()["staged_kernel"] == want, (P, k)
 

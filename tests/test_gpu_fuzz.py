@@ -33,7 +33,7 @@ from paper_1605_08325_b200.inputs import DISTS, worker_buffers
 
 pytestmark = pytest.mark.gpu
 
-FLAVOURS = [None, "reg", "tma", "ws", "tmaws", "oneshot", "ll"]
+FLAVOURS = [None, "reg", "tma", "ws", "tmaws", "oneshot", "ll", "ll2"]
 NCASES = int(os.environ.get("TM_FUZZ_CASES", "384"))
 NBSP = int(os.environ.get("TM_FUZZ_BSP_CASES", "64"))
 

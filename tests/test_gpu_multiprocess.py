@@ -73,7 +73,7 @@ def launch(tmp_path, k, strategy, P, dist, mode="normal", timeout=240, extra_env
     return res
 
 
-KERNEL_ID = {"reg": 0, "tma": 1, "ws": 2, "tmaws": 3, "oneshot": 4, "ll": 5}
+KERNEL_ID = {"reg": 0, "tma": 1, "ws": 2, "tmaws": 3, "oneshot": 4, "ll": 5, "ll2": 6}
 
 
 @pytest.mark.parametrize("strategy,k,op,kernel", [("asa16", 2, "avg", "ws"), ("asa", 2, "avg", "ws"),
@@ -84,7 +84,9 @@ KERNEL_ID = {"reg": 0, "tma": 1, "ws": 2, "tmaws": 3, "oneshot": 4, "ll": 5}
                                                   ("asa", 3, "range", "tmaws"), ("asa16", 3, "sum", "tmaws"),
                                                   ("asa16", 2, "avg", "oneshot"), ("asa", 3, "range", "oneshot"),
                                                   ("asa16", 4, "sum", "oneshot"), ("asa16", 2, "avg", "ll"),
-                                                  ("asa", 3, "range", "ll"), ("asa16", 4, "sum", "ll")])
+                                                  ("asa", 3, "range", "ll"), ("asa16", 4, "sum", "ll"),
+                                                  ("asa16", 2, "avg", "ll2"), ("asa", 3, "range", "ll2"),
+                                                  ("asa16", 4, "sum", "ll2")])
 def test_multiprocess_bitwise(tmp_path, strategy, k, op, kernel):
     P = 100_003
     env = {"TM_STAGED_KERNEL": kernel}
@@ -107,7 +109,8 @@ def test_multiprocess_bitwise(tmp_path, strategy, k, op, kernel):
                                                     ("asa16", 2, "bsp", "reg"), ("asa", 3, "bspmom", "reg"),
                                                     ("asa16", 3, "bspmom", "tmaws"), ("asa16", 3, "bspmom", "oneshot"),
                                                     ("asa", 2, "bsp", "oneshot"), ("asa16", 3, "bspmom", "ll"),
-                                                    ("asa", 2, "bsp", "ll")])
+                                                    ("asa", 2, "bsp", "ll"), ("asa16", 3, "bspmom", "ll2"),
+                                                    ("asa", 2, "bsp", "ll2")])
 def test_multiprocess_bsp_fused_bitwise(tmp_path, strategy, k, mode, kernel):
     """tm_bsp_step across processes: the momentum-SGD step is fused into the
     staged kernel's pre-cast; two iterations vs oracle/bsp.py."""
@@ -230,12 +233,12 @@ def test_multiprocess_k4_k8_cross_rank_identity(tmp_path, k, kernel):
         assert_bitwise(got[r], got[0], f"rank {r} vs rank 0")
 
 
-@pytest.mark.parametrize("kernel", ["reg", "tma", "ws", "tmaws", "oneshot", "ll"])
+@pytest.mark.parametrize("kernel", ["reg", "tma", "ws", "tmaws", "oneshot", "ll", "ll2"])
 def test_multiprocess_timeout_instead_of_hang(tmp_path, kernel):
     """Fault injection: rank 1 never calls tm_exchange; rank 0's
     kernel times out in its first barrier, sets TM_E_TIMEOUT and exits -- every
     staged flavour (the warp-specialised ones time out in the reducer group)."""
-    P = 4096 if kernel in ("reg", "oneshot", "ll") else 300_007
+    P = 4096 if kernel in ("reg", "oneshot", "ll", "ll2") else 300_007
     res = launch(tmp_path, 2, "asa16", P, "D1", mode="skip1", extra_env={"TM_STAGED_KERNEL": kernel})
     assert res[0]["code"] == 7 and res[0]["bits"] & 4  # TM_E_TIMEOUT
 
@@ -350,7 +353,8 @@ def test_multiprocess_async_easgd_loop(tmp_path, k):
 
 
 @pytest.mark.parametrize("strategy,kernel", [("asa16", "ws"), ("asa", "reg"), ("asa16", "tma"),
-                                             ("asa16", "tmaws"), ("asa16", "oneshot"), ("asa16", "ll")])
+                                             ("asa16", "tmaws"), ("asa16", "oneshot"), ("asa16", "ll"),
+                                             ("asa", "ll2")])
 def test_multiprocess_stress_random_delays(tmp_path, strategy, kernel):
     """STRESS_ITERS (60; TM_STRESS_ITERS overrides) back-to-back exchanges per rank, each after a per-rank delta and a random
     host delay on half of them: every rank ends bitwise at the oracle's sequence."""
@@ -369,7 +373,7 @@ def test_multiprocess_stress_random_delays(tmp_path, strategy, kernel):
 
 
 @pytest.mark.parametrize("strategy,k,kernel", [("asa16", 2, "tmaws"), ("asa", 3, "tma"), ("asa16", 4, "oneshot"),
-                                               ("asa16", 3, "ll")])
+                                               ("asa16", 3, "ll"), ("asa16", 4, "ll2")])
 def test_multiprocess_bootstrap_selfcheck(tmp_path, strategy, k, kernel):
     """The bootstrap's known-answer probe passes on every rank (tm_layout
     selfcheck = 1) and the chosen flavour stays."""
@@ -420,7 +424,7 @@ def test_multiprocess_allgather_decision_table(tmp_path):
 
 
 @pytest.mark.parametrize("strategy,k,kernel", [("asa16", 2, "oneshot"), ("asa16", 3, "tmaws"), ("asa", 4, "oneshot"),
-                                               ("asa16", 2, "reg"), ("asa", 3, "ll")])
+                                               ("asa16", 2, "reg"), ("asa", 3, "ll"), ("asa16", 3, "ll2")])
 def test_multiprocess_cuda_graph_replays(tmp_path, strategy, k, kernel):
     """Each process captures 4 x (its delta, exchange) in a CUDA graph and
     replays it 3 times: device-side epochs (and the one-shot kernel's device call

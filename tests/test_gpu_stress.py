@@ -19,7 +19,7 @@ N_EXCHANGES = 10_000
 PER_GRAPH = 100
 
 
-@pytest.mark.parametrize("kernel", ["reg", "tma", "ws", "tmaws", "oneshot", "ll"])
+@pytest.mark.parametrize("kernel", ["reg", "tma", "ws", "tmaws", "oneshot", "ll", "ll2"])
 @pytest.mark.parametrize("strategy", ["asa16", "asa"])
 def test_ten_thousand_exchanges(monkeypatch, kernel, strategy):
     monkeypatch.setenv("TM_STAGED_KERNEL", kernel)

@@ -16,6 +16,7 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 @pytest.mark.parametrize("env", [{"TM_STAGED_LDG": "1"}, {"TM_STAGED_KERNEL": "ws"},
                                  {"TM_STAGED_KERNEL": "tma"}, {"TM_STAGED_KERNEL": "tmaws"}, {"TM_ALLGATHER": "ce"},
                                  {"TM_STAGED_KERNEL": "oneshot"}, {"TM_STAGED_KERNEL": "ll"},
+                                 {"TM_STAGED_KERNEL": "ll2"},
                                  {"TM_DIRECT_LDG": "1"}, {"TM_DIRECT_TMA": "1"},
                                  {"TM_TMA_CFG": "8", "TM_DIRECT_TMA": "1"}, {"TM_TMA_CFG": "3", "TM_DIRECT_TMA": "1"}])
 def test_kernel_variants_bitwise(env):

@@ -21,7 +21,7 @@ sys.path.insert(0, os.path.join(ROOT, "tools"))
 from paper_1605_08325_b200 import tm  # noqa: E402
 from sweep import timeit  # noqa: E402
 
-NAMES = {0: "reg", 1: "tma", 2: "ws", 3: "tmaws", 4: "oneshot", 5: "ll"}
+NAMES = {0: "reg", 1: "tma", 2: "ws", 3: "tmaws", 4: "oneshot", 5: "ll", 6: "ll2"}
 
 
 def main():

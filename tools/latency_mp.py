@@ -22,7 +22,7 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 from paper_1605_08325_b200 import tm  # noqa: E402
 
-NAMES = {0: "reg", 1: "tma", 2: "ws", 3: "tmaws", 4: "oneshot", 5: "ll"}
+NAMES = {0: "reg", 1: "tma", 2: "ws", 3: "tmaws", 4: "oneshot", 5: "ll", 6: "ll2"}
 
 
 def main():
