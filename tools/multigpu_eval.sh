@@ -29,8 +29,9 @@ for N in 2 4 8; do
   [ "$N" -le "$NG" ] || continue
   run "$N" "bench_n${N}_default" --no-e2e
   for WL in alexnet googlenet 1m; do
-    for FL in tmaws tma oneshot reg; do
+    for FL in tmaws tma oneshot reg ll ll2; do
       for AG in sm ce nccl; do
+        case "$FL" in ll|ll2|oneshot) [ "$AG" = sm ] || continue ;; esac  # no separate allgather phase
         TM_STAGED_KERNEL=$FL TM_ALLGATHER=$AG run "$N" "bench_n${N}_${WL}_${FL}_ag${AG}" --workload "$WL" --no-e2e \
           --no-cpu-baseline --no-nccl-compare
       done
@@ -41,6 +42,17 @@ for N in 2 4 8; do
   done
 done
 python tools/ag_decide.py "$OUT" > "$OUT/ag_table.txt"
+# small-message latency per flavour over NVLink (64 exchanges per graph): the
+# data for the LL / LL2 / one-shot / two-phase thresholds, which were set from
+# one-GPU (MPS) tables
+for N in 2 4 8; do
+  [ "$N" -le "$NG" ] || continue
+  PORT=$((PORT + 1))
+  timeout 1800 python -m torch.distributed.run --nnodes=1 --nproc-per-node "$N" --master-addr 127.0.0.1 \
+    --master-port "$PORT" tools/latency_mp.py --flavours default,ll,ll2,oneshot,reg,tma,tmaws \
+    --P 2048,32768,131072,524288,1048576,2097152,4194304 > "$OUT/latency_flavours_n$N.jsonl" 2> "$OUT/latency_flavours_n$N.err"
+  echo "latency N=$N rc=$?"
+done
 # config 5: message-size sweep 64 KB .. 1 GB (fp32 bytes per rank), ASA16 vs NCCL's allreduce
 for N in 2 4 8; do
   [ "$N" -le "$NG" ] || continue
