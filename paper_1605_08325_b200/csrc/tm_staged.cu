@@ -31,14 +31,22 @@ cudaError_t launch_widen16(const void* gather, float* x, int64_t P, cudaStream_t
 }
 
 int exchange_max_ctas(int device, bool wire16, int k, int fl) {
-  const void* fn = pick_exchange<false>(k, wire16, true, fl);
-  if (!fn) return 0;
-  if (prepare(fn, fl) != cudaSuccess) return 0;
-  int per_sm = 0;
-  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, flavour_threads(fl),
-                                                    flavour_smem(fl)) != cudaSuccess)
-    return 0;
-  return per_sm * sm_count(device);
+  // every instantiation a launch of this flavour may use: plain and with the
+  // fused BSP step (its own register allocation), GPU and system scope -- the
+  // cooperative launch needs all of the grid co-resident for any of them
+  int per_sm_min = -1;
+  for (int sgd = 0; sgd < 2; ++sgd)
+    for (int sys = 0; sys < 2; ++sys) {
+      const void* fn = sgd ? pick_exchange_sgd(k, wire16, sys != 0, fl) : pick_exchange<false>(k, wire16, sys != 0, fl);
+      if (!fn) return 0;
+      if (prepare(fn, fl) != cudaSuccess) return 0;
+      int per_sm = 0;
+      if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, flavour_threads(fl), flavour_smem(fl)) !=
+          cudaSuccess)
+        return 0;
+      per_sm_min = per_sm_min < 0 ? per_sm : std::min(per_sm_min, per_sm);
+    }
+  return per_sm_min * sm_count(device);
 }
 
 cudaError_t launch_exchange(const ExchangeArgs& a, int nlocal, bool wire16, int fl, cudaStream_t s) {
@@ -52,8 +60,10 @@ cudaError_t launch_exchange(const ExchangeArgs& a, int nlocal, bool wire16, int 
   void* params[] = {const_cast<ExchangeArgs*>(&a)};
   // Cooperative launch: guarantees every CTA is co-resident, which the
   // per-CTA flag barriers need when several ranks share this device.
-  return cudaLaunchCooperativeKernel(fn, dim3(nlocal * a.C), dim3(flavour_threads(fl)), params,
-                                     flavour_smem(fl), s);
+  e = cudaLaunchCooperativeKernel(fn, dim3(nlocal * a.C), dim3(flavour_threads(fl)), params,
+                                  flavour_smem(fl), s);
+  if (e != cudaSuccess) cudaGetLastError();  // returned here; do not leave it for the next launch's check
+  return e;
 }
 
 }  // namespace tmx
