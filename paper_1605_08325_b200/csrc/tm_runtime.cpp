@@ -89,6 +89,7 @@ struct Ctx {
   bool inited = false, ready = false;
   int64_t P = 0, L = 0, Lc = 0;
   int k = 0, rank0 = 0, nlocal = 0, device = 0, strategy = 0, C = 0;
+  int flag_c = 0;  // CTA stride of the flag pad, fixed at init (C may shrink on a self-check fallback)
   int nprocs = 1, proc = 0;
   int64_t rank_stride = 0, off_stage = 0, off_avg = 0, off_flags = 0, off_center = 0;
   int64_t stage_stride = 0, avg_stride = 0;  // bytes between staging / avg buffers (vectors, parities)
@@ -266,7 +267,7 @@ ExchangeArgs make_args(float* const* bufs, int64_t off, int64_t n) {
   a.nvec_alloc = g.nvec_alloc;
   a.stage_stride = g.stage_stride;
   a.avg_stride = g.avg_stride;
-  a.flag_stride = g.C;
+  a.flag_stride = g.flag_c;
   a.k = g.k;
   a.rank0 = g.rank0;
   a.sum = g.sum ? 1 : 0;
@@ -447,9 +448,18 @@ int do_bsp(float* const* w, float* const* v, const float* const* gr, int nbufs, 
 // TM_SELFCHECK=0 skips it; TM_SELFCHECK_FAULT=r makes rank r report a mismatch
 // (fault injection for the tests).
 // ---------------------------------------------------------------------------
+// CTAs per rank a cooperative launch of flavour fl can keep co-resident (all
+// local ranks' grids at once).  TM_PROCS_PER_GPU=n: n processes share this GPU
+// concurrently (CUDA MPS), so each may keep only 1/n of them (every rank's CTA c
+// must be resident at once for the per-CTA flag barriers).
+int flavour_cmax(int device, int strategy, int k, int nlocal, int fl) {
+  const int share = std::max(1, getenv("TM_PROCS_PER_GPU") ? atoi(getenv("TM_PROCS_PER_GPU")) : 1);
+  return tmx::exchange_max_ctas(device, wire16(strategy), k, fl) / nlocal / share;
+}
+
 uint32_t* pad_tail(int rank) {
   return reinterpret_cast<uint32_t*>(g.rank_base[rank] + g.off_flags +
-                                     ((int64_t)tmx::kPhases * TM_MAX_RANKS + 1) * g.C * 4) ;
+                                     ((int64_t)tmx::kPhases * TM_MAX_RANKS + 1) * g.flag_c * 4);
 }
 
 int probe_once(float* probe, int64_t n, cudaStream_t st, bool* ok) {
@@ -566,6 +576,16 @@ int self_check() {
     }
     if (getenv("TM_DEBUG")) fprintf(stderr, "[tm] rank %d: self-check failed, register flavour\n", g.rank0);
     g.staged_kernel = tmx::kStagedReg;  // every rank takes the same decision (same votes)
+    // C was sized for the failed flavour; the register kernel may keep fewer CTAs
+    // co-resident (its cooperative launch would fail).  Every rank computes the
+    // same C; the flag pad keeps its stride (flag_c).
+    const int creg = flavour_cmax(g.device, g.strategy, g.k, g.nlocal, g.staged_kernel);
+    if (creg < 1) {
+      rc = TM_E_CUDA;
+      break;
+    }
+    g.C = std::min(g.C, creg);
+    g.Lc = round_up((g.L + g.C - 1) / g.C, tmx::kAlign);
   }
   cudaStreamDestroy(st);
   cudaFree(probe);
@@ -671,12 +691,8 @@ int tm_exchange_init(int64_t nparams, const tm_world* world, int strategy) {
     if (ag && !strcmp(ag, "ce")) c.ag_mode = TM_AG_CE;
     c.want_nccl_ag = ag && !strcmp(ag, "nccl") && c.nprocs > 1;
     if (c.want_nccl_ag) c.ag_mode = TM_AG_NCCL;
-    // TM_PROCS_PER_GPU=n: n processes share this GPU concurrently (CUDA MPS), so
-    // each may keep only 1/n of the co-resident CTAs (every rank's CTA c must be
-    // resident at once for the per-CTA flag barriers).
-    const int share = std::max(1, getenv("TM_PROCS_PER_GPU") ? atoi(getenv("TM_PROCS_PER_GPU")) : 1);
-    int cmax = k >= 2 ? tmx::exchange_max_ctas(c.device, wire16(strategy), k, c.staged_kernel) / c.nlocal / share
-                      : 1;
+    // co-resident CTAs per rank (TM_PROCS_PER_GPU: see flavour_cmax)
+    int cmax = k >= 2 ? flavour_cmax(c.device, strategy, k, c.nlocal, c.staged_kernel) : 1;
     if (k >= 2 && cmax < 1) return TM_E_CUDA;
     const int64_t chunk = c.staged_kernel == tmx::kStagedOneShot ? oneshot_chunk() : tmx::kMinChunk;
     const bool ll = c.staged_kernel == tmx::kStagedLL || c.staged_kernel == tmx::kStagedLL2;
@@ -684,6 +700,7 @@ int tm_exchange_init(int64_t nparams, const tm_world* world, int strategy) {
                             : std::max<int64_t>(1, (c.L + chunk - 1) / chunk);
     c.C = (int)std::min<int64_t>(std::max(cmax, 1), want);
     c.Lc = round_up((c.L + c.C - 1) / c.C, tmx::kAlign);
+    c.flag_c = c.C;
     // The warp-specialised kernel overlaps the pre-cast with the pull only across
     // sub-chunks (>= kWsMinSub elements each); a chunk too short for two of them
     // would run both phases on half a CTA each with nothing to overlap, so the
@@ -720,7 +737,7 @@ int tm_exchange_init(int64_t nparams, const tm_world* world, int strategy) {
     c.off_stage = 0;
     c.off_avg = c.off_stage + nstage * c.stage_stride;
     c.off_flags = c.off_avg + c.nvec_alloc * c.avg_stride;
-    c.rank_stride = round_up(c.off_flags + ((int64_t)tmx::kPhases * TM_MAX_RANKS + 1) * c.C * 4 +
+    c.rank_stride = round_up(c.off_flags + ((int64_t)tmx::kPhases * TM_MAX_RANKS + 1) * c.flag_c * 4 +
                                  tmx::kPadTail * 4, 4096);
   } else if (strategy == TM_EASGD) {
     // Centre sharded by segment: rank s hosts c[s*L, min((s+1)*L, P)).

@@ -388,14 +388,16 @@ def test_multiprocess_bootstrap_selfcheck(tmp_path, strategy, k, kernel):
         assert_bitwise(np.load(os.path.join(tmp_path, f"rank{r}.npy")), want[r], f"rank {r}")
 
 
-@pytest.mark.parametrize("strategy,k,kernel,bad", [("asa16", 2, "tmaws", 1), ("asa", 3, "tma", 0),
-                                                   ("asa16", 4, "oneshot", 3)])
-def test_multiprocess_selfcheck_fault_falls_back(tmp_path, strategy, k, kernel, bad):
+@pytest.mark.parametrize("strategy,k,kernel,bad,P", [("asa16", 2, "tmaws", 1, 100_003), ("asa", 3, "tma", 0, 100_003),
+                                                     ("asa16", 4, "oneshot", 3, 100_003),
+                                                     ("asa16", 6, "ll", 2, 600_001)])
+def test_multiprocess_selfcheck_fault_falls_back(tmp_path, strategy, k, kernel, bad, P):
     """Fault injection (TM_SELFCHECK_FAULT=r: rank r reports a probe mismatch):
     the vote through peer memory reaches every rank, ALL ranks fall back to the
     register flavour together (selfcheck = 2, staged_kernel = 0), the re-run
-    probe passes, and the exchanges that follow are bitwise the oracle's."""
-    P = 100_003
+    probe passes, and the exchanges that follow are bitwise the oracle's.  The
+    k = 6 LL case has more CTAs per rank (587) than the register kernel keeps
+    co-resident at k = 6 (3 per SM): the fallback shrinks C with it."""
     res = launch(tmp_path, k, strategy, P, "D2",
                  extra_env={"TM_STAGED_KERNEL": kernel, "TM_SELFCHECK_FAULT": str(bad)})
     want = [worker_buffer(P, "D2", r, config=50) for r in range(k)]
