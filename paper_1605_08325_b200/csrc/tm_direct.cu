@@ -242,7 +242,7 @@ tm_direct_tma_kernel(const __grid_constant__ LocalBufs lb, int64_t ntiles, int64
 
 template <int K, bool Q16, int TILE, int RING_KB, int MINB>
 cudaError_t launch_tma(const LocalBufs& lb, int64_t P, uint32_t* status, unsigned long long* ctr,
-                       int dev, cudaStream_t s) {
+                       int dev, cudaStream_t s, int max_grid) {
   using Cfg = TmaCfg<K, TILE, RING_KB, MINB>;
   const int64_t ntiles = P / TILE;
   if (ntiles == 0) {  // smaller than one tile: the register kernel
@@ -254,7 +254,9 @@ cudaError_t launch_tma(const LocalBufs& lb, int64_t P, uint32_t* status, unsigne
   static std::atomic<uint64_t> optin{0};
   cudaError_t e0 = smem_optin(reinterpret_cast<const void*>(fn), Cfg::kSmem, dev, optin);
   if (e0 != cudaSuccess) return e0;
-  const int grid = (int)std::min<int64_t>(ntiles, (int64_t)MINB * sm_count(dev));
+  int64_t cap = (int64_t)MINB * sm_count(dev);
+  if (max_grid > 0) cap = std::min<int64_t>(cap, max_grid);  // CTA budget of a bucket
+  const int grid = (int)std::min<int64_t>(ntiles, cap);
   fn<<<grid, kThreads, Cfg::kSmem, s>>>(lb, ntiles, P, status, ctr);
   return cudaGetLastError();
 }
@@ -263,39 +265,39 @@ cudaError_t launch_tma(const LocalBufs& lb, int64_t P, uint32_t* status, unsigne
 // of the bulk-async kernel for k = 8; TM_DIRECT_LDG=1 forces the register path.
 template <int K, bool Q16>
 cudaError_t direct_tma(const LocalBufs& lb, int64_t P, uint32_t* status, unsigned long long* ctr,
-                       int dev, cudaStream_t s) {
+                       int dev, cudaStream_t s, int max_grid) {
   if constexpr (K == 8) {
     static const int cfg = env_int("TM_TMA_CFG", 0);
     switch (cfg) {
-      case 8: return launch_tma<K, Q16, 1024, 160, 1>(lb, P, status, ctr, dev, s);
-      case 1: return launch_tma<K, Q16, 1024, 96, 2>(lb, P, status, ctr, dev, s);
-      case 2: return launch_tma<K, Q16, 2048, 192, 1>(lb, P, status, ctr, dev, s);
-      case 3: return launch_tma<K, Q16, 1024, 64, 2>(lb, P, status, ctr, dev, s);
-      case 4: return launch_tma<K, Q16, 2048, 96, 2>(lb, P, status, ctr, dev, s);
-      case 5: return launch_tma<K, Q16, 2048, 96, 1>(lb, P, status, ctr, dev, s);
-      case 6: return launch_tma<K, Q16, 2048, 96, 3>(lb, P, status, ctr, dev, s);
-      case 7: return launch_tma<K, Q16, 2048, 192, 1>(lb, P, status, ctr, dev, s);
+      case 8: return launch_tma<K, Q16, 1024, 160, 1>(lb, P, status, ctr, dev, s, max_grid);
+      case 1: return launch_tma<K, Q16, 1024, 96, 2>(lb, P, status, ctr, dev, s, max_grid);
+      case 2: return launch_tma<K, Q16, 2048, 192, 1>(lb, P, status, ctr, dev, s, max_grid);
+      case 3: return launch_tma<K, Q16, 1024, 64, 2>(lb, P, status, ctr, dev, s, max_grid);
+      case 4: return launch_tma<K, Q16, 2048, 96, 2>(lb, P, status, ctr, dev, s, max_grid);
+      case 5: return launch_tma<K, Q16, 2048, 96, 1>(lb, P, status, ctr, dev, s, max_grid);
+      case 6: return launch_tma<K, Q16, 2048, 96, 3>(lb, P, status, ctr, dev, s, max_grid);
+      case 7: return launch_tma<K, Q16, 2048, 192, 1>(lb, P, status, ctr, dev, s, max_grid);
       default: break;
     }
   }
   if constexpr (K <= 4) {  // A/B for small k: larger tiles / deeper rings
     static const int cfg = env_int("TM_TMA_CFG", 0);
     switch (cfg) {
-      case 9: return launch_tma<K, Q16, 4096, 128, 1>(lb, P, status, ctr, dev, s);
-      case 10: return launch_tma<K, Q16, 2048, 128, 1>(lb, P, status, ctr, dev, s);
-      case 11: return launch_tma<K, Q16, 4096, 96, 1>(lb, P, status, ctr, dev, s);
-      case 12: return launch_tma<K, Q16, 2048, 160, 1>(lb, P, status, ctr, dev, s);
+      case 9: return launch_tma<K, Q16, 4096, 128, 1>(lb, P, status, ctr, dev, s, max_grid);
+      case 10: return launch_tma<K, Q16, 2048, 128, 1>(lb, P, status, ctr, dev, s, max_grid);
+      case 11: return launch_tma<K, Q16, 4096, 96, 1>(lb, P, status, ctr, dev, s, max_grid);
+      case 12: return launch_tma<K, Q16, 2048, 160, 1>(lb, P, status, ctr, dev, s, max_grid);
       default: break;
     }
   }
   // k = 2: 16 KB tiles per buffer, 3-deep ring: 0.146 vs 0.160 ms at AlexNet size
   // (profiles/r01/direct_small_k_cfg.txt; k = 4 measures the same either way).
-  if constexpr (K == 2) return launch_tma<K, Q16, 4096, 96, 1>(lb, P, status, ctr, dev, s);
+  if constexpr (K == 2) return launch_tma<K, Q16, 4096, 96, 1>(lb, P, status, ctr, dev, s, max_grid);
   // Default, from the r01 sweep at k = 8 (profiles/r01/README.md): 8 KB tiles per
   // buffer, a 2-deep ring for k = 8 (128 KB in flight per SM), one CTA per SM.
   // (With dynamic tiles every TM_TMA_CFG measures 0.570-0.572 ms; register stores
   // in place of the bulk stores measured 0.574 ms.)
-  return launch_tma<K, Q16, 2048, 96, 1>(lb, P, status, ctr, dev, s);
+  return launch_tma<K, Q16, 2048, 96, 1>(lb, P, status, ctr, dev, s, max_grid);
 }
 
 // Small exchanges are latency-bound: the register kernel spreads one float4 of
@@ -312,9 +314,11 @@ cudaError_t direct_k(const LocalBufs& lb, int64_t P, uint32_t* status, unsigned 
                      bool q16, int dev, cudaStream_t s, int max_ctas) {
   static const bool force_ldg = env_int("TM_DIRECT_LDG", 0) == 1;
   static const bool force_tma = env_int("TM_DIRECT_TMA", 0) == 1;  // diagnostics: TMA at every size
-  if (P >= 2048 && !force_ldg && max_ctas <= 0 && (force_tma || (int64_t)K * P > kDirectLdgMaxElems))
-    return q16 ? direct_tma<K, true>(lb, P, status, ctr, dev, s)
-               : direct_tma<K, false>(lb, P, status, ctr, dev, s);
+  static const bool range_tma = env_int("TM_RANGE_TMA", 0) == 1;  // A/B: budgeted buckets on the TMA kernel
+  if (P >= 2048 && !force_ldg && (max_ctas <= 0 || range_tma) &&
+      (force_tma || (int64_t)K * P > kDirectLdgMaxElems))
+    return q16 ? direct_tma<K, true>(lb, P, status, ctr, dev, s, max_ctas)
+               : direct_tma<K, false>(lb, P, status, ctr, dev, s, max_ctas);
   const int64_t want = (P / 4 + kThreads - 1) / kThreads;
   const int per_sm = K >= 7 ? 3 : 4;  // = the kernel's __launch_bounds__ residency
   const int64_t cap = max_ctas > 0 ? max_ctas : (int64_t)per_sm * sm_count(dev);
