@@ -282,7 +282,11 @@ int tm_easgd_update(float* worker_buf, float* center_buf, float alpha, void* str
  *                   signed zero, unlike the exclusive update;
  *   concurrent = 2  centre += e by a compare-and-swap loop around one IEEE
  *                   fp32 add (gradual underflow, reading Q6): every update is
- *                   exactly fl(c + e) of the value it replaced; slower.
+ *                   exactly fl(c + e) of the value it replaced.  A centre on
+ *                   this GPU takes one 128-bit CAS per 4 elements (16-byte
+ *                   aligned buffers; 1.31 vs 1.15 ms for concurrent = 1 at
+ *                   config 4); peer memory one 32-bit CAS per element (3.42
+ *                   ms).  TM_EASGD_CAS128=0 forces the 32-bit CAS.
  * TM_E_ARG for another value.  Does not need tm_exchange_init. */
 int tm_easgd_update_ex(float* worker_buf, float* center_buf, int64_t n, float alpha,
                        int concurrent, void* stream);

@@ -25,12 +25,17 @@ using namespace dev;
 //           signed zero;
 //   Mode 2: c += e with a compare-and-swap loop around __fadd_rn -- one exact
 //           IEEE add per update with gradual underflow (reading Q6), at the cost
-//           of a CAS round trip per element.
+//           of a CAS round trip per element;
+//   Mode 3: Mode 2's arithmetic on 16-byte vectors with ONE 128-bit CAS
+//           (atom.cas.b128, ATOMG.E.CAS.128) per 4 elements, its first expected
+//           value the c the update was computed from (no second read): each
+//           element still gets one exact add applied atomically, so the result
+//           is one of Mode 2's interleavings.  Launched only when the centre is
+//           on the launching GPU (the host checks; peers' memory keeps Mode 2).
 // ---------------------------------------------------------------------------
 template <bool SYS>
-__device__ __forceinline__ void cas_add(float* p, float v) {
+__device__ __forceinline__ void cas_add(float* p, float v, unsigned int old) {
   unsigned int* a = reinterpret_cast<unsigned int*>(p);
-  unsigned int old = __ldcg(a);
   for (;;) {
     const unsigned int want = __float_as_uint(__fadd_rn(__uint_as_float(old), v));
     const unsigned int got = SYS ? atomicCAS_system(a, old, want) : atomicCAS(a, old, want);
@@ -39,22 +44,55 @@ __device__ __forceinline__ void cas_add(float* p, float v) {
   }
 }
 
+// 128-bit compare-and-swap; on return (lo, hi) hold the value found
+__device__ __forceinline__ bool cas128(void* p, uint64_t& lo, uint64_t& hi, uint64_t nlo, uint64_t nhi) {
+  uint64_t olo, ohi;
+  asm volatile("{\n\t.reg .b128 cmp, val, old;\n\t"
+               "mov.b128 cmp, {%2, %3};\n\t"
+               "mov.b128 val, {%4, %5};\n\t"
+               "atom.relaxed.sys.global.cas.b128 old, [%6], cmp, val;\n\t"
+               "mov.b128 {%0, %1}, old;\n\t}"
+               : "=l"(olo), "=l"(ohi)
+               : "l"(lo), "l"(hi), "l"(nlo), "l"(nhi), "l"(p)
+               : "memory");
+  const bool ok = olo == lo && ohi == hi;
+  lo = olo;
+  hi = ohi;
+  return ok;
+}
+__device__ __forceinline__ uint64_t pack2(float a, float b) {
+  return (uint64_t)__float_as_uint(b) << 32 | __float_as_uint(a);
+}
+__device__ __forceinline__ float lo_f(uint64_t v) { return __uint_as_float((uint32_t)v); }
+__device__ __forceinline__ float hi_f(uint64_t v) { return __uint_as_float((uint32_t)(v >> 32)); }
+
+// c += e; cv = the centre value e was computed from (the CAS modes' first guess)
 template <int Mode, bool SYS>
-__device__ __forceinline__ void centre_add4(float* c, float4 e) {
+__device__ __forceinline__ void centre_add4(float* c, float4 e, float4 cv) {
   if constexpr (Mode == 1) {
     if (SYS) red_add4_sys(c, e);
     else red_add4_gpu(c, e);
+  } else if constexpr (Mode == 3) {
+    uint64_t lo = pack2(cv.x, cv.y), hi = pack2(cv.z, cv.w);
+    for (;;) {
+      const uint64_t nlo = pack2(__fadd_rn(lo_f(lo), e.x), __fadd_rn(hi_f(lo), e.y));
+      const uint64_t nhi = pack2(__fadd_rn(lo_f(hi), e.z), __fadd_rn(hi_f(hi), e.w));
+      if (cas128(c, lo, hi, nlo, nhi)) break;
+    }
   } else {
-    cas_add<SYS>(c, e.x); cas_add<SYS>(c + 1, e.y); cas_add<SYS>(c + 2, e.z); cas_add<SYS>(c + 3, e.w);
+    cas_add<SYS>(c, e.x, __float_as_uint(cv.x));
+    cas_add<SYS>(c + 1, e.y, __float_as_uint(cv.y));
+    cas_add<SYS>(c + 2, e.z, __float_as_uint(cv.z));
+    cas_add<SYS>(c + 3, e.w, __float_as_uint(cv.w));
   }
 }
 template <int Mode, bool SYS>
-__device__ __forceinline__ void centre_add1(float* c, float e) {
+__device__ __forceinline__ void centre_add1(float* c, float e, float cv) {
   if constexpr (Mode == 1) {
     if (SYS) red_add_sys(c, e);
     else red_add_gpu(c, e);
-  } else {
-    cas_add<SYS>(c, e);
+  } else {  // Modes 2 and 3 (scalar tail)
+    cas_add<SYS>(c, e, __float_as_uint(cv));
   }
 }
 
@@ -77,7 +115,7 @@ easgd_kernel(float* __restrict__ x, float* c, int64_t n, float alpha, int vec) {
       xv.z = __fsub_rn(xv.z, ez); xv.w = __fsub_rn(xv.w, ew);
       st16_f(x + v * 4, xv);
       if (Concurrent) {
-        centre_add4<Mode, true>(c + v * 4, make_float4(ex, ey, ez, ew));
+        centre_add4<Mode, true>(c + v * 4, make_float4(ex, ey, ez, ew), cv);
       } else {
         cv.x = __fadd_rn(cv.x, ex); cv.y = __fadd_rn(cv.y, ey);
         cv.z = __fadd_rn(cv.z, ez); cv.w = __fadd_rn(cv.w, ew);
@@ -91,7 +129,7 @@ easgd_kernel(float* __restrict__ x, float* c, int64_t n, float alpha, int vec) {
     const float ci = Concurrent ? __ldcg(c + i) : c[i];
     const float e = elastic_diff(xi, ci, alpha);
     x[i] = __fsub_rn(xi, e);
-    if (Concurrent) centre_add1<Mode, true>(c + i, e);
+    if (Concurrent) centre_add1<Mode, true>(c + i, e, ci);
     else c[i] = __fadd_rn(ci, e);
   }
 }
@@ -123,7 +161,7 @@ easgd_sharded_kernel(float* __restrict__ x, const __grid_constant__ ShardArgs sa
       xv.z = __fsub_rn(xv.z, ez); xv.w = __fsub_rn(xv.w, ew);
       st16_f(xs + v * 4, xv);
       if (Concurrent) {
-        centre_add4<Mode, SYS>(c + v * 4, make_float4(ex, ey, ez, ew));
+        centre_add4<Mode, SYS>(c + v * 4, make_float4(ex, ey, ez, ew), cv);
       } else {
         cv.x = __fadd_rn(cv.x, ex); cv.y = __fadd_rn(cv.y, ey);
         cv.z = __fadd_rn(cv.z, ez); cv.w = __fadd_rn(cv.w, ew);
@@ -135,7 +173,7 @@ easgd_sharded_kernel(float* __restrict__ x, const __grid_constant__ ShardArgs sa
       const float ci = __ldcg(c + i);
       const float e = elastic_diff(xi, ci, alpha);
       xs[i] = __fsub_rn(xi, e);
-      if (Concurrent) centre_add1<Mode, SYS>(c + i, e);
+      if (Concurrent) centre_add1<Mode, SYS>(c + i, e, ci);
       else c[i] = __fadd_rn(ci, e);
     }
   }
@@ -527,13 +565,29 @@ cast_rn16_kernel(const float* __restrict__ in, uint16_t* __restrict__ out, int64
   }
 }
 
+// The 128-bit CAS of Mode 3 only on memory of the launching GPU (peer memory
+// behind an IPC mapping keeps the 32-bit CAS of Mode 2); TM_EASGD_CAS128=0 turns
+// it off (A/B).
+bool cas128_ok(const void* p) {
+  if (env_int("TM_EASGD_CAS128", 1) == 0) return false;  // read per launch (tests switch it)
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return false;
+  cudaPointerAttributes at{};
+  if (cudaPointerGetAttributes(&at, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return at.type == cudaMemoryTypeDevice && at.device == dev;
+}
+
 }  // namespace
 
 cudaError_t launch_easgd(float* x, float* c, int64_t n, float alpha, int concurrent,
                          cudaStream_t s) {
   const int vec = ((reinterpret_cast<uintptr_t>(x) | reinterpret_cast<uintptr_t>(c)) & 15) == 0;
   const int grid = streaming_grid(vec ? n / 4 + 4 : n);
-  if (concurrent == 2) easgd_kernel<2><<<grid, kThreads, 0, s>>>(x, c, n, alpha, vec);
+  if (concurrent == 2 && vec && cas128_ok(c)) easgd_kernel<3><<<grid, kThreads, 0, s>>>(x, c, n, alpha, vec);
+  else if (concurrent == 2) easgd_kernel<2><<<grid, kThreads, 0, s>>>(x, c, n, alpha, vec);
   else if (concurrent) easgd_kernel<1><<<grid, kThreads, 0, s>>>(x, c, n, alpha, vec);
   else easgd_kernel<0><<<grid, kThreads, 0, s>>>(x, c, n, alpha, vec);
   return cudaGetLastError();
@@ -581,7 +635,11 @@ cudaError_t launch_easgd_round(float* const* w, int nw, const int32_t* order, in
 cudaError_t launch_easgd_sharded(float* x, const ShardArgs& sa, float alpha, int concurrent,
                                  cudaStream_t s) {
   const int grid = streaming_grid(sa.L / 4 + 4);
-  if (concurrent == 2) {
+  bool local = true;
+  for (int j = 0; j < sa.k; ++j) local = local && cas128_ok(sa.shard[j]);
+  if (concurrent == 2 && local) {
+    easgd_sharded_kernel<3, true><<<grid, kThreads, 0, s>>>(x, sa, alpha);
+  } else if (concurrent == 2) {
     if (sa.sys) easgd_sharded_kernel<2, true><<<grid, kThreads, 0, s>>>(x, sa, alpha);
     else easgd_sharded_kernel<2, false><<<grid, kThreads, 0, s>>>(x, sa, alpha);
   } else if (concurrent) {

@@ -141,10 +141,10 @@ def test_concurrent_workers_invariants():
     assert np.max(np.abs(gc.astype(np.float64) - wc)) < 0.25
 
 
-@pytest.mark.parametrize("mode", [True, "exact"])
+@pytest.mark.parametrize("mode", [True, "exact", "exact32"])
 @pytest.mark.parametrize("scale", ["D1", "subnormal"])
 @pytest.mark.parametrize("sharded", [False, True])
-def test_concurrent_updates_are_admissible_interleavings(mode, scale, sharded):
+def test_concurrent_updates_are_admissible_interleavings(mode, scale, sharded, monkeypatch):
     """4 workers update one centre concurrently from 4 streams (PAPER L573-581,
     reading Q15).  Every sampled element of every worker and of the centre must
     equal, bit for bit, one result of the oracle's enumeration of all
@@ -152,8 +152,14 @@ def test_concurrent_updates_are_admissible_interleavings(mode, scale, sharded):
     atomic adds, every centre state a worker can have read); the fast mode
     (red.add) against the flushing add, the exact mode (CAS) against the IEEE
     add.  Inputs of the 'subnormal' scale put the centre and the elastic
-    differences in fp32's subnormal range, where the two modes differ."""
+    differences in fp32's subnormal range, where the two modes differ.  The
+    exact mode on a centre of this GPU takes one 128-bit CAS per 4 elements;
+    "exact32" forces the 32-bit CAS per element (TM_EASGD_CAS128=0), the path
+    a centre on a peer GPU takes."""
     from oracle.easgd import easgd_concurrent_admissible
+    if mode == "exact32":
+        monkeypatch.setenv("TM_EASGD_CAS128", "0")
+        mode = "exact"
     nw, P = 4, 1 << 20
     alpha = np.float32(0.3)
     W = [worker_buffer(P, "D1", r, config=49) for r in range(nw)]
@@ -393,11 +399,14 @@ def test_concurrent_mode_flushes_subnormals():
 
 
 @pytest.mark.parametrize("dist", ["D1", "D6"])
-def test_exact_concurrent_mode_keeps_subnormals_bitwise(dist):
+@pytest.mark.parametrize("cas128", ["1", "0"])
+def test_exact_concurrent_mode_keeps_subnormals_bitwise(dist, cas128, monkeypatch):
     """Concurrent mode 2 ("exact") adds e to the centre with a compare-and-swap
     loop around one IEEE fp32 add (gradual underflow, reading Q6): a single
     worker's update is bitwise the exclusive update and the oracle's, subnormal
-    e and c' included (where mode 1's float atomic flushes them)."""
+    e and c' included (where mode 1's float atomic flushes them).  Both CAS
+    widths: 128-bit (centre on this GPU) and 32-bit (TM_EASGD_CAS128=0)."""
+    monkeypatch.setenv("TM_EASGD_CAS128", cas128)
     n = 100_003
     x = worker_buffer(n, dist, 0, config=47)
     c = worker_buffer(n, dist, 1, config=47)
@@ -412,13 +421,15 @@ def test_exact_concurrent_mode_keeps_subnormals_bitwise(dist):
     assert np.all(gc[:8] != 0)
 
 
-def test_exact_concurrent_workers_conserve_and_keep_subnormals():
+@pytest.mark.parametrize("cas128", ["1", "0"])
+def test_exact_concurrent_workers_conserve_and_keep_subnormals(cas128, monkeypatch):
     """8 workers on 8 streams in exact concurrent mode (Q15: no bitwise oracle,
     the order is the hardware's).  No update is lost: sum_w x_w + c is conserved
     within the rounding bound; and on a block of fp32-subnormal values -- where
     every subtraction, product by 2^-4 and sum is exact whatever the order (the
     values are multiples of 2^-149 below 2^-126) -- the centre is EXACTLY c plus
     the sum of the workers' moves, i.e. nothing was flushed to zero."""
+    monkeypatch.setenv("TM_EASGD_CAS128", cas128)
     n = 1 << 20
     nw, alpha = 8, 0.0625
     W = [worker_buffer(n, "D1", r, config=48) for r in range(nw)]

@@ -126,8 +126,13 @@ def easgd_rows(P, nw, alpha, pk):
     rows.append({"mode": f"{nw} concurrent updates (red.add, {nw} streams)", "us": ms * 1e3,
                  "hbm_GBps": 16.0 * P * nw / (ms * 1e-3) / 1e9})
     ms = timeit(lambda: concurrent("exact"))
-    rows.append({"mode": f"{nw} concurrent updates (exact: CAS-loop IEEE add, {nw} streams)", "us": ms * 1e3,
-                 "hbm_GBps": 16.0 * P * nw / (ms * 1e-3) / 1e9})
+    rows.append({"mode": f"{nw} concurrent updates (exact: CAS-loop IEEE add, 128-bit CAS, {nw} streams)",
+                 "us": ms * 1e3, "hbm_GBps": 16.0 * P * nw / (ms * 1e-3) / 1e9})
+    os.environ["TM_EASGD_CAS128"] = "0"  # the 32-bit CAS per element (a centre on a peer GPU)
+    ms = timeit(lambda: concurrent("exact"))
+    del os.environ["TM_EASGD_CAS128"]
+    rows.append({"mode": f"{nw} concurrent updates (exact: CAS-loop IEEE add, 32-bit CAS, {nw} streams)",
+                 "us": ms * 1e3, "hbm_GBps": 16.0 * P * nw / (ms * 1e-3) / 1e9})
     del c
     with tm.Exchanger(P, "easgd", size=nw, nlocal=nw) as ex:
         for sidx in range(nw):
