@@ -635,9 +635,9 @@ cudaError_t launch_easgd_round(float* const* w, int nw, const int32_t* order, in
 cudaError_t launch_easgd_sharded(float* x, const ShardArgs& sa, float alpha, int concurrent,
                                  cudaStream_t s) {
   const int grid = streaming_grid(sa.L / 4 + 4);
-  bool local = true;
-  for (int j = 0; j < sa.k; ++j) local = local && cas128_ok(sa.shard[j]);
-  if (concurrent == 2 && local) {
+  bool local = concurrent == 2;  // every shard on this GPU: the 128-bit CAS
+  for (int j = 0; local && j < sa.k; ++j) local = cas128_ok(sa.shard[j]);
+  if (local) {
     easgd_sharded_kernel<3, true><<<grid, kThreads, 0, s>>>(x, sa, alpha);
   } else if (concurrent == 2) {
     if (sa.sys) easgd_sharded_kernel<2, true><<<grid, kThreads, 0, s>>>(x, sa, alpha);
