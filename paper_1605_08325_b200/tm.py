@@ -236,12 +236,16 @@ def tm_easgd_update(worker, center, alpha, stream=None):
 
 
 def tm_easgd_update_ex(worker, center, alpha, concurrent=False, stream=None, n=None):
+    wptr = _fp32_cuda(worker)
     n = worker.numel() if n is None else int(n)
     if n < 0 or n > worker.numel():
         raise ValueError(f"n = {n} outside [0, {worker.numel()}]")
     cptr = center if isinstance(center, int) else _fp32_cuda(center, min_n=n).value
     mode = 2 if concurrent == "exact" else int(concurrent)  # 0, 1 (red.add), 2 / "exact" (CAS loop)
-    _check(lib().tm_easgd_update_ex(_fp32_cuda(worker), _P(cptr), int(n), ctypes.c_float(alpha),
+    if isinstance(center, torch.Tensor) and center.device != worker.device:
+        raise ValueError(f"centre on {center.device}, worker on {worker.device}: pass a peer-mapped "
+                         "pointer (int) for a centre on another GPU")
+    _check(lib().tm_easgd_update_ex(wptr, _P(cptr), int(n), ctypes.c_float(alpha),
                                     mode, _stream_handle(stream)), "tm_easgd_update_ex")
 
 
