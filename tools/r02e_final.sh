@@ -34,8 +34,4 @@ TM_PROCS_PER_GPU=$N timeout 900 python -m torch.distributed.run --nnodes=1 --npr
 echo "mps bench n$N rc=$?"
 done
 echo quit | nvidia-cuda-mps-control
-for T in memcheck racecheck synccheck; do
-  timeout 1500 compute-sanitizer --tool $T --error-exitcode 9 python tests/sanitize_driver.py > $O/san_default_${T}.txt 2>&1
-  echo "sanitizer $T rc=$?"; tail -1 $O/san_default_${T}.txt
-done
 timeout 300 python tools/sweep.py --only easgd > $O/easgd_sweep.jsonl 2> $O/easgd_sweep.err; echo "easgd sweep rc=$?"
