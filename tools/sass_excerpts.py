@@ -23,10 +23,13 @@ KERNELS = {
     "tm_exchange_tma_kernel_k8_asa16_gpu": r"tm_exchange_tma_kernelILi8ELb1ELb0ELb0E",
     "tm_exchange_oneshot_kernel_k8_asa16_sys": r"tm_exchange_oneshot_kernelILi8ELb1ELb1ELb0E",
     "easgd_round_tma_kernel_n8": r"easgd_round_tma_kernelILi8E",
+    "easgd_kernel_mode3_cas128": r"easgd_kernelILi3E",
+    "tm_exchange_ll_kernel_k8_asa16_sys": r"tm_exchange_ll_kernelILi8ELb1ELb1ELb0E",
+    "tm_exchange_ll2_kernel_k8_asa16_sys": r"tm_exchange_ll2_kernelILi8ELb1ELb1ELb0E",
 }
 PATTERNS = ["UBLKCP", "SYNCS", "LDG.E.128", "LDG.E.EL.128", "LDG.E.STRONG.GPU.128", "STG.E.128", "STG.E.EF.128",
             "STRONG.SYS", "STRONG.GPU", "FENCE", "MEMBAR", "REDG", "ATOMG", "BAR.SYNC", "F2FP.F16", "HADD2.F32",
-            "FADD", "FMUL", "NANOSLEEP", "CS2R"]
+            "FADD", "FMUL", "NANOSLEEP", "CS2R", "CAS.128", "LDG.E.128.STRONG.SYS", "STG.E.128.STRONG.SYS"]
 
 
 def main():
