@@ -314,7 +314,8 @@ cudaError_t direct_k(const LocalBufs& lb, int64_t P, uint32_t* status, unsigned 
                      bool q16, int dev, cudaStream_t s, int max_ctas) {
   static const bool force_ldg = env_int("TM_DIRECT_LDG", 0) == 1;
   static const bool force_tma = env_int("TM_DIRECT_TMA", 0) == 1;  // diagnostics: TMA at every size
-  static const bool range_tma = env_int("TM_RANGE_TMA", 0) == 1;  // A/B: budgeted buckets on the TMA kernel
+  // A/B: budgeted buckets on the TMA kernel (read per budgeted call, so tests can switch it)
+  const bool range_tma = max_ctas > 0 && env_int("TM_RANGE_TMA", 0) == 1;
   if (P >= 2048 && !force_ldg && (max_ctas <= 0 || range_tma) &&
       (force_tma || (int64_t)K * P > kDirectLdgMaxElems))
     return q16 ? direct_tma<K, true>(lb, P, status, ctr, dev, s, max_ctas)

@@ -566,3 +566,26 @@ def test_range_cta_budget_bitwise(path, budget):
     got = to_host(bufs)
     for r in range(k):
         assert_bitwise(got[r], want[r], f"rank {r}")
+
+
+@pytest.mark.parametrize("budget", [3, 40])
+def test_range_cta_budget_tma_kernel_bitwise(budget, monkeypatch):
+    """TM_RANGE_TMA=1 (the A/B knob, default off): budgeted buckets of the direct
+    path on the TMA kernel with a persistent grid of `budget` CTAs (buckets large
+    enough for it: k * count > 8 Mi elements) and the register kernel for the
+    small one -- the oracle's bits either way."""
+    monkeypatch.setenv("TM_RANGE_TMA", "1")
+    k, P = 4, 6_000_011
+    X = worker_buffers(P, k, "D2", config=161)
+    bufs = to_dev(X)
+    with tm.Exchanger(P, "asa16", size=k, nlocal=k, path="direct") as ex:
+        tm.tm_set_range_ctas(budget)
+        b1, b2 = 100_000, P // 2 // 4 * 4
+        for off, cnt in ((b2, P - b2), (b1, b2 - b1), (0, b1)):
+            ex.exchange_range(bufs, off, cnt)
+        code, _ = ex.status()
+    assert code == tm.TM_OK
+    want = ox.asa16_average(X)
+    got = to_host(bufs)
+    for r in range(k):
+        assert_bitwise(got[r], want[r], f"rank {r}")
