@@ -5,7 +5,7 @@ TM_BSP_TILE, TM_ROUND_STATIC, ...) take the value in this process's
 environment.  Every scenario compares the GPU result with the oracle bit for
 bit; exit code 0 = bitwise, 3 = mismatch.
 
-    python tests/knob_worker.py direct|bsp|round|oneshot|ranges|staged
+    python tests/knob_worker.py direct|direct_small_k|bsp|round|oneshot|ranges|staged
 """
 
 import os
@@ -69,6 +69,9 @@ def main():
     what = sys.argv[1]
     if what == "direct":  # k * P above the register-kernel threshold: the TMA direct kernel
         exchange_scenario(8, 1_500_007, ("asa16", "asa"), "direct")
+    elif what == "direct_small_k":  # k <= 4 on the TMA direct kernel (its own TM_TMA_CFG variants)
+        exchange_scenario(2, 5_000_011, ("asa16",), "direct")
+        exchange_scenario(4, 3_000_007, ("asa16", "asa"), "direct")
     elif what == "bsp":  # the fused BSP kernel on the TMA engine (k * P > 4 Mi)
         k, P, lr, mu = 8, 1_000_003, 0.01, 0.9
         W = worker_buffers(P, k, "D2", config=171)

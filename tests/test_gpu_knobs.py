@@ -16,6 +16,8 @@ CASES = [
     ("direct", {"TM_L2_HINT": "1"}),           # evict_first on the direct kernel's bulk loads
     ("direct", {"TM_L2_HINT": "3"}),           # ... and on its bulk stores
     ("direct", {"TM_DIRECT_STATIC": "1"}),     # static tile assignment instead of the claim counter
+] + [("direct", {"TM_TMA_CFG": c}) for c in ("1", "2", "4", "5", "6", "7")] + [   # k = 8 tile / ring / residency
+    ("direct_small_k", {"TM_TMA_CFG": c}) for c in ("9", "10", "11", "12")] + [    # k <= 4 variants
     ("bsp", {"TM_BSP_TILE": "512"}),
     ("bsp", {"TM_BSP_TILE": "2048"}),
     ("round", {"TM_ROUND_STATIC": "1"}),       # static tiles of the fused EASGD round
