@@ -316,7 +316,8 @@ int tm_easgd_center(int owner_rank, float** center);
  * concurrent == 0: the caller serialises the workers (bitwise equal to the
  * oracle's arrival order); 1 / 2: centre += e by the float atomic / the
  * CAS-loop IEEE add of tm_easgd_update_ex (system scope across processes), no
- * lost updates, order not fixed. */
+ * lost updates, order not fixed; mode 2 takes the 128-bit CAS when every shard
+ * is in this GPU's memory, the 32-bit CAS otherwise. */
 int tm_easgd_update_sharded(float* worker_buf, float alpha, int concurrent, void* stream);
 
 /* Per-worker ATOMIC exchange with the sharded centre (the server
