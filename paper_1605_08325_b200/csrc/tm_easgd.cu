@@ -567,9 +567,12 @@ cast_rn16_kernel(const float* __restrict__ in, uint16_t* __restrict__ out, int64
 
 // The 128-bit CAS of Mode 3 only on memory of the launching GPU (peer memory
 // behind an IPC mapping keeps the 32-bit CAS of Mode 2); TM_EASGD_CAS128=0 turns
-// it off (A/B).
+// it off (A/B), =2 forces it on peer memory too (for tools/multigpu_eval.sh:
+// 128-bit atomics over NVLink are untested on the one-GPU boxes).
 bool cas128_ok(const void* p) {
-  if (env_int("TM_EASGD_CAS128", 1) == 0) return false;  // read per launch (tests switch it)
+  const int mode = env_int("TM_EASGD_CAS128", 1);  // read per launch (tests switch it)
+  if (mode == 0) return false;
+  if (mode == 2) return true;
   int dev = 0;
   if (cudaGetDevice(&dev) != cudaSuccess) return false;
   cudaPointerAttributes at{};

@@ -9,6 +9,8 @@
 #   ag_table.txt              the allgather decision table (tools/ag_decide.py)
 #   nsys_n8.*                 an nsys capture with NVLink GPU metrics, if nsys exists
 #   pytest_multiprocess.txt   the multi-process GPU tests with one GPU per rank
+#   pytest_multiprocess_cas128_peer.txt   their concurrent-EASGD cases with the
+#                             128-bit CAS forced on peer memory (TM_EASGD_CAS128=2)
 #   bash tools/multigpu_eval.sh [steps]
 set -u
 STEPS=${1:-200}
@@ -73,4 +75,9 @@ else
 fi
 [ "$NG" -ge 8 ] && bash tools/nvlink_ncu.sh 8 "$OUT"
 timeout 3600 python -m pytest tests/test_gpu_multiprocess.py -x -q > "$OUT/pytest_multiprocess.txt" 2>&1
+# exact concurrent EASGD with the 128-bit CAS forced on peer GPUs' centre shards
+# (over NVLink; the default keeps the 32-bit CAS there): if this passes, the
+# 128-bit CAS can be allowed on peer memory too
+TM_EASGD_CAS128=2 timeout 900 python -m pytest tests/test_gpu_multiprocess.py -q -k "concurrent" \
+  > "$OUT/pytest_multiprocess_cas128_peer.txt" 2>&1
 echo "done: $OUT"
